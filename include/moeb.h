@@ -1,0 +1,202 @@
+/*
+ * moeb.h -- C ABI of the B200-native MoE-Beyond hot path (libmoeb.so).
+ *
+ * The reference (`moesim`, pure Python/numpy) has no native FFI: its hot path
+ * is a per-step Python callback protocol (predictor.predict(ctx) ->
+ * frozenset, ExpertCache.touch/prefetch). A per-step callback cannot be made
+ * GPU-native, so this ABI moves the boundary to BATCH granularity: every entry
+ * point processes whole packed traces. Each function names the reference
+ * interface it replaces (file:line under /root/reference/pkg/src/moesim/).
+ * INTEGRATION.md shows the ctypes binding the reference package would add.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *    unless the parameter says "host". The caller owns all memory; the
+ *    library allocates nothing and holds no global mutable state.
+ *  - `stream` is a cudaStream_t passed as void*. Calls are stream-ordered and
+ *    asynchronous; they return after enqueueing.
+ *  - Return 0 on success, a nonzero MOEB_E* code on failure; a thread-local
+ *    message is available from moeb_last_error(). Exceptions never cross.
+ *  - A trace row is one (prompt, token, layer) step. Rows of prompt p are the
+ *    half-open range [prompt_row_off[p], prompt_row_off[p+1]) in (token,
+ *    layer) order; every offset is therefore a multiple of L.
+ *  - An expert set is a bitmask of W = ceil(E/64) uint64 words per row (bit e
+ *    of word e/64 = expert e). E <= 256, L*E <= 65536.
+ *  - Counters are int64 and ACCUMULATED (+=) into the output, so results of
+ *    several launches (or several GPUs after an all-reduce) simply add.
+ */
+#ifndef MOEB_H_
+#define MOEB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MOEB_OK 0
+#define MOEB_EINVAL 1   /* bad argument (shape, range, null pointer) */
+#define MOEB_ECUDA 2    /* CUDA launch / runtime error */
+#define MOEB_ESMEM 3    /* per-simulation state does not fit in shared memory */
+#define MOEB_EDEVICE 4  /* device is not sm_100 (B200) */
+
+#define MOEB_MAX_PREDS 16
+
+/* Cache policies. LRU is the reference's ExpertCache (cache.py:58-154);
+ * LFU is builder-defined, parity unpinned. */
+#define MOEB_POLICY_LRU 0
+#define MOEB_POLICY_LFU 1
+
+const char* moeb_last_error(void);
+int moeb_version(void);
+/* 0 if the current device is sm_100 and the kernels are loadable. */
+int moeb_device_check(void);
+
+/*
+ * K1 -- prediction-guided cache replay.
+ * Replaces engine.replay_prompt / replay_traces (engine.py:113-238) with the
+ * ExpertCache protocol (cache.py:93-154): per prompt, warm-up rows touch the
+ * truth experts; measured rows run begin_step, prefetch(sorted(pred)[:budget]
+ * or all when unbounded), then touch every truth expert in ascending order.
+ * One simulation per (pred stream, capacity, prompt); all run concurrently.
+ *
+ *  truth            [rows][W]
+ *  preds            host array [n_preds] of device pointers [rows][W];
+ *                   a NULL entry means the empty prediction (lru_only)
+ *  covered          host array [n_preds] of device pointers [rows] uint8 or
+ *                   NULL (external predictor coverage, engine.py:175-176)
+ *  unbounded        host array [n_preds] (predictor.unbounded_prefetch)
+ *  capacities       host array [n_caps] of resolved entry counts
+ *                   (CacheConfig.resolve_capacity, cache.py:52-55)
+ *  counters         [n_preds][n_caps][4 + 3L] += measured_accesses,
+ *                   cache_hits, prediction_hits, uncovered_queries,
+ *                   layer_accesses[L], layer_cache_hits[L],
+ *                   layer_prediction_hits[L]          (engine.py:62-110)
+ *  per_prompt       [n_preds][n_caps][n_prompts][4] (nullable) +=
+ *                   measured_accesses, cache_hits, prediction_hits, uncovered
+ *  hit_masks        [n_preds][n_caps][rows][W] (nullable): bit e set iff the
+ *                   touch of truth expert e hit (warm-up rows included)
+ */
+int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* preds,
+                   const uint8_t* const* covered, const int32_t* unbounded, int n_preds,
+                   const int64_t* prompt_row_off, int n_prompts, int L, int E,
+                   int warmup_tokens, const int64_t* capacities, int n_caps, int budget,
+                   int policy, int64_t* counters, int64_t* per_prompt, uint64_t* hit_masks,
+                   void* stream);
+
+/*
+ * ExpertCache op stream (cache.py:58-154) for one cache, executed on device:
+ * ops[i] = 0 begin_step, 1 touch(keys[i]), 2 prefetch([keys[i]]).
+ * results[i] = touch hit / prefetch inserted. keys = layer*E + expert.
+ * Used for the reference's per-call API and its known-answer tests.
+ */
+int moeb_cache_ops(const int32_t* ops, const int32_t* keys, int64_t n, int L, int E,
+                   int64_t capacity, int policy, uint8_t* results, void* stream);
+
+/*
+ * K3 (+K2 +K7 fused) -- learned_linear predictor over whole traces.
+ * Replaces LearnedLinearPredictor.predict (predictors.py:262-268) with
+ * feature_vector / update_history (learner.py:52-72) and top_k_experts /
+ * threshold selection (learner.py:164-181). E <= 64.
+ *  weights     [E][L+E+1] fp64 (LinearModel.weights)
+ *  pred        [rows][W] predicted masks (every row; warm-up rows included)
+ *  logits      [rows][E] fp64 (nullable)
+ *  metrics     [3E+3] (nullable) += TP[E], FP[E], FN[E], positions,
+ *              exact matches, label-correct over rows with token >= warmup
+ *              (metrics.py:12-79)
+ */
+int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_row_off, int n_prompts,
+                        int L, int E, const double* weights, double decay, int budget,
+                        int threshold, int warmup_tokens, uint64_t* pred, double* logits,
+                        int64_t* metrics, void* stream);
+
+/*
+ * K2 -- mask head: logits -> top-k (ties to lower id) or logit > 0 masks.
+ * Replaces top_k_experts / predict_topk (learner.py:164-181). fp32 logits.
+ */
+int moeb_mask_head(const float* logits, int64_t rows, int E, int k, int threshold,
+                   uint64_t* masks, void* stream);
+
+/*
+ * K7 -- prediction-quality counters over rows with token >= warmup_tokens.
+ * Replaces macro_f1 / position_accuracy / label_accuracy (metrics.py:12-79);
+ * the host finishes F1 with the reference's numpy expression.
+ *  metrics [3E+3] += TP[E], FP[E], FN[E], positions, exact, label_correct
+ */
+int moeb_metrics(const uint64_t* pred, const uint64_t* truth, const int64_t* prompt_row_off,
+                 int n_prompts, int L, int E, int warmup_tokens, int64_t* metrics,
+                 void* stream);
+
+/*
+ * Rule-based predictors as mask tables (predictors.py:57-139).
+ *  kind 0 lru_only (empty), 1 oracle (truth truncated to the `budget` lowest
+ *  ids, :80-81), 2 next_layer_all (all E), 3 per-layer table
+ *  (global_frequency: table [L][W], :137-139).
+ */
+int moeb_policy_masks(int kind, const uint64_t* truth, int64_t rows, int L, int E, int budget,
+                      const uint64_t* layer_table, uint64_t* out, void* stream);
+
+/*
+ * Synthetic traces on device, bit-identical to traceio._generate_prompt
+ * (traceio.py:233-283). The host supplies, per prompt, the PCG64 state after
+ * the hot-key and token-id draws (state hi/lo, inc hi/lo) and the ordered hot
+ * set hot[p][L][h] (from np.argpartition on the host, traceio.py:255); the
+ * device replays the remaining draws (from_hot, hot_pick, uni_pick) with
+ * PCG64 jump-ahead and writes truth [P*T*L][W].
+ */
+int moeb_gen_traces(const uint64_t* pcg_state /*[P][4]*/, const uint8_t* hot /*[P][L][h]*/,
+                    int n_prompts, int T, int L, int E, int k, int h, double skew,
+                    uint64_t* truth, void* stream);
+
+/*
+ * K6 -- EAM cosine predictor (MoE-Infinity baseline) over whole traces.
+ * Replaces EamCosinePredictor / CosineMatchSession (predictors.py:151-219)
+ * and SketchCollection.match_nearest (sketches.py:165-184).
+ *
+ * moeb_eam_prepare: from raw sketches [S][L*E] fp64 (SketchCollection
+ *   .sketches) compute the unit-norm matrix TRANSPOSED, unit_t [L*E][S]
+ *   (sketches / ||row||, zero rows stay zero, sketches.py:157-160), and the
+ *   per-(sketch, layer) prediction table topw [S][L][W] = top-`budget`
+ *   strictly positive raw weights, ties to the lower id (_top_weights,
+ *   predictors.py:142-148, on the raw block sketches.py:186-189).
+ * moeb_eam_predict: for every row with token >= warmup: idx = argmax_s
+ *   U_s . normalize(partial rEAM before the row) (first max; zero query -> 0,
+ *   predictors.py:212-217); pred[row] = topw[idx][layer]; idx_out[row] = idx
+ *   (nullable; -1 on warm-up rows, whose pred is 0). S <= 8192.
+ */
+int moeb_eam_prepare(const double* sketches, int S, int L, int E, int budget, double* unit_t,
+                     uint64_t* topw, void* stream);
+int moeb_eam_predict(const uint64_t* truth, const int64_t* prompt_row_off, int n_prompts,
+                     int L, int E, int warmup_tokens, const double* unit_t,
+                     const uint64_t* topw, int S, int32_t* idx_out, uint64_t* pred,
+                     void* stream);
+
+/*
+ * K8 -- request-level activation matrices (rEAMs) from packed traces.
+ * moeb_ream_counts: counts[p][l*E+e] = activations of expert e at layer l in
+ *   prompt p over its first `max_tokens` tokens (all if max_tokens < 0);
+ *   ActivationMatrix.from_trace (core.py:196-205).
+ * moeb_sketch_normalize: sketches[p] = normalize(counts[p]) (core.py:221-231),
+ *   optionally binarized first (sketches._sketch_from_matrix, sketches.py:192-197).
+ */
+int moeb_ream_counts(const uint64_t* truth, const int64_t* prompt_row_off, int n_prompts, int L,
+                     int E, int max_tokens, int32_t* counts, void* stream);
+int moeb_sketch_normalize(const int32_t* counts, int n, int L, int E, int binarize,
+                          double* sketches, void* stream);
+
+/*
+ * Brute-force fp64 nearest-sketch scan for explicit query vectors:
+ * SketchCollection.match_nearest (sketches.py:165-184) for M queries at once.
+ *  queries [M][D] fp64, unit_t [D][S] (from moeb_eam_prepare).
+ *  idx_out [M] = argmax_s unit_s . q/|q| (first max; zero query -> 0),
+ *  sim_out [M] = that cosine clipped to [-1, 1] (0 for a zero query).
+ */
+int moeb_match_queries(const double* queries, int M, int D, const double* unit_t, int S,
+                       int32_t* idx_out, double* sim_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MOEB_H_ */

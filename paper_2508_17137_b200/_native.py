@@ -1,0 +1,118 @@
+"""ctypes binding of libmoeb.so (include/moeb.h) -- the only compute path.
+
+There is no CPU fallback: if the library is missing or no sm_100 GPU is
+visible, every entry point raises ``NativeUnavailable`` (a RuntimeError).
+Tensors are torch CUDA tensors used purely as device memory; masks are
+stored in int64 tensors holding the uint64 bit patterns.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmoeb.so")
+
+_lib = None
+_checked = False
+
+
+class NativeUnavailable(RuntimeError):
+    """libmoeb.so is not built or cannot run on this machine."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, fn: str, code: int, msg: str):
+        super().__init__(f"{fn} failed (code {code}): {msg}")
+        self.code = code
+
+
+P = ctypes.c_void_p
+I32, I64, DBL = ctypes.c_int, ctypes.c_int64, ctypes.c_double
+
+_SIGS = {
+    "moeb_cache_sim": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P, P],
+    "moeb_cache_ops": [P, P, I64, I32, I32, I64, I32, P, P],
+    "moeb_linear_predict": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P],
+    "moeb_mask_head": [P, I64, I32, I32, I32, P, P],
+    "moeb_metrics": [P, P, P, I32, I32, I32, I32, P, P],
+    "moeb_policy_masks": [I32, P, I64, I32, I32, I32, P, P, P],
+    "moeb_gen_traces": [P, P, I32, I32, I32, I32, I32, I32, DBL, P, P],
+    "moeb_eam_prepare": [P, I32, I32, I32, I32, P, P, P],
+    "moeb_eam_predict": [P, P, I32, I32, I32, I32, P, P, I32, P, P, P],
+    "moeb_ream_counts": [P, P, I32, I32, I32, I32, P, P],
+    "moeb_sketch_normalize": [P, I32, I32, I32, I32, P, P],
+    "moeb_match_queries": [P, I32, I32, P, I32, P, P, P],
+    "moeb_version": [],
+    "moeb_device_check": [],
+}
+
+EXPORTS = tuple(_SIGS) + ("moeb_last_error",)
+
+
+def load_library(require_gpu: bool = True):
+    """Load libmoeb.so; with require_gpu, also verify an sm_100 device."""
+    global _lib, _checked
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeUnavailable(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2508_17137_b200.build`")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        lib.moeb_last_error.argtypes = []
+        lib.moeb_last_error.restype = ctypes.c_char_p
+        _lib = lib
+    if require_gpu and not _checked:
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device visible; libmoeb has no CPU fallback")
+        torch.cuda.init()
+        rc = _lib.moeb_device_check()
+        if rc != 0:
+            raise NativeUnavailable(_lib.moeb_last_error().decode())
+        _checked = True
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    lib = load_library()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        raise NativeError(name, rc, lib.moeb_last_error().decode())
+
+
+def ptr(t):
+    """Device pointer of a CUDA tensor (None -> NULL)."""
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libmoeb takes CUDA tensors only")
+    if not t.is_contiguous():
+        raise ValueError("libmoeb takes contiguous tensors only")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr_array(tensors):
+    """Host array of device pointers (NULL for None entries)."""
+    arr = (ctypes.c_void_p * len(tensors))()
+    for i, t in enumerate(tensors):
+        arr[i] = None if t is None else t.data_ptr()
+    return arr
+
+
+def i32_array(vals):
+    return (ctypes.c_int32 * len(vals))(*[int(v) for v in vals])
+
+
+def i64_array(vals):
+    return (ctypes.c_int64 * len(vals))(*[int(v) for v in vals])

@@ -1,0 +1,649 @@
+// K1 -- prediction-guided expert-cache replay on device.
+//
+// Replaces engine.replay_prompt / replay_traces (engine.py:113-238) and the
+// ExpertCache protocol (cache.py:58-154). One CUDA thread owns one
+// simulation = (prediction stream, capacity, prompt); its whole cache state
+// lives in a private slice of shared memory, and the thread walks the
+// prompt's rows in (token, layer) order exactly as the reference loop does.
+// Every step touches only keys of ONE layer, so that layer's resident and
+// pinned bitmasks stay in registers for the step (written back on layer
+// change), and set-membership / prediction-hit tests are register bit ops
+// (popc(truth & pred) for prediction hits).
+//
+// LRU state (bit-exact with the reference OrderedDict, cache.py:68-124):
+//   stamp[key]  u16 recency stamp of each resident key (0 = not resident)
+//   q[]         ring deque of (stamp << 16 | layer << 8 | expert) entries in
+//               push order. A "move to end" pushes a fresh entry and leaves a
+//               stale one behind (lazy deletion): entry valid iff
+//               stamp[key] == entry stamp. The LRU key is the first valid
+//               entry from the head; eviction skips pinned ones in place
+//               (`_evict_one`, cache.py:93-100). When the ring is full or the
+//               16-bit clock is exhausted, the ring is compacted in order and
+//               stamps renumbered 1..n (order preserved).
+// LFU state (builder-defined; parity unpinned): slot array
+//   vals[slot] = pin << 63 | freq << 32 | clock, evict = argmin over slots.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr uint64_t kPin = 1ull << 63;
+
+struct SimArgs {
+  const uint64_t* truth;
+  const uint64_t* preds[MOEB_MAX_PREDS];
+  const uint8_t* covered[MOEB_MAX_PREDS];
+  uint32_t unbounded_bits;
+  int n_preds;
+  const int64_t* row_off;
+  int P, L, E, warmup, budget;
+  int64_t cap;
+  int64_t rows;
+  int64_t* counters;  // this capacity: + pred * pred_stride
+  int64_t counters_stride;
+  int64_t* per_prompt;
+  int64_t per_prompt_stride;
+  uint64_t* hits;
+  int64_t hits_stride;
+  // per-simulation shared-memory layout (bytes)
+  int off_r, off_q, off_c, sim_bytes;
+  uint32_t qmask;  // LRU ring size - 1; LFU: unused
+};
+
+template <int W>
+__device__ __forceinline__ uint64_t word_get(const uint64_t (&a)[W], int w) {
+  uint64_t v = a[0];
+#pragma unroll
+  for (int j = 1; j < W; ++j) v = (w == j) ? a[j] : v;
+  return v;
+}
+template <int W>
+__device__ __forceinline__ void word_or(uint64_t (&a)[W], int w, uint64_t bit) {
+#pragma unroll
+  for (int j = 0; j < W; ++j)
+    if (w == j) a[j] |= bit;
+}
+template <int W>
+__device__ __forceinline__ void word_clear(uint64_t (&a)[W], int w, uint64_t bit) {
+#pragma unroll
+  for (int j = 0; j < W; ++j)
+    if (w == j) a[j] &= ~bit;
+}
+
+// ---------------------------------------------------------------------------
+// LRU
+// ---------------------------------------------------------------------------
+template <int W, bool GENERAL>
+struct LruState {
+  uint16_t* stamp;  // [L*E]
+  uint64_t* R;      // [L*W] resident masks (stale for cur layer)
+  uint64_t* Psm;    // GENERAL only: [L*W] pin masks (stale for cur layer)
+  uint32_t* q;
+  uint32_t qmask, head, tail, clock;
+  int64_t count, cap;
+  int npins, E, L, cur;
+  uint64_t Rl[W], Pm[W];
+
+  __device__ void init(unsigned char* base, const SimArgs& a, int L_) {
+    L = L_;
+    E = a.E;
+    cap = a.cap;
+    stamp = reinterpret_cast<uint16_t*>(base);
+    R = reinterpret_cast<uint64_t*>(base + a.off_r);
+    Psm = GENERAL ? R + L * W : nullptr;
+    q = reinterpret_cast<uint32_t*>(base + a.off_q);
+    qmask = a.qmask;
+    head = tail = 0;
+    clock = 1;
+    count = 0;
+    npins = 0;
+    cur = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) Rl[j] = Pm[j] = 0;
+    // zero stamps and masks (16-byte stores; regions are 16-byte padded)
+    uint4* z = reinterpret_cast<uint4*>(base);
+    const int n16 = a.off_q / 16;
+    for (int i = 0; i < n16; ++i) z[i] = make_uint4(0, 0, 0, 0);
+  }
+
+  __device__ __forceinline__ void focus(int l) {
+    if (l == cur) return;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      R[cur * W + j] = Rl[j];
+      Rl[j] = R[l * W + j];
+      if (GENERAL) {
+        Psm[cur * W + j] = Pm[j];
+        Pm[j] = Psm[l * W + j];
+      }
+    }
+    cur = l;
+  }
+
+  __device__ __forceinline__ void writeback() {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      R[cur * W + j] = Rl[j];
+      if (GENERAL) Psm[cur * W + j] = Pm[j];
+    }
+  }
+
+  __device__ __forceinline__ bool is_pinned(int l, int ex) const {
+    const uint64_t bit = 1ull << (ex & 63);
+    if (l == cur) return (word_get<W>(Pm, ex >> 6) & bit) != 0;
+    if (GENERAL) return (Psm[l * W + (ex >> 6)] & bit) != 0;
+    return false;  // trace mode: pins only ever exist in the current layer
+  }
+
+  __device__ void compact() {
+    uint32_t n = 0;
+    for (uint32_t i = head; i != tail; ++i) {
+      const uint32_t e = q[i & qmask];
+      const uint32_t qk = e & 0xFFFFu;
+      const int sidx = (int)(qk >> 8) * E + (int)(qk & 0xFFu);
+      if (stamp[sidx] == (e >> 16)) {
+        ++n;
+        stamp[sidx] = (uint16_t)n;
+        q[(head + n - 1) & qmask] = (n << 16) | qk;
+      }
+    }
+    tail = head + n;
+    clock = n + 1;
+  }
+
+  __device__ __forceinline__ void push(int l, int ex) {
+    if (tail - head > qmask || clock >= 0xFFFFu) compact();
+    stamp[l * E + ex] = (uint16_t)clock;
+    q[tail & qmask] = (clock << 16) | ((uint32_t)l << 8) | (uint32_t)ex;
+    ++tail;
+    ++clock;
+  }
+
+  // _evict_one (cache.py:93-100). Precondition: count > npins.
+  __device__ void evict() {
+    uint32_t i = head;
+    bool at_head = true;
+    for (;;) {
+      const uint32_t e = q[i & qmask];
+      ++i;
+      const int l = (int)((e >> 8) & 0xFFu), ex = (int)(e & 0xFFu);
+      const int sidx = l * E + ex;
+      if (stamp[sidx] != (e >> 16)) {
+        if (at_head) head = i;
+        continue;
+      }
+      if (is_pinned(l, ex)) {
+        at_head = false;
+        continue;
+      }
+      stamp[sidx] = 0;
+      const uint64_t bit = 1ull << (ex & 63);
+      if (l == cur)
+        word_clear<W>(Rl, ex >> 6, bit);
+      else
+        R[l * W + (ex >> 6)] &= ~bit;
+      --count;
+      if (at_head) head = i;
+      return;
+    }
+  }
+
+  __device__ void begin_step(int l) {
+    if (GENERAL) {
+      for (int j = 0; j < L * W; ++j) Psm[j] = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) Pm[j] = 0;
+    npins = 0;
+    focus(l);
+  }
+
+  // touch (cache.py:106-124) of expert ex of the current layer.
+  __device__ __forceinline__ bool touch(int ex) {
+    const uint64_t bit = 1ull << (ex & 63);
+    if (word_get<W>(Rl, ex >> 6) & bit) {
+      push(cur, ex);
+      return true;
+    }
+    if (count >= cap) {
+      if (count <= npins) return false;  // every resident key pinned
+      evict();
+    }
+    word_or<W>(Rl, ex >> 6, bit);
+    ++count;
+    push(cur, ex);
+    return false;
+  }
+
+  // one key of prefetch (cache.py:141-153); returns true if inserted.
+  __device__ __forceinline__ bool prefetch(int ex) {
+    const int w = ex >> 6;
+    const uint64_t bit = 1ull << (ex & 63);
+    if (word_get<W>(Rl, w) & bit) {
+      push(cur, ex);
+      if (!(word_get<W>(Pm, w) & bit)) {
+        word_or<W>(Pm, w, bit);
+        ++npins;
+      }
+      return false;
+    }
+    if (count >= cap) {
+      if (count <= npins) return false;
+      evict();
+    }
+    word_or<W>(Rl, w, bit);
+    ++count;
+    push(cur, ex);
+    word_or<W>(Pm, w, bit);
+    ++npins;
+    return true;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// LFU (builder-defined): evict the non-pinned resident key with the fewest
+// demand touches since insertion, least-recently-used among ties. Touch
+// insert -> freq 1, prefetch insert -> freq 0, touch hit -> freq + 1,
+// prefetch refresh -> recency only.
+// ---------------------------------------------------------------------------
+template <int W, bool GENERAL>
+struct LfuState {
+  uint16_t* slot_of;  // [L*E] valid for resident keys only
+  uint64_t* R;        // [L*W]
+  uint64_t* vals;     // [cap]
+  uint16_t* skeys;    // [cap] (layer << 8 | expert)
+  int64_t count, cap;
+  uint32_t clock;
+  int npins, E, L, cur;
+  uint64_t Rl[W], Pm[W];
+
+  __device__ void init(unsigned char* base, const SimArgs& a, int L_) {
+    L = L_;
+    E = a.E;
+    cap = a.cap;
+    slot_of = reinterpret_cast<uint16_t*>(base);
+    R = reinterpret_cast<uint64_t*>(base + a.off_r);
+    vals = reinterpret_cast<uint64_t*>(base + a.off_q);
+    skeys = reinterpret_cast<uint16_t*>(base + a.off_q + 8 * a.cap);
+    count = 0;
+    clock = 1;
+    npins = 0;
+    cur = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) Rl[j] = Pm[j] = 0;
+    for (int j = 0; j < L * W; ++j) R[j] = 0;
+  }
+
+  __device__ __forceinline__ void focus(int l) {
+    if (l == cur) return;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      R[cur * W + j] = Rl[j];
+      Rl[j] = R[l * W + j];
+    }
+    cur = l;
+  }
+  __device__ __forceinline__ void writeback() {
+#pragma unroll
+    for (int j = 0; j < W; ++j) R[cur * W + j] = Rl[j];
+  }
+
+  __device__ int victim_slot() const {
+    uint64_t best = ~0ull;
+    int bs = 0;
+    for (int s = 0; s < (int)count; ++s) {
+      const uint64_t v = vals[s];
+      if (v < best) {
+        best = v;
+        bs = s;
+      }
+    }
+    return bs;
+  }
+
+  // Returns the slot to fill: a fresh one, or the evicted victim's.
+  __device__ int make_room() {
+    if (count < cap) return (int)count++;
+    const int s = victim_slot();
+    const uint32_t vk = skeys[s];
+    const int l = (int)(vk >> 8), ex = (int)(vk & 0xFFu);
+    const uint64_t bit = 1ull << (ex & 63);
+    if (l == cur)
+      word_clear<W>(Rl, ex >> 6, bit);
+    else
+      R[l * W + (ex >> 6)] &= ~bit;
+    return s;
+  }
+
+  __device__ void begin_step(int l) {
+    if (GENERAL) {
+      for (int s = 0; s < (int)count; ++s) vals[s] &= ~kPin;
+    } else {
+      MOEB_FOR_EACH_BIT(W, Pm, ex, { vals[slot_of[cur * E + ex]] &= ~kPin; })
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) Pm[j] = 0;
+    npins = 0;
+    focus(l);
+  }
+
+  __device__ __forceinline__ bool touch(int ex) {
+    const uint64_t bit = 1ull << (ex & 63);
+    const int key = cur * E + ex;
+    if (word_get<W>(Rl, ex >> 6) & bit) {
+      const int s = slot_of[key];
+      const uint64_t v = vals[s];
+      const uint64_t freq = ((v & ~kPin) >> 32) + 1;
+      vals[s] = (v & kPin) | (freq << 32) | clock++;
+      return true;
+    }
+    if (count >= cap && count <= npins) return false;
+    const int s = make_room();
+    vals[s] = (1ull << 32) | clock++;
+    skeys[s] = (uint16_t)((cur << 8) | ex);
+    slot_of[key] = (uint16_t)s;
+    word_or<W>(Rl, ex >> 6, bit);
+    return false;
+  }
+
+  __device__ __forceinline__ bool prefetch(int ex) {
+    const int w = ex >> 6;
+    const uint64_t bit = 1ull << (ex & 63);
+    const int key = cur * E + ex;
+    if (word_get<W>(Rl, w) & bit) {
+      const int s = slot_of[key];
+      const uint64_t v = vals[s];
+      vals[s] = kPin | (v & 0x7FFFFFFF00000000ull) | clock++;
+      if (!(v & kPin)) {
+        word_or<W>(Pm, w, bit);
+        ++npins;
+      }
+      return false;
+    }
+    if (count >= cap && count <= npins) return false;
+    const int s = make_room();
+    vals[s] = kPin | clock++;
+    skeys[s] = (uint16_t)((cur << 8) | ex);
+    slot_of[key] = (uint16_t)s;
+    word_or<W>(Rl, w, bit);
+    word_or<W>(Pm, w, bit);
+    ++npins;
+    return true;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Trace replay driver (engine.py:157-206), shared by both policies.
+// ---------------------------------------------------------------------------
+template <int W, class State>
+__global__ void __launch_bounds__(32) k_cache_sim(const SimArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t sim = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (sim >= (int64_t)a.n_preds * a.P) return;
+  const int pi = (int)(sim / a.P);
+  const int p = (int)(sim % a.P);
+  unsigned char* base = smem + (size_t)threadIdx.x * a.sim_bytes;
+  const int L = a.L;
+  uint32_t* lcnt = reinterpret_cast<uint32_t*>(base + a.off_c);
+  for (int j = 0; j < 3 * L; ++j) lcnt[j] = 0;
+
+  State st;
+  st.init(base, a, L);
+
+  const uint64_t* __restrict__ pred = a.preds[pi];
+  const uint8_t* __restrict__ cov = a.covered[pi];
+  const bool unbounded = (a.unbounded_bits >> pi) & 1u;
+  const int limit = unbounded ? a.E : a.budget;
+  uint64_t* hits = a.hits ? a.hits + pi * a.hits_stride : nullptr;
+
+  int64_t tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
+  const int64_t r0 = a.row_off[p], r1 = a.row_off[p + 1];
+  int l = 0, t = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    uint64_t tw[W], hw[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      tw[j] = __ldg(a.truth + r * W + j);
+      hw[j] = 0;
+    }
+    if (t < a.warmup) {  // engine.py:160-167: warm the cache, no counters
+      st.focus(l);
+      MOEB_FOR_EACH_BIT(W, tw, ex, {
+        if (st.touch(ex)) word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
+      })
+    } else {
+      uint64_t pw[W];
+#pragma unroll
+      for (int j = 0; j < W; ++j) pw[j] = pred ? __ldg(pred + r * W + j) : 0ull;
+      st.begin_step(l);  // engine.py:172
+      int taken = 0;     // prefetch(sorted(pred)[:limit]) (engine.py:173-174)
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint64_t m = pw[w];
+        while (m && taken < limit) {
+          const int ex = w * 64 + __ffsll((long long)m) - 1;
+          m &= m - 1;
+          st.prefetch(ex);
+          ++taken;
+        }
+      }
+      if (cov && !cov[r]) ++tot_unc;  // engine.py:175-176
+      int k = 0, ph = 0, ch = 0;
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        k += __popcll(tw[j]);
+        ph += __popcll(tw[j] & pw[j]);  // FULL predicted set (engine.py:181-182)
+      }
+      MOEB_FOR_EACH_BIT(W, tw, ex, {
+        if (st.touch(ex)) {
+          ++ch;
+          word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
+        }
+      })
+      tot_k += k;
+      tot_ch += ch;
+      tot_ph += ph;
+      lcnt[l] += k;
+      lcnt[L + l] += ch;
+      lcnt[2 * L + l] += ph;
+    }
+    if (hits) {
+#pragma unroll
+      for (int j = 0; j < W; ++j) hits[r * W + j] = hw[j];
+    }
+    if (++l == L) {
+      l = 0;
+      ++t;
+    }
+  }
+
+  int64_t* c = a.counters + pi * a.counters_stride;
+  atomicAdd(reinterpret_cast<unsigned long long*>(c + 0), (unsigned long long)tot_k);
+  atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot_ch);
+  atomicAdd(reinterpret_cast<unsigned long long*>(c + 2), (unsigned long long)tot_ph);
+  if (tot_unc) atomicAdd(reinterpret_cast<unsigned long long*>(c + 3), (unsigned long long)tot_unc);
+  for (int j = 0; j < 3 * L; ++j)
+    if (lcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)lcnt[j]);
+  if (a.per_prompt) {
+    int64_t* pp = a.per_prompt + pi * a.per_prompt_stride + 4 * (int64_t)p;
+    pp[0] += tot_k;
+    pp[1] += tot_ch;
+    pp[2] += tot_ph;
+    pp[3] += tot_unc;
+  }
+}
+
+// Op-stream interpreter (one cache): the reference's per-call API.
+template <int W, class State>
+__global__ void k_cache_ops(const SimArgs a, const int32_t* ops, const int32_t* keys, int64_t n,
+                            uint8_t* results) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  State st;
+  st.init(smem, a, a.L);
+  for (int64_t i = 0; i < n; ++i) {
+    uint8_t res = 0;
+    if (ops[i] == 0) {
+      st.begin_step(st.cur);
+    } else {
+      const int key = keys[i];
+      st.focus(key / a.E);
+      const int ex = key % a.E;
+      res = ops[i] == 1 ? (uint8_t)st.touch(ex) : (uint8_t)st.prefetch(ex);
+    }
+    results[i] = res;
+  }
+}
+
+inline int align16(int64_t x) { return (int)((x + 15) / 16 * 16); }
+
+// Shared-memory layout of one simulation.
+void layout(SimArgs& a, int policy, bool general) {
+  const int W = moeb::words_for(a.E);
+  const int64_t LE = (int64_t)a.L * a.E;
+  a.off_r = align16(2 * LE);
+  const int64_t rbytes = 8LL * a.L * W * (general ? 2 : 1);
+  a.off_q = align16(a.off_r + rbytes);
+  int64_t qbytes;
+  if (policy == MOEB_POLICY_LRU) {
+    uint32_t qn = 64;
+    const int64_t need = std::max<int64_t>(2 * a.cap, a.cap + 64);
+    while (qn < need) qn <<= 1;
+    a.qmask = qn - 1;
+    qbytes = 4LL * qn;
+  } else {
+    a.qmask = 0;
+    qbytes = 8LL * a.cap + 2LL * a.cap;
+  }
+  a.off_c = align16(a.off_q + qbytes);
+  // +16 bytes skews consecutive simulations across shared-memory banks
+  a.sim_bytes = align16(a.off_c + 4LL * 3 * a.L) + 16;
+}
+
+template <int W>
+int launch_sim(const SimArgs& a, int policy, cudaStream_t s) {
+  const int64_t sims = (int64_t)a.n_preds * a.P;
+  const int per_sm = std::max(1, moeb::max_smem_per_sm() / (a.sim_bytes + 256));
+  const int max_block = moeb::max_smem_per_block();
+  if (a.sim_bytes > max_block)
+    return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
+                      a.sim_bytes, max_block);
+  // Threads per block: keep >= 4 blocks per SM when the state allows it so
+  // the four SM sub-partitions all issue; never more than one warp.
+  int tpb = std::min(32, std::max(1, per_sm / 4));
+  tpb = std::min<int64_t>(tpb, std::max<int64_t>(1, sims));
+  while (tpb > 1 && tpb * a.sim_bytes > max_block) --tpb;
+  const size_t smem = (size_t)tpb * a.sim_bytes;
+  const int64_t blocks = (sims + tpb - 1) / tpb;
+  if (policy == MOEB_POLICY_LRU) {
+    auto k = k_cache_sim<W, LruState<W, false>>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)blocks, tpb, smem, s>>>(a);
+  } else {
+    auto k = k_cache_sim<W, LfuState<W, false>>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)blocks, tpb, smem, s>>>(a);
+  }
+  return moeb::check_launch("k_cache_sim");
+}
+
+}  // namespace
+
+extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* preds,
+                              const uint8_t* const* covered, const int32_t* unbounded,
+                              int n_preds, const int64_t* prompt_row_off, int n_prompts, int L,
+                              int E, int warmup_tokens, const int64_t* capacities, int n_caps,
+                              int budget, int policy, int64_t* counters, int64_t* per_prompt,
+                              uint64_t* hit_masks, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(truth && prompt_row_off && counters && capacities, "null argument");
+  MOEB_REQUIRE(n_preds >= 1 && n_preds <= MOEB_MAX_PREDS, "n_preds must be in [1, %d]",
+               MOEB_MAX_PREDS);
+  MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && E >= 1 && E <= 256 && L <= 255 && L * E <= 65536,
+               "unsupported shape L=%d E=%d", L, E);
+  MOEB_REQUIRE(warmup_tokens >= 0 && budget >= 1, "bad warmup/budget");
+  MOEB_REQUIRE(policy == MOEB_POLICY_LRU || policy == MOEB_POLICY_LFU, "unknown policy %d",
+               policy);
+  const int W = moeb::words_for(E);
+  int64_t rows = 0;
+  if (hit_masks) {
+    if (cudaMemcpy(&rows, prompt_row_off + n_prompts, sizeof(int64_t),
+                   cudaMemcpyDeviceToHost) != cudaSuccess)
+      return moeb::fail(MOEB_ECUDA, "reading prompt_row_off");
+  }
+  SimArgs a{};
+  a.truth = truth;
+  a.n_preds = n_preds;
+  for (int i = 0; i < n_preds; ++i) {
+    a.preds[i] = preds ? preds[i] : nullptr;
+    a.covered[i] = covered ? covered[i] : nullptr;
+    if (unbounded && unbounded[i]) a.unbounded_bits |= 1u << i;
+  }
+  a.row_off = prompt_row_off;
+  a.P = n_prompts;
+  a.L = L;
+  a.E = E;
+  a.warmup = warmup_tokens;
+  a.budget = budget;
+  a.rows = rows;
+  const int nc = 4 + 3 * L;
+  cudaStream_t s = moeb::as_stream(stream);
+  for (int c = 0; c < n_caps; ++c) {
+    MOEB_REQUIRE(capacities[c] >= 1 && capacities[c] <= (int64_t)L * E,
+                 "capacity %lld out of range [1, %d]", (long long)capacities[c], L * E);
+    a.cap = capacities[c];
+    a.counters = counters + (int64_t)c * nc;
+    a.counters_stride = (int64_t)n_caps * nc;
+    a.per_prompt = per_prompt ? per_prompt + (int64_t)c * n_prompts * 4 : nullptr;
+    a.per_prompt_stride = (int64_t)n_caps * n_prompts * 4;
+    a.hits = hit_masks ? hit_masks + (int64_t)c * rows * W : nullptr;
+    a.hits_stride = (int64_t)n_caps * rows * W;
+    layout(a, policy, false);
+    int rc = W == 1 ? launch_sim<1>(a, policy, s)
+             : W == 2 ? launch_sim<2>(a, policy, s)
+             : W == 3 ? launch_sim<3>(a, policy, s)
+                      : launch_sim<4>(a, policy, s);
+    if (rc) return rc;
+  }
+  return MOEB_OK;
+}
+
+template <int W>
+static int launch_ops(SimArgs& a, int policy, const int32_t* ops, const int32_t* keys, int64_t n,
+                      uint8_t* results, cudaStream_t s) {
+  layout(a, policy, true);
+  const size_t smem = a.sim_bytes;
+  if ((int)smem > moeb::max_smem_per_block())
+    return moeb::fail(MOEB_ESMEM, "cache state %zu B exceeds shared memory", smem);
+  if (policy == MOEB_POLICY_LRU) {
+    auto k = k_cache_ops<W, LruState<W, true>>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<1, 32, smem, s>>>(a, ops, keys, n, results);
+  } else {
+    auto k = k_cache_ops<W, LfuState<W, true>>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<1, 32, smem, s>>>(a, ops, keys, n, results);
+  }
+  return moeb::check_launch("k_cache_ops");
+}
+
+extern "C" int moeb_cache_ops(const int32_t* ops, const int32_t* keys, int64_t n, int L, int E,
+                              int64_t capacity, int policy, uint8_t* results, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(ops && keys && results, "null argument");
+  MOEB_REQUIRE(L >= 1 && E >= 1 && E <= 256 && L <= 255 && L * E <= 65536,
+               "unsupported shape L=%d E=%d", L, E);
+  MOEB_REQUIRE(capacity >= 1 && capacity <= (int64_t)L * E, "capacity out of range");
+  MOEB_REQUIRE(policy == MOEB_POLICY_LRU || policy == MOEB_POLICY_LFU, "unknown policy");
+  SimArgs a{};
+  a.L = L;
+  a.E = E;
+  a.cap = capacity;
+  const int W = moeb::words_for(E);
+  cudaStream_t s = moeb::as_stream(stream);
+  return W == 1 ? launch_ops<1>(a, policy, ops, keys, n, results, s)
+         : W == 2 ? launch_ops<2>(a, policy, ops, keys, n, results, s)
+         : W == 3 ? launch_ops<3>(a, policy, ops, keys, n, results, s)
+                  : launch_ops<4>(a, policy, ops, keys, n, results, s);
+}

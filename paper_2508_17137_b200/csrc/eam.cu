@@ -1,0 +1,375 @@
+// K6 -- EAM cosine predictor (MoE-Infinity baseline) over whole traces.
+//
+// Reference: EamCosinePredictor / CosineMatchSession (predictors.py:151-219),
+// SketchCollection.match_nearest / layer_block (sketches.py:145-189),
+// _top_weights (predictors.py:142-148), normalize (core.py:221-231).
+//
+// At a measured row (t, l) the query is the partial request-level activation
+// matrix (rEAM) before the row, normalised per layer. Every trace row adds
+// exactly k activations, so the row sums are R = k(t+1) for layers < l and
+// R = k t for layers >= l. With d_s(l') = U_s,l' . c(l')
+// (c = raw counts) the cosine score is, up to the positive factor 1/(k |q|)
+// that cannot change the argmax,
+//     score_s(t, l) = Dlow_s / (t + 1) + Dhigh_s / t,
+//     Dlow_s = sum_{l' < l} d_s(l'),  Dhigh_s = sum_{l' >= l} d_s(l')
+// (a t = 0 term is zero: normalize() leaves empty rows at zero). Accumulating
+// a row changes one d_s(l) by the sum of k entries of U (a coalesced gather
+// from the transposed unit matrix), so each step is O(S) work instead of the
+// reference session's O(S*E) or the direct form's O(S*L*E).
+//
+// Mapping: one CTA per prompt; thread j owns sketches j, j + blockDim, ...;
+// d_s(l') lives in shared memory [L][S]; a block argmax (warp shuffles, ties
+// to the lower index) picks the sketch; the prediction is a table lookup
+// topw[idx][l] precomputed by moeb_eam_prepare.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kSPT = 8;  // sketches per thread
+
+__global__ void k_eam_norms(const double* __restrict__ sk, int S, int D, double* __restrict__ unit_t) {
+  const int s = blockIdx.x;
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const double x = sk[(int64_t)s * D + d];
+    acc = fma(x, x, acc);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  double nrm = sqrt(red[0]);
+  if (!(nrm > 0.0)) nrm = 1.0;  // zero rows stay zero (sketches.py:158-160)
+  for (int d = threadIdx.x; d < D; d += blockDim.x)
+    unit_t[(int64_t)d * S + s] = sk[(int64_t)s * D + d] / nrm;
+}
+
+// topw[s][l] = top-`budget` strictly positive raw weights, ties to lower id.
+__global__ void k_eam_topw(const double* __restrict__ sk, int S, int L, int E, int budget,
+                           uint64_t* __restrict__ topw) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)S * L) return;
+  const int s = (int)(i / L), l = (int)(i % L);
+  const int W = (E + 63) / 64;
+  const double* blk = sk + (int64_t)s * L * E + (int64_t)l * E;
+  uint64_t m[4] = {0, 0, 0, 0};
+  for (int j = 0; j < budget; ++j) {
+    int best = -1;
+    double bv = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double v = blk[e];
+      if (!(v > 0.0) || ((m[e >> 6] >> (e & 63)) & 1ull)) continue;
+      if (best < 0 || v > bv) {
+        best = e;
+        bv = v;
+      }
+    }
+    if (best < 0) break;
+    m[best >> 6] |= 1ull << (best & 63);
+  }
+  for (int w = 0; w < W; ++w) topw[i * W + w] = m[w];
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_eam_predict(
+    const uint64_t* __restrict__ truth, const int64_t* __restrict__ row_off, int L, int E,
+    int warmup, const double* __restrict__ unit_t, const uint64_t* __restrict__ topw, int S,
+    int32_t* __restrict__ idx_out, uint64_t* __restrict__ pred) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* d = reinterpret_cast<double*>(smem_raw);  // [L][S]
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  const int p = blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  for (int i = tid; i < L * S; i += nt) d[i] = 0.0;
+  double dlo[kSPT], dhi[kSPT];
+#pragma unroll
+  for (int j = 0; j < kSPT; ++j) dlo[j] = dhi[j] = 0.0;
+  __syncthreads();
+
+  const int64_t r0 = row_off[p], r1 = row_off[p + 1];
+  int l = 0, t = 0;
+  for (int64_t r = r0; r < r1; ++r) {
+    uint64_t tw[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) tw[w] = __ldg(truth + r * W + w);
+    if (t >= warmup) {
+      const double a_lo = 1.0 / (double)(t + 1);
+      double best = -DBL_MAX;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < kSPT; ++j) {
+        const int s = tid + j * nt;
+        if (s < S) {
+          const double v = t > 0 ? dlo[j] * a_lo + dhi[j] / (double)t : dlo[j] * a_lo;
+          if (v > best) {  // ascending s within the thread: first max wins
+            best = v;
+            bi = s;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        red_v[wid] = best;
+        red_i[wid] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double bv = red_v[0];
+        int b = red_i[0];
+        for (int w = 1; w < (nt >> 5); ++w)
+          if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < b)) {
+            bv = red_v[w];
+            b = red_i[w];
+          }
+        if (idx_out) idx_out[r] = b;
+#pragma unroll
+        for (int w = 0; w < W; ++w) pred[r * W + w] = topw[((int64_t)b * L + l) * W + w];
+      }
+      __syncthreads();
+    } else if (tid == 0) {
+      if (idx_out) idx_out[r] = -1;
+#pragma unroll
+      for (int w = 0; w < W; ++w) pred[r * W + w] = 0;
+    }
+    // accumulate the row into the partial rEAM (core.py:182-194)
+#pragma unroll
+    for (int j = 0; j < kSPT; ++j) {
+      const int s = tid + j * nt;
+      if (s < S) {
+        double g = 0.0;
+        MOEB_FOR_EACH_BIT(W, tw, ex, { g += __ldg(unit_t + (int64_t)(l * E + ex) * S + s); })
+        const double dold = d[l * S + s];
+        const double dnew = dold + g;
+        d[l * S + s] = dnew;
+        dhi[j] -= dold;
+        dlo[j] += dnew;
+      }
+    }
+    if (++l == L) {
+      l = 0;
+      ++t;
+#pragma unroll
+      for (int j = 0; j < kSPT; ++j) {
+        dhi[j] = dlo[j];
+        dlo[j] = 0.0;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int moeb_eam_prepare(const double* sketches, int S, int L, int E, int budget,
+                                double* unit_t, uint64_t* topw, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(sketches && unit_t && topw, "null argument");
+  MOEB_REQUIRE(S >= 1 && L >= 1 && E >= 1 && E <= 256 && budget >= 1, "bad shape");
+  cudaStream_t s = moeb::as_stream(stream);
+  k_eam_norms<<<S, 256, 0, s>>>(sketches, S, L * E, unit_t);
+  if (int rc = moeb::check_launch("k_eam_norms")) return rc;
+  const int64_t n = (int64_t)S * L;
+  k_eam_topw<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(sketches, S, L, E, budget, topw);
+  return moeb::check_launch("k_eam_topw");
+}
+
+extern "C" int moeb_eam_predict(const uint64_t* truth, const int64_t* prompt_row_off,
+                                int n_prompts, int L, int E, int warmup_tokens,
+                                const double* unit_t, const uint64_t* topw, int S,
+                                int32_t* idx_out, uint64_t* pred, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(truth && prompt_row_off && unit_t && topw && pred, "null argument");
+  MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && E >= 1 && E <= 256 && warmup_tokens >= 0,
+               "bad shape");
+  MOEB_REQUIRE(S >= 1 && S <= 256 * kSPT, "eam_predict supports 1 <= S <= %d", 256 * kSPT);
+  int nt = ((S + kSPT - 1) / kSPT + 31) / 32 * 32;
+  nt = nt < 32 ? 32 : nt;
+  while (nt < 128 && nt < ((S + 31) / 32) * 32) nt += 32;
+  const size_t smem = sizeof(double) * (size_t)L * S;
+  if ((int)smem > moeb::max_smem_per_block())
+    return moeb::fail(MOEB_ESMEM, "eam state %zu B (L*S doubles) exceeds shared memory", smem);
+  cudaStream_t s = moeb::as_stream(stream);
+  const int W = moeb::words_for(E);
+#define MOEB_EAM_LAUNCH(WW)                                                                     \
+  do {                                                                                         \
+    cudaFuncSetAttribute(k_eam_predict<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                         (int)smem);                                                           \
+    k_eam_predict<WW><<<n_prompts, nt, smem, s>>>(truth, prompt_row_off, L, E, warmup_tokens, \
+                                                  unit_t, topw, S, idx_out, pred);             \
+  } while (0)
+  switch (W) {
+    case 1: MOEB_EAM_LAUNCH(1); break;
+    case 2: MOEB_EAM_LAUNCH(2); break;
+    case 3: MOEB_EAM_LAUNCH(3); break;
+    default: MOEB_EAM_LAUNCH(4); break;
+  }
+#undef MOEB_EAM_LAUNCH
+  return moeb::check_launch("k_eam_predict");
+}
+
+// ---------------------------------------------------------------------------
+// K8: rEAM counts and sketch normalisation; brute-force query matcher.
+// ---------------------------------------------------------------------------
+namespace {
+
+template <int W>
+__global__ void k_ream_counts(const uint64_t* __restrict__ truth, const int64_t* __restrict__ row_off,
+                              int L, int E, int max_tokens, int32_t* __restrict__ counts) {
+  const int p = blockIdx.x;
+  int32_t* c = counts + (int64_t)p * L * E;
+  for (int i = threadIdx.x; i < L * E; i += blockDim.x) c[i] = 0;
+  __syncthreads();
+  const int64_t r0 = row_off[p];
+  int64_t r1 = row_off[p + 1];
+  if (max_tokens >= 0 && r0 + (int64_t)max_tokens * L < r1) r1 = r0 + (int64_t)max_tokens * L;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    const int l = (int)((r - r0) % L);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint64_t m = __ldg(truth + r * W + w);
+      while (m) {
+        const int ex = w * 64 + __ffsll((long long)m) - 1;
+        m &= m - 1;
+        atomicAdd(c + l * E + ex, 1);
+      }
+    }
+  }
+}
+
+__global__ void k_sketch_normalize(const int32_t* __restrict__ counts, int L, int E, int binarize,
+                                   double* __restrict__ out) {
+  const int p = blockIdx.x;
+  for (int l = threadIdx.x >> 5; l < L; l += blockDim.x >> 5) {
+    const int32_t* c = counts + ((int64_t)p * L + l) * E;
+    int64_t sum = 0;
+    for (int e = threadIdx.x & 31; e < E; e += 32) sum += binarize ? (c[e] > 0) : c[e];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    double* o_ = out + ((int64_t)p * L + l) * E;
+    for (int e = threadIdx.x & 31; e < E; e += 32) {
+      const double v = binarize ? (double)(c[e] > 0) : (double)c[e];
+      o_[e] = sum > 0 ? v / (double)sum : 0.0;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_match_queries(const double* __restrict__ q, int D,
+                                                       const double* __restrict__ unit_t, int S,
+                                                       int32_t* __restrict__ idx_out,
+                                                       double* __restrict__ sim_out) {
+  extern __shared__ double qs[];
+  __shared__ double red_v[8];
+  __shared__ int red_i[8];
+  const int m = blockIdx.x;
+  const double* qm = q + (int64_t)m * D;
+  double n2 = 0.0;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    qs[d] = qm[d];
+    n2 = fma(qm[d], qm[d], n2);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+  if ((threadIdx.x & 31) == 0) red_v[threadIdx.x >> 5] = n2;
+  __syncthreads();
+  double qn2 = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) qn2 += red_v[w];
+  __syncthreads();
+  const double qn = sqrt(qn2);
+  double best = -DBL_MAX;
+  int bi = 0x7fffffff;
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    double acc = 0.0;
+    for (int d = 0; d < D; ++d) acc = fma(unit_t[(int64_t)d * S + s], qs[d] / qn, acc);
+    if (acc > best) {
+      best = acc;
+      bi = s;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red_v[threadIdx.x >> 5] = best;
+    red_i[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bv = red_v[0];
+    int b = red_i[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < b)) {
+        bv = red_v[w];
+        b = red_i[w];
+      }
+    if (qn2 == 0.0) {  // zero query: index 0, similarity 0 (sketches.py:179-181)
+      b = 0;
+      bv = 0.0;
+    }
+    idx_out[m] = b;
+    if (sim_out) sim_out[m] = bv > 1.0 ? 1.0 : (bv < -1.0 ? -1.0 : bv);
+  }
+}
+
+}  // namespace
+
+extern "C" int moeb_ream_counts(const uint64_t* truth, const int64_t* prompt_row_off,
+                                int n_prompts, int L, int E, int max_tokens, int32_t* counts,
+                                void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(truth && prompt_row_off && counts, "null argument");
+  MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && E >= 1 && E <= 256, "bad shape");
+  cudaStream_t s = moeb::as_stream(stream);
+  switch (moeb::words_for(E)) {
+    case 1: k_ream_counts<1><<<n_prompts, 256, 0, s>>>(truth, prompt_row_off, L, E, max_tokens, counts); break;
+    case 2: k_ream_counts<2><<<n_prompts, 256, 0, s>>>(truth, prompt_row_off, L, E, max_tokens, counts); break;
+    case 3: k_ream_counts<3><<<n_prompts, 256, 0, s>>>(truth, prompt_row_off, L, E, max_tokens, counts); break;
+    default: k_ream_counts<4><<<n_prompts, 256, 0, s>>>(truth, prompt_row_off, L, E, max_tokens, counts); break;
+  }
+  return moeb::check_launch("k_ream_counts");
+}
+
+extern "C" int moeb_sketch_normalize(const int32_t* counts, int n, int L, int E, int binarize,
+                                     double* sketches, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(counts && sketches && n >= 1 && L >= 1 && E >= 1, "bad arguments");
+  k_sketch_normalize<<<n, 256, 0, moeb::as_stream(stream)>>>(counts, L, E, binarize, sketches);
+  return moeb::check_launch("k_sketch_normalize");
+}
+
+extern "C" int moeb_match_queries(const double* queries, int M, int D, const double* unit_t,
+                                  int S, int32_t* idx_out, double* sim_out, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(queries && unit_t && idx_out && M >= 0 && D >= 1 && S >= 1, "bad arguments");
+  if (M == 0) return MOEB_OK;
+  const size_t smem = sizeof(double) * (size_t)D;
+  if ((int)smem > moeb::max_smem_per_block())
+    return moeb::fail(MOEB_ESMEM, "query length %d too long", D);
+  cudaFuncSetAttribute(k_match_queries, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_match_queries<<<M, 256, smem, moeb::as_stream(stream)>>>(queries, D, unit_t, S, idx_out,
+                                                            sim_out);
+  return moeb::check_launch("k_match_queries");
+}

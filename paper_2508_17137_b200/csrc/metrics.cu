@@ -1,0 +1,251 @@
+// K7 metrics, K2 mask head and the rule-based predictor mask tables.
+//
+// K7 replaces macro_f1 / position_accuracy / label_accuracy (metrics.py:12-79)
+// by their integer core: per-expert TP/FP/FN, position count, exact-set
+// matches and the label-correct sum. The host finishes with the reference's
+// numpy expressions, so the floats are identical given identical masks.
+// K2 replaces top_k_experts / predict_topk (learner.py:164-181).
+// Policy masks replace OraclePredictor / LruOnlyPredictor /
+// NextLayerAllPredictor / GlobalFrequencyPredictor.predict (predictors.py:57-139).
+#include "common.cuh"
+
+namespace {
+
+// One warp per prompt (grid-stride): lanes take 32 consecutive measured rows;
+// per expert, ballot+popc turns the 32 rows into one count that the owning
+// lane (expert % 32) accumulates. Block-level shared reduce, then one global
+// atomic per counter per block.
+template <int W>
+__global__ void __launch_bounds__(256) k_metrics(const uint64_t* __restrict__ pred,
+                                                 const uint64_t* __restrict__ truth,
+                                                 const int64_t* __restrict__ row_off, int P,
+                                                 int L, int E, int warmup, int64_t* out) {
+  constexpr int PER_LANE = W * 2;  // experts owned per lane: lane + 32*j
+  __shared__ unsigned long long scnt[3 * 256 + 3];
+  for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x) scnt[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t tp[PER_LANE], fp[PER_LANE], fn[PER_LANE];
+#pragma unroll
+  for (int j = 0; j < PER_LANE; ++j) tp[j] = fp[j] = fn[j] = 0;
+  uint64_t npos = 0, nexact = 0, nlabel = 0;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P; p += warps) {
+    const int64_t r0 = row_off[p] + (int64_t)warmup * L, r1 = row_off[p + 1];
+    for (int64_t base = r0; base < r1; base += 32) {
+      const int64_t r = base + lane;
+      const bool m = r < r1;
+      uint64_t pw[W], tw[W];
+      bool eq = m;
+      int mism = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        pw[w] = m ? __ldg(pred + r * W + w) : 0ull;
+        tw[w] = m ? __ldg(truth + r * W + w) : 0ull;
+        eq = eq && pw[w] == tw[w];
+        mism += __popcll(pw[w] ^ tw[w]);
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const uint64_t a = pw[w] & tw[w], b = pw[w] & ~tw[w], c = tw[w] & ~pw[w];
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const uint32_t c1 = __popc(__ballot_sync(0xffffffffu, (a >> e) & 1ull));
+          const uint32_t c2 = __popc(__ballot_sync(0xffffffffu, (b >> e) & 1ull));
+          const uint32_t c3 = __popc(__ballot_sync(0xffffffffu, (c >> e) & 1ull));
+          if (lane == (e & 31)) {
+            const int j = w * 2 + (e >> 5);
+            tp[j] += c1;
+            fp[j] += c2;
+            fn[j] += c3;
+          }
+        }
+      }
+      npos += m;
+      nexact += eq;
+      nlabel += m ? (uint64_t)(E - mism) : 0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PER_LANE; ++j) {
+    const int e = lane + 32 * j;
+    if (e < E) {
+      if (tp[j]) atomicAdd(&scnt[e], (unsigned long long)tp[j]);
+      if (fp[j]) atomicAdd(&scnt[E + e], (unsigned long long)fp[j]);
+      if (fn[j]) atomicAdd(&scnt[2 * E + e], (unsigned long long)fn[j]);
+    }
+  }
+  atomicAdd(&scnt[3 * E], (unsigned long long)npos);
+  atomicAdd(&scnt[3 * E + 1], (unsigned long long)nexact);
+  atomicAdd(&scnt[3 * E + 2], (unsigned long long)nlabel);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x)
+    if (scnt[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out + i), scnt[i]);
+}
+
+__device__ __forceinline__ uint32_t f32_order(float x) {
+  uint32_t b = __float_as_uint(x == 0.0f ? 0.0f : x);  // -0 ties +0, as in numpy
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// K2: one warp per row. Each lane holds E/32 logits; k passes of a warp-wide
+// max over (order(z), -id) pick the top-k with ties to the lower id.
+template <int PER_LANE>
+__global__ void __launch_bounds__(256) k_mask_head(const float* __restrict__ logits,
+                                                   int64_t rows, int E, int k, int threshold,
+                                                   uint64_t* __restrict__ masks) {
+  const int lane = threadIdx.x & 31;
+  const int W = (E + 63) / 64;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+    uint64_t key[PER_LANE];
+#pragma unroll
+    for (int j = 0; j < PER_LANE; ++j) {
+      const int e = lane + 32 * j;
+      key[j] = 0;
+      if (e < E) {
+        const float z = __ldg(logits + r * E + e);
+        key[j] = ((uint64_t)f32_order(z) << 32) | (uint32_t)(0xFFFFFFFFu - e);
+        if (threshold) key[j] = z > 0.0f ? 1ull : 0ull;
+      }
+    }
+    uint64_t out[4] = {0, 0, 0, 0};
+    if (threshold) {
+#pragma unroll
+      for (int j = 0; j < PER_LANE; ++j) {
+        const uint32_t b = __ballot_sync(0xffffffffu, key[j] != 0);
+        out[j >> 1] |= (uint64_t)b << (32 * (j & 1));
+      }
+    } else {
+      const int kk = k < E ? k : E;
+      for (int it = 0; it < kk; ++it) {
+        uint64_t best = 0;
+#pragma unroll
+        for (int j = 0; j < PER_LANE; ++j) best = key[j] > best ? key[j] : best;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const uint64_t other = __shfl_xor_sync(0xffffffffu, best, o);
+          best = other > best ? other : best;
+        }
+        const int e = (int)(0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFu));
+        out[e >> 6] |= 1ull << (e & 63);
+#pragma unroll
+        for (int j = 0; j < PER_LANE; ++j)
+          if (key[j] == best) key[j] = 0;
+      }
+    }
+    if (lane < W) {
+      uint64_t v = out[0];
+#pragma unroll
+      for (int w = 1; w < 4; ++w) v = lane == w ? out[w] : v;
+      masks[r * W + lane] = v;
+    }
+  }
+}
+
+template <int W>
+__global__ void k_policy_masks(int kind, const uint64_t* __restrict__ truth, int64_t rows, int L,
+                               int E, int budget, const uint64_t* __restrict__ table,
+                               uint64_t* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    uint64_t v[W];
+    if (kind == 1) {  // oracle: the `budget` lowest truth ids (predictors.py:80-81)
+      int left = budget;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint64_t m = __ldg(truth + r * W + w), keep = 0;
+        while (m && left > 0) {
+          keep |= m & (~m + 1);
+          m &= m - 1;
+          --left;
+        }
+        v[w] = keep;
+      }
+    } else if (kind == 2) {  // next_layer_all
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int bits = E - 64 * w;
+        v[w] = bits >= 64 ? ~0ull : (bits <= 0 ? 0ull : ((1ull << bits) - 1));
+      }
+    } else if (kind == 3) {  // per-layer table (global_frequency); rows of
+      const int l = (int)(r % L);  // a prompt start at a multiple of L
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] = __ldg(table + l * W + w);
+    } else {
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] = 0;
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) out[r * W + w] = v[w];
+  }
+}
+
+int grid_for(int64_t work, int threads) {
+  const int64_t want = (work + threads - 1) / threads;
+  const int64_t cap = (int64_t)moeb::num_sms() * 16;
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace
+
+extern "C" int moeb_metrics(const uint64_t* pred, const uint64_t* truth,
+                            const int64_t* prompt_row_off, int n_prompts, int L, int E,
+                            int warmup_tokens, int64_t* metrics, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(pred && truth && prompt_row_off && metrics, "null argument");
+  MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && E >= 1 && E <= 256, "bad shape");
+  MOEB_REQUIRE(warmup_tokens >= 0, "bad warmup");
+  const int W = moeb::words_for(E);
+  const int threads = 256;
+  const int blocks = grid_for((int64_t)n_prompts * 32, threads);
+  cudaStream_t s = moeb::as_stream(stream);
+  switch (W) {
+    case 1: k_metrics<1><<<blocks, threads, 0, s>>>(pred, truth, prompt_row_off, n_prompts, L, E, warmup_tokens, metrics); break;
+    case 2: k_metrics<2><<<blocks, threads, 0, s>>>(pred, truth, prompt_row_off, n_prompts, L, E, warmup_tokens, metrics); break;
+    case 3: k_metrics<3><<<blocks, threads, 0, s>>>(pred, truth, prompt_row_off, n_prompts, L, E, warmup_tokens, metrics); break;
+    default: k_metrics<4><<<blocks, threads, 0, s>>>(pred, truth, prompt_row_off, n_prompts, L, E, warmup_tokens, metrics); break;
+  }
+  return moeb::check_launch("k_metrics");
+}
+
+extern "C" int moeb_mask_head(const float* logits, int64_t rows, int E, int k, int threshold,
+                              uint64_t* masks, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(logits && masks, "null argument");
+  MOEB_REQUIRE(rows >= 0 && E >= 1 && E <= 256 && k >= 1, "bad shape");
+  if (rows == 0) return MOEB_OK;
+  const int threads = 256;
+  const int blocks = grid_for(rows * 32, threads);
+  cudaStream_t s = moeb::as_stream(stream);
+  const int per = (E + 31) / 32;
+  if (per <= 2)
+    k_mask_head<2><<<blocks, threads, 0, s>>>(logits, rows, E, k, threshold, masks);
+  else if (per <= 4)
+    k_mask_head<4><<<blocks, threads, 0, s>>>(logits, rows, E, k, threshold, masks);
+  else
+    k_mask_head<8><<<blocks, threads, 0, s>>>(logits, rows, E, k, threshold, masks);
+  return moeb::check_launch("k_mask_head");
+}
+
+extern "C" int moeb_policy_masks(int kind, const uint64_t* truth, int64_t rows, int L, int E,
+                                 int budget, const uint64_t* layer_table, uint64_t* out,
+                                 void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(out && rows >= 0 && L >= 1 && E >= 1 && E <= 256, "bad arguments");
+  MOEB_REQUIRE(kind >= 0 && kind <= 3, "unknown policy kind %d", kind);
+  MOEB_REQUIRE(kind != 1 || truth, "oracle masks need truth");
+  MOEB_REQUIRE(kind != 3 || layer_table, "table masks need a layer table");
+  if (rows == 0) return MOEB_OK;
+  const int W = moeb::words_for(E);
+  const int threads = 256;
+  const int blocks = grid_for(rows, threads);
+  cudaStream_t s = moeb::as_stream(stream);
+  switch (W) {
+    case 1: k_policy_masks<1><<<blocks, threads, 0, s>>>(kind, truth, rows, L, E, budget, layer_table, out); break;
+    case 2: k_policy_masks<2><<<blocks, threads, 0, s>>>(kind, truth, rows, L, E, budget, layer_table, out); break;
+    case 3: k_policy_masks<3><<<blocks, threads, 0, s>>>(kind, truth, rows, L, E, budget, layer_table, out); break;
+    default: k_policy_masks<4><<<blocks, threads, 0, s>>>(kind, truth, rows, L, E, budget, layer_table, out); break;
+  }
+  return moeb::check_launch("k_policy_masks");
+}

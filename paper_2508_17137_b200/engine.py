@@ -1,0 +1,261 @@
+"""Trace replay under a predictor and an expert cache (engine.py in the reference).
+
+Same configuration objects, report type and call signatures as
+``moesim.engine``; the work runs on the GPU in three stream-ordered launches
+per batch: predictor masks (predictors.py), the fused metrics counters, and
+the cache replay K1 (moeb_cache_sim) for every requested capacity at once.
+``jobs`` is accepted for signature compatibility; parallelism is the GPU's
+(multi-GPU sharding: distributed.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .cache import POLICIES, CacheConfig
+from .core import ConfigError, ModelShape
+from .metrics import MetricCounts, mask_metrics, metric_vector
+from .traces import PackedTraces, pack_traces
+
+
+@dataclass(frozen=True)
+class ReplayConfig:
+    shape: ModelShape
+    cache: CacheConfig
+    warmup_tokens: int = 8
+    history_decay: float = 0.9
+
+    def __post_init__(self):
+        if self.warmup_tokens < 0:
+            raise ConfigError(f"warmup_tokens must be >= 0, got {self.warmup_tokens}")
+        if not 0.0 <= self.history_decay < 1.0:
+            raise ConfigError(f"history_decay must be in [0, 1), got {self.history_decay}")
+
+
+@dataclass
+class PromptCounters:
+    measured_accesses: int = 0
+    cache_hits: int = 0
+    prediction_opportunities: int = 0
+    prediction_hits: int = 0
+
+
+def _rate(hits: int, denom: int):
+    return hits / denom if denom else None
+
+
+@dataclass
+class SimReport:
+    """Aggregate and per-prompt counters for one replay run (engine.py:62-110)."""
+
+    shape: ModelShape
+    measured_accesses: int = 0
+    cache_hits: int = 0
+    prediction_opportunities: int = 0
+    prediction_hits: int = 0
+    uncovered_queries: int = 0
+    layer_accesses: np.ndarray = None
+    layer_cache_hits: np.ndarray = None
+    layer_prediction_hits: np.ndarray = None
+    per_prompt: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        L = self.shape.num_layers
+        if self.layer_accesses is None:
+            self.layer_accesses = np.zeros(L, dtype=np.int64)
+        if self.layer_cache_hits is None:
+            self.layer_cache_hits = np.zeros(L, dtype=np.int64)
+        if self.layer_prediction_hits is None:
+            self.layer_prediction_hits = np.zeros(L, dtype=np.int64)
+
+    @property
+    def cache_hit_rate(self):
+        return _rate(self.cache_hits, self.measured_accesses)
+
+    @property
+    def prediction_hit_rate(self):
+        return _rate(self.prediction_hits, self.prediction_opportunities)
+
+    def merge(self, other: "SimReport") -> None:
+        self.measured_accesses += other.measured_accesses
+        self.cache_hits += other.cache_hits
+        self.prediction_opportunities += other.prediction_opportunities
+        self.prediction_hits += other.prediction_hits
+        self.uncovered_queries += other.uncovered_queries
+        self.layer_accesses += other.layer_accesses
+        self.layer_cache_hits += other.layer_cache_hits
+        self.layer_prediction_hits += other.layer_prediction_hits
+        self.per_prompt.update(other.per_prompt)
+
+    @classmethod
+    def aggregate(cls, shape: ModelShape, reports) -> "SimReport":
+        total = cls(shape)
+        for r in reports:
+            total.merge(r)
+        return total
+
+    @classmethod
+    def from_counters(cls, shape: ModelShape, vec, per_prompt=None, prompt_ids=None):
+        """From the K1 counter vector [4+3L] (and per-prompt [P,4])."""
+        v = np.asarray(vec, dtype=np.int64)
+        L = shape.num_layers
+        rep = cls(shape, int(v[0]), int(v[1]), int(v[0]), int(v[2]), int(v[3]),
+                  v[4:4 + L].copy(), v[4 + L:4 + 2 * L].copy(), v[4 + 2 * L:4 + 3 * L].copy())
+        if per_prompt is not None:
+            pp = np.asarray(per_prompt, dtype=np.int64)
+            for pid, row in zip(prompt_ids, pp):
+                rep.per_prompt[int(pid)] = PromptCounters(int(row[0]), int(row[1]), int(row[0]),
+                                                          int(row[2]))
+        return rep
+
+
+def _packed(traces, shape: ModelShape) -> PackedTraces:
+    return traces if isinstance(traces, PackedTraces) else pack_traces(traces, shape)
+
+
+def _check_lengths(packed: PackedTraces, warmup: int) -> None:
+    """replay_prompt refuses prompts not longer than the warm-up (engine.py:123-127)."""
+    short = np.nonzero(packed.num_tokens <= warmup)[0]
+    if len(short):
+        i = int(short[0])
+        raise ConfigError(f"prompt {int(packed.prompt_ids[i])} has {int(packed.num_tokens[i])} "
+                          f"tokens, not more than warmup_tokens={warmup}")
+
+
+def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget: int,
+                 policy: str = "lru", want_per_prompt: bool = True, want_hits: bool = False):
+    """Run K1 for every (prediction stream, capacity) pair in one call.
+
+    ``streams`` is a list of (masks | None, coverage | None, unbounded).
+    Returns device tensors counters [n][C][4+3L], per_prompt [n][C][P][4] or
+    None, hit masks [n][C][rows][W] or None.
+    """
+    shape = packed.shape
+    L = shape.num_layers
+    n, C, P = len(streams), len(capacities), packed.num_prompts
+    dev = packed.device
+    counters = torch.zeros((n, C, 4 + 3 * L), dtype=torch.int64, device=dev)
+    per_prompt = (torch.zeros((n, C, P, 4), dtype=torch.int64, device=dev)
+                  if want_per_prompt else None)
+    hits = (torch.zeros((n, C, packed.rows, shape.mask_words), dtype=torch.int64, device=dev)
+            if want_hits else None)
+    for lo in range(0, n, 16):
+        chunk = streams[lo:lo + 16]
+        nat.call("moeb_cache_sim", nat.ptr(packed.truth),
+                 nat.ptr_array([m for m, _, _ in chunk]),
+                 nat.ptr_array([c for _, c, _ in chunk]),
+                 nat.i32_array([int(bool(u)) for _, _, u in chunk]), len(chunk),
+                 nat.ptr(packed.row_off), P, L, shape.num_experts, int(warmup),
+                 nat.i64_array(capacities), C, int(budget), POLICIES[policy],
+                 nat.ptr(counters[lo:lo + 16]),
+                 nat.ptr(None if per_prompt is None else per_prompt[lo:lo + 16]),
+                 nat.ptr(None if hits is None else hits[lo:lo + 16]), nat.stream_ptr())
+    return counters, per_prompt, hits
+
+
+def predict_stream(predictor, packed: PackedTraces, config: ReplayConfig, metrics=None):
+    """(masks, coverage, unbounded) of one predictor over a packed batch."""
+    budget = config.cache.prefetch_budget
+    if getattr(predictor, "empty", False) and metrics is None:
+        return None, None, False
+    masks = predictor.predict_masks(packed, budget, config.warmup_tokens, metrics=metrics)
+    return masks, predictor.coverage(packed), bool(getattr(predictor, "unbounded_prefetch", False))
+
+
+def replay_traces(traces, predictor, config: ReplayConfig, jobs: int = 1, policy: str = "lru",
+                  per_prompt: bool = True) -> SimReport:
+    """Replay every prompt; counters identical to the reference for any batch split."""
+    packed = _packed(traces, config.shape)
+    _check_lengths(packed, config.warmup_tokens)
+    cap = config.cache.resolve_capacity(config.shape)
+    stream = predict_stream(predictor, packed, config)
+    counters, pp, _ = cache_replay(packed, [stream], [cap], config.warmup_tokens,
+                                   config.cache.prefetch_budget, policy, per_prompt)
+    return SimReport.from_counters(
+        config.shape, counters[0, 0].cpu().numpy(),
+        None if pp is None else pp[0, 0].cpu().numpy(), packed.prompt_ids)
+
+
+def replay_prompt(trace, predictor, config: ReplayConfig) -> SimReport:
+    return replay_traces([trace], predictor, config)
+
+
+def prediction_metrics(traces, predictor, config: ReplayConfig) -> MetricCounts:
+    """Integer metric counters over all measured steps (device), finishing on host."""
+    packed = _packed(traces, config.shape)
+    E = config.shape.num_experts
+    vec = metric_vector(E, packed.device)
+    if getattr(predictor, "kind", "") == "learned_linear" and E <= 64:
+        predictor.predict_masks(packed, config.cache.prefetch_budget, config.warmup_tokens,
+                                metrics=vec)
+    else:
+        masks = predictor.predict_masks(packed, config.cache.prefetch_budget, config.warmup_tokens)
+        mask_metrics(masks, packed.truth, packed.row_off, config.shape.num_layers, E,
+                     config.warmup_tokens, vec)
+    return MetricCounts.from_vector(vec.cpu().numpy(), E)
+
+
+def collect_prediction_sets(traces, predictor, config: ReplayConfig):
+    """(pred_sets, truth_sets, layer_ids) for every measured step (engine.py:241-272).
+
+    Masks are computed on device; the conversion to Python sets is host-side
+    compatibility glue (use prediction_metrics for bulk evaluation)."""
+    packed = _packed(traces, config.shape)
+    masks = predictor.predict_masks(packed, config.cache.prefetch_budget, config.warmup_tokens)
+    pm = masks.cpu().numpy().view(np.uint64)
+    tm = packed.truth.cpu().numpy().view(np.uint64)
+    L, E = config.shape.num_layers, config.shape.num_experts
+    pred_sets, truth_sets, layer_ids = [], [], []
+    for i in range(packed.num_prompts):
+        r0 = int(packed.row_off_host[i]) + config.warmup_tokens * L
+        for r in range(r0, int(packed.row_off_host[i + 1])):
+            pred_sets.append(_bits(pm[r], E))
+            truth_sets.append(_bits(tm[r], E))
+            layer_ids.append((r - int(packed.row_off_host[i])) % L)
+    return pred_sets, truth_sets, layer_ids
+
+
+def _bits(words, E) -> frozenset:
+    out = []
+    for w, word in enumerate(words):
+        word = int(word)
+        while word:
+            b = word & -word
+            out.append(w * 64 + b.bit_length() - 1)
+            word ^= b
+    return frozenset(e for e in out if e < E)
+
+
+@dataclass
+class SweepPoint:
+    capacity_fraction: float
+    predictor_kind: str
+    report: SimReport
+
+
+def sweep(traces, predictor_factory, predictor_kind: str, capacities, shape: ModelShape,
+          prefetch_budget: int, warmup_tokens: int, history_decay: float = 0.9,
+          jobs: int = 1, policy: str = "lru") -> list[SweepPoint]:
+    """One report per capacity fraction (engine.py:282-306). Predictions do not
+    depend on the cache, so one predictor pass feeds every capacity; all
+    capacities replay concurrently in one K1 launch per capacity."""
+    if traces is None or (not isinstance(traces, PackedTraces) and not traces):
+        raise ConfigError("sweep needs at least one trace")
+    if not capacities:
+        raise ConfigError("sweep needs at least one capacity")
+    packed = _packed(traces, shape)
+    _check_lengths(packed, warmup_tokens)
+    cfgs = [ReplayConfig(shape, CacheConfig(capacity_fraction=f, prefetch_budget=prefetch_budget),
+                         warmup_tokens, history_decay) for f in capacities]
+    stream = predict_stream(predictor_factory(), packed, cfgs[0])
+    caps = [c.cache.resolve_capacity(shape) for c in cfgs]
+    counters, pp, _ = cache_replay(packed, [stream], caps, warmup_tokens, prefetch_budget, policy)
+    counters = counters.cpu().numpy()
+    pp = pp.cpu().numpy()
+    return [SweepPoint(f, predictor_kind,
+                       SimReport.from_counters(shape, counters[0, j], pp[0, j], packed.prompt_ids))
+            for j, f in enumerate(capacities)]

@@ -1,0 +1,286 @@
+"""Expert-set predictors as device mask producers (predictors.py in the reference).
+
+The reference protocol is per step: ``predict(ctx) -> frozenset`` called from
+the replay loop. Here every predictor turns a whole ``PackedTraces`` batch
+into one bitmask row per trace row in a single device pass
+(``predict_masks``); predictions never depend on the cache
+(engine.py:244-246), so this is exactly the sequence of sets the reference
+loop would produce. The optional flags the reference engine reads with
+getattr (engine.py:128-141) keep their meaning: ``unbounded_prefetch``,
+``history_decay``, and coverage for the external predictor.
+
+Kinds: oracle, lru_only, next_layer_all, global_frequency, eam_cosine,
+external, learned_linear (predictors.py:29-37), plus ``transformer`` (the
+paper's predictor, transformer.py).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .core import ConfigError, ModelShape
+from .learner import LinearModel
+from .sketches import SketchCollection, ream_counts
+from .traces import PackedTraces, pack_traces
+
+PREDICTOR_KINDS = ("oracle", "lru_only", "next_layer_all", "global_frequency", "eam_cosine",
+                   "external", "learned_linear", "transformer")
+
+
+def _empty(packed: PackedTraces) -> torch.Tensor:
+    return torch.empty((packed.rows, packed.shape.mask_words), dtype=torch.int64,
+                       device=packed.device)
+
+
+def _policy(kind_code: int, packed: PackedTraces, budget: int, truth=None, table=None):
+    out = _empty(packed)
+    nat.call("moeb_policy_masks", kind_code, nat.ptr(truth), packed.rows,
+             packed.shape.num_layers, packed.shape.num_experts, int(budget), nat.ptr(table),
+             nat.ptr(out), nat.stream_ptr())
+    return out
+
+
+class DevicePredictor:
+    kind = "base"
+    unbounded_prefetch = False
+    #: True when the predictor's masks are all-empty (lru_only): the cache sim
+    #: then runs without reading a prediction stream at all.
+    empty = False
+
+    def predict_masks(self, packed: PackedTraces, budget: int, warmup: int = 0,
+                      metrics: torch.Tensor | None = None) -> torch.Tensor:
+        raise NotImplementedError
+
+    def coverage(self, packed: PackedTraces):
+        return None
+
+
+class OraclePredictor(DevicePredictor):
+    """Ground truth truncated to the budget lowest ids (predictors.py:57-82)."""
+
+    kind = "oracle"
+
+    def __init__(self, traces, shape: ModelShape):
+        self.shape = shape
+        self._packed = pack_traces(traces, shape)
+
+    def _truth_for(self, packed: PackedTraces) -> torch.Tensor:
+        mine = self._packed
+        if (np.array_equal(mine.prompt_ids, packed.prompt_ids)
+                and np.array_equal(mine.row_off_host, packed.row_off_host)):
+            return mine.truth.to(packed.device)
+        pos = {int(p): i for i, p in enumerate(mine.prompt_ids)}
+        idx = []
+        for i, pid in enumerate(packed.prompt_ids):
+            if int(pid) not in pos:
+                raise ConfigError(f"oracle has no trace for prompt {int(pid)}")
+            j = pos[int(pid)]
+            n = int(packed.row_off_host[i + 1] - packed.row_off_host[i])
+            if n > mine.row_off_host[j + 1] - mine.row_off_host[j]:
+                raise ConfigError(f"oracle trace for prompt {int(pid)} is shorter than replayed")
+            idx.append(np.arange(n) + mine.row_off_host[j])
+        gather = torch.from_numpy(np.concatenate(idx)).to(mine.truth.device)
+        return mine.truth.index_select(0, gather).to(packed.device).contiguous()
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None):
+        return _policy(1, packed, budget, truth=self._truth_for(packed))
+
+
+class LruOnlyPredictor(DevicePredictor):
+    kind = "lru_only"
+    empty = True
+
+    def __init__(self, shape: ModelShape):
+        self.shape = shape
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None):
+        return _policy(0, packed, budget)
+
+
+class NextLayerAllPredictor(DevicePredictor):
+    kind = "next_layer_all"
+    unbounded_prefetch = True
+
+    def __init__(self, shape: ModelShape):
+        self.shape = shape
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None):
+        return _policy(2, packed, budget)
+
+
+class GlobalFrequencyPredictor(DevicePredictor):
+    """Top experts per layer by training-workload counts, ties to the lower id
+    (predictors.py:111-139). Counting runs on device over the packed workload."""
+
+    kind = "global_frequency"
+
+    def __init__(self, train_traces, shape: ModelShape):
+        if train_traces is None or (not isinstance(train_traces, PackedTraces)
+                                    and not train_traces):
+            raise ConfigError("global_frequency needs a training workload")
+        self.shape = shape
+        packed = pack_traces(train_traces, shape)
+        per_prompt = ream_counts(packed)
+        self.counts = per_prompt.to(torch.int64).sum(0).cpu().numpy().reshape(
+            shape.num_layers, shape.num_experts)
+        E = shape.num_experts
+        # order[l] = ids by (-count, id): a stable argsort of -count
+        self._order = np.argsort(-self.counts, axis=1, kind="stable")
+        self._tables: dict[int, torch.Tensor] = {}
+
+    def _table(self, budget: int, device) -> torch.Tensor:
+        if budget not in self._tables:
+            L, W = self.shape.num_layers, self.shape.mask_words
+            m = min(budget, self.shape.num_experts)
+            tab = np.zeros((L, W), dtype=np.uint64)
+            for l in range(L):
+                for e in self._order[l, :m]:
+                    tab[l, e >> 6] |= np.uint64(1) << np.uint64(e & 63)
+            self._tables[budget] = torch.from_numpy(tab.view(np.int64)).to(device)
+        return self._tables[budget]
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None):
+        return _policy(3, packed, budget, table=self._table(budget, packed.device))
+
+
+class EamCosinePredictor(DevicePredictor):
+    """Nearest stored sketch by cosine over the partial rEAM; top-budget
+    positive weights of its block (predictors.py:151-219). Kernel K6."""
+
+    kind = "eam_cosine"
+    uses_partial_ream = True
+
+    def __init__(self, collection: SketchCollection):
+        if len(collection) == 0:
+            raise ConfigError("eam_cosine needs a non-empty sketch collection")
+        self.collection = collection
+        self.shape = collection.shape
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None, idx_out=None):
+        unit_t, topw = self.collection.device_tables(budget, packed.device)
+        out = _empty(packed)
+        s = self.shape
+        nat.call("moeb_eam_predict", nat.ptr(packed.truth), nat.ptr(packed.row_off),
+                 packed.num_prompts, s.num_layers, s.num_experts, int(warmup), nat.ptr(unit_t),
+                 nat.ptr(topw), len(self.collection), nat.ptr(idx_out), nat.ptr(out),
+                 nat.stream_ptr())
+        return out
+
+
+class ExternalPredictor(DevicePredictor):
+    """Lookup into an external prediction table; missing keys predict nothing
+    and count as uncovered (predictors.py:222-242, engine.py:175-176)."""
+
+    kind = "external"
+
+    def __init__(self, table: dict, shape: ModelShape):
+        self.shape = shape
+        self.table = table
+        self._cache = {}
+
+    def covers(self, prompt_id: int, token_index: int, layer_id: int) -> bool:
+        return (prompt_id, token_index, layer_id) in self.table
+
+    def _build(self, packed: PackedTraces):
+        key = (id(packed), packed.rows)
+        if key not in self._cache:
+            L, W = self.shape.num_layers, self.shape.mask_words
+            rows = packed.rows
+            masks = np.zeros((rows, W), dtype=np.uint64)
+            cov = np.zeros(rows, dtype=np.uint8)
+            off = packed.row_off_host
+            for i, pid in enumerate(packed.prompt_ids):
+                pid = int(pid)
+                for r in range(int(off[i]), int(off[i + 1])):
+                    t, l = divmod(r - int(off[i]), L)
+                    s = self.table.get((pid, t, l))
+                    if s is None:
+                        continue
+                    cov[r] = 1
+                    for e in s:
+                        masks[r, e >> 6] |= np.uint64(1) << np.uint64(e & 63)
+            self._cache = {key: (torch.from_numpy(masks.view(np.int64)).to(packed.device),
+                                 torch.from_numpy(cov).to(packed.device))}
+        return self._cache[key]
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None):
+        return self._build(packed)[0]
+
+    def coverage(self, packed):
+        return self._build(packed)[1]
+
+
+class LearnedLinearPredictor(DevicePredictor):
+    """Linear model over decayed-history features (predictors.py:245-268).
+    Kernel K3 with the selection head and (optionally) metrics fused."""
+
+    kind = "learned_linear"
+    uses_history = True
+
+    def __init__(self, model: LinearModel, threshold: bool = False):
+        if not model.trained:
+            raise ConfigError("learned_linear needs a trained model")
+        self.model = model
+        self.shape = model.shape
+        self.threshold = threshold
+        self._w = {}
+
+    @property
+    def history_decay(self) -> float:
+        return self.model.config.decay
+
+    def weights_on(self, device) -> torch.Tensor:
+        key = str(device)
+        if key not in self._w:
+            self._w[key] = torch.from_numpy(
+                np.ascontiguousarray(self.model.weights, dtype=np.float64)).to(device)
+        return self._w[key]
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None, logits=None):
+        s = self.shape
+        out = _empty(packed)
+        nat.call("moeb_linear_predict", nat.ptr(packed.truth), nat.ptr(packed.row_off),
+                 packed.num_prompts, s.num_layers, s.num_experts,
+                 nat.ptr(self.weights_on(packed.device)), float(self.history_decay),
+                 int(budget), int(bool(self.threshold)), int(warmup), nat.ptr(out),
+                 nat.ptr(logits), nat.ptr(metrics), nat.stream_ptr())
+        return out
+
+
+def make_predictor(kind: str, shape: ModelShape, *, traces=None, train_traces=None,
+                   eamc: SketchCollection | None = None, model: LinearModel | None = None,
+                   predictions: dict | None = None, threshold: bool = False,
+                   transformer=None):
+    """Build a predictor, checking its required state (predictors.py:271-303)."""
+    if kind == "oracle":
+        if traces is None:
+            raise ConfigError("oracle predictor needs the replayed traces")
+        return OraclePredictor(traces, shape)
+    if kind == "lru_only":
+        return LruOnlyPredictor(shape)
+    if kind == "next_layer_all":
+        return NextLayerAllPredictor(shape)
+    if kind == "global_frequency":
+        if train_traces is None:
+            raise ConfigError("global_frequency predictor needs training traces")
+        return GlobalFrequencyPredictor(train_traces, shape)
+    if kind == "eam_cosine":
+        if eamc is None:
+            raise ConfigError("eam_cosine predictor needs a sketch collection")
+        return EamCosinePredictor(eamc)
+    if kind == "external":
+        if predictions is None:
+            raise ConfigError("external predictor needs a prediction table")
+        return ExternalPredictor(predictions, shape)
+    if kind == "learned_linear":
+        if model is None:
+            raise ConfigError("learned_linear predictor needs a trained model")
+        return LearnedLinearPredictor(model, threshold=threshold)
+    if kind == "transformer":
+        from .transformer import TransformerPredictor
+        if transformer is None:
+            raise ConfigError("transformer predictor needs weights (TransformerWeights)")
+        return TransformerPredictor(transformer, shape, threshold=threshold)
+    raise ConfigError(f"unknown predictor kind {kind!r}")

@@ -1,0 +1,183 @@
+"""Sketch collections (EAMC) for the MoE-Infinity cosine matcher (sketches.py
+in the reference, :26-255).
+
+Sketches are row-normalised, layer-major flattened rEAMs. Building them from
+traces (counts + normalisation) and every match run on device; the raw
+sketches also stay on the host for JSON persistence. k-means EAMC
+construction (sketches.py:89-139) is the offline step before this path and is
+a DESIGN.md next component.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .core import ActivationMatrix, ConfigError, DimensionError, ModelShape
+
+
+@dataclass(frozen=True)
+class EamcConfig:
+    mode: str = "recent"
+    capacity: int = 100
+    binarize: bool = False
+    kmeans_max_iters: int = 100
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.mode not in ("recent", "kmeans"):
+            raise ConfigError(f"mode must be 'recent' or 'kmeans', got {self.mode!r}")
+        if self.capacity < 1:
+            raise ConfigError(f"capacity must be >= 1, got {self.capacity}")
+        if self.kmeans_max_iters < 1:
+            raise ConfigError(f"kmeans_max_iters must be >= 1, got {self.kmeans_max_iters}")
+
+
+class SketchCollection:
+    """Stored sketches with device-resident matching tables."""
+
+    def __init__(self, sketches, config: EamcConfig, shape: ModelShape):
+        if isinstance(sketches, torch.Tensor):
+            dev = sketches.to(torch.float64)
+            host = dev.cpu().numpy()
+        else:
+            host = np.asarray(sketches, dtype=np.float64)
+            dev = None
+        if host.ndim != 2 or host.shape[1] != shape.total_experts:
+            raise DimensionError(f"sketches must be 2-D with row length {shape.total_experts}")
+        if host.shape[0] > config.capacity:
+            raise ConfigError(f"{host.shape[0]} sketches exceed capacity {config.capacity}")
+        self.sketches = host
+        self.config = config
+        self.shape = shape
+        self._dev = dev
+        self._unit_t = None
+        self._topw: dict[int, torch.Tensor] = {}
+
+    def __len__(self) -> int:
+        return self.sketches.shape[0]
+
+    def device_tables(self, budget: int, device=None):
+        """(unit_t [D][S] fp64, topw [S][L][W]) on device (moeb_eam_prepare)."""
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        if self._dev is None or self._dev.device != dev:
+            self._dev = torch.from_numpy(np.ascontiguousarray(self.sketches)).to(dev)
+            self._unit_t = None
+            self._topw = {}
+        if self._unit_t is None or budget not in self._topw:
+            S, L, E = len(self), self.shape.num_layers, self.shape.num_experts
+            unit_t = torch.empty((L * E, S), dtype=torch.float64, device=dev)
+            topw = torch.empty((S, L, self.shape.mask_words), dtype=torch.int64, device=dev)
+            nat.call("moeb_eam_prepare", nat.ptr(self._dev), S, L, E, int(budget),
+                     nat.ptr(unit_t), nat.ptr(topw), nat.stream_ptr())
+            self._unit_t = unit_t
+            self._topw[budget] = topw
+        return self._unit_t, self._topw[budget]
+
+    def match_nearest_batch(self, queries) -> tuple[np.ndarray, np.ndarray]:
+        """Batched match_nearest for explicit query vectors [M][D] (device fp64 scan)."""
+        q = torch.as_tensor(np.ascontiguousarray(queries, dtype=np.float64)).cuda()
+        if q.ndim != 2 or q.shape[1] != self.sketches.shape[1]:
+            raise DimensionError(f"query length {tuple(q.shape)} != sketch length "
+                                 f"{self.sketches.shape[1]}")
+        unit_t, _ = self.device_tables(1, q.device)
+        M = q.shape[0]
+        idx = torch.empty(max(M, 1), dtype=torch.int32, device=q.device)
+        sim = torch.empty(max(M, 1), dtype=torch.float64, device=q.device)
+        nat.call("moeb_match_queries", nat.ptr(q), M, q.shape[1], nat.ptr(unit_t), len(self),
+                 nat.ptr(idx), nat.ptr(sim), nat.stream_ptr())
+        return idx[:M].cpu().numpy(), sim[:M].cpu().numpy()
+
+    def match_nearest(self, query) -> tuple[int, float]:
+        """Index and cosine of the nearest sketch (sketches.py:165-184)."""
+        if len(self) == 0:
+            raise ConfigError("no sketches in collection")
+        q = np.asarray(query, dtype=np.float64)
+        if q.shape != (self.sketches.shape[1],):
+            raise DimensionError(f"query length {q.shape} != sketch length "
+                                 f"{self.sketches.shape[1]}")
+        idx, sim = self.match_nearest_batch(q[None, :])
+        return int(idx[0]), float(sim[0])
+
+    def layer_block(self, index: int, layer_id: int) -> np.ndarray:
+        e = self.shape.num_experts
+        return self.sketches[index, layer_id * e:(layer_id + 1) * e]
+
+
+def ream_counts(packed, max_tokens: int | None = None) -> torch.Tensor:
+    """Per-prompt activation counts [P][L*E] int32 on device (core.py:196-205)."""
+    shape = packed.shape
+    P = packed.num_prompts
+    counts = torch.empty((P, shape.total_experts), dtype=torch.int32, device=packed.device)
+    nat.call("moeb_ream_counts", nat.ptr(packed.truth), nat.ptr(packed.row_off), P,
+             shape.num_layers, shape.num_experts, -1 if max_tokens is None else int(max_tokens),
+             nat.ptr(counts), nat.stream_ptr())
+    return counts
+
+
+def normalize_counts(counts: torch.Tensor, shape: ModelShape, binarize: bool = False):
+    """Sketches [n][L*E] fp64 from counts (core.normalize), on device."""
+    counts = counts.to(torch.int32).contiguous()
+    n = counts.shape[0]
+    out = torch.empty((n, shape.total_experts), dtype=torch.float64, device=counts.device)
+    nat.call("moeb_sketch_normalize", nat.ptr(counts), n, shape.num_layers, shape.num_experts,
+             int(bool(binarize)), nat.ptr(out), nat.stream_ptr())
+    return out
+
+
+def build_eamc(matrices, config: EamcConfig, shape: ModelShape | None = None) -> SketchCollection:
+    """Collection from rEAMs (sketches.py:200-216): ActivationMatrix list or
+    PackedTraces (one rEAM per prompt). Recent mode keeps the last `capacity`."""
+    from .traces import PackedTraces
+
+    if isinstance(matrices, PackedTraces):
+        shape = matrices.shape
+        counts = ream_counts(matrices)
+    else:
+        if not matrices:
+            raise ConfigError("at least one activation matrix is required")
+        shape = matrices[0].shape
+        counts = torch.as_tensor(np.stack([m.counts for m in matrices]).reshape(len(matrices), -1)
+                                 .astype(np.int32)).cuda()
+    if config.mode != "recent":
+        raise NotImplementedError("k-means EAMC construction is a DESIGN.md next component")
+    counts = counts[-config.capacity:]
+    return SketchCollection(normalize_counts(counts, shape, config.binarize), config, shape)
+
+
+def save_eamc(collection: SketchCollection, path) -> None:
+    payload = {
+        "mode": collection.config.mode,
+        "capacity": collection.config.capacity,
+        "binarize": collection.config.binarize,
+        "kmeans_max_iters": collection.config.kmeans_max_iters,
+        "seed": collection.config.seed,
+        "num_layers": collection.shape.num_layers,
+        "num_experts": collection.shape.num_experts,
+        "top_k": collection.shape.top_k,
+        "sketches": [[float(v) for v in row] for row in collection.sketches],
+    }
+    with open(path, "w", encoding="utf-8") as fh:
+        json.dump(payload, fh)
+        fh.write("\n")
+
+
+def load_eamc(path) -> SketchCollection:
+    """Same file format and checks as the reference (sketches.py:237-255)."""
+    with open(path, encoding="utf-8") as fh:
+        payload = json.load(fh)
+    try:
+        config = EamcConfig(mode=payload["mode"], capacity=payload["capacity"],
+                            binarize=payload["binarize"],
+                            kmeans_max_iters=payload["kmeans_max_iters"], seed=payload["seed"])
+        shape = ModelShape(payload["num_layers"], payload["num_experts"], payload["top_k"])
+        sketches = np.asarray(payload["sketches"], dtype=np.float64)
+    except (KeyError, TypeError) as exc:
+        raise ConfigError(f"bad sketch collection file {path}: {exc}") from None
+    if sketches.size == 0:
+        raise ConfigError(f"no sketches in {path}")
+    return SketchCollection(sketches, config, shape)

@@ -1,0 +1,220 @@
+"""Packed decode traces in HBM and the on-device synthetic generator.
+
+Layout: one uint64 bitmask row per (prompt, token,
+layer) step, W = ceil(E/64) words per row, prompts concatenated in (token,
+layer) order -- CSR over prompts with ``row_off[P+1]``. A DeepSeek-V2-Lite
+trace token (26 layers) is 208 bytes; the ~66 M-row C2 workload is 528 MB.
+
+``generate_packed`` reproduces the reference generator (traceio.py:208-283)
+bit for bit: the host replays the two small leading draw blocks with numpy
+itself (hot-key draws + np.argpartition ordering, token ids) and hands the
+PCG64 state to ``moeb_gen_traces``, which jumps straight to each token's
+slice of the large draw blocks on device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .core import ConfigError, ModelShape, PromptTrace, RangeError, TokenRecord
+
+_TOKEN_VOCAB = 32000  # traceio.py:230
+
+
+@dataclass(frozen=True)
+class GeneratorConfig:
+    """Synthetic trace generator settings (traceio.py:197-227), same validation."""
+
+    num_prompts: int
+    tokens_per_prompt: int
+    shape: ModelShape
+    hot_set_size: int
+    skew: float
+    seed: int
+    first_prompt_id: int = 0
+
+    def __post_init__(self):
+        if self.num_prompts < 1:
+            raise ConfigError(f"num_prompts must be >= 1, got {self.num_prompts}")
+        if self.tokens_per_prompt < 1:
+            raise ConfigError(f"tokens_per_prompt must be >= 1, got {self.tokens_per_prompt}")
+        if not self.shape.top_k <= self.hot_set_size <= self.shape.num_experts:
+            raise ConfigError(f"hot_set_size must be in [{self.shape.top_k}, "
+                              f"{self.shape.num_experts}], got {self.hot_set_size}")
+        if not 0.0 <= self.skew <= 1.0:
+            raise ConfigError(f"skew must be in [0, 1], got {self.skew}")
+        if self.seed < 0:
+            raise ConfigError(f"seed must be non-negative, got {self.seed}")
+        if self.first_prompt_id < 0:
+            raise ConfigError(f"first_prompt_id must be non-negative, got {self.first_prompt_id}")
+
+
+@dataclass
+class PackedTraces:
+    """Traces resident on one device as bitmask rows (CSR over prompts)."""
+
+    shape: ModelShape
+    truth: torch.Tensor            # int64 [rows, W] (uint64 bit patterns), device
+    row_off: torch.Tensor          # int64 [P+1], device
+    row_off_host: np.ndarray       # int64 [P+1]
+    prompt_ids: np.ndarray         # int64 [P]
+    token_ids: torch.Tensor | None = None  # int32 [rows // L] per trace token, device
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def num_prompts(self) -> int:
+        return len(self.prompt_ids)
+
+    @property
+    def rows(self) -> int:
+        return int(self.row_off_host[-1])
+
+    @property
+    def num_tokens(self) -> np.ndarray:
+        return np.diff(self.row_off_host) // self.shape.num_layers
+
+    @property
+    def device(self) -> torch.device:
+        return self.truth.device
+
+    def select(self, lo: int, hi: int) -> "PackedTraces":
+        """Prompts [lo, hi) as a new PackedTraces (views where possible)."""
+        r0, r1 = int(self.row_off_host[lo]), int(self.row_off_host[hi])
+        L = self.shape.num_layers
+        off = self.row_off_host[lo:hi + 1] - r0
+        return PackedTraces(
+            self.shape, self.truth[r0:r1], torch.as_tensor(off, device=self.device),
+            off, self.prompt_ids[lo:hi],
+            None if self.token_ids is None else self.token_ids[r0 // L:r1 // L], dict(self.meta))
+
+    def shard(self, rank: int, world: int) -> "PackedTraces":
+        """Contiguous prompt range of this rank with ~equal row counts."""
+        if world <= 1:
+            return self
+        targets = np.arange(1, world) * (self.rows / world)
+        cuts = np.searchsorted(self.row_off_host, targets)
+        bounds = [0] + [int(c) for c in cuts] + [self.num_prompts]
+        return self.select(bounds[rank], bounds[rank + 1])
+
+    def unpack(self) -> list[PromptTrace]:
+        """Host PromptTrace objects (slow; for compatibility and small cases)."""
+        truth = self.truth.cpu().numpy().view(np.uint64)
+        toks = None if self.token_ids is None else self.token_ids.cpu().numpy()
+        L, E = self.shape.num_layers, self.shape.num_experts
+        out = []
+        for i, pid in enumerate(self.prompt_ids):
+            tr = PromptTrace(int(pid))
+            r0, r1 = int(self.row_off_host[i]), int(self.row_off_host[i + 1])
+            for r in range(r0, r1):
+                ids = []
+                for w, word in enumerate(truth[r]):
+                    word = int(word)
+                    while word:
+                        b = word & -word
+                        ids.append(w * 64 + b.bit_length() - 1)
+                        word ^= b
+                t, l = (r - r0) // L, (r - r0) % L
+                tr.records.append(TokenRecord(int(pid), t, l, tuple(e for e in ids if e < E),
+                                              0 if toks is None else int(toks[r // L])))
+            out.append(tr)
+        return out
+
+
+def _device(device):
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def pack_traces(traces, shape: ModelShape, device=None) -> PackedTraces:
+    """Pack host PromptTrace objects (validated like the reference) to device rows."""
+    if isinstance(traces, PackedTraces):
+        return traces
+    nat.load_library()
+    device = _device(device)
+    L, W = shape.num_layers, shape.mask_words
+    offs = [0]
+    pids = []
+    rows = []
+    toks = []
+    for tr in traces:
+        if tr.records and (tr.records[0].token_index != 0 or tr.records[0].layer_id != 0):
+            tr = PromptTrace(tr.prompt_id, sorted(tr.records,
+                                                  key=lambda r: (r.token_index, r.layer_id)))
+        n = len(tr.records)
+        if n % L:
+            raise RangeError(f"prompt {tr.prompt_id}: incomplete layer coverage")
+        for j, rec in enumerate(tr.records):
+            if rec.token_index != j // L or rec.layer_id != j % L:
+                raise RangeError(f"prompt {tr.prompt_id}: records not a complete (token, layer) "
+                                 f"grid at position {j}")
+            m = [0] * W
+            for e in rec.expert_ids:
+                if not 0 <= e < shape.num_experts:
+                    raise RangeError(f"expert {e} out of range [0, {shape.num_experts})")
+                m[e >> 6] |= 1 << (e & 63)
+            rows.append(m)
+            if j % L == 0:
+                toks.append(rec.token_id)
+        offs.append(offs[-1] + n)
+        pids.append(tr.prompt_id)
+    arr = np.array(rows, dtype=np.uint64).reshape(-1, W) if rows else np.zeros((0, W), np.uint64)
+    off = np.array(offs, dtype=np.int64)
+    return PackedTraces(
+        shape, torch.from_numpy(arr.view(np.int64)).to(device), torch.from_numpy(off).to(device),
+        off, np.array(pids, dtype=np.int64),
+        torch.tensor(toks, dtype=torch.int32, device=device))
+
+
+def _prompt_prep(cfg: GeneratorConfig, pid: int):
+    """Host part of traceio._generate_prompt: the hot-key block (and the
+    argpartition order of the hot set) and the token-id block."""
+    shape = cfg.shape
+    L, E, T, h = shape.num_layers, shape.num_experts, cfg.tokens_per_prompt, cfg.hot_set_size
+    rng = np.random.default_rng(np.random.SeedSequence(cfg.seed, spawn_key=(pid,)))
+    hot_keys = rng.random((L, E))
+    token_ids = rng.integers(0, _TOKEN_VOCAB, size=T)
+    st = rng.bit_generator.state["state"]
+    hot = np.argpartition(-hot_keys, h - 1, axis=1)[:, :h]
+    s, inc = int(st["state"]), int(st["inc"])
+    m64 = (1 << 64) - 1
+    return (np.array([s >> 64, s & m64, inc >> 64, inc & m64], dtype=np.uint64),
+            hot.astype(np.uint8), token_ids.astype(np.int32))
+
+
+def generate_packed(config: GeneratorConfig, device=None) -> PackedTraces:
+    """All prompts of a generator config, generated on device (bit-identical
+    to traceio.generate_synthetic)."""
+    nat.load_library()
+    device = _device(device)
+    shape = config.shape
+    L, E, k = shape.num_layers, shape.num_experts, shape.top_k
+    T, P, h = config.tokens_per_prompt, config.num_prompts, config.hot_set_size
+    if E > 256 or k > 16:
+        raise ConfigError("device generator supports E <= 256 and top_k <= 16")
+    pids = np.arange(config.first_prompt_id, config.first_prompt_id + P, dtype=np.int64)
+    states = np.empty((P, 4), dtype=np.uint64)
+    hots = np.empty((P, L, h), dtype=np.uint8)
+    toks = np.empty((P, T), dtype=np.int32)
+    for i, pid in enumerate(pids):
+        states[i], hots[i], toks[i] = _prompt_prep(config, int(pid))
+    W = shape.mask_words
+    truth = torch.empty((P * T * L, W), dtype=torch.int64, device=device)
+    st_d = torch.from_numpy(states.view(np.int64)).to(device)
+    hot_d = torch.from_numpy(hots).to(device)
+    with torch.cuda.device(device):
+        nat.call("moeb_gen_traces", nat.ptr(st_d), nat.ptr(hot_d), P, T, L, E, k, h,
+                 float(config.skew), nat.ptr(truth), nat.stream_ptr())
+    off = np.arange(P + 1, dtype=np.int64) * (T * L)
+    return PackedTraces(shape, truth, torch.from_numpy(off).to(device), off, pids,
+                        torch.from_numpy(toks.reshape(-1)).to(device),
+                        {"generator": config})
+
+
+def generate_synthetic(config: GeneratorConfig) -> list[PromptTrace]:
+    """traceio.generate_synthetic (traceio.py:277-283), computed on device."""
+    return generate_packed(config).unpack()
