@@ -1,0 +1,425 @@
+"""Benchmark: trace tokens/sec of predict + cache-sim (+ F1/accuracy counters)
+on DeepSeek-V2-Lite-shaped synthetic traces (BASELINE.json configs[1], C2:
+6,994 prompts x 363 decode tokens x 26 MoE layers x 64 experts, top-6,
+~66 M trace rows per GPU), learned_linear predictor with random-init weights,
+expert cache at 10 % capacity (166 entries), prefetch budget 6, warm-up 8.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0 (contract in the task statement). Multi-GPU: one
+process per GPU under torchrun; every rank replays its own C2-sized prompt
+range (weak scaling, prompts are independent) and the int64 counters are
+summed with one NCCL all-reduce per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+C2 = dict(prompts=6994, tokens=363, layers=26, experts=64, top_k=6, hot=8, skew=0.9, seed=7)
+CAP_FRACTION = 0.1
+BUDGET = 6
+WARMUP_TOKENS = 8
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), float(
+            p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    smax = float(f[2])
+                except ValueError:
+                    continue
+                for n, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        except Exception:
+            pass
+        finally:
+            if self.path and os.path.exists(self.path):
+                os.remove(self.path)
+        busy = [s for s in sm if smax and s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# Reference CPU arm: the unmodified reference package (baseline/_ref).
+# ---------------------------------------------------------------------------
+
+def _import_reference():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "moesim")) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    import moesim  # noqa: F401
+    return moesim
+
+
+def reference_sample(n_prompts: int, tokens: int = C2["tokens"], first: int = 0):
+    moesim = _import_reference()
+    from moesim.learner import LearnerConfig, LinearModel
+    shape = moesim.ModelShape(C2["layers"], C2["experts"], C2["top_k"])
+    traces = moesim.generate_synthetic(moesim.GeneratorConfig(
+        n_prompts, tokens, shape, C2["hot"], C2["skew"], C2["seed"], first_prompt_id=first))
+    w = __import__("numpy").random.default_rng(0).normal(0.0, 0.01, (C2["experts"],
+                                                                   C2["layers"] + C2["experts"] + 1))
+    model = LinearModel(shape, LearnerConfig(epochs=0), w, trained=True)
+    pred = moesim.make_predictor("learned_linear", shape, model=model)
+    cfg = moesim.ReplayConfig(shape, moesim.CacheConfig(capacity_fraction=CAP_FRACTION,
+                                                        prefetch_budget=BUDGET),
+                              warmup_tokens=WARMUP_TOKENS)
+    return moesim, traces, pred, cfg
+
+
+def time_reference(n_prompts: int, jobs: int, repeats: int = 1, sample=None):
+    """Reference predict + cache-sim (replay_traces, its own ProcessPool with
+    `jobs` workers) over a bounded sample; returns (tok/s, seconds, report)."""
+    moesim, traces, pred, cfg = sample if sample is not None else reference_sample(n_prompts)
+    best = None
+    rep = None
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        rep = moesim.replay_traces(traces, pred, cfg, jobs=jobs)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    toks = n_prompts * C2["tokens"]
+    return toks / best, best, rep
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor()
+
+
+def run_reference(args):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    n_sample = max(cores, 32)  # one prompt (363 tokens) per worker, at least 32
+    try:
+        _import_reference()
+    except Exception as exc:  # pragma: no cover
+        print(json.dumps({"impl": "reference", "unavailable": f"reference import failed: {exc}"}))
+        return 0
+    sample = reference_sample(n_sample)  # generation is not timed
+    for _ in range(min(args.warmup, 1)):
+        time_reference(n_sample, cores, sample=sample)
+    vals = []
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        v, dt, rep = time_reference(n_sample, cores, sample=sample)
+        vals.append(v)
+    elapsed = time.perf_counter() - t_all
+    value = statistics.median(vals)
+    sample = (f"{n_sample} prompts x {C2['tokens']} tokens of the C2 generator (seed 7), "
+              f"learned_linear random-init + LRU 10%, moesim.replay_traces(jobs={cores})")
+    line = {
+        "impl": "reference", "metric": "trace tokens/sec (predict+cache-sim)",
+        "value": value, "unit": "trace tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / max(1, args.steps),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator)",
+        "config": {"workload": "C2 sample: DeepSeek-V2-Lite 26x64 top-6, 363-token prompts",
+                   "capacity_fraction": CAP_FRACTION, "prefetch_budget": BUDGET,
+                   "warmup_tokens": WARMUP_TOKENS, "predictor": "learned_linear"},
+        "cpu_baseline": {"value": value, "unit": "trace tokens/s", "cores": cores,
+                         "kind": "reference", "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "trace tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "hit_rate_10pct": {"learned_linear": rep.cache_hit_rate},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# Our arm.
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_17137_b200 as m
+
+    world, rank, local = _dist()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    m.load_library()
+    shape = m.ModelShape(C2["layers"], C2["experts"], C2["top_k"])
+    P = args.prompts
+    gen = m.GeneratorConfig(P, C2["tokens"], shape, C2["hot"], C2["skew"], C2["seed"],
+                            first_prompt_id=rank * P)
+    t0 = time.perf_counter()
+    packed = m.generate_packed(gen, dev)
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    rows = packed.rows
+    L, E = shape.num_layers, shape.num_experts
+    cap = m.CacheConfig(capacity_fraction=CAP_FRACTION).resolve_capacity(shape)
+    w = np.random.default_rng(0).normal(0.0, 0.01, (E, L + E + 1))
+    model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
+    pred = m.make_predictor("learned_linear", shape, model=model)
+    tokens_per_rank = P * C2["tokens"]
+
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(timing=None):
+        vec = m.metrics.metric_vector(E, dev)
+        e0, e1, e2 = ev(), ev(), ev()
+        e0.record(stream)
+        masks = pred.predict_masks(packed, BUDGET, WARMUP_TOKENS, metrics=vec)
+        e1.record(stream)
+        counters, _, _ = m.cache_replay(packed, [(masks, None, False)], [cap], WARMUP_TOKENS,
+                                        BUDGET, want_per_prompt=False)
+        e2.record(stream)
+        if world > 1:
+            buf = torch.cat([counters.view(-1), vec])
+            dist.all_reduce(buf)
+            counters, vec = buf[:counters.numel()].view(counters.shape), buf[counters.numel():]
+        if timing is not None:
+            timing.append((e0, e1, e2))
+        return counters, vec
+
+    # --- warm-up ---
+    for _ in range(args.warmup):
+        counters, vec = step()
+    torch.cuda.synchronize()
+
+    # --- timed region: device clock, max over ranks ---
+    hbm, bf16, bf16_sus, peak_kind = _peaks()
+    timing = []
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        start, end = ev(), ev()
+        start.record(stream)
+        for _ in range(args.steps):
+            counters, vec = step(timing)
+        end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = start.elapsed_time(end)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = tokens_per_rank * world / (ms / 1000.0) * args.steps
+    lin_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in timing)
+    sim_ms = statistics.mean(b.elapsed_time(c) for _, b, c in timing)
+    clock_info = clocks.summary()
+
+    c = counters[0, 0].cpu().numpy()
+    mc = m.MetricCounts.from_vector(vec.cpu().numpy(), E)
+
+    # --- end to end through the public API with host buffers ---
+    truth_host = packed.truth.cpu().pin_memory()
+    off_host = packed.row_off.cpu().pin_memory()
+    truth_d = torch.empty_like(packed.truth)
+    off_d = torch.empty_like(packed.row_off)
+    e2e_packed = m.PackedTraces(shape, truth_d, off_d, packed.row_off_host, packed.prompt_ids)
+    h2d = truth_host.numel() * 8 + off_host.numel() * 8
+    d2h = (4 + 3 * L) * 8 + (3 * E + 3) * 8
+
+    def e2e_step():
+        truth_d.copy_(truth_host, non_blocking=True)
+        off_d.copy_(off_host, non_blocking=True)
+        vec2 = m.metrics.metric_vector(E, dev)
+        masks = pred.predict_masks(e2e_packed, BUDGET, WARMUP_TOKENS, metrics=vec2)
+        cnt, _, _ = m.cache_replay(e2e_packed, [(masks, None, False)], [cap], WARMUP_TOKENS,
+                                   BUDGET, want_per_prompt=False)
+        if world > 1:
+            buf = torch.cat([cnt.view(-1), vec2])
+            dist.all_reduce(buf)
+            cnt, vec2 = buf[:cnt.numel()], buf[cnt.numel():]
+        return cnt.cpu(), vec2.cpu()
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s2, t2 = ev(), ev()
+    s2.record(stream)
+    for _ in range(args.steps):
+        cnt_h, _ = e2e_step()
+    t2.record(stream)
+    torch.cuda.synchronize()
+    ms2 = s2.elapsed_time(t2)
+    if world > 1:
+        t = torch.tensor([ms2], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms2 = float(t.item())
+    e2e_value = tokens_per_rank * world / (ms2 / 1000.0) * args.steps
+    assert np.array_equal(cnt_h.numpy().reshape(-1), counters.cpu().numpy().reshape(-1))
+
+    # --- roofline of the dominant kernel (HBM-bound integer work) ---
+    bytes_per_row = 16  # truth mask read + predicted mask (read by K1 / written by K3)
+    dom = "k_cache_sim" if sim_ms >= lin_ms else "k_linear_predict"
+    dom_ms = max(sim_ms, lin_ms)
+    achieved = rows * bytes_per_row / (dom_ms / 1000.0) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+
+    # --- per-policy hit rates at 10 % (outside the timed region) ---
+    hit = {"learned_linear": int(c[1]) / int(c[0])}
+    lru_c, _, _ = m.cache_replay(packed, [(None, None, False)], [cap], WARMUP_TOKENS, BUDGET,
+                                 want_per_prompt=False)
+    if world > 1:
+        dist.all_reduce(lru_c)
+    lc = lru_c[0, 0].cpu().numpy()
+    hit["lru_only"] = int(lc[1]) / int(lc[0])
+
+    cpu_base = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        n_sample = max(cores, 32)
+        try:
+            v, dt, _ = time_reference(n_sample, cores)
+            cpu_base = {"value": v, "unit": "trace tokens/s", "cores": cores, "kind": "reference",
+                        "sample": f"{n_sample} x {C2['tokens']}-token C2 prompts, "
+                                  f"moesim.replay_traces(jobs={cores}) learned_linear + LRU 10% "
+                                  f"({dt:.1f} s)", "cpu": cpu_model()}
+        except Exception as exc:
+            cpu_base = {"value": None, "unit": "trace tokens/s", "cores": 0, "kind": "reference",
+                        "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "trace tokens/sec (predict+cache-sim)",
+            "value": value, "unit": "trace tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
+            "data": "synthetic (reference generator, bit-identical, generated on device)",
+            "config": {"workload": f"C2: {P} prompts x {C2['tokens']} tokens per GPU, "
+                                   "DeepSeek-V2-Lite 26 MoE layers x 64 experts top-6",
+                       "rows_per_gpu": rows, "predictor": "learned_linear (random init, seed 0)",
+                       "capacity_entries": cap, "prefetch_budget": BUDGET,
+                       "warmup_tokens": WARMUP_TOKENS, "parallelism": f"prompt-sharded x{world}",
+                       "l2": "inputs (528 MB/GPU) larger than L2"},
+            "e2e": {"value": e2e_value, "unit": "trace tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": 2 * args.steps,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": traffic,
+                         "algorithmic_bytes": f"{bytes_per_row} B/row x {rows} rows"},
+            "kernels_ms": {"k_linear_predict": lin_ms, "k_cache_sim": sim_ms},
+            "hit_rate_10pct": hit,
+            "prediction": {"macro_f1": mc.macro_f1(), "position_accuracy": mc.position_accuracy,
+                           "label_accuracy": mc.label_accuracy},
+            "cpu_baseline": cpu_base,
+            "clocks": clock_info,
+            "setup": {"generate_s": gen_s},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--prompts", type=int, default=C2["prompts"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

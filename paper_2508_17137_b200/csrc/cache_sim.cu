@@ -48,7 +48,7 @@ struct SimArgs {
   int64_t hits_stride;
   // per-simulation shared-memory layout (bytes)
   int off_r, off_q, off_c, sim_bytes;
-  uint32_t qmask;  // LRU ring size - 1; LFU: unused
+  uint32_t magic;  // layer_of(key) = (key * magic) >> 22
 };
 
 template <int W>
@@ -72,39 +72,41 @@ __device__ __forceinline__ void word_clear(uint64_t (&a)[W], int w, uint64_t bit
 }
 
 // ---------------------------------------------------------------------------
-// LRU
+// LRU: an exact doubly-linked recency list over (layer, expert) keys, the
+// same structure as the reference's OrderedDict (cache.py:68). Node id = key
+// = layer*E + expert; node NK = L*E is a sentinel closing the ring, so
+// unlink/append are branch-free (two lanes of a warp on different paths only
+// diverge for a few instructions). Head (LRU) and tail (MRU) stay in registers.
 // ---------------------------------------------------------------------------
 template <int W, bool GENERAL>
 struct LruState {
-  uint16_t* stamp;  // [L*E]
-  uint64_t* R;      // [L*W] resident masks (stale for cur layer)
-  uint64_t* Psm;    // GENERAL only: [L*W] pin masks (stale for cur layer)
-  uint32_t* q;
-  uint32_t qmask, head, tail, clock;
+  uint16_t* prv;  // [NK+1]
+  uint16_t* nxt;  // [NK+1]
+  uint64_t* R;    // [L*W] resident masks (stale for the current layer)
+  uint64_t* Psm;  // GENERAL only: [L*W] pin masks
+  int head, tail, S, E, L, cur, npins;
+  uint32_t mE;  // layer_of(v) = (v * mE) >> 22, exact for v < NK (checked on host)
   int64_t count, cap;
-  int npins, E, L, cur;
   uint64_t Rl[W], Pm[W];
 
   __device__ void init(unsigned char* base, const SimArgs& a, int L_) {
     L = L_;
     E = a.E;
     cap = a.cap;
-    stamp = reinterpret_cast<uint16_t*>(base);
+    S = L * E;
+    mE = a.magic;
+    prv = reinterpret_cast<uint16_t*>(base);
+    nxt = prv + (S + 1);
     R = reinterpret_cast<uint64_t*>(base + a.off_r);
     Psm = GENERAL ? R + L * W : nullptr;
-    q = reinterpret_cast<uint32_t*>(base + a.off_q);
-    qmask = a.qmask;
-    head = tail = 0;
-    clock = 1;
+    prv[S] = nxt[S] = (uint16_t)S;
+    head = tail = S;
     count = 0;
     npins = 0;
     cur = 0;
 #pragma unroll
     for (int j = 0; j < W; ++j) Rl[j] = Pm[j] = 0;
-    // zero stamps and masks (16-byte stores; regions are 16-byte padded)
-    uint4* z = reinterpret_cast<uint4*>(base);
-    const int n16 = a.off_q / 16;
-    for (int i = 0; i < n16; ++i) z[i] = make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < L * W * (GENERAL ? 2 : 1); ++j) R[j] = 0;
   }
 
   __device__ __forceinline__ void focus(int l) {
@@ -121,72 +123,46 @@ struct LruState {
     cur = l;
   }
 
-  __device__ __forceinline__ void writeback() {
-#pragma unroll
-    for (int j = 0; j < W; ++j) {
-      R[cur * W + j] = Rl[j];
-      if (GENERAL) Psm[cur * W + j] = Pm[j];
-    }
-  }
+  __device__ __forceinline__ int layer_of(int v) const { return (int)(((uint32_t)v * mE) >> 22); }
 
-  __device__ __forceinline__ bool is_pinned(int l, int ex) const {
+  __device__ __forceinline__ bool is_pinned(int v) const {
+    const int l = layer_of(v), ex = v - l * E;
     const uint64_t bit = 1ull << (ex & 63);
     if (l == cur) return (word_get<W>(Pm, ex >> 6) & bit) != 0;
     if (GENERAL) return (Psm[l * W + (ex >> 6)] & bit) != 0;
     return false;  // trace mode: pins only ever exist in the current layer
   }
 
-  __device__ void compact() {
-    uint32_t n = 0;
-    for (uint32_t i = head; i != tail; ++i) {
-      const uint32_t e = q[i & qmask];
-      const uint32_t qk = e & 0xFFFFu;
-      const int sidx = (int)(qk >> 8) * E + (int)(qk & 0xFFu);
-      if (stamp[sidx] == (e >> 16)) {
-        ++n;
-        stamp[sidx] = (uint16_t)n;
-        q[(head + n - 1) & qmask] = (n << 16) | qk;
-      }
-    }
-    tail = head + n;
-    clock = n + 1;
+  __device__ __forceinline__ void unlink(int x) {
+    const int p = prv[x], n = nxt[x];
+    nxt[p] = (uint16_t)n;
+    prv[n] = (uint16_t)p;
+    head = (x == head) ? n : head;
+    tail = (x == tail) ? p : tail;
   }
 
-  __device__ __forceinline__ void push(int l, int ex) {
-    if (tail - head > qmask || clock >= 0xFFFFu) compact();
-    stamp[l * E + ex] = (uint16_t)clock;
-    q[tail & qmask] = (clock << 16) | ((uint32_t)l << 8) | (uint32_t)ex;
-    ++tail;
-    ++clock;
+  __device__ __forceinline__ void append(int x) {
+    prv[x] = (uint16_t)tail;
+    nxt[x] = (uint16_t)S;
+    nxt[tail] = (uint16_t)x;
+    prv[S] = (uint16_t)x;
+    head = (head == S) ? x : head;
+    tail = x;
   }
 
-  // _evict_one (cache.py:93-100). Precondition: count > npins.
-  __device__ void evict() {
-    uint32_t i = head;
-    bool at_head = true;
-    for (;;) {
-      const uint32_t e = q[i & qmask];
-      ++i;
-      const int l = (int)((e >> 8) & 0xFFu), ex = (int)(e & 0xFFu);
-      const int sidx = l * E + ex;
-      if (stamp[sidx] != (e >> 16)) {
-        if (at_head) head = i;
-        continue;
-      }
-      if (is_pinned(l, ex)) {
-        at_head = false;
-        continue;
-      }
-      stamp[sidx] = 0;
-      const uint64_t bit = 1ull << (ex & 63);
-      if (l == cur)
-        word_clear<W>(Rl, ex >> 6, bit);
-      else
-        R[l * W + (ex >> 6)] &= ~bit;
-      --count;
-      if (at_head) head = i;
-      return;
-    }
+  // _evict_one (cache.py:93-100): first non-pinned key from the LRU end.
+  // Precondition: count > npins.
+  __device__ __forceinline__ void evict() {
+    int v = head;
+    while (is_pinned(v)) v = nxt[v];  // rare: only when pins reach the LRU end
+    unlink(v);
+    const int l = layer_of(v), ex = v - l * E;
+    const uint64_t bit = 1ull << (ex & 63);
+    if (l == cur)
+      word_clear<W>(Rl, ex >> 6, bit);
+    else
+      R[l * W + (ex >> 6)] &= ~bit;
+    --count;
   }
 
   __device__ void begin_step(int l) {
@@ -201,43 +177,45 @@ struct LruState {
 
   // touch (cache.py:106-124) of expert ex of the current layer.
   __device__ __forceinline__ bool touch(int ex) {
+    const int k = cur * E + ex;
     const uint64_t bit = 1ull << (ex & 63);
-    if (word_get<W>(Rl, ex >> 6) & bit) {
-      push(cur, ex);
-      return true;
+    const bool hit = (word_get<W>(Rl, ex >> 6) & bit) != 0;
+    if (hit) {
+      unlink(k);  // move_to_end
+    } else {
+      if (count >= cap) {
+        if (count <= npins) return false;  // every resident key pinned: no insert
+        evict();
+      }
+      word_or<W>(Rl, ex >> 6, bit);
+      ++count;
     }
-    if (count >= cap) {
-      if (count <= npins) return false;  // every resident key pinned
-      evict();
-    }
-    word_or<W>(Rl, ex >> 6, bit);
-    ++count;
-    push(cur, ex);
-    return false;
+    append(k);
+    return hit;
   }
 
   // one key of prefetch (cache.py:141-153); returns true if inserted.
   __device__ __forceinline__ bool prefetch(int ex) {
+    const int k = cur * E + ex;
     const int w = ex >> 6;
     const uint64_t bit = 1ull << (ex & 63);
-    if (word_get<W>(Rl, w) & bit) {
-      push(cur, ex);
-      if (!(word_get<W>(Pm, w) & bit)) {
-        word_or<W>(Pm, w, bit);
-        ++npins;
+    const bool res = (word_get<W>(Rl, w) & bit) != 0;
+    if (res) {
+      unlink(k);  // refresh
+    } else {
+      if (count >= cap) {
+        if (count <= npins) return false;  // rejected, not pinned
+        evict();
       }
-      return false;
+      word_or<W>(Rl, w, bit);
+      ++count;
     }
-    if (count >= cap) {
-      if (count <= npins) return false;
-      evict();
+    append(k);
+    if (!(word_get<W>(Pm, w) & bit)) {
+      word_or<W>(Pm, w, bit);
+      ++npins;
     }
-    word_or<W>(Rl, w, bit);
-    ++count;
-    push(cur, ex);
-    word_or<W>(Pm, w, bit);
-    ++npins;
-    return true;
+    return !res;
   }
 };
 
@@ -375,103 +353,149 @@ struct LfuState {
 
 // ---------------------------------------------------------------------------
 // Trace replay driver (engine.py:157-206), shared by both policies.
+// One thread = one simulation; a warp = 32 simulations stepping in lockstep
+// over row index i of their own prompts. Every prompt starts at layer 0, so
+// all lanes are always at the same layer and the same warm-up phase: only
+// the cache operations themselves differ per lane. Per-layer counters are
+// warp-reduced each measured row into block-level shared counters.
 // ---------------------------------------------------------------------------
+constexpr int kPrefetchRows = 4;
+
 template <int W, class State>
 __global__ void __launch_bounds__(32) k_cache_sim(const SimArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int64_t sim = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (sim >= (int64_t)a.n_preds * a.P) return;
-  const int pi = (int)(sim / a.P);
-  const int p = (int)(sim % a.P);
-  unsigned char* base = smem + (size_t)threadIdx.x * a.sim_bytes;
   const int L = a.L;
-  uint32_t* lcnt = reinterpret_cast<uint32_t*>(base + a.off_c);
-  for (int j = 0; j < 3 * L; ++j) lcnt[j] = 0;
+  unsigned int* bcnt = reinterpret_cast<unsigned int*>(smem);  // [3L] block counters
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x) bcnt[j] = 0;
+  __syncthreads();
+  const int pi = blockIdx.y;  // prediction stream: never mixed within a block
+  const int64_t pg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = pg < a.P;
+  const int p = live ? (int)pg : 0;
+  unsigned char* base = smem + a.off_c + (size_t)threadIdx.x * a.sim_bytes;
+  const int64_t r0 = live ? a.row_off[p] : 0;
+  const int64_t nrows = live ? a.row_off[p + 1] - r0 : 0;
+  const unsigned full = 0xffffffffu;
+  int64_t nmax = nrows;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const int64_t other = __shfl_xor_sync(full, nmax, o);
+    nmax = other > nmax ? other : nmax;
+  }
 
   State st;
-  st.init(base, a, L);
+  if (live) st.init(base, a, L);
 
   const uint64_t* __restrict__ pred = a.preds[pi];
   const uint8_t* __restrict__ cov = a.covered[pi];
   const bool unbounded = (a.unbounded_bits >> pi) & 1u;
   const int limit = unbounded ? a.E : a.budget;
   uint64_t* hits = a.hits ? a.hits + pi * a.hits_stride : nullptr;
+  const uint64_t* __restrict__ tr = a.truth + r0 * W;
+  const uint64_t* __restrict__ pr = pred ? pred + r0 * W : nullptr;
 
   int64_t tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
-  const int64_t r0 = a.row_off[p], r1 = a.row_off[p + 1];
-  int l = 0, t = 0;
-  for (int64_t r = r0; r < r1; ++r) {
-    uint64_t tw[W], hw[W];
+  // software-pipelined row reads: rows i .. i+kPrefetchRows-1 in registers
+  uint64_t tbuf[kPrefetchRows][W], pbuf[kPrefetchRows][W];
 #pragma unroll
-    for (int j = 0; j < W; ++j) {
-      tw[j] = __ldg(a.truth + r * W + j);
-      hw[j] = 0;
+  for (int d = 0; d < kPrefetchRows; ++d)
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      tbuf[d][w] = d < nrows ? __ldg(tr + d * W + w) : 0ull;
+      pbuf[d][w] = (pr && d < nrows) ? __ldg(pr + d * W + w) : 0ull;
     }
-    if (t < a.warmup) {  // engine.py:160-167: warm the cache, no counters
-      st.focus(l);
-      MOEB_FOR_EACH_BIT(W, tw, ex, {
-        if (st.touch(ex)) word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
-      })
-    } else {
-      uint64_t pw[W];
+  int l = 0, t = 0;
+  for (int64_t i0 = 0; i0 < nmax; i0 += kPrefetchRows) {
 #pragma unroll
-      for (int j = 0; j < W; ++j) pw[j] = pred ? __ldg(pred + r * W + j) : 0ull;
-      st.begin_step(l);  // engine.py:172
-      int taken = 0;     // prefetch(sorted(pred)[:limit]) (engine.py:173-174)
+    for (int d = 0; d < kPrefetchRows; ++d) {
+      const int64_t i = i0 + d;
+      if (i >= nmax) break;  // warp-uniform
+      const bool valid = i < nrows;
+      uint64_t tw[W], pw[W], hw[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        uint64_t m = pw[w];
-        while (m && taken < limit) {
-          const int ex = w * 64 + __ffsll((long long)m) - 1;
-          m &= m - 1;
-          st.prefetch(ex);
-          ++taken;
+        tw[w] = tbuf[d][w];
+        pw[w] = pbuf[d][w];
+        hw[w] = 0;
+        const int64_t j = i + kPrefetchRows;  // refill this slot
+        tbuf[d][w] = j < nrows ? __ldg(tr + j * W + w) : 0ull;
+        pbuf[d][w] = (pr && j < nrows) ? __ldg(pr + j * W + w) : 0ull;
+      }
+      if (t < a.warmup) {  // engine.py:160-167: warm the cache, no counters
+        if (valid) {
+          st.focus(l);
+          MOEB_FOR_EACH_BIT(W, tw, ex, {
+            if (st.touch(ex)) word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
+          })
+        }
+      } else {
+        int k = 0, ph = 0, ch = 0;
+        if (valid) {
+          st.begin_step(l);  // engine.py:172
+          int taken = 0;     // prefetch(sorted(pred)[:limit]) (engine.py:173-174)
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            uint64_t m = pw[w];
+            while (m && taken < limit) {
+              const int ex = w * 64 + __ffsll((long long)m) - 1;
+              m &= m - 1;
+              st.prefetch(ex);
+              ++taken;
+            }
+          }
+          if (cov && !cov[r0 + i]) ++tot_unc;  // engine.py:175-176
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            k += __popcll(tw[w]);
+            ph += __popcll(tw[w] & pw[w]);  // FULL predicted set (engine.py:181-182)
+          }
+          MOEB_FOR_EACH_BIT(W, tw, ex, {
+            if (st.touch(ex)) {
+              ++ch;
+              word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
+            }
+          })
+          tot_k += k;
+          tot_ch += ch;
+          tot_ph += ph;
+        }
+        const unsigned sk = __reduce_add_sync(full, (unsigned)k);
+        const unsigned sc = __reduce_add_sync(full, (unsigned)ch);
+        const unsigned sp = __reduce_add_sync(full, (unsigned)ph);
+        if ((threadIdx.x & 31) == 0) {
+          atomicAdd(&bcnt[l], sk);
+          atomicAdd(&bcnt[L + l], sc);
+          atomicAdd(&bcnt[2 * L + l], sp);
         }
       }
-      if (cov && !cov[r]) ++tot_unc;  // engine.py:175-176
-      int k = 0, ph = 0, ch = 0;
+      if (hits && valid) {
 #pragma unroll
-      for (int j = 0; j < W; ++j) {
-        k += __popcll(tw[j]);
-        ph += __popcll(tw[j] & pw[j]);  // FULL predicted set (engine.py:181-182)
+        for (int w = 0; w < W; ++w) hits[(r0 + i) * W + w] = hw[w];
       }
-      MOEB_FOR_EACH_BIT(W, tw, ex, {
-        if (st.touch(ex)) {
-          ++ch;
-          word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
-        }
-      })
-      tot_k += k;
-      tot_ch += ch;
-      tot_ph += ph;
-      lcnt[l] += k;
-      lcnt[L + l] += ch;
-      lcnt[2 * L + l] += ph;
-    }
-    if (hits) {
-#pragma unroll
-      for (int j = 0; j < W; ++j) hits[r * W + j] = hw[j];
-    }
-    if (++l == L) {
-      l = 0;
-      ++t;
+      if (++l == L) {
+        l = 0;
+        ++t;
+      }
     }
   }
 
+  __syncthreads();
   int64_t* c = a.counters + pi * a.counters_stride;
-  atomicAdd(reinterpret_cast<unsigned long long*>(c + 0), (unsigned long long)tot_k);
-  atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot_ch);
-  atomicAdd(reinterpret_cast<unsigned long long*>(c + 2), (unsigned long long)tot_ph);
-  if (tot_unc) atomicAdd(reinterpret_cast<unsigned long long*>(c + 3), (unsigned long long)tot_unc);
-  for (int j = 0; j < 3 * L; ++j)
-    if (lcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)lcnt[j]);
-  if (a.per_prompt) {
-    int64_t* pp = a.per_prompt + pi * a.per_prompt_stride + 4 * (int64_t)p;
-    pp[0] += tot_k;
-    pp[1] += tot_ch;
-    pp[2] += tot_ph;
-    pp[3] += tot_unc;
+  if (live) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(c + 0), (unsigned long long)tot_k);
+    atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot_ch);
+    atomicAdd(reinterpret_cast<unsigned long long*>(c + 2), (unsigned long long)tot_ph);
+    if (tot_unc) atomicAdd(reinterpret_cast<unsigned long long*>(c + 3), (unsigned long long)tot_unc);
+    if (a.per_prompt) {
+      int64_t* pp = a.per_prompt + pi * a.per_prompt_stride + 4 * (int64_t)p;
+      pp[0] += tot_k;
+      pp[1] += tot_ch;
+      pp[2] += tot_ph;
+      pp[3] += tot_unc;
+    }
   }
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x)
+    if (bcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bcnt[j]);
 }
 
 // Op-stream interpreter (one cache): the reference's per-call API.
@@ -498,52 +522,53 @@ __global__ void k_cache_ops(const SimArgs a, const int32_t* ops, const int32_t* 
 
 inline int align16(int64_t x) { return (int)((x + 15) / 16 * 16); }
 
+uint32_t layer_magic(int L, int E) {
+  const uint32_t m = (uint32_t)(((1u << 22) + E - 1) / E);
+  for (int v = 0; v <= L * E; ++v)
+    if ((int)(((uint64_t)v * m) >> 22) != v / E) return 0;
+  return m;
+}
+
 // Shared-memory layout of one simulation.
 void layout(SimArgs& a, int policy, bool general) {
   const int W = moeb::words_for(a.E);
-  const int64_t LE = (int64_t)a.L * a.E;
-  a.off_r = align16(2 * LE);
+  const int64_t NK = (int64_t)a.L * a.E;
   const int64_t rbytes = 8LL * a.L * W * (general ? 2 : 1);
-  a.off_q = align16(a.off_r + rbytes);
-  int64_t qbytes;
   if (policy == MOEB_POLICY_LRU) {
-    uint32_t qn = 64;
-    const int64_t need = std::max<int64_t>(2 * a.cap, a.cap + 64);
-    while (qn < need) qn <<= 1;
-    a.qmask = qn - 1;
-    qbytes = 4LL * qn;
+    a.off_r = align16(4 * (NK + 1));  // prv, nxt
+    a.off_q = align16(a.off_r + rbytes);
+    a.sim_bytes = a.off_q + 16;  // +16 B skews simulations across smem banks
   } else {
-    a.qmask = 0;
-    qbytes = 8LL * a.cap + 2LL * a.cap;
+    a.off_r = align16(2 * NK);  // slot_of
+    a.off_q = align16(a.off_r + rbytes);  // vals [cap] u64, skeys [cap] u16
+    a.sim_bytes = align16(a.off_q + 10LL * a.cap) + 16;
   }
-  a.off_c = align16(a.off_q + qbytes);
-  // +16 bytes skews consecutive simulations across shared-memory banks
-  a.sim_bytes = align16(a.off_c + 4LL * 3 * a.L) + 16;
+  a.magic = layer_magic(a.L, a.E);
 }
 
 template <int W>
-int launch_sim(const SimArgs& a, int policy, cudaStream_t s) {
-  const int64_t sims = (int64_t)a.n_preds * a.P;
-  const int per_sm = std::max(1, moeb::max_smem_per_sm() / (a.sim_bytes + 256));
+int launch_sim(SimArgs a, int policy, cudaStream_t s) {
   const int max_block = moeb::max_smem_per_block();
-  if (a.sim_bytes > max_block)
+  const int head = align16(4LL * 3 * a.L);  // block counters
+  a.off_c = head;
+  if (a.magic == 0) return moeb::fail(MOEB_EINVAL, "layer magic failed for E=%d", a.E);
+  // Threads per block: one lockstep warp of simulations (fewer if the state
+  // is too large for 32 of them).
+  int tpb = 32;
+  while (tpb > 1 && head + (int64_t)tpb * a.sim_bytes > max_block) --tpb;
+  if (head + (int64_t)tpb * a.sim_bytes > max_block)
     return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
                       a.sim_bytes, max_block);
-  // Threads per block: keep >= 4 blocks per SM when the state allows it so
-  // the four SM sub-partitions all issue; never more than one warp.
-  int tpb = std::min(32, std::max(1, per_sm / 4));
-  tpb = std::min<int64_t>(tpb, std::max<int64_t>(1, sims));
-  while (tpb > 1 && tpb * a.sim_bytes > max_block) --tpb;
-  const size_t smem = (size_t)tpb * a.sim_bytes;
-  const int64_t blocks = (sims + tpb - 1) / tpb;
+  const size_t smem = head + (size_t)tpb * a.sim_bytes;
+  const dim3 blocks((unsigned)((a.P + tpb - 1) / tpb), (unsigned)a.n_preds);
   if (policy == MOEB_POLICY_LRU) {
     auto k = k_cache_sim<W, LruState<W, false>>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<(unsigned)blocks, tpb, smem, s>>>(a);
+    k<<<blocks, tpb, smem, s>>>(a);
   } else {
     auto k = k_cache_sim<W, LfuState<W, false>>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<(unsigned)blocks, tpb, smem, s>>>(a);
+    k<<<blocks, tpb, smem, s>>>(a);
   }
   return moeb::check_launch("k_cache_sim");
 }

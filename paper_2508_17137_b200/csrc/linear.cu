@@ -15,9 +15,9 @@
 // random-init weights; fp64 keeps the selection identical to numpy's, and
 // the recurrence's rounding drift stays ~1e-15 relative, tests assert 1e-12).
 //
-// Mapping: one thread per (layer, prompt) stream; consecutive threads take
-// consecutive prompts of the same layer so the per-layer bias reads are
-// shared-memory broadcasts. z[64] lives in registers; W_h columns and the
+// Mapping: one thread per (prompt, layer) stream; consecutive threads take
+// consecutive layers of the same prompt, so at every token a warp reads and
+// writes ~32 contiguous mask rows (coalesced). z[64] lives in registers; W_h columns and the
 // bias table live in shared memory (column-major, stride E+1 against bank
 // conflicts). Metrics: each warp turns its 32 rows of pred/truth masks into
 // per-expert TP/FP/FN counts with ballot+popc, then one shared-memory reduce
@@ -45,9 +45,9 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
   const int L = a.L, E = a.E, F = a.L + a.E + 1;
   const int ES = E + 1;  // padded stride
   double* colT = reinterpret_cast<double*>(smem_raw);  // [E][ES]: colT[e][j] = W[j][L+e]
-  double* bias = colT + E * ES;                        // [L][E]:  b_l[j]
-  double* bias2 = bias + L * E;                        // [L][E]:  (1 - decay) b_l[j]
-  unsigned long long* mcnt = reinterpret_cast<unsigned long long*>(bias2 + L * E);  // [3E+3]
+  double* bias = colT + E * ES;                        // [L][ES]: b_l[j]
+  double* bias2 = bias + L * ES;                       // [L][ES]: (1 - decay) b_l[j]
+  unsigned long long* mcnt = reinterpret_cast<unsigned long long*>(bias2 + L * ES);  // [3E+3]
   for (int i = threadIdx.x; i < E * E; i += blockDim.x) {
     const int e = i / E, j = i % E;
     colT[e * ES + j] = a.Wt[(int64_t)j * F + L + e];
@@ -55,8 +55,8 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
   for (int i = threadIdx.x; i < L * E; i += blockDim.x) {
     const int l = i / E, j = i % E;
     const double b = a.Wt[(int64_t)j * F + l] + a.Wt[(int64_t)j * F + L + E];
-    bias[i] = b;
-    bias2[i] = (1.0 - a.decay) * b;
+    bias[l * ES + j] = b;
+    bias2[l * ES + j] = (1.0 - a.decay) * b;
   }
   if (a.metrics)
     for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x) mcnt[i] = 0;
@@ -64,8 +64,8 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
 
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = g < (int64_t)a.L * a.P;
-  const int l = live ? (int)(g / a.P) : 0;
-  const int p = live ? (int)(g % a.P) : 0;
+  const int p = live ? (int)(g / L) : 0;
+  const int l = live ? (int)(g % L) : 0;
   const int64_t r0 = live ? a.row_off[p] : 0;
   const int T = live ? (int)((a.row_off[p + 1] - r0) / L) : 0;
   // warp-uniform trip count so ballots see every lane
@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
 
   double z[64];
 #pragma unroll
-  for (int e = 0; e < 64; ++e) z[e] = e < E ? bias[l * E + e] : 0.0;
+  for (int e = 0; e < 64; ++e) z[e] = e < E ? bias[l * ES + e] : 0.0;
   const int lane = threadIdx.x & 31;
   uint32_t tp_lo = 0, tp_hi = 0, fp_lo = 0, fp_hi = 0, fn_lo = 0, fn_hi = 0;
   uint32_t npos = 0, nexact = 0;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
       nlabel += m ? (uint64_t)(E - __popcll((pm ^ tw) & emask)) : 0;
     }
     if (valid) {  // update_history (learner.py:62-72), as a logit recurrence
-      const double* b2 = bias2 + l * E;
+      const double* b2 = bias2 + l * ES;
 #pragma unroll
       for (int e = 0; e < 64; ++e)
         if (e < E) z[e] = fma(a.decay, z[e], b2[e]);
@@ -192,7 +192,7 @@ extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_
   MOEB_REQUIRE(decay >= 0.0 && decay < 1.0, "decay must be in [0, 1)");
   LinArgs a{truth, prompt_row_off, n_prompts, L, E, weights, decay, budget,
             threshold ? 1 : 0, warmup_tokens, pred, logits, metrics};
-  const size_t smem = sizeof(double) * ((size_t)E * (E + 1) + 2 * (size_t)L * E) +
+  const size_t smem = sizeof(double) * ((size_t)E * (E + 1) + 2 * (size_t)L * (E + 1)) +
                       sizeof(unsigned long long) * (3 * E + 3);
   if ((int)smem > moeb::max_smem_per_block())
     return moeb::fail(MOEB_ESMEM, "learned_linear tables need %zu B of shared memory", smem);
