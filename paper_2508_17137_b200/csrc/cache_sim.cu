@@ -47,7 +47,7 @@ struct SimArgs {
   uint64_t* hits;
   int64_t hits_stride;
   // per-simulation shared-memory layout (bytes)
-  int off_r, off_q, off_c, sim_bytes;
+  int off_r, off_q, off_k, off_c, sim_bytes;
   uint32_t magic;  // layer_of(key) = (key * magic) >> 22
 };
 
@@ -72,41 +72,55 @@ __device__ __forceinline__ void word_clear(uint64_t (&a)[W], int w, uint64_t bit
 }
 
 // ---------------------------------------------------------------------------
-// LRU: an exact doubly-linked recency list over (layer, expert) keys, the
-// same structure as the reference's OrderedDict (cache.py:68). Node id = key
-// = layer*E + expert; node NK = L*E is a sentinel closing the ring, so
-// unlink/append are branch-free (two lanes of a warp on different paths only
-// diverge for a few instructions). Head (LRU) and tail (MRU) stay in registers.
+// LRU: the resident keys of one cache form a circular doubly-linked ring of
+// `cap` slots, ordered like the reference's OrderedDict (cache.py:68): head
+// is the least recently used slot, its ring predecessor (`tail`) the most
+// recently used. slot_of[key] maps a resident key to its slot. With IDX =
+// uint8_t (cap < 255) one simulation needs ~2.5 KB at 10 % capacity, so every
+// prompt of the C2 workload is resident at once. The dominant operation at
+// small capacities -- a miss in a full cache -- is a rotation: the LRU slot
+// takes the new key and becomes the tail (head = nx[head]), one dependent
+// shared-memory load.
 // ---------------------------------------------------------------------------
-template <int W, bool GENERAL>
+template <int W, int ES, typename IDX, bool GENERAL>
 struct LruState {
-  uint16_t* prv;  // [NK+1]
-  uint16_t* nxt;  // [NK+1]
-  uint64_t* R;    // [L*W] resident masks (stale for the current layer)
-  uint64_t* Psm;  // GENERAL only: [L*W] pin masks
-  int head, tail, S, E, L, cur, npins;
-  uint32_t mE;  // layer_of(v) = (v * mE) >> 22, exact for v < NK (checked on host)
-  int64_t count, cap;
+  IDX* slot_of;     // [NK]  (valid for resident keys only)
+  IDX* nx;          // [cap] ring successor
+  IDX* pv;          // [cap] ring predecessor
+  uint16_t* skey;   // [cap] key of each slot
+  uint64_t* R;      // [L*W] resident masks (stale for the current layer)
+  uint64_t* Psm;    // GENERAL only: [L*W] pin masks
+  int head, tail, count, cap, npins, cur, E, L;
+  uint32_t mE;
   uint64_t Rl[W], Pm[W];
 
   __device__ void init(unsigned char* base, const SimArgs& a, int L_) {
     L = L_;
     E = a.E;
-    cap = a.cap;
-    S = L * E;
+    cap = (int)a.cap;
     mE = a.magic;
-    prv = reinterpret_cast<uint16_t*>(base);
-    nxt = prv + (S + 1);
+    const int NK = L * E;
+    slot_of = reinterpret_cast<IDX*>(base);
     R = reinterpret_cast<uint64_t*>(base + a.off_r);
     Psm = GENERAL ? R + L * W : nullptr;
-    prv[S] = nxt[S] = (uint16_t)S;
-    head = tail = S;
+    nx = reinterpret_cast<IDX*>(base + a.off_q);
+    pv = nx + cap;
+    skey = reinterpret_cast<uint16_t*>(base + a.off_k);
+    (void)NK;
+    head = tail = 0;
     count = 0;
     npins = 0;
     cur = 0;
 #pragma unroll
     for (int j = 0; j < W; ++j) Rl[j] = Pm[j] = 0;
     for (int j = 0; j < L * W * (GENERAL ? 2 : 1); ++j) R[j] = 0;
+  }
+
+  __device__ __forceinline__ int layer_of(int k) const {
+    return ES >= 0 ? (k >> ES) : (int)(((uint32_t)k * mE) >> 22);
+  }
+  __device__ __forceinline__ int key_of(int l, int ex) const {
+    return ES >= 0 ? ((l << ES) | ex) : l * E + ex;
   }
 
   __device__ __forceinline__ void focus(int l) {
@@ -123,46 +137,69 @@ struct LruState {
     cur = l;
   }
 
-  __device__ __forceinline__ int layer_of(int v) const { return (int)(((uint32_t)v * mE) >> 22); }
-
-  __device__ __forceinline__ bool is_pinned(int v) const {
-    const int l = layer_of(v), ex = v - l * E;
+  __device__ __forceinline__ bool is_pinned(int k) const {
+    const int l = layer_of(k), ex = k - l * E;
     const uint64_t bit = 1ull << (ex & 63);
     if (l == cur) return (word_get<W>(Pm, ex >> 6) & bit) != 0;
     if (GENERAL) return (Psm[l * W + (ex >> 6)] & bit) != 0;
     return false;  // trace mode: pins only ever exist in the current layer
   }
 
-  __device__ __forceinline__ void unlink(int x) {
-    const int p = prv[x], n = nxt[x];
-    nxt[p] = (uint16_t)n;
-    prv[n] = (uint16_t)p;
-    head = (x == head) ? n : head;
-    tail = (x == tail) ? p : tail;
-  }
-
-  __device__ __forceinline__ void append(int x) {
-    prv[x] = (uint16_t)tail;
-    nxt[x] = (uint16_t)S;
-    nxt[tail] = (uint16_t)x;
-    prv[S] = (uint16_t)x;
-    head = (head == S) ? x : head;
-    tail = x;
-  }
-
-  // _evict_one (cache.py:93-100): first non-pinned key from the LRU end.
-  // Precondition: count > npins.
-  __device__ __forceinline__ void evict() {
-    int v = head;
-    while (is_pinned(v)) v = nxt[v];  // rare: only when pins reach the LRU end
-    unlink(v);
-    const int l = layer_of(v), ex = v - l * E;
+  __device__ __forceinline__ void clear_resident(int k) {
+    const int l = layer_of(k), ex = k - l * E;
     const uint64_t bit = 1ull << (ex & 63);
     if (l == cur)
       word_clear<W>(Rl, ex >> 6, bit);
     else
       R[l * W + (ex >> 6)] &= ~bit;
-    --count;
+  }
+
+  // move slot s to the MRU end (OrderedDict.move_to_end)
+  __device__ __forceinline__ void to_tail(int s) {
+    if (s == tail) return;
+    if (s == head) {  // rotation
+      head = nx[s];
+      tail = s;
+      return;
+    }
+    const int p = pv[s], n = nx[s];
+    nx[p] = (IDX)n;
+    pv[n] = (IDX)p;
+    nx[tail] = (IDX)s;
+    pv[s] = (IDX)tail;
+    nx[s] = (IDX)head;
+    pv[head] = (IDX)s;
+    tail = s;
+  }
+
+  // Insert key k at the MRU end, evicting the LRU non-pinned key when full
+  // (_evict_one, cache.py:93-100). Precondition: count < cap or count > npins.
+  __device__ __forceinline__ void insert(int k) {
+    int s;
+    if (count < cap) {
+      s = count++;
+      if (s == 0) {
+        nx[0] = pv[0] = 0;
+        head = 0;
+      } else {
+        nx[tail] = (IDX)s;
+        pv[s] = (IDX)tail;
+        nx[s] = (IDX)head;
+        pv[head] = (IDX)s;
+      }
+      tail = s;
+    } else {
+      s = head;
+      int vk = skey[s];
+      while (is_pinned(vk)) {  // rare: pins reach the LRU end (tiny caches)
+        s = nx[s];
+        vk = skey[s];
+      }
+      clear_resident(vk);
+      to_tail(s);
+    }
+    skey[s] = (uint16_t)k;
+    slot_of[k] = (IDX)s;
   }
 
   __device__ void begin_step(int l) {
@@ -177,45 +214,37 @@ struct LruState {
 
   // touch (cache.py:106-124) of expert ex of the current layer.
   __device__ __forceinline__ bool touch(int ex) {
-    const int k = cur * E + ex;
+    const int k = key_of(cur, ex);
     const uint64_t bit = 1ull << (ex & 63);
-    const bool hit = (word_get<W>(Rl, ex >> 6) & bit) != 0;
-    if (hit) {
-      unlink(k);  // move_to_end
-    } else {
-      if (count >= cap) {
-        if (count <= npins) return false;  // every resident key pinned: no insert
-        evict();
-      }
-      word_or<W>(Rl, ex >> 6, bit);
-      ++count;
+    if (word_get<W>(Rl, ex >> 6) & bit) {
+      to_tail(slot_of[k]);
+      return true;
     }
-    append(k);
-    return hit;
+    if (count >= cap && count <= npins) return false;  // every resident key pinned
+    insert(k);
+    word_or<W>(Rl, ex >> 6, bit);
+    return false;
   }
 
   // one key of prefetch (cache.py:141-153); returns true if inserted.
   __device__ __forceinline__ bool prefetch(int ex) {
-    const int k = cur * E + ex;
+    const int k = key_of(cur, ex);
     const int w = ex >> 6;
     const uint64_t bit = 1ull << (ex & 63);
-    const bool res = (word_get<W>(Rl, w) & bit) != 0;
-    if (res) {
-      unlink(k);  // refresh
+    bool inserted = false;
+    if (word_get<W>(Rl, w) & bit) {
+      to_tail(slot_of[k]);  // refresh
     } else {
-      if (count >= cap) {
-        if (count <= npins) return false;  // rejected, not pinned
-        evict();
-      }
+      if (count >= cap && count <= npins) return false;  // rejected, not pinned
+      insert(k);
       word_or<W>(Rl, w, bit);
-      ++count;
+      inserted = true;
     }
-    append(k);
     if (!(word_get<W>(Pm, w) & bit)) {
       word_or<W>(Pm, w, bit);
       ++npins;
     }
-    return !res;
+    return inserted;
   }
 };
 
@@ -529,21 +558,40 @@ uint32_t layer_magic(int L, int E) {
   return m;
 }
 
-// Shared-memory layout of one simulation.
-void layout(SimArgs& a, int policy, bool general) {
+// Shared-memory layout of one simulation (LRU: slot map, masks, ring links,
+// slot keys; LFU: slot map, masks, slot values/keys).
+void layout(SimArgs& a, int policy, bool general, int idx_bytes) {
   const int W = moeb::words_for(a.E);
   const int64_t NK = (int64_t)a.L * a.E;
   const int64_t rbytes = 8LL * a.L * W * (general ? 2 : 1);
   if (policy == MOEB_POLICY_LRU) {
-    a.off_r = align16(4 * (NK + 1));  // prv, nxt
+    a.off_r = align16(idx_bytes * NK);
     a.off_q = align16(a.off_r + rbytes);
-    a.sim_bytes = a.off_q + 16;  // +16 B skews simulations across smem banks
+    a.off_k = align16(a.off_q + 2LL * idx_bytes * a.cap);
+    a.sim_bytes = align16(a.off_k + 2LL * a.cap) + 16;  // +16 B skews smem banks
   } else {
     a.off_r = align16(2 * NK);  // slot_of
     a.off_q = align16(a.off_r + rbytes);  // vals [cap] u64, skeys [cap] u16
+    a.off_k = 0;
     a.sim_bytes = align16(a.off_q + 10LL * a.cap) + 16;
   }
   a.magic = layer_magic(a.L, a.E);
+}
+
+template <class K>
+int launch_kernel(K k, const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const dim3 blocks((unsigned)((a.P + tpb - 1) / tpb), (unsigned)a.n_preds);
+  k<<<blocks, tpb, smem, s>>>(a);
+  return moeb::check_launch("k_cache_sim");
+}
+
+// LRU instance: E = 64 / 256 get shift-based key math, others the generic
+// multiply; uint8_t ring links when the capacity allows.
+template <int W, int ES>
+int launch_lru(const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
+  if (a.cap < 255) return launch_kernel(k_cache_sim<W, LruState<W, ES, uint8_t, false>>, a, tpb, smem, s);
+  return launch_kernel(k_cache_sim<W, LruState<W, ES, uint16_t, false>>, a, tpb, smem, s);
 }
 
 template <int W>
@@ -552,25 +600,18 @@ int launch_sim(SimArgs a, int policy, cudaStream_t s) {
   const int head = align16(4LL * 3 * a.L);  // block counters
   a.off_c = head;
   if (a.magic == 0) return moeb::fail(MOEB_EINVAL, "layer magic failed for E=%d", a.E);
-  // Threads per block: one lockstep warp of simulations (fewer if the state
-  // is too large for 32 of them).
+  // One lockstep warp of simulations per block (fewer if the state is large).
   int tpb = 32;
   while (tpb > 1 && head + (int64_t)tpb * a.sim_bytes > max_block) --tpb;
   if (head + (int64_t)tpb * a.sim_bytes > max_block)
     return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
                       a.sim_bytes, max_block);
   const size_t smem = head + (size_t)tpb * a.sim_bytes;
-  const dim3 blocks((unsigned)((a.P + tpb - 1) / tpb), (unsigned)a.n_preds);
-  if (policy == MOEB_POLICY_LRU) {
-    auto k = k_cache_sim<W, LruState<W, false>>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<blocks, tpb, smem, s>>>(a);
-  } else {
-    auto k = k_cache_sim<W, LfuState<W, false>>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<blocks, tpb, smem, s>>>(a);
-  }
-  return moeb::check_launch("k_cache_sim");
+  if (policy == MOEB_POLICY_LFU)
+    return launch_kernel(k_cache_sim<W, LfuState<W, false>>, a, tpb, smem, s);
+  if (W == 1 && a.E == 64) return launch_lru<1, 6>(a, tpb, smem, s);
+  if (W == 4 && a.E == 256) return launch_lru<4, 8>(a, tpb, smem, s);
+  return launch_lru<W, -1>(a, tpb, smem, s);
 }
 
 }  // namespace
@@ -624,7 +665,7 @@ extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* pred
     a.per_prompt_stride = (int64_t)n_caps * n_prompts * 4;
     a.hits = hit_masks ? hit_masks + (int64_t)c * rows * W : nullptr;
     a.hits_stride = (int64_t)n_caps * rows * W;
-    layout(a, policy, false);
+    layout(a, policy, false, a.cap < 255 ? 1 : 2);
     int rc = W == 1 ? launch_sim<1>(a, policy, s)
              : W == 2 ? launch_sim<2>(a, policy, s)
              : W == 3 ? launch_sim<3>(a, policy, s)
@@ -637,12 +678,12 @@ extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* pred
 template <int W>
 static int launch_ops(SimArgs& a, int policy, const int32_t* ops, const int32_t* keys, int64_t n,
                       uint8_t* results, cudaStream_t s) {
-  layout(a, policy, true);
+  layout(a, policy, true, 2);
   const size_t smem = a.sim_bytes;
   if ((int)smem > moeb::max_smem_per_block())
     return moeb::fail(MOEB_ESMEM, "cache state %zu B exceeds shared memory", smem);
   if (policy == MOEB_POLICY_LRU) {
-    auto k = k_cache_ops<W, LruState<W, true>>;
+    auto k = k_cache_ops<W, LruState<W, -1, uint16_t, true>>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<1, 32, smem, s>>>(a, ops, keys, n, results);
   } else {
