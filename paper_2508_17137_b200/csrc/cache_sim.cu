@@ -49,6 +49,7 @@ struct SimArgs {
   // per-simulation shared-memory layout (bytes)
   int off_r, off_q, off_k, off_c, sim_bytes;
   uint32_t magic;  // layer_of(key) = (key * magic) >> 22
+  uint32_t qmask;  // LRU queue size - 1
 };
 
 template <int W>
@@ -72,26 +73,29 @@ __device__ __forceinline__ void word_clear(uint64_t (&a)[W], int w, uint64_t bit
 }
 
 // ---------------------------------------------------------------------------
-// LRU: the resident keys of one cache form a circular doubly-linked ring of
-// `cap` slots, ordered like the reference's OrderedDict (cache.py:68): head
-// is the least recently used slot, its ring predecessor (`tail`) the most
-// recently used. slot_of[key] maps a resident key to its slot. With IDX =
-// uint8_t (cap < 255) one simulation needs ~2.5 KB at 10 % capacity, so every
-// prompt of the C2 workload is resident at once. The dominant operation at
-// small capacities -- a miss in a full cache -- is a rotation: the LRU slot
-// takes the new key and becomes the tail (head = nx[head]), one dependent
-// shared-memory load.
+// LRU: lazy-deletion recency queue, exactly the reference's OrderedDict order
+// (cache.py:68). Every access (touch hit/miss, prefetch insert/refresh)
+// appends the key at the queue tail and records pos_of[key] = its queue
+// index (mod 2^16); an entry q[i] is valid iff pos_of[q[i]] == i, so moving a
+// key to the MRU end is two stores and its old entry simply goes stale. The
+// LRU key is the first valid entry from the head: `_evict_one`
+// (cache.py:93-100) pops stale entries, skips pinned ones in place, and
+// invalidates the victim (pos_of set outside the live window). The head
+// entry and its validity are kept pre-loaded in registers, so a miss usually
+// has no shared-memory load on its critical path. When the queue is full it
+// is compacted in place, order preserved.
 // ---------------------------------------------------------------------------
-template <int W, int ES, typename IDX, bool GENERAL>
+template <int W, int ES, bool GENERAL>
 struct LruState {
-  IDX* slot_of;     // [NK]  (valid for resident keys only)
-  IDX* nx;          // [cap] ring successor
-  IDX* pv;          // [cap] ring predecessor
-  uint16_t* skey;   // [cap] key of each slot
-  uint64_t* R;      // [L*W] resident masks (stale for the current layer)
-  uint64_t* Psm;    // GENERAL only: [L*W] pin masks
-  int head, tail, count, cap, npins, cur, E, L;
+  uint16_t* pos_of;  // [NK] queue index (mod 2^16) of the key's latest entry
+  uint16_t* q;       // [qn] keys in access order
+  uint64_t* R;       // [L*W] resident masks (stale for the current layer)
+  uint64_t* Psm;     // GENERAL only: [L*W] pin masks
+  uint32_t head, tail, qmask;
+  int count, cap, npins, cur, E, L;
   uint32_t mE;
+  int hk;    // q[head] (pre-loaded)
+  bool hv;   // entry at head is valid (pre-loaded)
   uint64_t Rl[W], Pm[W];
 
   __device__ void init(unsigned char* base, const SimArgs& a, int L_) {
@@ -99,18 +103,17 @@ struct LruState {
     E = a.E;
     cap = (int)a.cap;
     mE = a.magic;
-    const int NK = L * E;
-    slot_of = reinterpret_cast<IDX*>(base);
+    qmask = a.qmask;
+    pos_of = reinterpret_cast<uint16_t*>(base);
     R = reinterpret_cast<uint64_t*>(base + a.off_r);
     Psm = GENERAL ? R + L * W : nullptr;
-    nx = reinterpret_cast<IDX*>(base + a.off_q);
-    pv = nx + cap;
-    skey = reinterpret_cast<uint16_t*>(base + a.off_k);
-    (void)NK;
+    q = reinterpret_cast<uint16_t*>(base + a.off_q);
     head = tail = 0;
     count = 0;
     npins = 0;
     cur = 0;
+    hk = 0;
+    hv = false;
 #pragma unroll
     for (int j = 0; j < W; ++j) Rl[j] = Pm[j] = 0;
     for (int j = 0; j < L * W * (GENERAL ? 2 : 1); ++j) R[j] = 0;
@@ -118,6 +121,9 @@ struct LruState {
 
   __device__ __forceinline__ int layer_of(int k) const {
     return ES >= 0 ? (k >> ES) : (int)(((uint32_t)k * mE) >> 22);
+  }
+  __device__ __forceinline__ int expert_of(int k, int l) const {
+    return ES >= 0 ? (k & ((1 << (ES >= 0 ? ES : 0)) - 1)) : k - l * E;
   }
   __device__ __forceinline__ int key_of(int l, int ex) const {
     return ES >= 0 ? ((l << ES) | ex) : l * E + ex;
@@ -138,68 +144,71 @@ struct LruState {
   }
 
   __device__ __forceinline__ bool is_pinned(int k) const {
-    const int l = layer_of(k), ex = k - l * E;
+    const int l = layer_of(k), ex = expert_of(k, l);
     const uint64_t bit = 1ull << (ex & 63);
     if (l == cur) return (word_get<W>(Pm, ex >> 6) & bit) != 0;
     if (GENERAL) return (Psm[l * W + (ex >> 6)] & bit) != 0;
     return false;  // trace mode: pins only ever exist in the current layer
   }
 
-  __device__ __forceinline__ void clear_resident(int k) {
-    const int l = layer_of(k), ex = k - l * E;
+  __device__ __forceinline__ void load_head() {
+    hk = q[head & qmask];
+    hv = head != tail && pos_of[hk] == (uint16_t)head;
+  }
+
+  __device__ __noinline__ void compact() {
+    uint32_t n = head;
+    for (uint32_t i = head; i != tail; ++i) {
+      const int k = q[i & qmask];
+      if (pos_of[k] == (uint16_t)i) {
+        q[n & qmask] = (uint16_t)k;
+        pos_of[k] = (uint16_t)n;
+        ++n;
+      }
+    }
+    tail = n;
+  }
+
+  // Append key k at the MRU end (move_to_end / insert).
+  __device__ __forceinline__ void push(int k) {
+    if (__any_sync(__activemask(), tail - head > qmask)) {
+      if (tail - head > qmask) compact();
+      load_head();
+    }
+    q[tail & qmask] = (uint16_t)k;
+    pos_of[k] = (uint16_t)tail;
+    hv = hv && hk != k;  // the head entry of k just went stale
+    ++tail;
+  }
+
+  // Remove the LRU non-pinned key. Precondition: count > npins.
+  __device__ __forceinline__ void evict() {
+    // pop stale entries
+    while (!hv) {
+      ++head;
+      load_head();
+    }
+    int v = hk;
+    if (is_pinned(v)) {  // rare: pins reach the LRU end (tiny caches)
+      uint32_t i = head + 1;
+      for (;; ++i) {
+        const int k = q[i & qmask];
+        if (pos_of[k] == (uint16_t)i && !is_pinned(k)) break;
+      }
+      v = q[i & qmask];
+      pos_of[v] = (uint16_t)(i + 0x8000u);  // invalidate in place
+    } else {
+      pos_of[v] = (uint16_t)(head + 0x8000u);
+      ++head;
+      load_head();
+    }
+    const int l = layer_of(v), ex = expert_of(v, l);
     const uint64_t bit = 1ull << (ex & 63);
     if (l == cur)
       word_clear<W>(Rl, ex >> 6, bit);
     else
       R[l * W + (ex >> 6)] &= ~bit;
-  }
-
-  // move slot s to the MRU end (OrderedDict.move_to_end)
-  __device__ __forceinline__ void to_tail(int s) {
-    if (s == tail) return;
-    if (s == head) {  // rotation
-      head = nx[s];
-      tail = s;
-      return;
-    }
-    const int p = pv[s], n = nx[s];
-    nx[p] = (IDX)n;
-    pv[n] = (IDX)p;
-    nx[tail] = (IDX)s;
-    pv[s] = (IDX)tail;
-    nx[s] = (IDX)head;
-    pv[head] = (IDX)s;
-    tail = s;
-  }
-
-  // Insert key k at the MRU end, evicting the LRU non-pinned key when full
-  // (_evict_one, cache.py:93-100). Precondition: count < cap or count > npins.
-  __device__ __forceinline__ void insert(int k) {
-    int s;
-    if (count < cap) {
-      s = count++;
-      if (s == 0) {
-        nx[0] = pv[0] = 0;
-        head = 0;
-      } else {
-        nx[tail] = (IDX)s;
-        pv[s] = (IDX)tail;
-        nx[s] = (IDX)head;
-        pv[head] = (IDX)s;
-      }
-      tail = s;
-    } else {
-      s = head;
-      int vk = skey[s];
-      while (is_pinned(vk)) {  // rare: pins reach the LRU end (tiny caches)
-        s = nx[s];
-        vk = skey[s];
-      }
-      clear_resident(vk);
-      to_tail(s);
-    }
-    skey[s] = (uint16_t)k;
-    slot_of[k] = (IDX)s;
+    --count;
   }
 
   __device__ void begin_step(int l) {
@@ -216,14 +225,15 @@ struct LruState {
   __device__ __forceinline__ bool touch(int ex) {
     const int k = key_of(cur, ex);
     const uint64_t bit = 1ull << (ex & 63);
-    if (word_get<W>(Rl, ex >> 6) & bit) {
-      to_tail(slot_of[k]);
-      return true;
+    const bool hit = (word_get<W>(Rl, ex >> 6) & bit) != 0;
+    const bool reject = !hit && count >= cap && count <= npins;
+    if (!hit && !reject) {
+      if (count >= cap) evict();
+      word_or<W>(Rl, ex >> 6, bit);
+      ++count;
     }
-    if (count >= cap && count <= npins) return false;  // every resident key pinned
-    insert(k);
-    word_or<W>(Rl, ex >> 6, bit);
-    return false;
+    if (!reject) push(k);
+    return hit;
   }
 
   // one key of prefetch (cache.py:141-153); returns true if inserted.
@@ -231,20 +241,21 @@ struct LruState {
     const int k = key_of(cur, ex);
     const int w = ex >> 6;
     const uint64_t bit = 1ull << (ex & 63);
-    bool inserted = false;
-    if (word_get<W>(Rl, w) & bit) {
-      to_tail(slot_of[k]);  // refresh
-    } else {
-      if (count >= cap && count <= npins) return false;  // rejected, not pinned
-      insert(k);
+    const bool res = (word_get<W>(Rl, w) & bit) != 0;
+    const bool reject = !res && count >= cap && count <= npins;
+    if (!res && !reject) {
+      if (count >= cap) evict();
       word_or<W>(Rl, w, bit);
-      inserted = true;
+      ++count;
     }
-    if (!(word_get<W>(Pm, w) & bit)) {
-      word_or<W>(Pm, w, bit);
-      ++npins;
+    if (!reject) {
+      push(k);
+      if (!(word_get<W>(Pm, w) & bit)) {
+        word_or<W>(Pm, w, bit);
+        ++npins;
+      }
     }
-    return inserted;
+    return !res && !reject;
   }
 };
 
@@ -560,16 +571,20 @@ uint32_t layer_magic(int L, int E) {
 
 // Shared-memory layout of one simulation (LRU: slot map, masks, ring links,
 // slot keys; LFU: slot map, masks, slot values/keys).
-void layout(SimArgs& a, int policy, bool general, int idx_bytes) {
+void layout(SimArgs& a, int policy, bool general) {
   const int W = moeb::words_for(a.E);
   const int64_t NK = (int64_t)a.L * a.E;
   const int64_t rbytes = 8LL * a.L * W * (general ? 2 : 1);
   if (policy == MOEB_POLICY_LRU) {
-    a.off_r = align16(idx_bytes * NK);
+    uint32_t qn = 64;  // >= 2 * cap: compaction at most every cap pushes
+    while (qn < 2 * a.cap + 32) qn <<= 1;
+    a.qmask = qn - 1;
+    a.off_r = align16(2 * NK);  // pos_of
     a.off_q = align16(a.off_r + rbytes);
-    a.off_k = align16(a.off_q + 2LL * idx_bytes * a.cap);
-    a.sim_bytes = align16(a.off_k + 2LL * a.cap) + 16;  // +16 B skews smem banks
+    a.off_k = 0;
+    a.sim_bytes = align16(a.off_q + 2LL * qn) + 16;  // +16 B skews smem banks
   } else {
+    a.qmask = 0;
     a.off_r = align16(2 * NK);  // slot_of
     a.off_q = align16(a.off_r + rbytes);  // vals [cap] u64, skeys [cap] u16
     a.off_k = 0;
@@ -587,11 +602,10 @@ int launch_kernel(K k, const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
 }
 
 // LRU instance: E = 64 / 256 get shift-based key math, others the generic
-// multiply; uint8_t ring links when the capacity allows.
+// multiply.
 template <int W, int ES>
 int launch_lru(const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
-  if (a.cap < 255) return launch_kernel(k_cache_sim<W, LruState<W, ES, uint8_t, false>>, a, tpb, smem, s);
-  return launch_kernel(k_cache_sim<W, LruState<W, ES, uint16_t, false>>, a, tpb, smem, s);
+  return launch_kernel(k_cache_sim<W, LruState<W, ES, false>>, a, tpb, smem, s);
 }
 
 template <int W>
@@ -665,7 +679,7 @@ extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* pred
     a.per_prompt_stride = (int64_t)n_caps * n_prompts * 4;
     a.hits = hit_masks ? hit_masks + (int64_t)c * rows * W : nullptr;
     a.hits_stride = (int64_t)n_caps * rows * W;
-    layout(a, policy, false, a.cap < 255 ? 1 : 2);
+    layout(a, policy, false);
     int rc = W == 1 ? launch_sim<1>(a, policy, s)
              : W == 2 ? launch_sim<2>(a, policy, s)
              : W == 3 ? launch_sim<3>(a, policy, s)
@@ -678,12 +692,12 @@ extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* pred
 template <int W>
 static int launch_ops(SimArgs& a, int policy, const int32_t* ops, const int32_t* keys, int64_t n,
                       uint8_t* results, cudaStream_t s) {
-  layout(a, policy, true, 2);
+  layout(a, policy, true);
   const size_t smem = a.sim_bytes;
   if ((int)smem > moeb::max_smem_per_block())
     return moeb::fail(MOEB_ESMEM, "cache state %zu B exceeds shared memory", smem);
   if (policy == MOEB_POLICY_LRU) {
-    auto k = k_cache_ops<W, LruState<W, -1, uint16_t, true>>;
+    auto k = k_cache_ops<W, LruState<W, -1, true>>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<1, 32, smem, s>>>(a, ops, keys, n, results);
   } else {
