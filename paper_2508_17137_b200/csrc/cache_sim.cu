@@ -156,7 +156,7 @@ struct LruState {
     hv = head != tail && pos_of[hk] == (uint16_t)head;
   }
 
-  __device__ __noinline__ void compact() {
+  __device__ __forceinline__ void compact() {
     uint32_t n = head;
     for (uint32_t i = head; i != tail; ++i) {
       const int k = q[i & qmask];
@@ -169,46 +169,85 @@ struct LruState {
     tail = n;
   }
 
-  // Append key k at the MRU end (move_to_end / insert).
-  __device__ __forceinline__ void push(int k) {
-    if (__any_sync(__activemask(), tail - head > qmask)) {
-      if (tail - head > qmask) compact();
-      load_head();
-    }
-    q[tail & qmask] = (uint16_t)k;
-    pos_of[k] = (uint16_t)tail;
-    hv = hv && hk != k;  // the head entry of k just went stale
-    ++tail;
-  }
-
-  // Remove the LRU non-pinned key. Precondition: count > npins.
-  __device__ __forceinline__ void evict() {
-    // pop stale entries
-    while (!hv) {
-      ++head;
-      load_head();
-    }
-    int v = hk;
-    if (is_pinned(v)) {  // rare: pins reach the LRU end (tiny caches)
-      uint32_t i = head + 1;
-      for (;; ++i) {
-        const int k = q[i & qmask];
-        if (pos_of[k] == (uint16_t)i && !is_pinned(k)) break;
-      }
-      v = q[i & qmask];
-      pos_of[v] = (uint16_t)(i + 0x8000u);  // invalidate in place
-    } else {
-      pos_of[v] = (uint16_t)(head + 0x8000u);
-      ++head;
-      load_head();
-    }
+  __device__ __forceinline__ void clear_resident(int v) {
     const int l = layer_of(v), ex = expert_of(v, l);
     const uint64_t bit = 1ull << (ex & 63);
     if (l == cur)
       word_clear<W>(Rl, ex >> 6, bit);
     else
       R[l * W + (ex >> 6)] &= ~bit;
-    --count;
+  }
+
+  // One access of expert ex of the current layer: touch (cache.py:106-124)
+  // or, with pin, one key of prefetch (cache.py:141-153). Returns whether
+  // the key was resident. Straight-line except the stale-entry pops and the
+  // warp-uniform rare paths.
+  __device__ __forceinline__ bool access(int ex, bool pin, bool active) {
+    const unsigned am = __activemask();
+    const int k = key_of(cur, ex);
+    const int w = ex >> 6;
+    const uint64_t bit = 1ull << (ex & 63);
+    const bool hit = (word_get<W>(Rl, w) & bit) != 0;
+    const bool full = count >= cap;
+    const bool reject = !active || (!hit && full && count <= npins);
+    const bool ev = !hit && full && !reject;
+    if (__any_sync(am, ev)) {
+      if (ev) {
+        while (!hv) {  // pop stale entries
+          ++head;
+          load_head();
+        }
+      }
+      // `_evict_one` (cache.py:93-100) skips pinned keys in place; pins only
+      // reach the LRU end in tiny caches.
+      if (__any_sync(am, ev && is_pinned(hk))) {
+        if (ev && is_pinned(hk)) {
+          uint32_t i = head + 1;
+          int v = q[i & qmask];
+          while (pos_of[v] != (uint16_t)i || is_pinned(v)) {
+            ++i;
+            v = q[i & qmask];
+          }
+          pos_of[v] = (uint16_t)(i + 0x8000u);  // invalidate in place
+          clear_resident(v);
+          hv = true;  // head entry unchanged and still valid
+        } else if (ev) {
+          pos_of[hk] = (uint16_t)(head + 0x8000u);
+          clear_resident(hk);
+          ++head;
+          hv = false;
+        }
+      } else if (ev) {
+        pos_of[hk] = (uint16_t)(head + 0x8000u);
+        clear_resident(hk);
+        ++head;
+        hv = false;  // reloaded after the push below
+      }
+    }
+    const bool ins = !hit && !reject;
+    if (ins) {
+      word_or<W>(Rl, w, bit);
+      count += full ? 0 : 1;
+    }
+    // append at the MRU end
+    if (__any_sync(am, !reject && tail - head > qmask)) {
+      if (!reject && tail - head > qmask) {
+        compact();
+        load_head();
+      }
+    }
+    if (!reject) {
+      q[tail & qmask] = (uint16_t)k;
+      pos_of[k] = (uint16_t)tail;
+      hv = hv && hk != k;  // k's old entry (if at the head) just went stale
+      ++tail;
+    }
+    if (ev && !hv) load_head();
+    if (pin && !reject && !(word_get<W>(Pm, w) & bit)) {
+      word_or<W>(Pm, w, bit);
+      ++npins;
+    }
+    return hit;
   }
 
   __device__ void begin_step(int l) {
@@ -221,41 +260,11 @@ struct LruState {
     focus(l);
   }
 
-  // touch (cache.py:106-124) of expert ex of the current layer.
-  __device__ __forceinline__ bool touch(int ex) {
-    const int k = key_of(cur, ex);
-    const uint64_t bit = 1ull << (ex & 63);
-    const bool hit = (word_get<W>(Rl, ex >> 6) & bit) != 0;
-    const bool reject = !hit && count >= cap && count <= npins;
-    if (!hit && !reject) {
-      if (count >= cap) evict();
-      word_or<W>(Rl, ex >> 6, bit);
-      ++count;
-    }
-    if (!reject) push(k);
-    return hit;
-  }
-
-  // one key of prefetch (cache.py:141-153); returns true if inserted.
+  __device__ __forceinline__ bool touch(int ex) { return access(ex, false, true); }
   __device__ __forceinline__ bool prefetch(int ex) {
-    const int k = key_of(cur, ex);
-    const int w = ex >> 6;
-    const uint64_t bit = 1ull << (ex & 63);
-    const bool res = (word_get<W>(Rl, w) & bit) != 0;
-    const bool reject = !res && count >= cap && count <= npins;
-    if (!res && !reject) {
-      if (count >= cap) evict();
-      word_or<W>(Rl, w, bit);
-      ++count;
-    }
-    if (!reject) {
-      push(k);
-      if (!(word_get<W>(Pm, w) & bit)) {
-        word_or<W>(Pm, w, bit);
-        ++npins;
-      }
-    }
-    return !res && !reject;
+    const bool was = (word_get<W>(Rl, ex >> 6) & (1ull << (ex & 63))) != 0;
+    access(ex, true, true);
+    return !was && (word_get<W>(Rl, ex >> 6) & (1ull << (ex & 63))) != 0;
   }
 };
 
@@ -365,6 +374,16 @@ struct LfuState {
     return false;
   }
 
+  __device__ __forceinline__ bool access(int ex, bool pin, bool active) {
+    if (!active) return false;
+    const bool was = (word_get<W>(Rl, ex >> 6) & (1ull << (ex & 63))) != 0;
+    if (pin) {
+      prefetch(ex);
+      return was;
+    }
+    return touch(ex);
+  }
+
   __device__ __forceinline__ bool prefetch(int ex) {
     const int w = ex >> 6;
     const uint64_t bit = 1ull << (ex & 63);
@@ -461,44 +480,68 @@ __global__ void __launch_bounds__(32) k_cache_sim(const SimArgs a) {
         tbuf[d][w] = j < nrows ? __ldg(tr + j * W + w) : 0ull;
         pbuf[d][w] = (pr && j < nrows) ? __ldg(pr + j * W + w) : 0ull;
       }
-      if (t < a.warmup) {  // engine.py:160-167: warm the cache, no counters
-        if (valid) {
-          st.focus(l);
-          MOEB_FOR_EACH_BIT(W, tw, ex, {
-            if (st.touch(ex)) word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
-          })
-        }
-      } else {
-        int k = 0, ph = 0, ch = 0;
-        if (valid) {
-          st.begin_step(l);  // engine.py:172
-          int taken = 0;     // prefetch(sorted(pred)[:limit]) (engine.py:173-174)
+      // One flat op stream per row: prefetch(sorted(pred)[:limit]) then touch
+      // every truth expert ascending (engine.py:160-184). Warm-up rows only
+      // touch (no begin_step, no counters).
+      const bool measured = t >= a.warmup;
+      uint64_t mk[W], mt[W];
 #pragma unroll
-          for (int w = 0; w < W; ++w) {
-            uint64_t m = pw[w];
-            while (m && taken < limit) {
-              const int ex = w * 64 + __ffsll((long long)m) - 1;
-              m &= m - 1;
-              st.prefetch(ex);
-              ++taken;
-            }
-          }
-          if (cov && !cov[r0 + i]) ++tot_unc;  // engine.py:175-176
+      for (int w = 0; w < W; ++w) {
+        mk[w] = (valid && measured) ? pw[w] : 0ull;
+        mt[w] = valid ? tw[w] : 0ull;
+      }
+      if (valid && measured) st.begin_step(l);  // engine.py:172
+      else if (valid) st.focus(l);
+      int k = 0, ph = 0, ch = 0, taken = 0;
+      if (valid && measured) {
 #pragma unroll
-          for (int w = 0; w < W; ++w) {
-            k += __popcll(tw[w]);
-            ph += __popcll(tw[w] & pw[w]);  // FULL predicted set (engine.py:181-182)
-          }
-          MOEB_FOR_EACH_BIT(W, tw, ex, {
-            if (st.touch(ex)) {
-              ++ch;
-              word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
-            }
-          })
-          tot_k += k;
-          tot_ch += ch;
-          tot_ph += ph;
+        for (int w = 0; w < W; ++w) {
+          k += __popcll(tw[w]);
+          ph += __popcll(tw[w] & pw[w]);  // FULL predicted set (engine.py:181-182)
         }
+        if (cov && !cov[r0 + i]) ++tot_unc;  // engine.py:175-176
+      }
+      if (limit <= 0) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) mk[w] = 0;
+      }
+      for (;;) {
+        bool any_k = false, any_t = false;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          any_k |= mk[w] != 0;
+          any_t |= mt[w] != 0;
+        }
+        const bool act = any_k || any_t;
+        if (!__any_sync(full, act)) break;
+        const bool pf = any_k;
+        int ex = 0;
+        bool found = false;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const uint64_t m = pf ? mk[w] : mt[w];
+          if (!found && m) {
+            ex = w * 64 + __ffsll((long long)m) - 1;
+            found = true;
+            if (pf) mk[w] = m & (m - 1); else mt[w] = m & (m - 1);
+          }
+        }
+        const bool hit = st.access(ex, pf, act);
+        if (act && !pf && hit) {
+          ++ch;
+          word_or<W>(hw, ex >> 6, 1ull << (ex & 63));
+        }
+        if (act && pf && ++taken >= limit) {
+#pragma unroll
+          for (int w = 0; w < W; ++w) mk[w] = 0;
+        }
+      }
+      if (measured) {
+        if (!valid) ch = 0;
+        if (!measured) ch = 0;
+        tot_k += k;
+        tot_ch += ch;
+        tot_ph += ph;
         const unsigned sk = __reduce_add_sync(full, (unsigned)k);
         const unsigned sc = __reduce_add_sync(full, (unsigned)ch);
         const unsigned sp = __reduce_add_sync(full, (unsigned)ph);
