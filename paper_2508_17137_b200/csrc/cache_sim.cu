@@ -636,6 +636,328 @@ void layout(SimArgs& a, int policy, bool general) {
   a.magic = layer_magic(a.L, a.E);
 }
 
+// ---------------------------------------------------------------------------
+// K1 LRU, warp-per-simulation, row-batched. One warp owns one (stream,
+// prompt) simulation and resolves a whole trace row at once:
+//   accesses A = [K = sorted(pred)[:limit]] ++ [T = truth], all in layer l;
+//   with R_l the layer's resident mask at row start and no interplay,
+//     touch hits   = T & (R_l | K)
+//     inserts m    = |K \ R_l| + |T \ (R_l | K)|
+//     evictions e  = max(0, count + m - cap), the first e VALID queue entries
+//   (found with one 32-wide ballot per queue chunk), and the row's keys are
+//   appended in access order ((K \ T) ascending, then T ascending -- the
+//   order the reference's OrderedDict ends in; the superseded first push of
+//   a K&T key is stale anyway). "Interplay" -- a victim that the same row
+//   accesses, or a cache so small that pins/rejections can matter -- makes
+//   that warp replay the row with the exact sequential state machine
+//   (LruState::access), executed by all lanes in lockstep.
+// Trace rows are read as coalesced 32-row windows (one row per lane,
+// double-buffered) and broadcast with shuffles.
+// ---------------------------------------------------------------------------
+template <int W>
+__device__ __forceinline__ void keep_lowest(uint64_t (&m)[W], int n) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    int c = __popcll(m[w]);
+    if (n <= 0) {
+      m[w] = 0;
+    } else if (c > n) {
+      uint64_t x = m[w], keep = 0;
+      for (int i = 0; i < n; ++i) {
+        keep |= x & (~x + 1);
+        x &= x - 1;
+      }
+      m[w] = keep;
+      c = n;
+    }
+    n -= c;
+  }
+}
+
+template <int W>
+__device__ __forceinline__ int popc_w(const uint64_t (&m)[W]) {
+  int c = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) c += __popcll(m[w]);
+  return c;
+}
+
+// number of set bits of m below expert e
+template <int W>
+__device__ __forceinline__ int rank_below(const uint64_t (&m)[W], int e) {
+  int c = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const int lo = w * 64;
+    if (e >= lo + 64)
+      c += __popcll(m[w]);
+    else if (e > lo)
+      c += __popcll(m[w] & ((1ull << (e - lo)) - 1));
+  }
+  return c;
+}
+
+template <int W, int ES>
+__global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int L = a.L, E = a.E;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned int* bcnt = reinterpret_cast<unsigned int*>(smem);  // [3L] block counters
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x) bcnt[j] = 0;
+  __syncthreads();
+  const int pi = blockIdx.y;
+  const int p = blockIdx.x * nw + wib;
+  const unsigned full = 0xffffffffu;
+  if (p < a.P) {
+    unsigned char* base = smem + a.off_c + (size_t)wib * a.sim_bytes;
+    LruState<W, ES, false> st;
+    st.init(base, a, L);  // every lane holds the same (warp-uniform) state
+    uint16_t* pos_of = st.pos_of;
+    uint16_t* q = st.q;
+    uint64_t* R = st.R;
+    const uint32_t qmask = st.qmask;
+    const uint64_t* __restrict__ pred = a.preds[pi];
+    const uint8_t* __restrict__ cov = a.covered[pi];
+    const bool unbounded = (a.unbounded_bits >> pi) & 1u;
+    const int limit = unbounded ? E : a.budget;
+    uint64_t* hits = a.hits ? a.hits + pi * a.hits_stride : nullptr;
+    const int64_t r0 = a.row_off[p];
+    const int64_t nrows = a.row_off[p + 1] - r0;
+    const uint64_t* __restrict__ tr = a.truth + r0 * W;
+    const uint64_t* __restrict__ pr = pred ? pred + r0 * W : nullptr;
+    int64_t tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
+
+    uint64_t wt[W], wp[W], nt[W], np[W];  // current / next 32-row windows
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      wt[w] = lane < nrows ? __ldg(tr + (int64_t)lane * W + w) : 0ull;
+      wp[w] = (pr && lane < nrows) ? __ldg(pr + (int64_t)lane * W + w) : 0ull;
+    }
+    int l = 0, t = 0;
+    for (int64_t i = 0; i < nrows; ++i) {
+      const int slot = (int)(i & 31);
+      if (slot == 0) {  // prefetch the next window
+        const int64_t j = i + 32 + lane;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          nt[w] = j < nrows ? __ldg(tr + j * W + w) : 0ull;
+          np[w] = (pr && j < nrows) ? __ldg(pr + j * W + w) : 0ull;
+        }
+      }
+      uint64_t T[W], P[W], K[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        T[w] = __shfl_sync(full, wt[w], slot);
+        P[w] = __shfl_sync(full, wp[w], slot);
+      }
+      if (slot == 31) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          wt[w] = nt[w];
+          wp[w] = np[w];
+        }
+      }
+      const bool measured = t >= a.warmup;
+#pragma unroll
+      for (int w = 0; w < W; ++w) K[w] = measured ? P[w] : 0ull;
+      keep_lowest<W>(K, limit);
+      uint64_t Rl[W], S[W], Hm[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        Rl[w] = R[l * W + w];
+        S[w] = K[w] | T[w];
+      }
+      int m = 0, refresh = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        m += __popcll(K[w] & ~Rl[w]) + __popcll(T[w] & ~(Rl[w] | K[w]));
+        refresh += __popcll(S[w] & Rl[w]);
+        Hm[w] = T[w] & (Rl[w] | K[w]);
+      }
+      const int e = st.count + m - st.cap > 0 ? st.count + m - st.cap : 0;
+      bool fallback = (st.cap <= popc_w<W>(K)) || (e > st.count - refresh);
+      uint32_t newhead = st.head;
+      if (!fallback && e > 0) {  // scan: find the e-th valid entry, check interplay
+        int found = 0;
+        uint32_t pos = st.head;
+        while (found < e) {
+          const uint32_t idx = pos + lane;
+          const bool inr = idx - st.head < st.tail - st.head;
+          const int key = q[idx & qmask];
+          const bool valid = inr && pos_of[key] == (uint16_t)idx;
+          const unsigned vb = __ballot_sync(full, valid);
+          const int need = e - found;
+          const int rank = __popc(vb & ((1u << lane) - 1));
+          const bool victim = valid && rank < need;
+          bool bad = false;
+          if (victim) {
+            const int vl = st.layer_of(key), ve = st.expert_of(key, vl);
+            bad = vl == l && ((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull);
+          }
+          if (__any_sync(full, bad)) {
+            fallback = true;
+            break;
+          }
+          const int nv = __popc(vb);
+          if (nv >= need) {
+            const int last = __fns(vb, 0, need);  // lane of the e-th victim
+            newhead = pos + last + 1;
+            found = e;
+          } else {
+            found += nv;
+            pos += 32;
+          }
+        }
+      }
+      int ch;
+      if (!fallback) {
+        // evict: every valid entry in [head, newhead) is a victim
+        for (uint32_t pos = st.head; pos != newhead; pos += 32) {
+          const uint32_t idx = pos + lane;
+          if (idx - pos < newhead - pos) {
+            const int key = q[idx & qmask];
+            if (pos_of[key] == (uint16_t)idx) {
+              pos_of[key] = (uint16_t)(idx + 0x8000u);
+              const int vl = st.layer_of(key), ve = st.expert_of(key, vl);
+              atomicAnd(reinterpret_cast<unsigned long long*>(R + vl * W + (ve >> 6)),
+                        ~(1ull << (ve & 63)));
+            }
+          }
+          if (newhead - pos <= 32) break;
+        }
+        st.head = newhead;
+        st.count += m - e;
+        const int ns = popc_w<W>(S);
+        if (st.tail - st.head + (uint32_t)ns > qmask + 1) {  // warp compaction
+          __syncwarp();
+          uint32_t n = st.head;
+          for (uint32_t pos = st.head; pos != st.tail; pos += 32) {
+            const uint32_t idx = pos + lane;
+            const bool inr = idx - pos < st.tail - pos;
+            const int key = q[idx & qmask];
+            const bool valid = inr && pos_of[key] == (uint16_t)idx;
+            const unsigned vb = __ballot_sync(full, valid);
+            __syncwarp();
+            if (valid) {
+              const uint32_t dst = n + __popc(vb & ((1u << lane) - 1));
+              q[dst & qmask] = (uint16_t)key;
+              pos_of[key] = (uint16_t)dst;
+            }
+            __syncwarp();
+            n += __popc(vb);
+            if (st.tail - pos <= 32) break;
+          }
+          st.tail = n;
+        }
+        // append the row's keys: (K \ T) ascending, then T ascending
+        uint64_t A[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) A[w] = K[w] & ~T[w];
+        const int na = popc_w<W>(A);
+#pragma unroll
+        for (int j = 0; j < 2 * W; ++j) {
+          const int ex = lane + 32 * j;
+          if (ex < E) {
+            const uint64_t bit = 1ull << (ex & 63);
+            int slot2 = -1;
+            if (word_get<W>(A, ex >> 6) & bit) slot2 = rank_below<W>(A, ex);
+            else if (word_get<W>(T, ex >> 6) & bit) slot2 = na + rank_below<W>(T, ex);
+            if (slot2 >= 0) {
+              const uint32_t dst = st.tail + (uint32_t)slot2;
+              const int key = st.key_of(l, ex);
+              q[dst & qmask] = (uint16_t)key;
+              pos_of[key] = (uint16_t)dst;
+            }
+          }
+        }
+        st.tail += ns;
+        __syncwarp();
+        if (lane < W) {
+          uint64_t v = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (w == lane) v = R[l * W + w] | S[w];
+          R[l * W + lane] = v;
+        }
+        __syncwarp();
+        ch = popc_w<W>(Hm);
+      } else {
+        // exact sequential replay of this row (all lanes in lockstep)
+        st.cur = l;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          st.Rl[w] = R[l * W + w];
+          st.Pm[w] = 0;
+          Hm[w] = 0;
+        }
+        st.npins = 0;
+        st.load_head();
+        MOEB_FOR_EACH_BIT(W, K, ex, { st.access(ex, true, true); })
+        ch = 0;
+        MOEB_FOR_EACH_BIT(W, T, ex, {
+          if (st.access(ex, false, true)) {
+            ++ch;
+            word_or<W>(Hm, ex >> 6, 1ull << (ex & 63));
+          }
+        })
+        __syncwarp();
+        if (lane < W) {
+          uint64_t v = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (w == lane) v = st.Rl[w];
+          R[l * W + lane] = v;
+        }
+        __syncwarp();
+      }
+      if (hits && lane < W) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          if (w == lane) v = Hm[w];
+        hits[(r0 + i) * W + lane] = v;
+      }
+      if (measured) {
+        const int k = popc_w<W>(T);
+        int ph = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) ph += __popcll(T[w] & P[w]);  // FULL predicted set
+        if (cov && cov[r0 + i] == 0) ++tot_unc;                  // engine.py:175-176
+        tot_k += k;
+        tot_ch += ch;
+        tot_ph += ph;
+        if (lane == 0) {
+          atomicAdd(&bcnt[l], (unsigned)k);
+          atomicAdd(&bcnt[L + l], (unsigned)ch);
+          atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
+        }
+      }
+      if (++l == L) {
+        l = 0;
+        ++t;
+      }
+    }
+    int64_t* c = a.counters + pi * a.counters_stride;
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(c + 0), (unsigned long long)tot_k);
+      atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot_ch);
+      atomicAdd(reinterpret_cast<unsigned long long*>(c + 2), (unsigned long long)tot_ph);
+      if (tot_unc) atomicAdd(reinterpret_cast<unsigned long long*>(c + 3), (unsigned long long)tot_unc);
+      if (a.per_prompt) {
+        int64_t* pp = a.per_prompt + pi * a.per_prompt_stride + 4 * (int64_t)p;
+        pp[0] += tot_k;
+        pp[1] += tot_ch;
+        pp[2] += tot_ph;
+        pp[3] += tot_unc;
+      }
+    }
+  }
+  __syncthreads();
+  int64_t* c = a.counters + pi * a.counters_stride;
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x)
+    if (bcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bcnt[j]);
+}
+
 template <class K>
 int launch_kernel(K k, const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -644,11 +966,23 @@ int launch_kernel(K k, const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
   return moeb::check_launch("k_cache_sim");
 }
 
-// LRU instance: E = 64 / 256 get shift-based key math, others the generic
-// multiply.
+// LRU: warp-per-simulation kernel; E = 64 / 256 get shift-based key math.
 template <int W, int ES>
-int launch_lru(const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
-  return launch_kernel(k_cache_sim<W, LruState<W, ES, false>>, a, tpb, smem, s);
+int launch_lru(SimArgs a, cudaStream_t s) {
+  const int max_block = moeb::max_smem_per_block();
+  const int head = align16(4LL * 3 * a.L);
+  a.off_c = head;
+  int nw = 4;  // simulations (warps) per block
+  while (nw > 1 && head + (int64_t)nw * a.sim_bytes > max_block) --nw;
+  if (head + (int64_t)nw * a.sim_bytes > max_block)
+    return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
+                      a.sim_bytes, max_block);
+  const size_t smem = head + (size_t)nw * a.sim_bytes;
+  auto k = k_cache_sim_warp<W, ES>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const dim3 blocks((unsigned)((a.P + nw - 1) / nw), (unsigned)a.n_preds);
+  k<<<blocks, 32 * nw, smem, s>>>(a);
+  return moeb::check_launch("k_cache_sim_warp");
 }
 
 template <int W>
@@ -666,9 +1000,9 @@ int launch_sim(SimArgs a, int policy, cudaStream_t s) {
   const size_t smem = head + (size_t)tpb * a.sim_bytes;
   if (policy == MOEB_POLICY_LFU)
     return launch_kernel(k_cache_sim<W, LfuState<W, false>>, a, tpb, smem, s);
-  if (W == 1 && a.E == 64) return launch_lru<1, 6>(a, tpb, smem, s);
-  if (W == 4 && a.E == 256) return launch_lru<4, 8>(a, tpb, smem, s);
-  return launch_lru<W, -1>(a, tpb, smem, s);
+  if (W == 1 && a.E == 64) return launch_lru<1, 6>(a, s);
+  if (W == 4 && a.E == 256) return launch_lru<4, 8>(a, s);
+  return launch_lru<W, -1>(a, s);
 }
 
 }  // namespace
