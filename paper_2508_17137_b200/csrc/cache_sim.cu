@@ -30,6 +30,19 @@ namespace {
 
 constexpr uint64_t kPin = 1ull << 63;
 
+// The sequential state machines are __host__ __device__ so that
+// tests/native/lru_host_test.cu can run them on the CPU against the oracle.
+#define MOEB_HD __host__ __device__
+#ifdef __CUDA_ARCH__
+#define MOEB_ANY(x) __any_sync(__activemask(), (x))
+__device__ __forceinline__ int moeb_ffs64(uint64_t x) { return __ffsll((long long)x); }
+__device__ __forceinline__ int moeb_popc64(uint64_t x) { return __popcll(x); }
+#else
+#define MOEB_ANY(x) (x)
+inline int moeb_ffs64(uint64_t x) { return __builtin_ffsll((long long)x); }
+inline int moeb_popc64(uint64_t x) { return __builtin_popcountll(x); }
+#endif
+
 struct SimArgs {
   const uint64_t* truth;
   const uint64_t* preds[MOEB_MAX_PREDS];
@@ -53,20 +66,20 @@ struct SimArgs {
 };
 
 template <int W>
-__device__ __forceinline__ uint64_t word_get(const uint64_t (&a)[W], int w) {
+MOEB_HD __forceinline__ uint64_t word_get(const uint64_t (&a)[W], int w) {
   uint64_t v = a[0];
 #pragma unroll
   for (int j = 1; j < W; ++j) v = (w == j) ? a[j] : v;
   return v;
 }
 template <int W>
-__device__ __forceinline__ void word_or(uint64_t (&a)[W], int w, uint64_t bit) {
+MOEB_HD __forceinline__ void word_or(uint64_t (&a)[W], int w, uint64_t bit) {
 #pragma unroll
   for (int j = 0; j < W; ++j)
     if (w == j) a[j] |= bit;
 }
 template <int W>
-__device__ __forceinline__ void word_clear(uint64_t (&a)[W], int w, uint64_t bit) {
+MOEB_HD __forceinline__ void word_clear(uint64_t (&a)[W], int w, uint64_t bit) {
 #pragma unroll
   for (int j = 0; j < W; ++j)
     if (w == j) a[j] &= ~bit;
@@ -98,7 +111,7 @@ struct LruState {
   bool hv;   // entry at head is valid (pre-loaded)
   uint64_t Rl[W], Pm[W];
 
-  __device__ void init(unsigned char* base, const SimArgs& a, int L_) {
+  MOEB_HD void init(unsigned char* base, const SimArgs& a, int L_) {
     L = L_;
     E = a.E;
     cap = (int)a.cap;
@@ -119,17 +132,17 @@ struct LruState {
     for (int j = 0; j < L * W * (GENERAL ? 2 : 1); ++j) R[j] = 0;
   }
 
-  __device__ __forceinline__ int layer_of(int k) const {
+  MOEB_HD __forceinline__ int layer_of(int k) const {
     return ES >= 0 ? (k >> ES) : (int)(((uint32_t)k * mE) >> 22);
   }
-  __device__ __forceinline__ int expert_of(int k, int l) const {
+  MOEB_HD __forceinline__ int expert_of(int k, int l) const {
     return ES >= 0 ? (k & ((1 << (ES >= 0 ? ES : 0)) - 1)) : k - l * E;
   }
-  __device__ __forceinline__ int key_of(int l, int ex) const {
+  MOEB_HD __forceinline__ int key_of(int l, int ex) const {
     return ES >= 0 ? ((l << ES) | ex) : l * E + ex;
   }
 
-  __device__ __forceinline__ void focus(int l) {
+  MOEB_HD __forceinline__ void focus(int l) {
     if (l == cur) return;
 #pragma unroll
     for (int j = 0; j < W; ++j) {
@@ -143,7 +156,7 @@ struct LruState {
     cur = l;
   }
 
-  __device__ __forceinline__ bool is_pinned(int k) const {
+  MOEB_HD __forceinline__ bool is_pinned(int k) const {
     const int l = layer_of(k), ex = expert_of(k, l);
     const uint64_t bit = 1ull << (ex & 63);
     if (l == cur) return (word_get<W>(Pm, ex >> 6) & bit) != 0;
@@ -151,12 +164,12 @@ struct LruState {
     return false;  // trace mode: pins only ever exist in the current layer
   }
 
-  __device__ __forceinline__ void load_head() {
+  MOEB_HD __forceinline__ void load_head() {
     hk = q[head & qmask];
     hv = head != tail && pos_of[hk] == (uint16_t)head;
   }
 
-  __device__ __forceinline__ void compact() {
+  MOEB_HD __forceinline__ void compact() {
     uint32_t n = head;
     for (uint32_t i = head; i != tail; ++i) {
       const int k = q[i & qmask];
@@ -169,7 +182,7 @@ struct LruState {
     tail = n;
   }
 
-  __device__ __forceinline__ void clear_resident(int v) {
+  MOEB_HD __forceinline__ void clear_resident(int v) {
     const int l = layer_of(v), ex = expert_of(v, l);
     const uint64_t bit = 1ull << (ex & 63);
     if (l == cur)
@@ -182,8 +195,7 @@ struct LruState {
   // or, with pin, one key of prefetch (cache.py:141-153). Returns whether
   // the key was resident. Straight-line except the stale-entry pops and the
   // warp-uniform rare paths.
-  __device__ __forceinline__ bool access(int ex, bool pin, bool active) {
-    const unsigned am = __activemask();
+  MOEB_HD __forceinline__ bool access(int ex, bool pin, bool active) {
     const int k = key_of(cur, ex);
     const int w = ex >> 6;
     const uint64_t bit = 1ull << (ex & 63);
@@ -191,16 +203,16 @@ struct LruState {
     const bool full = count >= cap;
     const bool reject = !active || (!hit && full && count <= npins);
     const bool ev = !hit && full && !reject;
-    if (__any_sync(am, ev)) {
+    if (MOEB_ANY(ev)) {
       if (ev) {
-        while (!hv) {  // pop stale entries
+        while (!hv && head != tail) {  // pop stale entries (bounded by the live window)
           ++head;
           load_head();
         }
       }
       // `_evict_one` (cache.py:93-100) skips pinned keys in place; pins only
       // reach the LRU end in tiny caches.
-      if (__any_sync(am, ev && is_pinned(hk))) {
+      if (MOEB_ANY(ev && is_pinned(hk))) {
         if (ev && is_pinned(hk)) {
           uint32_t i = head + 1;
           int v = q[i & qmask];
@@ -230,16 +242,18 @@ struct LruState {
       count += full ? 0 : 1;
     }
     // append at the MRU end
-    if (__any_sync(am, !reject && tail - head > qmask)) {
+    if (MOEB_ANY(!reject && tail - head > qmask)) {
       if (!reject && tail - head > qmask) {
         compact();
         load_head();
       }
     }
     if (!reject) {
+      const bool empty = tail == head;
       q[tail & qmask] = (uint16_t)k;
       pos_of[k] = (uint16_t)tail;
-      hv = hv && hk != k;  // k's old entry (if at the head) just went stale
+      hv = empty || (hv && hk != k);  // k's old entry (if at the head) just went stale
+      hk = empty ? k : hk;
       ++tail;
     }
     if (ev && !hv) load_head();
@@ -250,7 +264,7 @@ struct LruState {
     return hit;
   }
 
-  __device__ void begin_step(int l) {
+  MOEB_HD void begin_step(int l) {
     if (GENERAL) {
       for (int j = 0; j < L * W; ++j) Psm[j] = 0;
     }
@@ -260,8 +274,8 @@ struct LruState {
     focus(l);
   }
 
-  __device__ __forceinline__ bool touch(int ex) { return access(ex, false, true); }
-  __device__ __forceinline__ bool prefetch(int ex) {
+  MOEB_HD __forceinline__ bool touch(int ex) { return access(ex, false, true); }
+  MOEB_HD __forceinline__ bool prefetch(int ex) {
     const bool was = (word_get<W>(Rl, ex >> 6) & (1ull << (ex & 63))) != 0;
     access(ex, true, true);
     return !was && (word_get<W>(Rl, ex >> 6) & (1ull << (ex & 63))) != 0;
@@ -285,7 +299,7 @@ struct LfuState {
   int npins, E, L, cur;
   uint64_t Rl[W], Pm[W];
 
-  __device__ void init(unsigned char* base, const SimArgs& a, int L_) {
+  MOEB_HD void init(unsigned char* base, const SimArgs& a, int L_) {
     L = L_;
     E = a.E;
     cap = a.cap;
@@ -302,7 +316,7 @@ struct LfuState {
     for (int j = 0; j < L * W; ++j) R[j] = 0;
   }
 
-  __device__ __forceinline__ void focus(int l) {
+  MOEB_HD __forceinline__ void focus(int l) {
     if (l == cur) return;
 #pragma unroll
     for (int j = 0; j < W; ++j) {
@@ -311,12 +325,12 @@ struct LfuState {
     }
     cur = l;
   }
-  __device__ __forceinline__ void writeback() {
+  MOEB_HD __forceinline__ void writeback() {
 #pragma unroll
     for (int j = 0; j < W; ++j) R[cur * W + j] = Rl[j];
   }
 
-  __device__ int victim_slot() const {
+  MOEB_HD int victim_slot() const {
     uint64_t best = ~0ull;
     int bs = 0;
     for (int s = 0; s < (int)count; ++s) {
@@ -330,7 +344,7 @@ struct LfuState {
   }
 
   // Returns the slot to fill: a fresh one, or the evicted victim's.
-  __device__ int make_room() {
+  MOEB_HD int make_room() {
     if (count < cap) return (int)count++;
     const int s = victim_slot();
     const uint32_t vk = skeys[s];
@@ -343,11 +357,18 @@ struct LfuState {
     return s;
   }
 
-  __device__ void begin_step(int l) {
+  MOEB_HD void begin_step(int l) {
     if (GENERAL) {
       for (int s = 0; s < (int)count; ++s) vals[s] &= ~kPin;
     } else {
-      MOEB_FOR_EACH_BIT(W, Pm, ex, { vals[slot_of[cur * E + ex]] &= ~kPin; })
+      for (int w = 0; w < W; ++w) {
+        uint64_t m = Pm[w];
+        while (m) {
+          const int ex = w * 64 + moeb_ffs64(m) - 1;
+          m &= m - 1;
+          vals[slot_of[cur * E + ex]] &= ~kPin;
+        }
+      }
     }
 #pragma unroll
     for (int j = 0; j < W; ++j) Pm[j] = 0;
@@ -355,7 +376,7 @@ struct LfuState {
     focus(l);
   }
 
-  __device__ __forceinline__ bool touch(int ex) {
+  MOEB_HD __forceinline__ bool touch(int ex) {
     const uint64_t bit = 1ull << (ex & 63);
     const int key = cur * E + ex;
     if (word_get<W>(Rl, ex >> 6) & bit) {
@@ -374,7 +395,7 @@ struct LfuState {
     return false;
   }
 
-  __device__ __forceinline__ bool access(int ex, bool pin, bool active) {
+  MOEB_HD __forceinline__ bool access(int ex, bool pin, bool active) {
     if (!active) return false;
     const bool was = (word_get<W>(Rl, ex >> 6) & (1ull << (ex & 63))) != 0;
     if (pin) {
@@ -384,7 +405,7 @@ struct LfuState {
     return touch(ex);
   }
 
-  __device__ __forceinline__ bool prefetch(int ex) {
+  MOEB_HD __forceinline__ bool prefetch(int ex) {
     const int w = ex >> 6;
     const uint64_t bit = 1ull << (ex & 63);
     const int key = cur * E + ex;
@@ -777,10 +798,43 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       const int e = st.count + m - st.cap > 0 ? st.count + m - st.cap : 0;
       bool fallback = (st.cap <= popc_w<W>(K)) || (e > st.count - refresh);
       uint32_t newhead = st.head;
-      if (!fallback && e > 0) {  // scan: find the e-th valid entry, check interplay
+      bool applied = false;
+      if (!fallback && e > 0) {  // common case: every victim in the first chunk
+        const uint32_t idx = st.head + lane;
+        const bool inr = (uint32_t)lane < st.tail - st.head;
+        const int key = q[idx & qmask];
+        const bool valid = inr && pos_of[key] == (uint16_t)idx;
+        const unsigned vb = __ballot_sync(full, valid);
+        if (__popc(vb) >= e) {
+          const bool victim = valid && __popc(vb & ((1u << lane) - 1)) < e;
+          int vl = 0, ve = 0;
+          bool bad = false;
+          if (victim) {
+            vl = st.layer_of(key);
+            ve = st.expert_of(key, vl);
+            bad = vl == l && ((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull);
+          }
+          if (__any_sync(full, bad)) {
+            fallback = true;
+          } else {
+            if (victim) {
+              pos_of[key] = (uint16_t)(idx + 0x8000u);
+              atomicAnd(reinterpret_cast<unsigned int*>(R + vl * W + (ve >> 6)) + ((ve >> 5) & 1),
+                        ~(1u << (ve & 31)));
+            }
+            newhead = st.head + __fns(vb, 0, e) + 1;
+            applied = true;
+          }
+        }
+      }
+      if (!fallback && e > 0 && !applied) {  // scan: find the e-th valid entry, check interplay
         int found = 0;
         uint32_t pos = st.head;
         while (found < e) {
+          if (pos - st.head >= st.tail - st.head) {  // cannot happen; never spin
+            fallback = true;
+            break;
+          }
           const uint32_t idx = pos + lane;
           const bool inr = idx - st.head < st.tail - st.head;
           const int key = q[idx & qmask];
@@ -812,15 +866,15 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       int ch;
       if (!fallback) {
         // evict: every valid entry in [head, newhead) is a victim
-        for (uint32_t pos = st.head; pos != newhead; pos += 32) {
+        for (uint32_t pos = st.head; !applied && pos != newhead; pos += 32) {
           const uint32_t idx = pos + lane;
           if (idx - pos < newhead - pos) {
             const int key = q[idx & qmask];
             if (pos_of[key] == (uint16_t)idx) {
               pos_of[key] = (uint16_t)(idx + 0x8000u);
               const int vl = st.layer_of(key), ve = st.expert_of(key, vl);
-              atomicAnd(reinterpret_cast<unsigned long long*>(R + vl * W + (ve >> 6)),
-                        ~(1ull << (ve & 63)));
+              atomicAnd(reinterpret_cast<unsigned int*>(R + vl * W + (ve >> 6)) + ((ve >> 5) & 1),
+                        ~(1u << (ve & 31)));
             }
           }
           if (newhead - pos <= 32) break;

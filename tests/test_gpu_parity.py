@@ -11,7 +11,7 @@ import torch
 
 from conftest import CASES, load_case
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(180)]
 
 
 @pytest.fixture(scope="module")

@@ -4,7 +4,7 @@
 #   tools/profile.sh TAG [kernel-regex ...]
 TAG=${1:-run}; shift
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/tests_$TAG.log 2>&1; tail -3 gpurun_out/tests_$TAG.log
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/tests_$TAG.log 2>&1; tail -3 gpurun_out/tests_$TAG.log
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 cat gpurun_out/bench_$TAG.json; tail -3 gpurun_out/bench_$TAG.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
