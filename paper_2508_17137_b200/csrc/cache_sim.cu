@@ -746,7 +746,11 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     const int64_t nrows = a.row_off[p + 1] - r0;
     const uint64_t* __restrict__ tr = a.truth + r0 * W;
     const uint64_t* __restrict__ pr = pred ? pred + r0 * W : nullptr;
-    int64_t tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
+    int tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
+    constexpr int kLC = 2;  // per-layer counters for layers lane + 32*j (L <= 64; else smem)
+    unsigned lck[kLC], lcc[kLC], lcp[kLC];
+#pragma unroll
+    for (int j = 0; j < kLC; ++j) lck[j] = lcc[j] = lcp[j] = 0;
 
     uint64_t wt[W], wp[W], nt[W], np[W];  // current / next 32-row windows
 #pragma unroll
@@ -822,7 +826,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
               atomicAnd(reinterpret_cast<unsigned int*>(R + vl * W + (ve >> 6)) + ((ve >> 5) & 1),
                         ~(1u << (ve & 31)));
             }
-            newhead = st.head + __fns(vb, 0, e) + 1;
+            newhead = st.head + (32 - __clz(__ballot_sync(full, victim)));
             applied = true;
           }
         }
@@ -854,8 +858,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
           }
           const int nv = __popc(vb);
           if (nv >= need) {
-            const int last = __fns(vb, 0, need);  // lane of the e-th victim
-            newhead = pos + last + 1;
+            newhead = pos + (32 - __clz(__ballot_sync(full, victim)));  // after the e-th victim
             found = e;
           } else {
             found += nv;
@@ -908,6 +911,26 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
 #pragma unroll
         for (int w = 0; w < W; ++w) A[w] = K[w] & ~T[w];
         const int na = popc_w<W>(A);
+        if (W == 1) {
+          const uint32_t lt = (1u << lane) - 1;
+          const uint32_t alo = (uint32_t)A[0], ahi = (uint32_t)(A[0] >> 32);
+          const uint32_t tlo = (uint32_t)T[0], thi = (uint32_t)(T[0] >> 32);
+          const int ca = __popc(alo), ct = __popc(tlo);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int ex = lane + 32 * h;
+            const uint32_t am = h ? ahi : alo, tm = h ? thi : tlo;
+            const bool ina = (am >> lane) & 1u, int_ = (tm >> lane) & 1u;
+            const int ra = (h ? ca : 0) + __popc(am & lt);
+            const int rt = (h ? ct : 0) + __popc(tm & lt);
+            if (ex < E && (ina || int_)) {
+              const uint32_t dst = st.tail + (uint32_t)(ina ? ra : na + rt);
+              const int key = st.key_of(l, ex);
+              q[dst & qmask] = (uint16_t)key;
+              pos_of[key] = (uint16_t)dst;
+            }
+          }
+        } else
 #pragma unroll
         for (int j = 0; j < 2 * W; ++j) {
           const int ex = lane + 32 * j;
@@ -980,7 +1003,15 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         tot_k += k;
         tot_ch += ch;
         tot_ph += ph;
-        if (lane == 0) {
+        if (L <= 32 * kLC) {
+#pragma unroll
+          for (int j = 0; j < kLC; ++j)
+            if (l == lane + 32 * j) {
+              lck[j] += k;
+              lcc[j] += ch;
+              lcp[j] += ph;
+            }
+        } else if (lane == 0) {
           atomicAdd(&bcnt[l], (unsigned)k);
           atomicAdd(&bcnt[L + l], (unsigned)ch);
           atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
@@ -989,6 +1020,15 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       if (++l == L) {
         l = 0;
         ++t;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kLC; ++j) {
+      const int ll = lane + 32 * j;
+      if (ll < L) {
+        if (lck[j]) atomicAdd(&bcnt[ll], lck[j]);
+        if (lcc[j]) atomicAdd(&bcnt[L + ll], lcc[j]);
+        if (lcp[j]) atomicAdd(&bcnt[2 * L + ll], lcp[j]);
       }
     }
     int64_t* c = a.counters + pi * a.counters_stride;
