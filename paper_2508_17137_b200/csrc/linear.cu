@@ -15,13 +15,15 @@
 // random-init weights; fp64 keeps the selection identical to numpy's, and
 // the recurrence's rounding drift stays ~1e-15 relative, tests assert 1e-12).
 //
-// Mapping: one thread per (prompt, layer) stream; consecutive threads take
-// consecutive layers of the same prompt, so at every token a warp reads and
-// writes ~32 contiguous mask rows (coalesced). z[64] lives in registers; W_h columns and the
-// bias table live in shared memory (column-major, stride E+1 against bank
-// conflicts). Metrics: each warp turns its 32 rows of pred/truth masks into
-// per-expert TP/FP/FN counts with ballot+popc, then one shared-memory reduce
-// and one global atomic per counter per block.
+// Mapping: two threads per (prompt, layer) stream (adjacent lanes), each
+// owning 32 experts: z[32] fp64 in registers (~100 registers -> 20 warps/SM),
+// 16-byte column reads from shared memory. Top-k = k passes; in each pass
+// every thread finds the first maximum of its unchosen half and the pair
+// combines the two candidates with one shuffle (larger value, then lower id):
+// exactly lexsort's (-score, id) order. Consecutive streams are consecutive
+// layers of the same prompt, so mask rows are read/written contiguously.
+// Metrics: ballot+popc per expert over the warp's 16 rows, then one
+// shared-memory reduce and one global atomic per counter per block.
 #include "common.cuh"
 
 namespace {
@@ -40,137 +42,169 @@ struct LinArgs {
   int64_t* metrics;
 };
 
+constexpr int kES = 66;  // padded row stride (doubles), keeps rows 16-byte aligned
+
 __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = a.L, E = a.E, F = a.L + a.E + 1;
-  const int ES = E + 1;  // padded stride
-  double* colT = reinterpret_cast<double*>(smem_raw);  // [E][ES]: colT[e][j] = W[j][L+e]
-  double* bias = colT + E * ES;                        // [L][ES]: b_l[j]
-  double* bias2 = bias + L * ES;                       // [L][ES]: (1 - decay) b_l[j]
-  unsigned long long* mcnt = reinterpret_cast<unsigned long long*>(bias2 + L * ES);  // [3E+3]
-  for (int i = threadIdx.x; i < E * E; i += blockDim.x) {
-    const int e = i / E, j = i % E;
-    colT[e * ES + j] = a.Wt[(int64_t)j * F + L + e];
+  double* colT = reinterpret_cast<double*>(smem_raw);  // [E][kES]: colT[e][j] = W[j][L+e]
+  double* bias = colT + E * kES;                       // [L][kES]: b_l[j]
+  double* bias2 = bias + L * kES;                      // [L][kES]: (1 - decay) b_l[j]
+  unsigned long long* mcnt = reinterpret_cast<unsigned long long*>(bias2 + L * kES);  // [3E+3]
+  for (int i = threadIdx.x; i < E * 64; i += blockDim.x) {
+    const int e = i / 64, j = i % 64;
+    colT[e * kES + j] = j < E ? a.Wt[(int64_t)j * F + L + e] : 0.0;
   }
-  for (int i = threadIdx.x; i < L * E; i += blockDim.x) {
-    const int l = i / E, j = i % E;
-    const double b = a.Wt[(int64_t)j * F + l] + a.Wt[(int64_t)j * F + L + E];
-    bias[l * ES + j] = b;
-    bias2[l * ES + j] = (1.0 - a.decay) * b;
+  for (int i = threadIdx.x; i < L * 64; i += blockDim.x) {
+    const int l = i / 64, j = i % 64;
+    const double b = j < E ? a.Wt[(int64_t)j * F + l] + a.Wt[(int64_t)j * F + L + E] : 0.0;
+    bias[l * kES + j] = b;
+    bias2[l * kES + j] = (1.0 - a.decay) * b;
   }
   if (a.metrics)
     for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x) mcnt[i] = 0;
   __syncthreads();
 
+  const unsigned full = 0xffffffffu;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = g < (int64_t)a.L * a.P;
-  const int p = live ? (int)(g / L) : 0;
-  const int l = live ? (int)(g % L) : 0;
+  const int64_t sidx = g >> 1;  // stream
+  const int h = (int)(g & 1);   // which 32 experts
+  const int e0 = 32 * h;
+  const bool live = sidx < (int64_t)a.L * a.P;
+  const int p = live ? (int)(sidx / L) : 0;
+  const int l = live ? (int)(sidx % L) : 0;
   const int64_t r0 = live ? a.row_off[p] : 0;
   const int T = live ? (int)((a.row_off[p + 1] - r0) / L) : 0;
-  // warp-uniform trip count so ballots see every lane
-  int Tw = T;
+  int Tw = T;  // warp-uniform trip count so ballots/shuffles see every lane
 #pragma unroll
-  for (int o = 16; o; o >>= 1) Tw = max(Tw, __shfl_xor_sync(0xffffffffu, Tw, o));
+  for (int o = 16; o; o >>= 1) Tw = max(Tw, __shfl_xor_sync(full, Tw, o));
 
-  double z[64];
+  double z[32];
 #pragma unroll
-  for (int e = 0; e < 64; ++e) z[e] = e < E ? bias[l * ES + e] : 0.0;
+  for (int j = 0; j < 32; ++j) z[j] = bias[l * kES + e0 + j];
   const int lane = threadIdx.x & 31;
-  uint32_t tp_lo = 0, tp_hi = 0, fp_lo = 0, fp_hi = 0, fn_lo = 0, fn_hi = 0;
+  uint32_t tp_e = 0, fp_e = 0, fn_e = 0;  // packed counts of experts lane, lane + 32
   uint32_t npos = 0, nexact = 0;
   uint64_t nlabel = 0;
   const uint64_t emask = E == 64 ? ~0ull : ((1ull << E) - 1);
   const int k = a.budget < E ? a.budget : E;
+  const double NEG = -__longlong_as_double(0x7ff0000000000000LL);
 
   for (int t = 0; t < Tw; ++t) {
     const bool valid = t < T;
     const int64_t r = r0 + (int64_t)t * L + l;
-    uint64_t pm = 0, tw = 0;
-    if (valid) {
-      tw = __ldg(a.truth + r);
-      if (a.threshold) {
+    const uint64_t tw = valid ? __ldg(a.truth + r) : 0ull;
+    uint64_t pm = 0;
+    if (a.threshold) {
+      uint32_t m = 0;
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
-          if (e < E && z[e] > 0.0) pm |= 1ull << e;
-      } else {
-        // k passes of "first maximum among the unchosen": exactly lexsort's
-        // (-score, id) order (learner.py:164-169).
-        for (int j = 0; j < k; ++j) {
-          double best = -__longlong_as_double(0x7ff0000000000000LL);
-          int bi = -1;
+      for (int j = 0; j < 32; ++j)
+        if (e0 + j < E && z[j] > 0.0) m |= 1u << j;
+      const uint32_t other = __shfl_xor_sync(full, m, 1);
+      pm = h ? ((uint64_t)m << 32 | other) : ((uint64_t)other << 32 | m);
+    } else {
+      uint32_t chosen = 0;
+      for (int it = 0; it < k; ++it) {
+        double best = NEG;
+        int bi = -1;
 #pragma unroll
-          for (int e = 0; e < 64; ++e) {
-            const bool ok = e < E && !((pm >> e) & 1ull) && (bi < 0 || z[e] > best);
-            best = ok ? z[e] : best;
-            bi = ok ? e : bi;
-          }
-          pm |= 1ull << bi;
+        for (int j = 0; j < 32; ++j) {
+          const bool ok = e0 + j < E && !((chosen >> j) & 1u) && (bi < 0 || z[j] > best);
+          best = ok ? z[j] : best;
+          bi = ok ? j : bi;
         }
+        const int gi = bi < 0 ? -1 : e0 + bi;
+        const double ob = __shfl_xor_sync(full, best, 1);
+        const int oi = __shfl_xor_sync(full, gi, 1);
+        const bool take_other = oi >= 0 && (gi < 0 || ob > best || (ob == best && oi < gi));
+        const int win = take_other ? oi : gi;
+        if (win >= e0 && win < e0 + 32) chosen |= 1u << (win - e0);
+        pm |= 1ull << win;
       }
-      a.pred[r] = pm;
+    }
+    pm &= valid ? ~0ull : 0ull;
+    if (valid) {
+      if (h == 0) a.pred[r] = pm;
       if (a.logits) {
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
-          if (e < E) a.logits[r * E + e] = z[e];
+        for (int j = 0; j < 32; ++j)
+          if (e0 + j < E) a.logits[r * E + e0 + j] = z[j];
       }
     }
     if (a.metrics) {
+      // lane 2i reports experts [0, 32), lane 2i+1 experts [32, 64) of its row
       const bool m = valid && t >= a.warmup;
-      const uint64_t tpm = m ? (pm & tw) : 0, fpm = m ? (pm & ~tw) : 0,
-                     fnm = m ? (tw & ~pm) : 0;
+      const uint64_t tpm = m ? (pm & tw) : 0, fpm = m ? (pm & ~tw) : 0, fnm = m ? (tw & ~pm) : 0;
 #pragma unroll
-      for (int e = 0; e < 64; ++e) {
-        const uint32_t c1 = __popc(__ballot_sync(0xffffffffu, (tpm >> e) & 1ull));
-        const uint32_t c2 = __popc(__ballot_sync(0xffffffffu, (fpm >> e) & 1ull));
-        const uint32_t c3 = __popc(__ballot_sync(0xffffffffu, (fnm >> e) & 1ull));
-        if (lane == (e & 31)) {
-          if (e < 32) {
-            tp_lo += c1;
-            fp_lo += c2;
-            fn_lo += c3;
-          } else {
-            tp_hi += c1;
-            fp_hi += c2;
-            fn_hi += c3;
-          }
+      for (int j = 0; j < 32; ++j) {
+        const uint32_t b1 = __ballot_sync(full, (tpm >> (e0 + j)) & 1ull);
+        const uint32_t b2 = __ballot_sync(full, (fpm >> (e0 + j)) & 1ull);
+        const uint32_t b3 = __ballot_sync(full, (fnm >> (e0 + j)) & 1ull);
+        if (lane == j) {  // lane j owns experts j (low 16 bits) and j + 32 (high 16 bits)
+          tp_e += (uint32_t)__popc(b1 & 0x55555555u) | ((uint32_t)__popc(b1 & 0xAAAAAAAAu) << 16);
+          fp_e += (uint32_t)__popc(b2 & 0x55555555u) | ((uint32_t)__popc(b2 & 0xAAAAAAAAu) << 16);
+          fn_e += (uint32_t)__popc(b3 & 0x55555555u) | ((uint32_t)__popc(b3 & 0xAAAAAAAAu) << 16);
         }
       }
-      npos += m;
-      nexact += m && pm == tw;
-      nlabel += m ? (uint64_t)(E - __popcll((pm ^ tw) & emask)) : 0;
+      const bool m0 = m && h == 0;
+      npos += m0;
+      nexact += m0 && pm == tw;
+      nlabel += m0 ? (uint64_t)(E - __popcll((pm ^ tw) & emask)) : 0;
+      if ((t & 1023) == 1023) {  // flush packed 16-bit counts before they overflow
+        const int j = lane;
+        {
+          if (j < E) {
+            atomicAdd(&mcnt[j], tp_e & 0xFFFFu);
+            atomicAdd(&mcnt[E + j], fp_e & 0xFFFFu);
+            atomicAdd(&mcnt[2 * E + j], fn_e & 0xFFFFu);
+          }
+          if (j + 32 < E) {
+            atomicAdd(&mcnt[j + 32], tp_e >> 16);
+            atomicAdd(&mcnt[E + j + 32], fp_e >> 16);
+            atomicAdd(&mcnt[2 * E + j + 32], fn_e >> 16);
+          }
+        }
+        tp_e = fp_e = fn_e = 0;
+      }
     }
     if (valid) {  // update_history (learner.py:62-72), as a logit recurrence
-      const double* b2 = bias2 + l * ES;
+      const double2* b2 = reinterpret_cast<const double2*>(bias2 + l * kES + e0);
 #pragma unroll
-      for (int e = 0; e < 64; ++e)
-        if (e < E) z[e] = fma(a.decay, z[e], b2[e]);
+      for (int j = 0; j < 16; ++j) {
+        const double2 v = b2[j];
+        z[2 * j] = fma(a.decay, z[2 * j], v.x);
+        z[2 * j + 1] = fma(a.decay, z[2 * j + 1], v.y);
+      }
       uint64_t m = tw;
       while (m) {
         const int ex = __ffsll((long long)m) - 1;
         m &= m - 1;
-        const double* col = colT + ex * ES;
+        const double2* col = reinterpret_cast<const double2*>(colT + ex * kES + e0);
 #pragma unroll
-        for (int e = 0; e < 64; ++e)
-          if (e < E) z[e] += col[e];
+        for (int j = 0; j < 16; ++j) {
+          const double2 v = col[j];
+          z[2 * j] += v.x;
+          z[2 * j + 1] += v.y;
+        }
       }
     }
   }
 
   if (a.metrics) {
-    if (lane < E) {
-      atomicAdd(&mcnt[lane], tp_lo);
-      atomicAdd(&mcnt[E + lane], fp_lo);
-      atomicAdd(&mcnt[2 * E + lane], fn_lo);
+    const int j = lane;
+    if (j < E) {
+      atomicAdd(&mcnt[j], (unsigned long long)(tp_e & 0xFFFFu));
+      atomicAdd(&mcnt[E + j], (unsigned long long)(fp_e & 0xFFFFu));
+      atomicAdd(&mcnt[2 * E + j], (unsigned long long)(fn_e & 0xFFFFu));
     }
-    if (lane + 32 < E) {
-      atomicAdd(&mcnt[lane + 32], tp_hi);
-      atomicAdd(&mcnt[E + lane + 32], fp_hi);
-      atomicAdd(&mcnt[2 * E + lane + 32], fn_hi);
+    if (j + 32 < E) {
+      atomicAdd(&mcnt[j + 32], (unsigned long long)(tp_e >> 16));
+      atomicAdd(&mcnt[E + j + 32], (unsigned long long)(fp_e >> 16));
+      atomicAdd(&mcnt[2 * E + j + 32], (unsigned long long)(fn_e >> 16));
     }
-    atomicAdd(&mcnt[3 * E], npos);
-    atomicAdd(&mcnt[3 * E + 1], nexact);
-    atomicAdd(&mcnt[3 * E + 2], nlabel);
+    atomicAdd(&mcnt[3 * E], (unsigned long long)npos);
+    atomicAdd(&mcnt[3 * E + 1], (unsigned long long)nexact);
+    atomicAdd(&mcnt[3 * E + 2], (unsigned long long)nlabel);
     __syncthreads();
     for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x)
       if (mcnt[i]) atomicAdd(reinterpret_cast<unsigned long long*>(a.metrics + i), mcnt[i]);
@@ -192,13 +226,13 @@ extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_
   MOEB_REQUIRE(decay >= 0.0 && decay < 1.0, "decay must be in [0, 1)");
   LinArgs a{truth, prompt_row_off, n_prompts, L, E, weights, decay, budget,
             threshold ? 1 : 0, warmup_tokens, pred, logits, metrics};
-  const size_t smem = sizeof(double) * ((size_t)E * (E + 1) + 2 * (size_t)L * (E + 1)) +
+  const size_t smem = sizeof(double) * ((size_t)E * kES + 2 * (size_t)L * kES) +
                       sizeof(unsigned long long) * (3 * E + 3);
   if ((int)smem > moeb::max_smem_per_block())
     return moeb::fail(MOEB_ESMEM, "learned_linear tables need %zu B of shared memory", smem);
   cudaFuncSetAttribute(k_linear_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t streams = (int64_t)L * n_prompts;
-  const int64_t blocks = (streams + kThreads - 1) / kThreads;
+  const int64_t threads = 2 * (int64_t)L * n_prompts;  // two per (prompt, layer) stream
+  const int64_t blocks = (threads + kThreads - 1) / kThreads;
   k_linear_predict<<<(unsigned)blocks, kThreads, smem, moeb::as_stream(stream)>>>(a);
   return moeb::check_launch("k_linear_predict");
 }
