@@ -42,8 +42,14 @@ struct LinArgs {
   int64_t* metrics;
 };
 
-constexpr int kES = 66;  // padded row stride (doubles), keeps rows 16-byte aligned
+// Shared-memory rows of 64 doubles as two 32-double halves with a 16-byte
+// gap (half h starts at double 34*h) and a row stride of 74 doubles = 37
+// 16-byte units: the 16-byte chunks a quarter-warp reads (4 streams x 2
+// halves, random columns) spread over all 8 bank groups.
+constexpr int kES = 74;
+__host__ __device__ constexpr int half_off(int h) { return 34 * h; }
 
+template <bool FULL>  // FULL: E == 64, no per-expert bounds checks
 __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = a.L, E = a.E, F = a.L + a.E + 1;
@@ -53,13 +59,13 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
   unsigned long long* mcnt = reinterpret_cast<unsigned long long*>(bias2 + L * kES);  // [3E+3]
   for (int i = threadIdx.x; i < E * 64; i += blockDim.x) {
     const int e = i / 64, j = i % 64;
-    colT[e * kES + j] = j < E ? a.Wt[(int64_t)j * F + L + e] : 0.0;
+    colT[e * kES + half_off(j >> 5) + (j & 31)] = j < E ? a.Wt[(int64_t)j * F + L + e] : 0.0;
   }
   for (int i = threadIdx.x; i < L * 64; i += blockDim.x) {
     const int l = i / 64, j = i % 64;
     const double b = j < E ? a.Wt[(int64_t)j * F + l] + a.Wt[(int64_t)j * F + L + E] : 0.0;
-    bias[l * kES + j] = b;
-    bias2[l * kES + j] = (1.0 - a.decay) * b;
+    bias[l * kES + half_off(j >> 5) + (j & 31)] = b;
+    bias2[l * kES + half_off(j >> 5) + (j & 31)] = (1.0 - a.decay) * b;
   }
   if (a.metrics)
     for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x) mcnt[i] = 0;
@@ -81,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
 
   double z[32];
 #pragma unroll
-  for (int j = 0; j < 32; ++j) z[j] = bias[l * kES + e0 + j];
+  for (int j = 0; j < 32; ++j) z[j] = bias[l * kES + half_off(h) + j];
   const int lane = threadIdx.x & 31;
   uint32_t tp_e = 0, fp_e = 0, fn_e = 0;  // packed counts of experts lane, lane + 32
   uint32_t npos = 0, nexact = 0;
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
       uint32_t m = 0;
 #pragma unroll
       for (int j = 0; j < 32; ++j)
-        if (e0 + j < E && z[j] > 0.0) m |= 1u << j;
+        if ((FULL || e0 + j < E) && z[j] > 0.0) m |= 1u << j;
       const uint32_t other = __shfl_xor_sync(full, m, 1);
       pm = h ? ((uint64_t)m << 32 | other) : ((uint64_t)other << 32 | m);
     } else {
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
         int bi = -1;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const bool ok = e0 + j < E && !((chosen >> j) & 1u) && (bi < 0 || z[j] > best);
+          const bool ok = (FULL || e0 + j < E) && !((chosen >> j) & 1u) && z[j] > best;
           best = ok ? z[j] : best;
           bi = ok ? j : bi;
         }
@@ -168,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
       }
     }
     if (valid) {  // update_history (learner.py:62-72), as a logit recurrence
-      const double2* b2 = reinterpret_cast<const double2*>(bias2 + l * kES + e0);
+      const double2* b2 = reinterpret_cast<const double2*>(bias2 + l * kES + half_off(h));
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const double2 v = b2[j];
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
       while (m) {
         const int ex = __ffsll((long long)m) - 1;
         m &= m - 1;
-        const double2* col = reinterpret_cast<const double2*>(colT + ex * kES + e0);
+        const double2* col = reinterpret_cast<const double2*>(colT + ex * kES + half_off(h));
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const double2 v = col[j];
@@ -230,9 +236,10 @@ extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_
                       sizeof(unsigned long long) * (3 * E + 3);
   if ((int)smem > moeb::max_smem_per_block())
     return moeb::fail(MOEB_ESMEM, "learned_linear tables need %zu B of shared memory", smem);
-  cudaFuncSetAttribute(k_linear_predict, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = E == 64 ? k_linear_predict<true> : k_linear_predict<false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int64_t threads = 2 * (int64_t)L * n_prompts;  // two per (prompt, layer) stream
   const int64_t blocks = (threads + kThreads - 1) / kThreads;
-  k_linear_predict<<<(unsigned)blocks, kThreads, smem, moeb::as_stream(stream)>>>(a);
+  kern<<<(unsigned)blocks, kThreads, smem, moeb::as_stream(stream)>>>(a);
   return moeb::check_launch("k_linear_predict");
 }
