@@ -195,6 +195,37 @@ int moeb_sketch_normalize(const int32_t* counts, int n, int L, int E, int binari
 int moeb_match_queries(const double* queries, int M, int D, const double* unit_t, int S,
                        int32_t* idx_out, double* sim_out, void* stream);
 
+/*
+ * K4 -- tcgen05 GEMM (TMA + tensor memory), transformer predictor building
+ * block: C[M][N] = A[M][K] . B[N][K]^T, A/B 16-bit (fp16 if `fp16` else
+ * bf16), row strides lda/ldb elements, fp32 accumulation, fused epilogue:
+ *  0 F32: out32 = C + bias (bias nullable)       1 BIAS: out16 = C + bias
+ *  2 BIAS_RELU: out16 = relu(C + bias)             3 BIAS_GELU: gelu (erf)
+ *  4 RESID_LN (N == 512): out32 = LayerNorm(out32 + C + bias; ln_w, ln_b,
+ *    ln_eps) in place, out16 = 16-bit copy (post-norm encoder sublayer)
+ * K % 64 == 0, N % 64 == 0.
+ */
+int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K, int fp16,
+              int epi, const float* bias, float* out32, void* out16, int ld16,
+              const float* ln_w, const float* ln_b, float ln_eps, void* stream);
+
+/*
+ * K5 -- windowed multi-head attention of the transformer predictor: qkv
+ * [rows][1536] 16-bit (q | k | v, 8 heads x 64), windows (start row, length
+ * <= max_len) of consecutive rows, bidirectional with key padding;
+ * out [rows][512] 16-bit.
+ */
+int moeb_window_attention(const void* qkv, void* out, const int64_t* win_start,
+                          const int32_t* win_len, int n_windows, int max_len, int fp16,
+                          void* stream);
+
+/* Transformer input rows: out32[r] = ptok[token_ids[r / L]] + play[r % L]
+ * (factorised input projection), out16 = 16-bit copy. Rows of 512. */
+int moeb_embed_rows(const float* ptok, const float* play, const int32_t* token_ids, int L,
+                    int64_t rows, float* out32, void* out16, int fp16, void* stream);
+/* fp32 -> 16-bit (fp16 or bf16) conversion (weight packing). */
+int moeb_to16(const float* x, void* y, int64_t n, int fp16, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -46,6 +46,11 @@ _SIGS = {
     "moeb_ream_counts": [P, P, I32, I32, I32, I32, P, P],
     "moeb_sketch_normalize": [P, I32, I32, I32, I32, P, P],
     "moeb_match_queries": [P, I32, I32, P, I32, P, P, P],
+    "moeb_gemm": [P, I32, P, I32, I32, I32, I32, I32, I32, P, P, P, I32, P, P,
+                  ctypes.c_float, P],
+    "moeb_window_attention": [P, P, P, P, I32, I32, I32, P],
+    "moeb_embed_rows": [P, P, P, I32, I64, P, P, I32, P],
+    "moeb_to16": [P, P, I64, I32, P],
     "moeb_version": [],
     "moeb_device_check": [],
 }

@@ -1,0 +1,367 @@
+// K4 -- tcgen05 GEMM for the transformer predictor (sm_100a).
+//
+//   C[M x N] = A[M x K] . B[N x K]^T   (both K-major, 16-bit bf16/fp16, fp32
+//   accumulation in tensor memory), with a fused epilogue:
+//     EPI_F32        C + bias -> fp32
+//     EPI_BIAS       C + bias -> 16-bit
+//     EPI_BIAS_RELU  relu(C + bias) -> 16-bit
+//     EPI_BIAS_GELU  gelu(C + bias) -> 16-bit (erf form, as torch)
+//     EPI_RESID_LN   x = resid + C + bias; y = LayerNorm(x) -> fp32 resid
+//                    (in place) and a 16-bit copy (post-norm encoder layers;
+//                    needs the whole row: BN = N = 512)
+// Persistent, warp-specialised: warp 0 = TMA producer (128-byte-swizzled
+// tiles, mbarrier ring of STAGES), warp 1 = MMA issuer (one elected thread,
+// tcgen05.mma.cta_group::1.kind::f16, M = 128, N <= 256 per instruction),
+// warps 2..5 = epilogue (tcgen05.ld 32x32b, one TMEM lane = one output row).
+// Two TMEM accumulators (when BN <= 256) let the epilogue of tile i overlap
+// the mainloop of tile i+1.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "tc_sm100.cuh"
+
+namespace {
+
+using namespace moeb::tc;
+
+enum : int { EPI_F32 = 0, EPI_BIAS = 1, EPI_BIAS_RELU = 2, EPI_BIAS_GELU = 3, EPI_RESID_LN = 4 };
+
+struct GemmArgs {
+  int M, N, K;
+  const float* bias;   // [N] (nullable for EPI_F32)
+  float* out32;        // [M][N]: EPI_F32 output / EPI_RESID_LN residual (in place)
+  void* out16;         // [M][ld16] 16-bit output
+  int ld16;
+  const float* ln_w;
+  const float* ln_b;
+  float ln_eps;
+};
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 16-bit elements = one 128-byte swizzle row
+
+__device__ __forceinline__ uint16_t to16(float x, bool fp16) {
+  if (fp16) return __half_as_ushort(__float2half_rn(x));
+  return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+
+__device__ __forceinline__ float gelu_erf(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+
+template <int BN, int STAGES, int EPI, bool FP16>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const GemmArgs g) {
+  constexpr int ACC = BN <= 256 ? 2 : 1;           // TMEM accumulator buffers
+  constexpr uint32_t TMEM_COLS = BN * ACC <= 32 ? 32 : BN * ACC;
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr int BOX_N = BN < 256 ? BN : 256;        // TMA box rows for B
+  constexpr int UMMA_N = BN < 256 ? BN : 256;
+  constexpr uint32_t IDESC = umma_idesc_f16(BM, UMMA_N, FP16 ? 0 : 1);
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte aligned carve-up (SW128 atoms need 1024-byte alignment)
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = base;
+  unsigned char* sB = base + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + ACC;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + ACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles_m = (g.M + BM - 1) / BM, tiles_n = g.N / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int nk = g.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < ACC; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_base_smem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_smem;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        // n-fastest raster: consecutive CTAs share the A tile in L2
+        const int tn = tile % tiles_n, tm = tile / tiles_n;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, tm * BM);
+#pragma unroll
+          for (int j = 0; j < BN / BOX_N; ++j)
+            tma_load_2d(sB + stage * B_BYTES + j * BOX_N * 128, &tmB, &full[stage], kb * BK,
+                        tn * BN + j * BOX_N);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this buffer
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = umma_desc_sw128(a0 + k * 32);
+#pragma unroll
+            for (int j = 0; j < BN / UMMA_N; ++j) {
+              const uint64_t bd = umma_desc_sw128(b0 + j * UMMA_N * 128 + k * 32);
+              mma_f16_ss(d_tmem + j * UMMA_N, ad, bd, IDESC, (kb | k) != 0);
+            }
+          }
+          mma_commit(&empty[stage]);  // frees the smem stage when these MMAs finish
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        if (++acc == ACC) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===== epilogue warps 2..5: TMEM lane quarter = warp % 4 =====
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int tn = tile % tiles_n, tm = tile / tiles_n;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * BM + quarter * 32 + lane;
+      const bool rv = row < g.M;
+      const uint32_t t0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      if (EPI == EPI_RESID_LN) {
+        float s1 = 0.f, s2 = 0.f;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(t0 + c0, r);
+          tmem_ld_wait();
+          if (rv) {
+            const float4* res = reinterpret_cast<const float4*>(g.out32 + (int64_t)row * g.N + c0);
+            const float4* bb = reinterpret_cast<const float4*>(g.bias + c0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 x = res[q], b = bb[q];
+              const float v0 = __uint_as_float(r[4 * q]) + b.x + x.x;
+              const float v1 = __uint_as_float(r[4 * q + 1]) + b.y + x.y;
+              const float v2 = __uint_as_float(r[4 * q + 2]) + b.z + x.z;
+              const float v3 = __uint_as_float(r[4 * q + 3]) + b.w + x.w;
+              s1 += (v0 + v1) + (v2 + v3);
+              s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
+            }
+          }
+        }
+        const float mean = s1 / BN;
+        const float var = fmaxf(s2 / BN - mean * mean, 0.f);
+        const float rstd = rsqrtf(var + g.ln_eps);
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(t0 + c0, r);
+          tmem_ld_wait();
+          if (rv) {
+            float4* res = reinterpret_cast<float4*>(g.out32 + (int64_t)row * g.N + c0);
+            const float4* bb = reinterpret_cast<const float4*>(g.bias + c0);
+            const float4* ww = reinterpret_cast<const float4*>(g.ln_w + c0);
+            const float4* lb = reinterpret_cast<const float4*>(g.ln_b + c0);
+            uint32_t packed[16];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 x = res[q], b = bb[q], w = ww[q], o = lb[q];
+              float4 y;
+              y.x = (__uint_as_float(r[4 * q]) + b.x + x.x - mean) * rstd * w.x + o.x;
+              y.y = (__uint_as_float(r[4 * q + 1]) + b.y + x.y - mean) * rstd * w.y + o.y;
+              y.z = (__uint_as_float(r[4 * q + 2]) + b.z + x.z - mean) * rstd * w.z + o.z;
+              y.w = (__uint_as_float(r[4 * q + 3]) + b.w + x.w - mean) * rstd * w.w + o.w;
+              res[q] = y;
+              packed[2 * q] = to16(y.x, FP16) | ((uint32_t)to16(y.y, FP16) << 16);
+              packed[2 * q + 1] = to16(y.z, FP16) | ((uint32_t)to16(y.w, FP16) << 16);
+            }
+            uint4* o16 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(g.out16) +
+                                                  (int64_t)row * g.ld16 + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              o16[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
+                                  packed[4 * q + 3]);
+          }
+        }
+      } else {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(t0 + c0, r);
+          tmem_ld_wait();
+          if (!rv) continue;
+          const int col = tn * BN + c0;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = __uint_as_float(r[j]) + (g.bias ? g.bias[col + j] : 0.f);
+            if (EPI == EPI_BIAS_RELU) v[j] = fmaxf(v[j], 0.f);
+            if (EPI == EPI_BIAS_GELU) v[j] = gelu_erf(v[j]);
+          }
+          if (EPI == EPI_F32) {
+            float4* o = reinterpret_cast<float4*>(g.out32 + (int64_t)row * g.N + col);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(g.out16) +
+                                                (int64_t)row * g.ld16 + col);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t w[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                w[u] = to16(v[8 * q + 2 * u], FP16) | ((uint32_t)to16(v[8 * q + 2 * u + 1], FP16) << 16);
+              o[q] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == ACC) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+// ---------------------------------------------------------------------------
+// Host side: tensor maps and launch.
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// 2-D K-major tensor [rows][K] (row stride ld elements), box [box_rows][64].
+int make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld, int box_rows, bool fp16) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return moeb::fail(MOEB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return moeb::fail(MOEB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return MOEB_OK;
+}
+
+template <int BN, int STAGES, int EPI, bool FP16>
+int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
+  constexpr int ACC = BN <= 256 ? 2 : 1;
+  const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
+                      8 * (2 * STAGES + 2 * ACC) + 16;
+  auto k = k_gemm<BN, STAGES, EPI, FP16>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
+  const int grid = tiles < moeb::num_sms() ? tiles : moeb::num_sms();
+  k<<<grid, 192, smem, s>>>(ta, tb, g);
+  return moeb::check_launch("k_gemm");
+}
+
+template <int EPI, bool FP16>
+int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn,
+             cudaStream_t s) {
+  if (bn == 512) return launch_gemm<512, 2, EPI, FP16>(ta, tb, g, s);
+  if (bn == 256) return launch_gemm<256, 4, EPI, FP16>(ta, tb, g, s);
+  if (bn == 128) return launch_gemm<128, 6, EPI, FP16>(ta, tb, g, s);
+  return launch_gemm<64, 8, EPI, FP16>(ta, tb, g, s);
+}
+
+}  // namespace
+
+extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K,
+                         int fp16, int epi, const float* bias, float* out32, void* out16,
+                         int ld16, const float* ln_w, const float* ln_b, float ln_eps,
+                         void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(A && B && M >= 1 && N >= 1 && K >= 1, "bad GEMM arguments");
+  MOEB_REQUIRE(K % BK == 0, "K must be a multiple of %d (got %d)", BK, K);
+  MOEB_REQUIRE(epi >= EPI_F32 && epi <= EPI_RESID_LN, "unknown epilogue %d", epi);
+  int bn;
+  if (epi == EPI_RESID_LN) {
+    MOEB_REQUIRE(N == 512, "LayerNorm epilogue needs N == 512");
+    MOEB_REQUIRE(out32 && out16 && bias && ln_w && ln_b, "LayerNorm epilogue arguments");
+    bn = 512;
+  } else {
+    bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : 0;
+    MOEB_REQUIRE(bn, "N must be a multiple of 64 (got %d)", N);
+    MOEB_REQUIRE(epi == EPI_F32 ? out32 != nullptr : out16 != nullptr, "missing output");
+  }
+  CUtensorMap ta, tb;
+  if (int rc = make_map(&ta, A, M, K, lda, BM, fp16)) return rc;
+  if (int rc = make_map(&tb, B, N, K, ldb, bn < 256 ? bn : 256, fp16)) return rc;
+  GemmArgs g{M, N, K, bias, out32, out16, ld16, ln_w, ln_b, ln_eps};
+  cudaStream_t s = moeb::as_stream(stream);
+  switch (epi) {
+    case EPI_F32: return fp16 ? dispatch<EPI_F32, true>(ta, tb, g, bn, s) : dispatch<EPI_F32, false>(ta, tb, g, bn, s);
+    case EPI_BIAS: return fp16 ? dispatch<EPI_BIAS, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS, false>(ta, tb, g, bn, s);
+    case EPI_BIAS_RELU: return fp16 ? dispatch<EPI_BIAS_RELU, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS_RELU, false>(ta, tb, g, bn, s);
+    case EPI_BIAS_GELU: return fp16 ? dispatch<EPI_BIAS_GELU, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS_GELU, false>(ta, tb, g, bn, s);
+    default: return fp16 ? launch_gemm<512, 2, EPI_RESID_LN, true>(ta, tb, g, s) : launch_gemm<512, 2, EPI_RESID_LN, false>(ta, tb, g, s);
+  }
+}

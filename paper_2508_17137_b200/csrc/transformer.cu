@@ -1,0 +1,90 @@
+// Transformer predictor glue kernels (the GEMMs are K4, attention K5).
+//
+// Input projection, factorised: Linear(2560 -> 512) over [tok_emb | layer_emb]
+// equals tok_emb . W_tok^T + (layer_emb . W_lay^T + b), so with
+// the per-vocabulary table P_tok[32000][512] and the per-layer table
+// P_lay[L][512] (both computed once per model by K4) the projected input of a
+// trace row is a two-row gather-add.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace {
+
+template <bool FP16>
+__global__ void __launch_bounds__(128) k_embed_rows(const float* __restrict__ ptok,
+                                                    const float* __restrict__ play,
+                                                    const int32_t* __restrict__ tok, int L,
+                                                    int64_t rows, float* __restrict__ out32,
+                                                    uint16_t* __restrict__ out16) {
+  // one warp per row, 512 columns = 32 lanes x 16 floats
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int t = tok[r / L], l = (int)(r % L);
+  const float4* a = reinterpret_cast<const float4*>(ptok + (int64_t)t * 512) + lane * 4;
+  const float4* b = reinterpret_cast<const float4*>(play + (int64_t)l * 512) + lane * 4;
+  float4* o = reinterpret_cast<float4*>(out32 + r * 512) + lane * 4;
+  uint32_t p[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 x = a[q], y = b[q];
+    const float4 v = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+    o[q] = v;
+    if (FP16) {
+      const __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
+      p[2 * q] = *reinterpret_cast<const uint32_t*>(&h0);
+      p[2 * q + 1] = *reinterpret_cast<const uint32_t*>(&h1);
+    } else {
+      const __nv_bfloat162 h0 = __floats2bfloat162_rn(v.x, v.y), h1 = __floats2bfloat162_rn(v.z, v.w);
+      p[2 * q] = *reinterpret_cast<const uint32_t*>(&h0);
+      p[2 * q + 1] = *reinterpret_cast<const uint32_t*>(&h1);
+    }
+  }
+  uint4* o16 = reinterpret_cast<uint4*>(out16 + r * 512) + lane * 2;
+  o16[0] = make_uint4(p[0], p[1], p[2], p[3]);
+  o16[1] = make_uint4(p[4], p[5], p[6], p[7]);
+}
+
+template <bool FP16>
+__global__ void k_to16(const float* __restrict__ x, uint16_t* __restrict__ y, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    y[i] = FP16 ? __half_as_ushort(__float2half_rn(x[i]))
+                : __bfloat16_as_ushort(__float2bfloat16_rn(x[i]));
+}
+
+}  // namespace
+
+extern "C" int moeb_embed_rows(const float* ptok, const float* play, const int32_t* token_ids,
+                               int L, int64_t rows, float* out32, void* out16, int fp16,
+                               void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(ptok && play && token_ids && out32 && out16 && L >= 1 && rows >= 0, "bad args");
+  if (rows == 0) return MOEB_OK;
+  const unsigned blocks = (unsigned)((rows * 32 + 127) / 128);
+  cudaStream_t s = moeb::as_stream(stream);
+  if (fp16)
+    k_embed_rows<true><<<blocks, 128, 0, s>>>(ptok, play, token_ids, L, rows, out32,
+                                              static_cast<uint16_t*>(out16));
+  else
+    k_embed_rows<false><<<blocks, 128, 0, s>>>(ptok, play, token_ids, L, rows, out32,
+                                               static_cast<uint16_t*>(out16));
+  return moeb::check_launch("k_embed_rows");
+}
+
+extern "C" int moeb_to16(const float* x, void* y, int64_t n, int fp16, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(x && y && n >= 0, "bad args");
+  if (n == 0) return MOEB_OK;
+  cudaStream_t s = moeb::as_stream(stream);
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  if (fp16)
+    k_to16<true><<<blocks, 256, 0, s>>>(x, static_cast<uint16_t*>(y), n);
+  else
+    k_to16<false><<<blocks, 256, 0, s>>>(x, static_cast<uint16_t*>(y), n);
+  return moeb::check_launch("k_to16");
+}

@@ -1,0 +1,122 @@
+"""Transformer predictor kernels (K4 tcgen05 GEMM, K5 attention) and the full
+predictor against the PyTorch fp32 oracle (oracle/transformer_ref.py).
+
+Bars (north star): logits within 1e-2 absolute of the fp32 oracle, threshold
+decisions agreeing on >= 99.9 % of labels; selection masks bit-exact when the
+selection head (K2) is fed the oracle's logits. Kernel-level tests compare
+against torch fp32 math on the same 16-bit operands (torch is the checker)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(600)]
+
+
+@pytest.fixture(scope="module")
+def tr():
+    import paper_2508_17137_b200 as m
+    from paper_2508_17137_b200 import transformer as t
+    m.load_library()
+    return t
+
+
+@pytest.mark.parametrize("fp16", [True, False])
+@pytest.mark.parametrize("M,N,K", [(300, 256, 512), (1000, 1536, 512), (129, 64, 256),
+                                   (700, 512, 2048), (5, 128, 64)])
+def test_gemm_epilogues(tr, fp16, M, N, K):
+    dt = torch.float16 if fp16 else torch.bfloat16
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    a = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(dt)
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.05).to(dt)
+    bias = torch.randn(N, device="cuda", generator=g) * 0.1
+    ref = a.float() @ b.float().T + bias
+    tol = 2e-3 * math.sqrt(K / 512)
+    out32 = torch.empty(M, N, device="cuda")
+    tr.gemm(a, b, M, N, K, tr.EPI_F32, bias=bias, out32=out32, fp16=fp16)
+    torch.testing.assert_close(out32, ref, atol=tol, rtol=1e-3)
+    q = 1e-2 if not fp16 else 2e-3
+    for epi, fn in ((tr.EPI_BIAS, lambda x: x), (tr.EPI_BIAS_RELU, torch.relu),
+                    (tr.EPI_BIAS_GELU, torch.nn.functional.gelu)):
+        out16 = torch.empty(M, N, device="cuda", dtype=dt)
+        tr.gemm(a, b, M, N, K, epi, bias=bias, out16=out16, fp16=fp16)
+        torch.testing.assert_close(out16.float(), fn(ref), atol=tol + q, rtol=q)
+    if N == 512:
+        resid = torch.randn(M, N, device="cuda", generator=g)
+        lw = 1 + 0.1 * torch.randn(N, device="cuda", generator=g)
+        lb = 0.1 * torch.randn(N, device="cuda", generator=g)
+        want = torch.nn.functional.layer_norm(resid + ref, (N,), lw, lb, 1e-5)
+        h32 = resid.clone()
+        h16 = torch.empty(M, N, device="cuda", dtype=dt)
+        tr.gemm(a, b, M, N, K, tr.EPI_RESID_LN, bias=bias, out32=h32, out16=h16, ln=(lw, lb),
+                fp16=fp16)
+        torch.testing.assert_close(h32, want, atol=5e-3, rtol=1e-3)
+        torch.testing.assert_close(h16.float(), want, atol=5e-3 + q, rtol=q)
+
+
+@pytest.mark.parametrize("fp16", [True, False])
+def test_window_attention(tr, fp16):
+    from paper_2508_17137_b200 import _native as nat
+    dt = torch.float16 if fp16 else torch.bfloat16
+    off = np.array([0, 700, 700 + 512, 700 + 512 + 37, 700 + 512 + 37 + 1100])
+    ws, wl = tr.windows_of(off)
+    rows = int(off[-1])
+    g = torch.Generator(device="cuda").manual_seed(3)
+    qkv = torch.randn(rows, 1536, device="cuda", generator=g).to(dt)
+    out = torch.zeros(rows, 512, device="cuda", dtype=dt)
+    nat.call("moeb_window_attention", nat.ptr(qkv), nat.ptr(out),
+             nat.ptr(torch.from_numpy(ws).cuda()), nat.ptr(torch.from_numpy(wl).cuda()), len(ws),
+             512, int(fp16), nat.stream_ptr())
+    x = qkv.float()
+    for s, n in zip(ws, wl):
+        q = x[s:s + n, :512].view(n, 8, 64).transpose(0, 1)
+        k = x[s:s + n, 512:1024].view(n, 8, 64).transpose(0, 1)
+        v = x[s:s + n, 1024:].view(n, 8, 64).transpose(0, 1)
+        a = torch.softmax(q @ k.transpose(1, 2) / 8.0, dim=-1) @ v
+        want = a.transpose(0, 1).reshape(n, 512)
+        torch.testing.assert_close(out[s:s + n].float(), want, atol=2e-2, rtol=2e-2)
+
+
+@pytest.fixture(scope="module")
+def small_case():
+    import paper_2508_17137_b200 as m
+    shape = m.ModelShape(26, 64, 6)
+    packed = m.generate_packed(m.GeneratorConfig(3, 30, shape, 8, 0.9, 7))
+    return shape, packed
+
+
+@pytest.mark.parametrize("fp16", [True, False])
+def test_transformer_vs_fp32_oracle(tr, small_case, oracle, fp16):
+    import paper_2508_17137_b200 as m
+    from oracle import transformer_ref as R
+    shape, packed = small_case
+    ref = R.TransformerRef(R.TransformerSpec(26, 64, seed=0))
+    tok, lay = R.row_inputs(packed.token_ids.cpu().numpy(), packed.row_off_host, 26)
+    want = ref.logits(tok, lay, packed.row_off_host).numpy()
+    W = tr.TransformerWeights(R.export_weights(ref), 26, 64, fp16=fp16)
+    pred = m.make_predictor("transformer", shape, transformer=W)
+    z = pred.forward_logits(packed).cpu().numpy()
+    err = np.abs(z - want)
+    agree = np.mean((z > 0) == (want > 0))
+    print(f"fp16={fp16}: max|dz|={err.max():.2e} mean|dz|={err.mean():.2e} "
+          f"threshold agreement={agree:.6f}")
+    assert err.max() < 1e-2
+    if fp16:
+        assert agree >= 0.999
+    # selection head is bit-exact on the oracle's logits
+    masks = oracle.mask_head(want.astype(np.float32), 6)
+    from paper_2508_17137_b200 import _native as nat
+    zt = torch.from_numpy(want.astype(np.float32)).cuda()
+    out = torch.zeros((len(want), 1), dtype=torch.int64, device="cuda")
+    nat.call("moeb_mask_head", nat.ptr(zt), len(want), 64, 6, 0, nat.ptr(out), nat.stream_ptr())
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), masks)
+
+
+def test_transformer_weights_match_oracle_init(tr):
+    from oracle import transformer_ref as R
+    ref = R.export_weights(R.TransformerRef(R.TransformerSpec(26, 64, seed=0)))
+    mine = tr.init_state(26, 64, seed=0)
+    assert set(ref) == set(mine)
+    for k in ref:
+        assert np.array_equal(ref[k], mine[k]), k
