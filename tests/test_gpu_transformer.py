@@ -65,9 +65,9 @@ def test_window_attention(tr, fp16):
     g = torch.Generator(device="cuda").manual_seed(3)
     qkv = torch.randn(rows, 1536, device="cuda", generator=g).to(dt)
     out = torch.zeros(rows, 512, device="cuda", dtype=dt)
-    nat.call("moeb_window_attention", nat.ptr(qkv), nat.ptr(out),
-             nat.ptr(torch.from_numpy(ws).cuda()), nat.ptr(torch.from_numpy(wl).cuda()), len(ws),
-             512, int(fp16), nat.stream_ptr())
+    ws_d, wl_d = torch.from_numpy(ws).cuda(), torch.from_numpy(wl).cuda()  # keep alive
+    nat.call("moeb_window_attention", nat.ptr(qkv), nat.ptr(out), nat.ptr(ws_d), nat.ptr(wl_d),
+             len(ws), 512, int(fp16), nat.stream_ptr())
     x = qkv.float()
     for s, n in zip(ws, wl):
         q = x[s:s + n, :512].view(n, 8, 64).transpose(0, 1)
