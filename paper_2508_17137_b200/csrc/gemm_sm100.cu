@@ -74,6 +74,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + ACC;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + ACC);
+  // per-epilogue-warp 32 x 33 fp32 transpose tiles (LayerNorm epilogue)
+  float* tbuf = reinterpret_cast<float*>(tmem_base_smem + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (g.M + BM - 1) / BM, tiles_n = g.N / BN;
@@ -173,58 +175,56 @@ __global__ void __launch_bounds__(192, 1)
       const bool rv = row < g.M;
       const uint32_t t0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       if (EPI == EPI_RESID_LN) {
+        // pass 1: x = resid + acc + bias, stashed back into TMEM; row stats.
+        // Residual chunks [32 rows x 32 cols] are read coalesced (one row per
+        // instruction, lane = column) and transposed through shared memory.
+        float* T = tbuf + quarter * (32 * 33);
+        const int rowbase = tm * BM + quarter * 32;
         float s1 = 0.f, s2 = 0.f;
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
-          tmem_ld_wait();
-          if (rv) {
-            const float4* res = reinterpret_cast<const float4*>(g.out32 + (int64_t)row * g.N + c0);
-            const float4* bb = reinterpret_cast<const float4*>(g.bias + c0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 x = res[q], b = bb[q];
-              const float v0 = __uint_as_float(r[4 * q]) + b.x + x.x;
-              const float v1 = __uint_as_float(r[4 * q + 1]) + b.y + x.y;
-              const float v2 = __uint_as_float(r[4 * q + 2]) + b.z + x.z;
-              const float v3 = __uint_as_float(r[4 * q + 3]) + b.w + x.w;
-              s1 += (v0 + v1) + (v2 + v3);
-              s2 += (v0 * v0 + v1 * v1) + (v2 * v2 + v3 * v3);
-            }
+#pragma unroll 8
+          for (int i = 0; i < 32; ++i) {
+            const int rr = rowbase + i;
+            T[i * 33 + lane] = rr < g.M ? g.out32[(int64_t)rr * g.N + c0 + lane] : 0.f;
           }
+          __syncwarp();
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float x = __uint_as_float(r[j]) + g.bias[c0 + j] + T[lane * 33 + j];
+            r[j] = __float_as_uint(x);
+            s1 += x;
+            s2 += x * x;
+          }
+          __syncwarp();
+          tmem_st32(t0 + c0, r);
         }
+        tmem_st_wait();
         const float mean = s1 / BN;
         const float var = fmaxf(s2 / BN - mean * mean, 0.f);
         const float rstd = rsqrtf(var + g.ln_eps);
+        // pass 2: y = LN(x); coalesced stores of fp32 (in place) and 16-bit
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
           tmem_ld_wait();
-          if (rv) {
-            float4* res = reinterpret_cast<float4*>(g.out32 + (int64_t)row * g.N + c0);
-            const float4* bb = reinterpret_cast<const float4*>(g.bias + c0);
-            const float4* ww = reinterpret_cast<const float4*>(g.ln_w + c0);
-            const float4* lb = reinterpret_cast<const float4*>(g.ln_b + c0);
-            uint32_t packed[16];
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const float4 x = res[q], b = bb[q], w = ww[q], o = lb[q];
-              float4 y;
-              y.x = (__uint_as_float(r[4 * q]) + b.x + x.x - mean) * rstd * w.x + o.x;
-              y.y = (__uint_as_float(r[4 * q + 1]) + b.y + x.y - mean) * rstd * w.y + o.y;
-              y.z = (__uint_as_float(r[4 * q + 2]) + b.z + x.z - mean) * rstd * w.z + o.z;
-              y.w = (__uint_as_float(r[4 * q + 3]) + b.w + x.w - mean) * rstd * w.w + o.w;
-              res[q] = y;
-              packed[2 * q] = to16(y.x, FP16) | ((uint32_t)to16(y.y, FP16) << 16);
-              packed[2 * q + 1] = to16(y.z, FP16) | ((uint32_t)to16(y.w, FP16) << 16);
+          for (int j = 0; j < 32; ++j)
+            T[lane * 33 + j] = (__uint_as_float(r[j]) - mean) * rstd * g.ln_w[c0 + j] + g.ln_b[c0 + j];
+          __syncwarp();
+          uint16_t* o16 = reinterpret_cast<uint16_t*>(g.out16);
+#pragma unroll 8
+          for (int i = 0; i < 32; ++i) {
+            const int rr = rowbase + i;
+            if (rr < g.M) {
+              const float y = T[i * 33 + lane];
+              g.out32[(int64_t)rr * g.N + c0 + lane] = y;
+              o16[(int64_t)rr * g.ld16 + c0 + lane] = to16(y, FP16);
             }
-            uint4* o16 = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(g.out16) +
-                                                  (int64_t)row * g.ld16 + c0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              o16[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
-                                  packed[4 * q + 3]);
           }
+          __syncwarp();
         }
       } else {
         for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -314,7 +314,8 @@ template <int BN, int STAGES, int EPI, bool FP16>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
-                      8 * (2 * STAGES + 2 * ACC) + 16;
+                      8 * (2 * STAGES + 2 * ACC) + 16 +
+                      (EPI == EPI_RESID_LN ? 4 * 32 * 33 * sizeof(float) : 0);
   auto k = k_gemm<BN, STAGES, EPI, FP16>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
