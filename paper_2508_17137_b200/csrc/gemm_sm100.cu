@@ -64,9 +64,10 @@ __global__ void __launch_bounds__(192, 1)
   constexpr uint32_t IDESC = umma_idesc_f16(BM, UMMA_N, FP16 ? 0 : 1);
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte aligned carve-up (SW128 atoms need 1024-byte alignment)
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // The dynamic shared-memory window starts 1024-byte aligned (no static
+  // shared memory here), as SW128 atoms require; keeping smem_raw as the base
+  // lets the compiler emit shared (not generic) loads/stores.
+  unsigned char* base = smem_raw;
   unsigned char* sA = base;
   unsigned char* sB = base + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
@@ -181,13 +182,23 @@ __global__ void __launch_bounds__(192, 1)
         float* T = tbuf + quarter * (32 * 33);
         const int rowbase = tm * BM + quarter * 32;
         float s1 = 0.f, s2 = 0.f;
+        float nxt[32];  // next chunk's residual column (software pipelined)
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int rr = rowbase + i;
+          nxt[i] = rr < g.M ? __ldg(g.out32 + (int64_t)rr * g.N + lane) : 0.f;
+        }
         for (int c0 = 0; c0 < BN; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
-#pragma unroll 8
-          for (int i = 0; i < 32; ++i) {
-            const int rr = rowbase + i;
-            T[i * 33 + lane] = rr < g.M ? g.out32[(int64_t)rr * g.N + c0 + lane] : 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) T[i * 33 + lane] = nxt[i];
+          if (c0 + 32 < BN) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int rr = rowbase + i;
+              nxt[i] = rr < g.M ? __ldg(g.out32 + (int64_t)rr * g.N + c0 + 32 + lane) : 0.f;
+            }
           }
           __syncwarp();
           tmem_ld_wait();
