@@ -357,6 +357,58 @@ def run_ours(args):
     lc = lru_c[0, 0].cpu().numpy()
     hit["lru_only"] = int(lc[1]) / int(lc[0])
 
+    # --- the paper's transformer predictor (tcgen05 path) on a C2 slice ---
+    tr_info = None
+    if args.transformer_prompts > 0:
+        from paper_2508_17137_b200 import transformer as TR
+        Pt = min(args.transformer_prompts, P)
+        tpk = packed.select(0, Pt)
+        Wt = TR.TransformerWeights.random(L, E, seed=0, fp16=True, device=dev)
+        tpred = m.make_predictor("transformer", shape, transformer=Wt)
+
+        def tr_step(timing=None):
+            vec_t = m.metrics.metric_vector(E, dev)
+            mk = tpred.predict_masks(tpk, BUDGET, WARMUP_TOKENS, metrics=vec_t, timing=timing)
+            cnt_t, _, _ = m.cache_replay(tpk, [(mk, None, False)], [cap], WARMUP_TOKENS, BUDGET,
+                                         want_per_prompt=False)
+            return cnt_t, vec_t
+
+        for _ in range(2):
+            tr_step()
+        torch.cuda.synchronize()
+        timing = {}
+        ts, te = ev(), ev()
+        ts.record(stream)
+        nt = max(1, min(3, args.steps))
+        for _ in range(nt):
+            cnt_t, vec_t = tr_step(timing)
+        te.record(stream)
+        torch.cuda.synchronize()
+        tms = ts.elapsed_time(te) / nt
+        ker = {}
+        for name, lst in timing.items():
+            msum = sum(a.elapsed_time(b) for a, b, _ in lst) / nt
+            fl = sum(f for _, _, f in lst) / nt
+            ker[name] = {"ms": msum, "tflops": fl / (msum / 1e3) / 1e12}
+        dom = max((k for k in ker if k.startswith("gemm")), key=lambda k: ker[k]["ms"])
+        tot_flops = sum(sum(f for _, _, f in lst) for lst in timing.values()) / nt
+        ct = cnt_t[0, 0].cpu().numpy()
+        mct = m.MetricCounts.from_vector(vec_t.cpu().numpy(), E)
+        tr_info = {
+            "workload": f"C2 slice: {Pt} prompts x {C2['tokens']} tokens (rows {tpk.rows})",
+            "predictor": "transformer 4x(d512,h8,ff2048), windows 512, fp16 operands / fp32 acc",
+            "trace_tok_per_s": Pt * C2["tokens"] / (tms / 1e3), "ms_per_step": tms,
+            "tflops_achieved": tot_flops / (tms / 1e3) / 1e12, "kernels": ker,
+            "roofline": {"bound": "tensor", "kernel": dom, "achieved": ker[dom]["tflops"],
+                         "peak": bf16_sus, "unit": "TFLOP/s",
+                         "frac": ker[dom]["tflops"] / bf16_sus,
+                         "peak_kind": f"{peak_kind} dense bf16/fp16 sustained"},
+            "hit_rate_10pct": int(ct[1]) / int(ct[0]),
+            "prediction": {"macro_f1": mct.macro_f1(), "position_accuracy": mct.position_accuracy,
+                           "label_accuracy": mct.label_accuracy},
+        }
+        del Wt, tpred
+
     cpu_base = None
     if rank == 0 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
@@ -396,6 +448,7 @@ def run_ours(args):
             "prediction": {"macro_f1": mc.macro_f1(), "position_accuracy": mc.position_accuracy,
                            "label_accuracy": mc.label_accuracy},
             "cpu_baseline": cpu_base,
+            "transformer": tr_info,
             "clocks": clock_info,
             "setup": {"generate_s": gen_s},
         }
@@ -413,6 +466,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--prompts", type=int, default=C2["prompts"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transformer-prompts", type=int, default=700,
+                    help="C2 prompts replayed with the transformer predictor (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

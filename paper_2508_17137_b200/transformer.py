@@ -157,8 +157,12 @@ class TransformerPredictor:
             yield lo, hi
             lo = hi
 
-    def forward_logits(self, packed: PackedTraces, logits_out: torch.Tensor | None = None):
-        """fp32 logits [rows][E] for every trace row (chunked over prompts)."""
+    def forward_logits(self, packed: PackedTraces, logits_out: torch.Tensor | None = None,
+                       timing: dict | None = None):
+        """fp32 logits [rows][E] for every trace row (chunked over prompts).
+
+        With `timing` (a dict), CUDA events are recorded around every launch
+        and timing[name] collects (start, end, flops) per launch."""
         W, s = self.weights, self.shape
         E, L = s.num_experts, s.num_layers
         dev = packed.device
@@ -174,6 +178,15 @@ class TransformerPredictor:
         att = torch.empty((cap, D_MODEL), dtype=dt, device=dev)
         ff = torch.empty((cap, D_FF), dtype=dt, device=dev)
         y = torch.empty((cap, D_HEAD_MLP), dtype=dt, device=dev)
+        def timed(name, flops, fn, *a, **k):
+            if timing is None:
+                return fn(*a, **k)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(*a, **k)
+            e1.record()
+            timing.setdefault(name, []).append((e0, e1, flops))
+
         for lo, hi in self._chunks(packed):
             sub = packed.select(lo, hi)
             r0 = int(packed.row_off_host[lo])
@@ -184,26 +197,35 @@ class TransformerPredictor:
             tok = sub.token_ids.contiguous()
             nat.call("moeb_embed_rows", nat.ptr(W.ptok), nat.ptr(W.play), nat.ptr(tok), L, M,
                      nat.ptr(h32), nat.ptr(h16), int(W.fp16), nat.stream_ptr())
+            att_flops = 4 * float(np.sum(wl.astype(np.float64) ** 2)) * D_MODEL
             for lay in W.layers:
-                gemm(h16, lay["qkv"], M, 3 * D_MODEL, D_MODEL, EPI_BIAS, bias=lay["qkv_b"],
-                     out16=qkv, fp16=W.fp16)
-                nat.call("moeb_window_attention", nat.ptr(qkv), nat.ptr(att), nat.ptr(ws_d),
-                         nat.ptr(wl_d), len(ws), WINDOW, int(W.fp16), nat.stream_ptr())
-                gemm(att, lay["o"], M, D_MODEL, D_MODEL, EPI_RESID_LN, bias=lay["o_b"],
-                     out32=h32, out16=h16, ln=(lay["n1_w"], lay["n1_b"]), fp16=W.fp16)
-                gemm(h16, lay["f1"], M, D_FF, D_MODEL, EPI_BIAS_RELU, bias=lay["f1_b"],
-                     out16=ff, fp16=W.fp16)
-                gemm(ff, lay["f2"], M, D_MODEL, D_FF, EPI_RESID_LN, bias=lay["f2_b"],
-                     out32=h32, out16=h16, ln=(lay["n2_w"], lay["n2_b"]), fp16=W.fp16)
-            gemm(h16, W.h1_w, M, D_HEAD_MLP, D_MODEL, EPI_BIAS_GELU, bias=W.h1_b, out16=y,
-                 fp16=W.fp16)
-            gemm(y, W.h2_w, M, E, D_HEAD_MLP, EPI_F32, bias=W.h2_b, out32=out[r0:r0 + M],
-                 fp16=W.fp16)
+                timed("gemm_qkv", 2.0 * M * 3 * D_MODEL * D_MODEL, gemm, h16, lay["qkv"], M,
+                      3 * D_MODEL, D_MODEL, EPI_BIAS, bias=lay["qkv_b"], out16=qkv, fp16=W.fp16)
+                timed("attention", att_flops, nat.call, "moeb_window_attention", nat.ptr(qkv),
+                      nat.ptr(att), nat.ptr(ws_d), nat.ptr(wl_d), len(ws), WINDOW, int(W.fp16),
+                      nat.stream_ptr())
+                timed("gemm_out_ln", 2.0 * M * D_MODEL * D_MODEL, gemm, att, lay["o"], M, D_MODEL,
+                      D_MODEL, EPI_RESID_LN, bias=lay["o_b"], out32=h32, out16=h16,
+                      ln=(lay["n1_w"], lay["n1_b"]), fp16=W.fp16)
+                timed("gemm_ffn1", 2.0 * M * D_FF * D_MODEL, gemm, h16, lay["f1"], M, D_FF,
+                      D_MODEL, EPI_BIAS_RELU, bias=lay["f1_b"], out16=ff, fp16=W.fp16)
+                timed("gemm_ffn2_ln", 2.0 * M * D_MODEL * D_FF, gemm, ff, lay["f2"], M, D_MODEL,
+                      D_FF, EPI_RESID_LN, bias=lay["f2_b"], out32=h32, out16=h16,
+                      ln=(lay["n2_w"], lay["n2_b"]), fp16=W.fp16)
+            timed("gemm_head", 2.0 * M * (D_HEAD_MLP * D_MODEL + E * D_HEAD_MLP), self._head,
+                  h16, y, out[r0:r0 + M], M)
         return out
 
+    def _head(self, h16, y, out, M):
+        W = self.weights
+        gemm(h16, W.h1_w, M, D_HEAD_MLP, D_MODEL, EPI_BIAS_GELU, bias=W.h1_b, out16=y,
+             fp16=W.fp16)
+        gemm(y, W.h2_w, M, self.shape.num_experts, D_HEAD_MLP, EPI_F32, bias=W.h2_b, out32=out,
+             fp16=W.fp16)
+
     def predict_masks(self, packed: PackedTraces, budget: int, warmup: int = 0, metrics=None,
-                      logits=None):
-        z = self.forward_logits(packed, logits)
+                      logits=None, timing=None):
+        z = self.forward_logits(packed, logits, timing)
         E = self.shape.num_experts
         masks = torch.empty((packed.rows, self.shape.mask_words), dtype=torch.int64,
                             device=packed.device)
