@@ -203,6 +203,8 @@ int moeb_match_queries(const double* queries, int M, int D, const double* unit_t
  *  2 BIAS_RELU: out16 = relu(C + bias)             3 BIAS_GELU: gelu (erf)
  *  4 RESID_LN (N == 512): out32 = LayerNorm(out32 + C + bias; ln_w, ln_b,
  *    ln_eps) in place, out16 = 16-bit copy (post-norm encoder sublayer)
+ *  5 ROW-MAX (N % 256 == 0): out32 [M][N/256] = max of each 256-column tile
+ *    of each row, out16 (as int32) = its first argmax column (m-fastest raster)
  * K % 64 == 0, N % 64 == 0.
  */
 int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K, int fp16,
@@ -225,6 +227,35 @@ int moeb_embed_rows(const float* ptok, const float* play, const int32_t* token_i
                     int64_t rows, float* out32, void* out16, int fp16, void* stream);
 /* fp32 -> 16-bit (fp16 or bf16) conversion (weight packing). */
 int moeb_to16(const float* x, void* y, int64_t n, int fp16, void* stream);
+
+/*
+ * K6b -- EAM matching at scale on tensor cores (BASELINE C4): queries are
+ * integer activation-count vectors (exact in fp16 up to 2048), sketches are
+ * unit-normalised and split U = U_hi + 2^-11 U_lo' into fp16.
+ *  moeb_eam_pack_library: sketches [S][D] fp64 -> uu [S_pad][2D] fp16
+ *    (rows >= S zero), norms [S] fp64 (sketches.py:157-160)
+ *  moeb_eam_pack_queries: counts [M][D] int32 -> cc [M][2D] fp16 [C | C/2048]
+ *  then moeb_gemm(cc, uu, M, S_pad, 2D, fp16=1, epi=5 ROW-MAX) writes per
+ *    (query, 256-sketch tile) max (pval [M][S_pad/256] fp32) and first argmax
+ *  moeb_eam_rerank: exact fp64 re-score of every tile within 2*eps_rel of the
+ *    query's approximate max; idx_out [M] = first argmax of unit . q
+ *    (zero query -> 0), sim_out [M] cosine (nullable), n_rerank [M] tiles
+ *    re-scored (nullable). SketchCollection.match_nearest (sketches.py:165-184).
+ */
+int moeb_eam_pack_library(const double* sketches, int S, int D, int S_pad, void* uu,
+                          double* norms, void* stream);
+int moeb_eam_pack_queries(const int32_t* counts, int M, int D, void* cc, void* stream);
+int moeb_eam_rerank(const float* pval, const int32_t* pidx, int ntiles, const int32_t* counts,
+                    const double* sketches, const double* norms, int M, int S, int D,
+                    double eps_rel, int32_t* idx_out, double* sim_out, int32_t* n_rerank,
+                    void* stream);
+
+/* C4 queries: for every prompt and token t >= warmup, the partial rEAM counts
+ * at layer 0 (all rows of tokens < t); out [sum_p (T_p - warmup)][L*E] int32,
+ * prompt p's rows start at query_off[p]. */
+int moeb_token_prefix_counts(const uint64_t* truth, const int64_t* prompt_row_off,
+                             const int64_t* query_off, int n_prompts, int L, int E,
+                             int warmup_tokens, int32_t* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,7 @@
 // to the lower index) picks the sketch; the prediction is a table lookup
 // topw[idx][l] precomputed by moeb_eam_prepare.
 #include <cfloat>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -372,4 +373,232 @@ extern "C" int moeb_match_queries(const double* queries, int M, int D, const dou
   k_match_queries<<<M, 256, smem, moeb::as_stream(stream)>>>(queries, D, unit_t, S, idx_out,
                                                             sim_out);
   return moeb::check_launch("k_match_queries");
+}
+
+// ---------------------------------------------------------------------------
+// K6b -- EAM matching at scale on tensor cores (BASELINE C4).
+//
+// scores[m][s] = C_m . U_s with C_m integer activation counts (exact in fp16
+// up to 2048) and U_s the unit sketch split U = U_hi + 2^-11 U_lo' (both fp16,
+// U_lo' = 2^11 (U - U_hi) kept in the normal fp16 range). The split is
+// K-concatenated, so ONE tcgen05 GEMM computes
+//   [C | 2^-11 C] . [U_hi | U_lo']^T = C . (U_hi + 2^-11 U_lo')
+// with a fused per-(query, 256-sketch tile) max/argmax epilogue (K4
+// EPI_ROWMAX). moeb_eam_rerank then re-scores, in fp64, every tile whose
+// approximate maximum lies within 2 eps of the query's approximate maximum
+// (eps bounds the split + fp32 accumulation error), and returns the exact
+// first argmax -- SketchCollection.match_nearest semantics (sketches.py:165-184).
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void k_eam_pack_library(const double* __restrict__ sk, int S, int D,
+                                   __half* __restrict__ uu, double* __restrict__ norms) {
+  const int s = blockIdx.x;  // rows >= S are zero padding
+  __shared__ double red[32];
+  double acc = 0.0;
+  if (s < S)
+    for (int d = threadIdx.x; d < D; d += blockDim.x) acc = fma(sk[(int64_t)s * D + d], sk[(int64_t)s * D + d], acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  double n2 = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) n2 += red[w];
+  double nrm = sqrt(n2);
+  if (!(nrm > 0.0)) nrm = 1.0;  // zero rows stay zero (sketches.py:158-160)
+  if (threadIdx.x == 0 && s < S) norms[s] = nrm;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    const double u = s < S ? sk[(int64_t)s * D + d] / nrm : 0.0;
+    const __half hi = __double2half(u);
+    const __half lo = __double2half((u - (double)__half2float(hi)) * 2048.0);
+    uu[(int64_t)s * 2 * D + d] = hi;
+    uu[(int64_t)s * 2 * D + D + d] = lo;
+  }
+}
+
+__global__ void k_eam_pack_queries(const int32_t* __restrict__ counts, int M, int D,
+                                   __half* __restrict__ cc) {
+  const int64_t n = (int64_t)M * D;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / D, d = i % D;
+    const float c = (float)counts[i];
+    cc[m * 2 * D + d] = __float2half_rn(c);
+    cc[m * 2 * D + D + d] = __float2half_rn(c * (1.0f / 2048.0f));  // exact: power-of-two scale
+  }
+}
+
+__global__ void __launch_bounds__(256) k_eam_rerank(
+    const float* __restrict__ pval, const int32_t* __restrict__ pidx, int ntiles,
+    const int32_t* __restrict__ counts, const double* __restrict__ sk,
+    const double* __restrict__ norms, int S, int D, double eps_rel, int32_t* __restrict__ idx_out,
+    double* __restrict__ sim_out, int32_t* __restrict__ n_rerank) {
+  extern __shared__ double cq[];  // query counts as doubles [D]
+  __shared__ float red_f[8];
+  __shared__ double red_v[8];
+  __shared__ int red_i[8];
+  const int m = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double q2 = 0.0;
+  for (int d = tid; d < D; d += blockDim.x) {
+    const double c = counts[(int64_t)m * D + d];
+    cq[d] = c;
+    q2 += c * c;
+  }
+  float gm = -INFINITY;
+  for (int t = tid; t < ntiles; t += blockDim.x) gm = fmaxf(gm, pval[(int64_t)m * ntiles + t]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+  }
+  if (lane == 0) {
+    red_f[warp] = gm;
+    red_v[warp] = q2;
+  }
+  __syncthreads();
+  gm = red_f[0];
+  q2 = red_v[0];
+  for (int w = 1; w < 8; ++w) {
+    gm = fmaxf(gm, red_f[w]);
+    q2 += red_v[w];
+  }
+  __syncthreads();
+  if (q2 == 0.0) {  // zero query: index 0, similarity 0 (sketches.py:179-181)
+    if (tid == 0) {
+      idx_out[m] = 0;
+      if (sim_out) sim_out[m] = 0.0;
+    }
+    return;
+  }
+  const float thr = (float)((double)gm - 2.0 * (eps_rel * fabs((double)gm) + 1e-30));
+  double best = -1.0;
+  int bi = 0x7fffffff, cnt = 0;
+  for (int t = 0; t < ntiles; ++t) {
+    if (pval[(int64_t)m * ntiles + t] < thr) continue;  // block-uniform
+    ++cnt;
+    // one warp per sketch, lanes over d (coalesced rows)
+    for (int j = warp; j < 256; j += 8) {
+      const int s = t * 256 + j;
+      if (s >= S) break;
+      const double* row = sk + (int64_t)s * D;
+      double acc = 0.0;
+      for (int d = lane; d < D; d += 32) acc = fma(row[d], cq[d], acc);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const double v = acc / norms[s];
+      if (v > best || (v == best && s < bi)) {
+        best = v;
+        bi = s;
+      }
+    }
+  }
+  if (lane == 0) {
+    red_v[warp] = best;
+    red_i[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < 8; ++w)
+      if (red_v[w] > best || (red_v[w] == best && red_i[w] < bi)) {
+        best = red_v[w];
+        bi = red_i[w];
+      }
+    idx_out[m] = bi;
+    if (sim_out) {
+      const double c = best / sqrt(q2);
+      sim_out[m] = c > 1.0 ? 1.0 : (c < -1.0 ? -1.0 : c);
+    }
+    if (n_rerank) n_rerank[m] = cnt;
+  }
+}
+
+}  // namespace
+
+extern "C" int moeb_eam_pack_library(const double* sketches, int S, int D, int S_pad,
+                                     void* uu, double* norms, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(sketches && uu && norms && S >= 1 && S_pad >= S && D >= 1, "bad arguments");
+  k_eam_pack_library<<<S_pad, 256, 0, moeb::as_stream(stream)>>>(
+      sketches, S, D, static_cast<__half*>(uu), norms);
+  return moeb::check_launch("k_eam_pack_library");
+}
+
+extern "C" int moeb_eam_pack_queries(const int32_t* counts, int M, int D, void* cc,
+                                     void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(counts && cc && M >= 0 && D >= 1, "bad arguments");
+  if (M == 0) return MOEB_OK;
+  k_eam_pack_queries<<<148 * 8, 256, 0, moeb::as_stream(stream)>>>(counts, M, D,
+                                                                   static_cast<__half*>(cc));
+  return moeb::check_launch("k_eam_pack_queries");
+}
+
+extern "C" int moeb_eam_rerank(const float* pval, const int32_t* pidx, int ntiles,
+                               const int32_t* counts, const double* sketches,
+                               const double* norms, int M, int S, int D, double eps_rel,
+                               int32_t* idx_out, double* sim_out, int32_t* n_rerank,
+                               void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(pval && counts && sketches && norms && idx_out && M >= 0, "bad arguments");
+  if (M == 0) return MOEB_OK;
+  const size_t smem = sizeof(double) * (size_t)D;
+  cudaFuncSetAttribute(k_eam_rerank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_eam_rerank<<<M, 256, smem, moeb::as_stream(stream)>>>(pval, pidx, ntiles, counts, sketches,
+                                                          norms, S, D, eps_rel, idx_out, sim_out,
+                                                          n_rerank);
+  return moeb::check_launch("k_eam_rerank");
+}
+
+// Per-token partial rEAM counts at layer 0 (C4 queries): for every prompt
+// and token t >= warmup, the counts of all rows of tokens < t.
+namespace {
+template <int W>
+__global__ void k_token_prefix_counts(const uint64_t* __restrict__ truth,
+                                      const int64_t* __restrict__ row_off,
+                                      const int64_t* __restrict__ q_off, int L, int E, int warmup,
+                                      int32_t* __restrict__ out) {
+  extern __shared__ int32_t cnt[];  // [L*E]
+  const int p = blockIdx.x;
+  const int D = L * E;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  const int64_t r0 = row_off[p];
+  const int T = (int)((row_off[p + 1] - r0) / L);
+  int64_t q = q_off[p];
+  for (int t = 0; t < T; ++t) {
+    if (t >= warmup) {
+      for (int i = threadIdx.x; i < D; i += blockDim.x) out[q * D + i] = cnt[i];
+      ++q;
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+      const uint64_t* row = truth + (r0 + (int64_t)t * L + l) * W;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        uint64_t m = row[w];
+        while (m) {
+          cnt[l * E + w * 64 + __ffsll((long long)m) - 1] += 1;
+          m &= m - 1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+extern "C" int moeb_token_prefix_counts(const uint64_t* truth, const int64_t* prompt_row_off,
+                                        const int64_t* query_off, int n_prompts, int L, int E,
+                                        int warmup_tokens, int32_t* out, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(truth && prompt_row_off && query_off && out && n_prompts >= 1, "bad arguments");
+  const size_t smem = sizeof(int32_t) * (size_t)L * E;
+  cudaStream_t s = moeb::as_stream(stream);
+  switch (moeb::words_for(E)) {
+    case 1: k_token_prefix_counts<1><<<n_prompts, 128, smem, s>>>(truth, prompt_row_off, query_off, L, E, warmup_tokens, out); break;
+    case 2: k_token_prefix_counts<2><<<n_prompts, 128, smem, s>>>(truth, prompt_row_off, query_off, L, E, warmup_tokens, out); break;
+    case 3: k_token_prefix_counts<3><<<n_prompts, 128, smem, s>>>(truth, prompt_row_off, query_off, L, E, warmup_tokens, out); break;
+    default: k_token_prefix_counts<4><<<n_prompts, 128, smem, s>>>(truth, prompt_row_off, query_off, L, E, warmup_tokens, out); break;
+  }
+  return moeb::check_launch("k_token_prefix_counts");
 }

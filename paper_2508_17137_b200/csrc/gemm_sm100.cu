@@ -26,7 +26,14 @@ namespace {
 
 using namespace moeb::tc;
 
-enum : int { EPI_F32 = 0, EPI_BIAS = 1, EPI_BIAS_RELU = 2, EPI_BIAS_GELU = 3, EPI_RESID_LN = 4 };
+enum : int {
+  EPI_F32 = 0,
+  EPI_BIAS = 1,
+  EPI_BIAS_RELU = 2,
+  EPI_BIAS_GELU = 3,
+  EPI_RESID_LN = 4,
+  EPI_ROWMAX = 5  // per (row, N-tile): max value (out32) and first argmax column (out16 as int32)
+};
 
 struct GemmArgs {
   int M, N, K;
@@ -37,6 +44,7 @@ struct GemmArgs {
   const float* ln_w;
   const float* ln_b;
   float ln_eps;
+  int raster_m;  // 1: m-fastest tile order (B tiles stream from HBM once)
 };
 
 constexpr int BM = 128;
@@ -108,8 +116,10 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        // n-fastest raster: consecutive CTAs share the A tile in L2
-        const int tn = tile % tiles_n, tm = tile / tiles_n;
+        // n-fastest raster: consecutive CTAs share the A tile in L2 (m-fastest
+        // when B is the large streamed operand)
+        const int tn = g.raster_m ? tile / tiles_m : tile % tiles_n;
+        const int tm = g.raster_m ? tile % tiles_m : tile / tiles_n;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
@@ -169,7 +179,8 @@ __global__ void __launch_bounds__(192, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int tn = tile % tiles_n, tm = tile / tiles_n;
+      const int tn = g.raster_m ? tile / tiles_m : tile % tiles_n;
+      const int tm = g.raster_m ? tile % tiles_m : tile / tiles_n;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = tm * BM + quarter * 32 + lane;
@@ -236,6 +247,27 @@ __global__ void __launch_bounds__(192, 1)
             }
           }
           __syncwarp();
+        }
+      } else if (EPI == EPI_ROWMAX) {
+        float best = -INFINITY;
+        int bi = 0;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(t0 + c0, r);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float v = __uint_as_float(r[j]);
+            if (v > best) {  // ascending columns: first maximum
+              best = v;
+              bi = tn * BN + c0 + j;
+            }
+          }
+        }
+        if (rv) {
+          const int ntl = g.N / BN;
+          g.out32[(int64_t)row * ntl + tn] = best;
+          reinterpret_cast<int32_t*>(g.out16)[(int64_t)row * ntl + tn] = bi;
         }
       } else {
         for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -353,7 +385,7 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
   moeb::clear_error();
   MOEB_REQUIRE(A && B && M >= 1 && N >= 1 && K >= 1, "bad GEMM arguments");
   MOEB_REQUIRE(K % BK == 0, "K must be a multiple of %d (got %d)", BK, K);
-  MOEB_REQUIRE(epi >= EPI_F32 && epi <= EPI_RESID_LN, "unknown epilogue %d", epi);
+  MOEB_REQUIRE(epi >= EPI_F32 && epi <= EPI_ROWMAX, "unknown epilogue %d", epi);
   int bn;
   if (epi == EPI_RESID_LN) {
     MOEB_REQUIRE(N == 512, "LayerNorm epilogue needs N == 512");
@@ -363,17 +395,19 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
     bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : 0;
     MOEB_REQUIRE(bn, "N must be a multiple of 64 (got %d)", N);
     MOEB_REQUIRE(epi == EPI_F32 ? out32 != nullptr : out16 != nullptr, "missing output");
+    MOEB_REQUIRE(epi != EPI_ROWMAX || (out32 && bn == 256), "row-max epilogue needs N % 256 == 0");
   }
   CUtensorMap ta, tb;
   if (int rc = make_map(&ta, A, M, K, lda, BM, fp16)) return rc;
   if (int rc = make_map(&tb, B, N, K, ldb, bn < 256 ? bn : 256, fp16)) return rc;
-  GemmArgs g{M, N, K, bias, out32, out16, ld16, ln_w, ln_b, ln_eps};
+  GemmArgs g{M, N, K, bias, out32, out16, ld16, ln_w, ln_b, ln_eps, epi == EPI_ROWMAX ? 1 : 0};
   cudaStream_t s = moeb::as_stream(stream);
   switch (epi) {
     case EPI_F32: return fp16 ? dispatch<EPI_F32, true>(ta, tb, g, bn, s) : dispatch<EPI_F32, false>(ta, tb, g, bn, s);
     case EPI_BIAS: return fp16 ? dispatch<EPI_BIAS, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS, false>(ta, tb, g, bn, s);
     case EPI_BIAS_RELU: return fp16 ? dispatch<EPI_BIAS_RELU, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS_RELU, false>(ta, tb, g, bn, s);
     case EPI_BIAS_GELU: return fp16 ? dispatch<EPI_BIAS_GELU, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS_GELU, false>(ta, tb, g, bn, s);
+    case EPI_ROWMAX: return fp16 ? launch_gemm<256, 4, EPI_ROWMAX, true>(ta, tb, g, s) : launch_gemm<256, 4, EPI_ROWMAX, false>(ta, tb, g, s);
     default: return fp16 ? launch_gemm<512, 2, EPI_RESID_LN, true>(ta, tb, g, s) : launch_gemm<512, 2, EPI_RESID_LN, false>(ta, tb, g, s);
   }
 }

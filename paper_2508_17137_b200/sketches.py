@@ -181,3 +181,66 @@ def load_eamc(path) -> SketchCollection:
     if sketches.size == 0:
         raise ConfigError(f"no sketches in {path}")
     return SketchCollection(sketches, config, shape)
+
+
+class TensorCoreMatcher:
+    """SketchCollection.match_nearest for many count-vector queries at once on
+    tensor cores (BASELINE C4; K6b): one tcgen05 GEMM over the
+    fp16-split unit sketches with a fused per-tile max/argmax epilogue, then
+    an fp64 re-rank of near-tie tiles. Exact first-argmax semantics."""
+
+    EPS_REL = 3e-5  # bound on split + fp32-accumulation error, relative to the max score
+
+    def __init__(self, collection: SketchCollection, device=None):
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        S, D = collection.sketches.shape
+        if D % 32:
+            raise DimensionError("sketch length must be a multiple of 32")
+        self.S, self.D, self.S_pad = S, D, (S + 255) // 256 * 256
+        self.sketches = torch.from_numpy(np.ascontiguousarray(collection.sketches)).to(dev)
+        self.uu = torch.empty((self.S_pad, 2 * D), dtype=torch.float16, device=dev)
+        self.norms = torch.empty(S, dtype=torch.float64, device=dev)
+        nat.call("moeb_eam_pack_library", nat.ptr(self.sketches), S, D, self.S_pad,
+                 nat.ptr(self.uu), nat.ptr(self.norms), nat.stream_ptr())
+        self.device = dev
+
+    def match_counts(self, counts: torch.Tensor, timing: dict | None = None):
+        """counts [M][D] int32 (partial rEAM counts with equal per-layer row sums,
+        e.g. layer-0 queries) -> (idx int32 [M], cosine fp64 [M], tiles re-ranked)."""
+        from .transformer import gemm
+        counts = counts.to(torch.int32).contiguous()
+        M = counts.shape[0]
+        dev = self.device
+        cc = torch.empty((max(M, 1), 2 * self.D), dtype=torch.float16, device=dev)
+        nat.call("moeb_eam_pack_queries", nat.ptr(counts), M, self.D, nat.ptr(cc),
+                 nat.stream_ptr())
+        nt = self.S_pad // 256
+        pval = torch.empty((max(M, 1), nt), dtype=torch.float32, device=dev)
+        pidx = torch.empty((max(M, 1), nt), dtype=torch.int32, device=dev)
+        e0 = e1 = None
+        if timing is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        gemm(cc, self.uu, M, self.S_pad, 2 * self.D, 5, out32=pval, out16=pidx, fp16=True)
+        if timing is not None:
+            e1.record()
+            timing.setdefault("gemm_rowmax", []).append((e0, e1, 2.0 * M * self.S * self.D))
+        idx = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        sim = torch.empty(max(M, 1), dtype=torch.float64, device=dev)
+        nrr = torch.empty(max(M, 1), dtype=torch.int32, device=dev)
+        nat.call("moeb_eam_rerank", nat.ptr(pval), nat.ptr(pidx), nt, nat.ptr(counts),
+                 nat.ptr(self.sketches), nat.ptr(self.norms), M, self.S, self.D,
+                 float(self.EPS_REL), nat.ptr(idx), nat.ptr(sim), nat.ptr(nrr), nat.stream_ptr())
+        return idx[:M], sim[:M], nrr[:M]
+
+
+def token_query_counts(packed, warmup: int) -> torch.Tensor:
+    """Layer-0 partial rEAM counts for every prompt token >= warmup (C4 queries)."""
+    L, E = packed.shape.num_layers, packed.shape.num_experts
+    per = np.maximum(packed.num_tokens - warmup, 0)
+    qoff = np.concatenate([[0], np.cumsum(per)]).astype(np.int64)
+    out = torch.empty((max(int(qoff[-1]), 1), L * E), dtype=torch.int32, device=packed.device)
+    qd = torch.from_numpy(qoff).to(packed.device)
+    nat.call("moeb_token_prefix_counts", nat.ptr(packed.truth), nat.ptr(packed.row_off),
+             nat.ptr(qd), packed.num_prompts, L, E, int(warmup), nat.ptr(out), nat.stream_ptr())
+    return out[:int(qoff[-1])]
