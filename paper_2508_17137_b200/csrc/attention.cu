@@ -3,9 +3,11 @@
 //
 // qkv [rows][1536] 16-bit from the QKV GEMM (q | k | v, head h at columns
 // 64h..64h+63 of each third); out [rows][512] 16-bit. One CTA = (window,
-// head, 64-query block); 4 warps x 16 queries; key blocks of 64 staged in
-// XOR-swizzled shared memory; S = Q K^T and O += P V with mma.sync
-// m16n8k16 (fp32 accumulate), online softmax in fp32 (exp2 form).
+// head, 128-query block); key blocks of 64 staged in
+// XOR-swizzled shared memory, double-buffered with cp.async (zero-filled
+// beyond the window); 8 warps x 16 queries = 128 queries per CTA; S = Q K^T
+// and O += P V with mma.sync m16n8k16 (fp32 accumulate), online softmax in
+// fp32 (exp2 form).
 // (Round-1 kernel: the tcgen05/TMEM attention is the DESIGN.md next step.)
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -15,7 +17,7 @@
 namespace {
 
 constexpr int D = 64;
-constexpr int QB = 64;  // queries per CTA
+constexpr int QB = 128;  // queries per CTA (8 warps x 16)
 constexpr int KB = 64;  // keys per block
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -69,10 +71,33 @@ __device__ __forceinline__ uint32_t pack2(float x, float y) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// copy a [64 rows][64] 16-bit block (rows beyond n zero-filled) into a
-// swizzled tile; 128 threads, 16 bytes each x 4
-__device__ __forceinline__ void load_tile(uint16_t* tile, const uint16_t* src, int ld, int n) {
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// asynchronously copy a [64 rows][64] 16-bit block (rows >= n zero-filled)
+__device__ __forceinline__ void load_tile_async(uint16_t* tile, const uint16_t* src, int ld,
+                                                int n) {
   for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x) {
+    const int row = i >> 3, ch = i & 7;
+    const bool v = row < n;
+    cp_async16(smem_u32(tile + swz(row, ch * 8)), src + (int64_t)(v ? row : 0) * ld + ch * 8, v);
+  }
+}
+
+// copy a [rows][64] 16-bit block (rows beyond n zero-filled) into a
+// swizzled tile
+template <int ROWS = 64>
+__device__ __forceinline__ void load_tile(uint16_t* tile, const uint16_t* src, int ld, int n) {
+  for (int i = threadIdx.x; i < ROWS * 8; i += blockDim.x) {
     const int row = i >> 3, ch = i & 7;
     uint4 v = make_uint4(0, 0, 0, 0);
     if (row < n) v = *reinterpret_cast<const uint4*>(src + (int64_t)row * ld + ch * 8);
@@ -81,13 +106,13 @@ __device__ __forceinline__ void load_tile(uint16_t* tile, const uint16_t* src, i
 }
 
 template <bool FP16>
-__global__ void __launch_bounds__(128) k_window_attention(const uint16_t* __restrict__ qkv,
-                                                          uint16_t* __restrict__ out,
-                                                          const int64_t* __restrict__ win_start,
-                                                          const int32_t* __restrict__ win_len) {
+__global__ void __launch_bounds__(256, 2) k_window_attention(const uint16_t* __restrict__ qkv,
+                                                             uint16_t* __restrict__ out,
+                                                             const int64_t* __restrict__ win_start,
+                                                             const int32_t* __restrict__ win_len) {
   __shared__ __align__(128) uint16_t sQ[QB * D];
-  __shared__ __align__(128) uint16_t sK[KB * D];
-  __shared__ __align__(128) uint16_t sV[KB * D];
+  __shared__ __align__(128) uint16_t sK[2][KB * D];
+  __shared__ __align__(128) uint16_t sV[2][KB * D];
   const int w = blockIdx.x, head = blockIdx.y, qb = blockIdx.z;
   const int n = win_len[w];
   if (qb * QB >= n) return;
@@ -97,7 +122,10 @@ __global__ void __launch_bounds__(128) k_window_attention(const uint16_t* __rest
   const uint16_t* Kg = qkv + r0 * ld + 512 + head * D;
   const uint16_t* Vg = qkv + r0 * ld + 1024 + head * D;
   const int nq = min(QB, n - qb * QB);
-  load_tile(sQ, Qg, ld, nq);
+  load_tile_async(sK[0], Kg, ld, n);
+  load_tile_async(sV[0], Vg, ld, n);
+  cp_async_commit();
+  load_tile<QB>(sQ, Qg, ld, nq);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tig = lane & 3;
@@ -108,21 +136,28 @@ __global__ void __launch_bounds__(128) k_window_attention(const uint16_t* __rest
   for (int j = 0; j < 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
   float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
   uint32_t qa[4][4];  // Q fragments for the 4 k-steps of d = 64
-
-  for (int kb0 = 0; kb0 < n; kb0 += KB) {
-    const int nk = min(KB, n - kb0);
-    __syncthreads();
-    load_tile(sK, Kg + (int64_t)kb0 * ld, ld, nk);
-    load_tile(sV, Vg + (int64_t)kb0 * ld, ld, nk);
-    __syncthreads();
-    if (kb0 == 0) {
+  __syncthreads();
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const int row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-        const int col = ks * 16 + (lane >> 4) * 8;
-        ldsm_x4(smem_u32(sQ + swz(row, col)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
-      }
+  for (int ks = 0; ks < 4; ++ks) {
+    const int row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+    const int col = ks * 16 + (lane >> 4) * 8;
+    ldsm_x4(smem_u32(sQ + swz(row, col)), qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+  }
+
+  int buf = 0;
+  for (int kb0 = 0; kb0 < n; kb0 += KB, buf ^= 1) {
+    const int nk = min(KB, n - kb0);
+    if (kb0 + KB < n) {  // prefetch the next key block into the other buffer
+      load_tile_async(sK[buf ^ 1], Kg + (int64_t)(kb0 + KB) * ld, ld, n - kb0 - KB);
+      load_tile_async(sV[buf ^ 1], Vg + (int64_t)(kb0 + KB) * ld, ld, n - kb0 - KB);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
+    __syncthreads();
+    const uint16_t* cK = sK[buf];
+    const uint16_t* cV = sV[buf];
     // S = Q K^T : 16 x 64 per warp
     float s[8][4];
 #pragma unroll
@@ -134,7 +169,7 @@ __global__ void __launch_bounds__(128) k_window_attention(const uint16_t* __rest
         uint32_t b0, b1, b2, b3;
         const int key = jp * 16 + (lane & 7) + (lane >> 4) * 8;
         const int col = ks * 16 + ((lane >> 3) & 1) * 8;
-        ldsm_x4(smem_u32(sK + swz(key, col)), b0, b1, b2, b3);
+        ldsm_x4(smem_u32(cK + swz(key, col)), b0, b1, b2, b3);
         mma16816<FP16>(s[2 * jp], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
         mma16816<FP16>(s[2 * jp + 1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
       }
@@ -187,11 +222,12 @@ __global__ void __launch_bounds__(128) k_window_attention(const uint16_t* __rest
         uint32_t b0, b1, b2, b3;
         const int key = ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
         const int col = jp * 16 + (lane >> 4) * 8;
-        ldsm_x4_t(smem_u32(sV + swz(key, col)), b0, b1, b2, b3);
+        ldsm_x4_t(smem_u32(cV + swz(key, col)), b0, b1, b2, b3);
         mma16816<FP16>(o[2 * jp], a0, a1, a2, a3, b0, b1);
         mma16816<FP16>(o[2 * jp + 1], a0, a1, a2, a3, b2, b3);
       }
     }
+    __syncthreads();  // buffer `buf` is refilled two iterations later
   }
   // finalize: row sums across the 4 threads of a row group
 #pragma unroll
@@ -225,10 +261,10 @@ extern "C" int moeb_window_attention(const void* qkv, void* out, const int64_t* 
   dim3 grid((unsigned)n_windows, 8, (unsigned)((max_len + QB - 1) / QB));
   cudaStream_t s = moeb::as_stream(stream);
   if (fp16)
-    k_window_attention<true><<<grid, 128, 0, s>>>(static_cast<const uint16_t*>(qkv),
+    k_window_attention<true><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(qkv),
                                                   static_cast<uint16_t*>(out), win_start, win_len);
   else
-    k_window_attention<false><<<grid, 128, 0, s>>>(static_cast<const uint16_t*>(qkv),
+    k_window_attention<false><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(qkv),
                                                    static_cast<uint16_t*>(out), win_start, win_len);
   return moeb::check_launch("k_window_attention");
 }
