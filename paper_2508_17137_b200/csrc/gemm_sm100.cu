@@ -12,7 +12,8 @@
 // Persistent, warp-specialised: warp 0 = TMA producer (128-byte-swizzled
 // tiles, mbarrier ring of STAGES), warp 1 = MMA issuer (one elected thread,
 // tcgen05.mma.cta_group::1.kind::f16, M = 128, N <= 256 per instruction),
-// warps 2..5 = epilogue (tcgen05.ld 32x32b, one TMEM lane = one output row).
+// warps 2..9 = epilogue (tcgen05.ld 32x32b, one TMEM lane = one output row;
+// two warps per lane quarter split the columns).
 // Two TMEM accumulators (when BN <= 256) let the epilogue of tile i overlap
 // the mainloop of tile i+1.
 #include <cuda.h>
@@ -60,7 +61,7 @@ __device__ __forceinline__ float gelu_erf(float x) {
 }
 
 template <int BN, int STAGES, int EPI, bool FP16>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const GemmArgs g) {
   constexpr int ACC = BN <= 256 ? 2 : 1;           // TMEM accumulator buffers
@@ -83,7 +84,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + ACC;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(tempty + ACC);
-  // per-epilogue-warp 32 x 33 fp32 transpose tiles (LayerNorm epilogue)
+  // per-epilogue-warp 32 x 33 fp32 transpose tiles (LayerNorm epilogue),
+  // then the pair-exchange area (8 warps x 32 lanes x 8 bytes)
   float* tbuf = reinterpret_cast<float*>(tmem_base_smem + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int b = 0; b < ACC; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[b], 8);  // one arrive per epilogue warp
     }
     fence_mbar_init();
   }
@@ -174,8 +176,17 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ===== epilogue warps 2..5: TMEM lane quarter = warp % 4 =====
+    // ===== epilogue warps 2..9: TMEM lane quarter = warp % 4; the two warps
+    // of a quarter split the tile's columns (half = (warp - 2) / 4) =====
     const int quarter = warp & 3;
+    const int ew = warp - 2;
+    const int half = ew >> 2;
+    constexpr int HC = BN / 2;  // columns per epilogue warp
+    const int cb = half * HC;
+    float2* xch = reinterpret_cast<float2*>(tbuf + (EPI == EPI_RESID_LN ? 8 * 32 * 33 : 0));
+    auto pair_sync = [&]() {  // the two warps sharing this lane quarter
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+    };
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -187,24 +198,24 @@ __global__ void __launch_bounds__(192, 1)
       const bool rv = row < g.M;
       const uint32_t t0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       if (EPI == EPI_RESID_LN) {
-        // pass 1: x = resid + acc + bias, stashed back into TMEM; row stats.
-        // Residual chunks [32 rows x 32 cols] are read coalesced (one row per
-        // instruction, lane = column) and transposed through shared memory.
-        float* T = tbuf + quarter * (32 * 33);
+        // pass 1: x = resid + acc + bias, stashed back into TMEM; partial row
+        // stats over this warp's columns. Residual chunks [32 rows x 32 cols]
+        // are read coalesced (lane = column) and transposed via shared memory.
+        float* T = tbuf + ew * (32 * 33);
         const int rowbase = tm * BM + quarter * 32;
         float s1 = 0.f, s2 = 0.f;
         float nxt[32];  // next chunk's residual column (software pipelined)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const int rr = rowbase + i;
-          nxt[i] = rr < g.M ? __ldg(g.out32 + (int64_t)rr * g.N + lane) : 0.f;
+          nxt[i] = rr < g.M ? __ldg(g.out32 + (int64_t)rr * g.N + cb + lane) : 0.f;
         }
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = cb; c0 < cb + HC; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
 #pragma unroll
           for (int i = 0; i < 32; ++i) T[i * 33 + lane] = nxt[i];
-          if (c0 + 32 < BN) {
+          if (c0 + 32 < cb + HC) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               const int rr = rowbase + i;
@@ -215,7 +226,7 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const float x = __uint_as_float(r[j]) + g.bias[c0 + j] + T[lane * 33 + j];
+            const float x = __uint_as_float(r[j]) + __ldg(g.bias + c0 + j) + T[lane * 33 + j];
             r[j] = __float_as_uint(x);
             s1 += x;
             s2 += x * x;
@@ -224,17 +235,24 @@ __global__ void __launch_bounds__(192, 1)
           tmem_st32(t0 + c0, r);
         }
         tmem_st_wait();
+        xch[ew * 32 + lane] = make_float2(s1, s2);
+        pair_sync();
+        const float2 o = xch[(ew ^ 4) * 32 + lane];
+        pair_sync();  // partner read done before the next tile overwrites
+        s1 += o.x;
+        s2 += o.y;
         const float mean = s1 / BN;
         const float var = fmaxf(s2 / BN - mean * mean, 0.f);
         const float rstd = rsqrtf(var + g.ln_eps);
         // pass 2: y = LN(x); coalesced stores of fp32 (in place) and 16-bit
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = cb; c0 < cb + HC; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            T[lane * 33 + j] = (__uint_as_float(r[j]) - mean) * rstd * g.ln_w[c0 + j] + g.ln_b[c0 + j];
+            T[lane * 33 + j] = (__uint_as_float(r[j]) - mean) * rstd * __ldg(g.ln_w + c0 + j) +
+                               __ldg(g.ln_b + c0 + j);
           __syncwarp();
           uint16_t* o16 = reinterpret_cast<uint16_t*>(g.out16);
 #pragma unroll 8
@@ -251,7 +269,7 @@ __global__ void __launch_bounds__(192, 1)
       } else if (EPI == EPI_ROWMAX) {
         float best = -INFINITY;
         int bi = 0;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = cb; c0 < cb + HC; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
           tmem_ld_wait();
@@ -264,22 +282,43 @@ __global__ void __launch_bounds__(192, 1)
             }
           }
         }
-        if (rv) {
-          const int ntl = g.N / BN;
-          g.out32[(int64_t)row * ntl + tn] = best;
-          reinterpret_cast<int32_t*>(g.out16)[(int64_t)row * ntl + tn] = bi;
+        xch[ew * 32 + lane] = make_float2(best, __int_as_float(bi));
+        pair_sync();
+        if (half == 0) {
+          const float2 o = xch[(ew ^ 4) * 32 + lane];  // upper columns: wins only if larger
+          if (o.x > best) {
+            best = o.x;
+            bi = __float_as_int(o.y);
+          }
+          if (rv) {
+            const int ntl = g.N / BN;
+            g.out32[(int64_t)row * ntl + tn] = best;
+            reinterpret_cast<int32_t*>(g.out16)[(int64_t)row * ntl + tn] = bi;
+          }
         }
+        pair_sync();
       } else {
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = cb; c0 < cb + HC; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
+          const int col = tn * BN + c0;
+          float4 bb[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            bb[q] = g.bias ? __ldg(reinterpret_cast<const float4*>(g.bias + col) + q)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
           tmem_ld_wait();
           if (!rv) continue;
-          const int col = tn * BN + c0;
           float v[32];
 #pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            v[4 * q] = __uint_as_float(r[4 * q]) + bb[q].x;
+            v[4 * q + 1] = __uint_as_float(r[4 * q + 1]) + bb[q].y;
+            v[4 * q + 2] = __uint_as_float(r[4 * q + 2]) + bb[q].z;
+            v[4 * q + 3] = __uint_as_float(r[4 * q + 3]) + bb[q].w;
+          }
+#pragma unroll
           for (int j = 0; j < 32; ++j) {
-            v[j] = __uint_as_float(r[j]) + (g.bias ? g.bias[col + j] : 0.f);
             if (EPI == EPI_BIAS_RELU) v[j] = fmaxf(v[j], 0.f);
             if (EPI == EPI_BIAS_GELU) v[j] = gelu_erf(v[j]);
           }
@@ -358,12 +397,12 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
-                      (EPI == EPI_RESID_LN ? 4 * 32 * 33 * sizeof(float) : 0);
+                      (EPI == EPI_RESID_LN ? 8 * 32 * 33 * sizeof(float) : 0) + 8 * 32 * 8;
   auto k = k_gemm<BN, STAGES, EPI, FP16>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
   const int grid = tiles < moeb::num_sms() ? tiles : moeb::num_sms();
-  k<<<grid, 192, smem, s>>>(ta, tb, g);
+  k<<<grid, 320, smem, s>>>(ta, tb, g);
   return moeb::check_launch("k_gemm");
 }
 
