@@ -243,21 +243,15 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    pipe = m.PipelinedReplay(packed, args.chunks)
+
     def step(timing=None):
         vec = m.metrics.metric_vector(E, dev)
-        e0, e1, e2 = ev(), ev(), ev()
-        e0.record(stream)
-        masks = pred.predict_masks(packed, BUDGET, WARMUP_TOKENS, metrics=vec)
-        e1.record(stream)
-        counters, _, _ = m.cache_replay(packed, [(masks, None, False)], [cap], WARMUP_TOKENS,
-                                        BUDGET, want_per_prompt=False)
-        e2.record(stream)
+        counters = pipe.run(pred, [cap], WARMUP_TOKENS, BUDGET, metrics=vec, timing=timing)
         if world > 1:
             buf = torch.cat([counters.view(-1), vec])
             dist.all_reduce(buf)
             counters, vec = buf[:counters.numel()].view(counters.shape), buf[counters.numel():]
-        if timing is not None:
-            timing.append((e0, e1, e2))
         return counters, vec
 
     # --- warm-up ---
@@ -287,8 +281,11 @@ def run_ours(args):
         ms = float(t.item())
     ms_step = ms / args.steps
     value = tokens_per_rank * world / (ms / 1000.0) * args.steps
-    lin_ms = statistics.mean(a.elapsed_time(b) for a, b, _ in timing)
-    sim_ms = statistics.mean(b.elapsed_time(c) for _, b, c in timing)
+    # per-step kernel time of each stage (sum over the step's chunk launches;
+    # launches of the two stages overlap on separate streams)
+    lin_ms = sum(a.elapsed_time(b) for k, a, b, _ in timing if k == "predict") / args.steps
+    sim_ms = sum(a.elapsed_time(b) for k, a, b, _ in timing if k == "replay") / args.steps
+    n_launch = len(timing) // args.steps
     clock_info = clocks.summary()
 
     c = counters[0, 0].cpu().numpy()
@@ -300,16 +297,14 @@ def run_ours(args):
     truth_d = torch.empty_like(packed.truth)
     off_d = torch.empty_like(packed.row_off)
     e2e_packed = m.PackedTraces(shape, truth_d, off_d, packed.row_off_host, packed.prompt_ids)
-    h2d = truth_host.numel() * 8 + off_host.numel() * 8
+    e2e_pipe = m.PipelinedReplay(e2e_packed, args.chunks)
+    h2d = truth_host.numel() * 8 + e2e_pipe.h2d_offset_bytes
     d2h = (4 + 3 * L) * 8 + (3 * E + 3) * 8
 
     def e2e_step():
-        truth_d.copy_(truth_host, non_blocking=True)
-        off_d.copy_(off_host, non_blocking=True)
         vec2 = m.metrics.metric_vector(E, dev)
-        masks = pred.predict_masks(e2e_packed, BUDGET, WARMUP_TOKENS, metrics=vec2)
-        cnt, _, _ = m.cache_replay(e2e_packed, [(masks, None, False)], [cap], WARMUP_TOKENS,
-                                   BUDGET, want_per_prompt=False)
+        cnt = e2e_pipe.run(pred, [cap], WARMUP_TOKENS, BUDGET, metrics=vec2,
+                           host_truth=truth_host)
         if world > 1:
             buf = torch.cat([cnt.view(-1), vec2])
             dist.all_reduce(buf)
@@ -478,12 +473,14 @@ def run_ours(args):
                        "l2": "inputs (528 MB/GPU) larger than L2"},
             "e2e": {"value": e2e_value, "unit": "trace tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": 2 * args.steps,
+            # per chunk: K3 (k_linear_predict) + K7 (k_metrics64) + K1 (k_cache_sim_warp)
+            "gpu_launches": 3 * len(pipe.bounds) * args.steps,
+            "pipeline": {"chunks": len(pipe.bounds), "streams": "predict || replay (|| H2D in e2e)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic,
                          "algorithmic_bytes": f"{bytes_per_row} B/row x {rows} rows"},
-            "kernels_ms": {"k_linear_predict": lin_ms, "k_cache_sim": sim_ms},
+            "kernels_ms": {"k_linear_predict+k_metrics64": lin_ms, "k_cache_sim": sim_ms},
             "hit_rate_10pct": hit,
             "prediction": {"macro_f1": mc.macro_f1(), "position_accuracy": mc.position_accuracy,
                            "label_accuracy": mc.label_accuracy},
@@ -506,6 +503,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--prompts", type=int, default=C2["prompts"])
+    ap.add_argument("--chunks", type=int, default=1,
+                    help="prompt chunks pipelined across the predict / replay streams")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eam-sketches", type=int, default=100000,
                     help="EAM library size for the C4 matcher leg (0: skip)")

@@ -718,21 +718,29 @@ __device__ __forceinline__ int rank_below(const uint64_t (&m)[W], int e) {
   return c;
 }
 
-template <int W, int ES>
+template <int W, int ES, int G>
 __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
+  // G lanes per simulation (32: one per warp; 16: two per warp). All
+  // collectives below are restricted to the group's lanes (gmask), so the
+  // two groups of a warp may diverge (fallback rows, different row counts).
+  static_assert(G == 16 || G == 32, "G must be 16 or 32");
   extern __shared__ __align__(16) unsigned char smem[];
   const int L = a.L, E = a.E;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int hl = lane & (G - 1), gbase = lane - hl;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (0xffffu << gbase);
+  const unsigned glow = G == 32 ? 0xffffffffu : 0xffffu;
   unsigned int* bcnt = reinterpret_cast<unsigned int*>(smem);  // [3L] block counters
   for (int j = threadIdx.x; j < 3 * L; j += blockDim.x) bcnt[j] = 0;
   __syncthreads();
   const int pi = blockIdx.y;
-  const int p = blockIdx.x * nw + wib;
-  const unsigned full = 0xffffffffu;
+  const int sims_per_block = nw * (32 / G);
+  const int sl = wib * (32 / G) + lane / G;  // simulation within the block
+  const int p = blockIdx.x * sims_per_block + sl;
   if (p < a.P) {
-    unsigned char* base = smem + a.off_c + (size_t)wib * a.sim_bytes;
+    unsigned char* base = smem + a.off_c + (size_t)sl * a.sim_bytes;
     LruState<W, ES, false> st;
-    st.init(base, a, L);  // every lane holds the same (warp-uniform) state
+    st.init(base, a, L);  // every lane of the group holds the same state
     uint16_t* pos_of = st.pos_of;
     uint16_t* q = st.q;
     uint64_t* R = st.R;
@@ -747,22 +755,23 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     const uint64_t* __restrict__ tr = a.truth + r0 * W;
     const uint64_t* __restrict__ pr = pred ? pred + r0 * W : nullptr;
     int tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
-    constexpr int kLC = 2;  // per-layer counters for layers lane + 32*j (L <= 64; else smem)
+    constexpr int kLC = 64 / G;  // per-layer counters for layers hl + G*j (L <= 64; else smem)
     unsigned lck[kLC], lcc[kLC], lcp[kLC];
 #pragma unroll
     for (int j = 0; j < kLC; ++j) lck[j] = lcc[j] = lcp[j] = 0;
+    __syncwarp(gmask);
 
-    uint64_t wt[W], wp[W], nt[W], np[W];  // current / next 32-row windows
+    uint64_t wt[W], wp[W], nt[W], np[W];  // current / next G-row windows
 #pragma unroll
     for (int w = 0; w < W; ++w) {
-      wt[w] = lane < nrows ? __ldg(tr + (int64_t)lane * W + w) : 0ull;
-      wp[w] = (pr && lane < nrows) ? __ldg(pr + (int64_t)lane * W + w) : 0ull;
+      wt[w] = hl < nrows ? __ldg(tr + (int64_t)hl * W + w) : 0ull;
+      wp[w] = (pr && hl < nrows) ? __ldg(pr + (int64_t)hl * W + w) : 0ull;
     }
     int l = 0, t = 0;
     for (int64_t i = 0; i < nrows; ++i) {
-      const int slot = (int)(i & 31);
+      const int slot = (int)(i & (G - 1));
       if (slot == 0) {  // prefetch the next window
-        const int64_t j = i + 32 + lane;
+        const int64_t j = i + G + hl;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
           nt[w] = j < nrows ? __ldg(tr + j * W + w) : 0ull;
@@ -772,10 +781,10 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       uint64_t T[W], P[W], K[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        T[w] = __shfl_sync(full, wt[w], slot);
-        P[w] = __shfl_sync(full, wp[w], slot);
+        T[w] = __shfl_sync(gmask, wt[w], slot, G);
+        P[w] = __shfl_sync(gmask, wp[w], slot, G);
       }
-      if (slot == 31) {
+      if (slot == G - 1) {
 #pragma unroll
         for (int w = 0; w < W; ++w) {
           wt[w] = nt[w];
@@ -783,9 +792,13 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         }
       }
       const bool measured = t >= a.warmup;
+      int npk = 0;
 #pragma unroll
-      for (int w = 0; w < W; ++w) K[w] = measured ? P[w] : 0ull;
-      keep_lowest<W>(K, limit);
+      for (int w = 0; w < W; ++w) {
+        K[w] = measured ? P[w] : 0ull;
+        npk += __popcll(K[w]);
+      }
+      if (npk > limit) keep_lowest<W>(K, limit);
       uint64_t Rl[W], S[W], Hm[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
@@ -804,13 +817,13 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       uint32_t newhead = st.head;
       bool applied = false;
       if (!fallback && e > 0) {  // common case: every victim in the first chunk
-        const uint32_t idx = st.head + lane;
-        const bool inr = (uint32_t)lane < st.tail - st.head;
+        const uint32_t idx = st.head + hl;
+        const bool inr = (uint32_t)hl < st.tail - st.head;
         const int key = q[idx & qmask];
         const bool valid = inr && pos_of[key] == (uint16_t)idx;
-        const unsigned vb = __ballot_sync(full, valid);
+        const unsigned vb = (__ballot_sync(gmask, valid) >> gbase) & glow;
         if (__popc(vb) >= e) {
-          const bool victim = valid && __popc(vb & ((1u << lane) - 1)) < e;
+          const bool victim = valid && __popc(vb & ((1u << hl) - 1)) < e;
           int vl = 0, ve = 0;
           bool bad = false;
           if (victim) {
@@ -818,7 +831,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
             ve = st.expert_of(key, vl);
             bad = vl == l && ((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull);
           }
-          if (__any_sync(full, bad)) {
+          if (__any_sync(gmask, bad)) {
             fallback = true;
           } else {
             if (victim) {
@@ -826,7 +839,8 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
               atomicAnd(reinterpret_cast<unsigned int*>(R + vl * W + (ve >> 6)) + ((ve >> 5) & 1),
                         ~(1u << (ve & 31)));
             }
-            newhead = st.head + (32 - __clz(__ballot_sync(full, victim)));
+            const unsigned vict = (__ballot_sync(gmask, victim) >> gbase) & glow;
+            newhead = st.head + (32 - __clz(vict));
             applied = true;
           }
         }
@@ -839,38 +853,39 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
             fallback = true;
             break;
           }
-          const uint32_t idx = pos + lane;
+          const uint32_t idx = pos + hl;
           const bool inr = idx - st.head < st.tail - st.head;
           const int key = q[idx & qmask];
           const bool valid = inr && pos_of[key] == (uint16_t)idx;
-          const unsigned vb = __ballot_sync(full, valid);
+          const unsigned vb = (__ballot_sync(gmask, valid) >> gbase) & glow;
           const int need = e - found;
-          const int rank = __popc(vb & ((1u << lane) - 1));
+          const int rank = __popc(vb & ((1u << hl) - 1));
           const bool victim = valid && rank < need;
           bool bad = false;
           if (victim) {
             const int vl = st.layer_of(key), ve = st.expert_of(key, vl);
             bad = vl == l && ((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull);
           }
-          if (__any_sync(full, bad)) {
+          if (__any_sync(gmask, bad)) {
             fallback = true;
             break;
           }
           const int nv = __popc(vb);
           if (nv >= need) {
-            newhead = pos + (32 - __clz(__ballot_sync(full, victim)));  // after the e-th victim
+            const unsigned vict = (__ballot_sync(gmask, victim) >> gbase) & glow;
+            newhead = pos + (32 - __clz(vict));  // after the e-th victim
             found = e;
           } else {
             found += nv;
-            pos += 32;
+            pos += G;
           }
         }
       }
       int ch;
       if (!fallback) {
         // evict: every valid entry in [head, newhead) is a victim
-        for (uint32_t pos = st.head; !applied && pos != newhead; pos += 32) {
-          const uint32_t idx = pos + lane;
+        for (uint32_t pos = st.head; !applied && pos != newhead; pos += G) {
+          const uint32_t idx = pos + hl;
           if (idx - pos < newhead - pos) {
             const int key = q[idx & qmask];
             if (pos_of[key] == (uint16_t)idx) {
@@ -880,29 +895,29 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
                         ~(1u << (ve & 31)));
             }
           }
-          if (newhead - pos <= 32) break;
+          if (newhead - pos <= (uint32_t)G) break;
         }
         st.head = newhead;
         st.count += m - e;
         const int ns = popc_w<W>(S);
-        if (st.tail - st.head + (uint32_t)ns > qmask + 1) {  // warp compaction
-          __syncwarp();
+        if (st.tail - st.head + (uint32_t)ns > qmask + 1) {  // group compaction
+          __syncwarp(gmask);
           uint32_t n = st.head;
-          for (uint32_t pos = st.head; pos != st.tail; pos += 32) {
-            const uint32_t idx = pos + lane;
+          for (uint32_t pos = st.head; pos != st.tail; pos += G) {
+            const uint32_t idx = pos + hl;
             const bool inr = idx - pos < st.tail - pos;
             const int key = q[idx & qmask];
             const bool valid = inr && pos_of[key] == (uint16_t)idx;
-            const unsigned vb = __ballot_sync(full, valid);
-            __syncwarp();
+            const unsigned vb = (__ballot_sync(gmask, valid) >> gbase) & glow;
+            __syncwarp(gmask);
             if (valid) {
-              const uint32_t dst = n + __popc(vb & ((1u << lane) - 1));
+              const uint32_t dst = n + __popc(vb & ((1u << hl) - 1));
               q[dst & qmask] = (uint16_t)key;
               pos_of[key] = (uint16_t)dst;
             }
-            __syncwarp();
+            __syncwarp(gmask);
             n += __popc(vb);
-            if (st.tail - pos <= 32) break;
+            if (st.tail - pos <= (uint32_t)G) break;
           }
           st.tail = n;
         }
@@ -912,19 +927,14 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         for (int w = 0; w < W; ++w) A[w] = K[w] & ~T[w];
         const int na = popc_w<W>(A);
         if (W == 1) {
-          const uint32_t lt = (1u << lane) - 1;
-          const uint32_t alo = (uint32_t)A[0], ahi = (uint32_t)(A[0] >> 32);
-          const uint32_t tlo = (uint32_t)T[0], thi = (uint32_t)(T[0] >> 32);
-          const int ca = __popc(alo), ct = __popc(tlo);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int ex = lane + 32 * h;
-            const uint32_t am = h ? ahi : alo, tm = h ? thi : tlo;
-            const bool ina = (am >> lane) & 1u, int_ = (tm >> lane) & 1u;
-            const int ra = (h ? ca : 0) + __popc(am & lt);
-            const int rt = (h ? ct : 0) + __popc(tm & lt);
+          for (int j = 0; j < 64 / G; ++j) {
+            const int ex = hl + G * j;
+            const uint64_t below = (1ull << ex) - 1;
+            const bool ina = (A[0] >> ex) & 1ull, int_ = (T[0] >> ex) & 1ull;
             if (ex < E && (ina || int_)) {
-              const uint32_t dst = st.tail + (uint32_t)(ina ? ra : na + rt);
+              const int rank = ina ? __popcll(A[0] & below) : na + __popcll(T[0] & below);
+              const uint32_t dst = st.tail + (uint32_t)rank;
               const int key = st.key_of(l, ex);
               q[dst & qmask] = (uint16_t)key;
               pos_of[key] = (uint16_t)dst;
@@ -932,8 +942,8 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
           }
         } else
 #pragma unroll
-        for (int j = 0; j < 2 * W; ++j) {
-          const int ex = lane + 32 * j;
+        for (int j = 0; j < 64 * W / G; ++j) {
+          const int ex = hl + G * j;
           if (ex < E) {
             const uint64_t bit = 1ull << (ex & 63);
             int slot2 = -1;
@@ -948,18 +958,18 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
           }
         }
         st.tail += ns;
-        __syncwarp();
-        if (lane < W) {
+        __syncwarp(gmask);
+        if (hl < W) {
           uint64_t v = 0;
 #pragma unroll
           for (int w = 0; w < W; ++w)
-            if (w == lane) v = R[l * W + w] | S[w];
-          R[l * W + lane] = v;
+            if (w == hl) v = R[l * W + w] | S[w];
+          R[l * W + hl] = v;
         }
-        __syncwarp();
+        __syncwarp(gmask);
         ch = popc_w<W>(Hm);
       } else {
-        // exact sequential replay of this row (all lanes in lockstep)
+        // exact sequential replay of this row (all lanes of the group in lockstep)
         st.cur = l;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
@@ -977,22 +987,22 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
             word_or<W>(Hm, ex >> 6, 1ull << (ex & 63));
           }
         })
-        __syncwarp();
-        if (lane < W) {
+        __syncwarp(gmask);
+        if (hl < W) {
           uint64_t v = 0;
 #pragma unroll
           for (int w = 0; w < W; ++w)
-            if (w == lane) v = st.Rl[w];
-          R[l * W + lane] = v;
+            if (w == hl) v = st.Rl[w];
+          R[l * W + hl] = v;
         }
-        __syncwarp();
+        __syncwarp(gmask);
       }
-      if (hits && lane < W) {
+      if (hits && hl < W) {
         uint64_t v = 0;
 #pragma unroll
         for (int w = 0; w < W; ++w)
-          if (w == lane) v = Hm[w];
-        hits[(r0 + i) * W + lane] = v;
+          if (w == hl) v = Hm[w];
+        hits[(r0 + i) * W + hl] = v;
       }
       if (measured) {
         const int k = popc_w<W>(T);
@@ -1003,15 +1013,15 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         tot_k += k;
         tot_ch += ch;
         tot_ph += ph;
-        if (L <= 32 * kLC) {
+        if (L <= G * kLC) {
 #pragma unroll
           for (int j = 0; j < kLC; ++j)
-            if (l == lane + 32 * j) {
+            if (l == hl + G * j) {
               lck[j] += k;
               lcc[j] += ch;
               lcp[j] += ph;
             }
-        } else if (lane == 0) {
+        } else if (hl == 0) {
           atomicAdd(&bcnt[l], (unsigned)k);
           atomicAdd(&bcnt[L + l], (unsigned)ch);
           atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
@@ -1024,7 +1034,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     }
 #pragma unroll
     for (int j = 0; j < kLC; ++j) {
-      const int ll = lane + 32 * j;
+      const int ll = hl + G * j;
       if (ll < L) {
         if (lck[j]) atomicAdd(&bcnt[ll], lck[j]);
         if (lcc[j]) atomicAdd(&bcnt[L + ll], lcc[j]);
@@ -1032,7 +1042,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       }
     }
     int64_t* c = a.counters + pi * a.counters_stride;
-    if (lane == 0) {
+    if (hl == 0) {
       atomicAdd(reinterpret_cast<unsigned long long*>(c + 0), (unsigned long long)tot_k);
       atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot_ch);
       atomicAdd(reinterpret_cast<unsigned long long*>(c + 2), (unsigned long long)tot_ph);
@@ -1066,15 +1076,26 @@ int launch_lru(SimArgs a, cudaStream_t s) {
   const int max_block = moeb::max_smem_per_block();
   const int head = align16(4LL * 3 * a.L);
   a.off_c = head;
-  int nw = 4;  // simulations (warps) per block
-  while (nw > 1 && head + (int64_t)nw * a.sim_bytes > max_block) --nw;
-  if (head + (int64_t)nw * a.sim_bytes > max_block)
-    return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
-                      a.sim_bytes, max_block);
-  const size_t smem = head + (size_t)nw * a.sim_bytes;
-  auto k = k_cache_sim_warp<W, ES>;
+  // Two simulations per warp (16 lanes each) unless the state is so large
+  // that only one or two simulations fit a block.
+  constexpr int G = 16;
+  int nw = 4;  // warps per block
+  while (nw > 1 && head + (int64_t)nw * (32 / G) * a.sim_bytes > max_block) --nw;
+  if (head + (int64_t)nw * (32 / G) * a.sim_bytes > max_block) {
+    if (head + (int64_t)a.sim_bytes > max_block)
+      return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
+                        a.sim_bytes, max_block);
+    const size_t smem1 = head + (size_t)a.sim_bytes;
+    auto k1 = k_cache_sim_warp<W, ES, 32>;
+    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    k1<<<dim3((unsigned)a.P, (unsigned)a.n_preds), 32, smem1, s>>>(a);
+    return moeb::check_launch("k_cache_sim_warp");
+  }
+  const size_t smem = head + (size_t)nw * (32 / G) * a.sim_bytes;
+  auto k = k_cache_sim_warp<W, ES, G>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const dim3 blocks((unsigned)((a.P + nw - 1) / nw), (unsigned)a.n_preds);
+  const int spb = nw * (32 / G);
+  const dim3 blocks((unsigned)((a.P + spb - 1) / spb), (unsigned)a.n_preds);
   k<<<blocks, 32 * nw, smem, s>>>(a);
   return moeb::check_launch("k_cache_sim_warp");
 }

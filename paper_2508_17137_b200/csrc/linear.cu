@@ -15,20 +15,36 @@
 // random-init weights; fp64 keeps the selection identical to numpy's, and
 // the recurrence's rounding drift stays ~1e-15 relative, tests assert 1e-12).
 //
-// Mapping: two threads per (prompt, layer) stream (adjacent lanes), each
-// owning 32 experts: z[32] fp64 in registers (~100 registers -> 20 warps/SM),
-// 16-byte column reads from shared memory. Top-k = k passes; in each pass
-// every thread finds the first maximum of its unchosen half and the pair
-// combines the two candidates with one shuffle (larger value, then lower id):
-// exactly lexsort's (-score, id) order. Consecutive streams are consecutive
-// layers of the same prompt, so mask rows are read/written contiguously.
-// Metrics: ballot+popc per expert over the warp's 16 rows, then one
-// shared-memory reduce and one global atomic per counter per block.
+// Mapping: TPS threads per (prompt, layer) stream (TPS = 2: adjacent lanes,
+// part q = lane % TPS), each owning NS = 64 / TPS experts as z[NS] fp64 in
+// registers, 16-byte column reads from shared memory. Consecutive streams are
+// consecutive layers of the same prompt, so mask rows are read/written
+// contiguously. Persistent CTAs (2 per SM) loop over groups of streams, so
+// the 92 KB weight tables are staged once per CTA.
+//
+// Bank-conflict-free column reads: a quarter-warp (8 lanes) reads 8
+// different, data-dependent columns at once. Every (column, part) is stored
+// as NS 16-byte units -- its NS/2 units followed by a copy -- and a lane reads
+// units [rot, rot + NS/2) with rot = lane & 7, so register pair j holds unit
+// (j + rot) mod NS/2 and the 8 lanes of a quarter-warp always hit 8 distinct
+// bank groups, whatever the columns. Slot s of part q thus holds expert
+// NS q + ((s + 2 rot) mod NS).
+//
+// Selection (top-k, learner.py:164-169): 32-bit keys = order-preserving map
+// of the fp64 high word with the low log2(NS) bits replaced by the register
+// slot; k + 1 passes of "largest key below the last winner" (2 integer ops
+// per element) pick the k largest keys, and the (k+1)-th confirms the cut: if
+// the k-th and (k+1)-th truncated keys are >= 2 buckets apart, the selected
+// set is exactly the fp64 top-k (the key map is monotone; equal fp64 values
+// -- including +-0 -- land in equal or adjacent buckets). Otherwise the
+// stream redoes the row with exact fp64 passes, ties to the lower expert id
+// (lexsort's (-score, id) order). The metric counters (K7) run as a separate
+// HBM-streaming pass over the predicted masks (metrics.cu).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
-
-constexpr int kThreads = 128;
 
 struct LinArgs {
   const uint64_t* truth;
@@ -39,182 +55,231 @@ struct LinArgs {
   int budget, threshold, warmup;
   uint64_t* pred;
   double* logits;
-  int64_t* metrics;
 };
 
-// Shared-memory rows of 64 doubles as two 32-double halves with a 16-byte
-// gap (half h starts at double 34*h) and a row stride of 74 doubles = 37
-// 16-byte units: the 16-byte chunks a quarter-warp reads (4 streams x 2
-// halves, random columns) spread over all 8 bank groups.
-constexpr int kES = 74;
-__host__ __device__ constexpr int half_off(int h) { return 34 * h; }
+template <int TPS>
+struct K3Cfg {
+  static constexpr int NS = 64 / TPS;                    // experts (slots) per thread
+  static constexpr int kThreads = TPS == 2 ? 192 : 256;  // 2 CTAs per SM
+  static constexpr int kStreams = kThreads / TPS;
+  static constexpr int kUnits = NS;                      // 16-byte units per (column, part)
+};
 
-template <bool FULL>  // FULL: E == 64, no per-expert bounds checks
-__global__ void __launch_bounds__(kThreads) k_linear_predict(const LinArgs a) {
+// rot as an opaque value, so per-slot expert ids are recomputed where used
+// instead of being hoisted into NS live registers
+__device__ __forceinline__ int opaque(int v) {
+  int r;
+  asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+  return r;
+}
+
+template <int NS>
+__device__ __forceinline__ int slot_expert(int s, int q, int rot) {
+  return NS * q + ((s + 2 * rot) & (NS - 1));
+}
+
+template <int NS>
+__device__ __forceinline__ uint32_t order_key(double z, int s) {
+  const uint32_t hi = (uint32_t)__double2hiint(z);
+  const uint32_t ord = hi ^ ((uint32_t)((int32_t)hi >> 31) | 0x80000000u);
+  return (ord & ~(uint32_t)(NS - 1)) | (uint32_t)s;
+}
+
+// (key, found, part) of the better of this lane's and lane ^ o's candidate:
+// larger key first, equal keys -> lower part first
+__device__ __forceinline__ void combine(uint32_t& k, bool& f, int& q, int o) {
+  const uint32_t ok = __shfl_xor_sync(0xffffffffu, k, o);
+  const bool of = __shfl_xor_sync(0xffffffffu, (int)f, o) != 0;
+  const int oq = __shfl_xor_sync(0xffffffffu, q, o);
+  const bool take = of && (!f || ok > k || (ok == k && oq < q));
+  k = take ? ok : k;
+  f = f || of;
+  q = take ? oq : q;
+}
+
+template <int TPS, bool FULL>  // FULL: E == 64, no per-expert bounds checks
+__global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(const LinArgs a) {
+  using C = K3Cfg<TPS>;
+  constexpr int NS = C::NS, NU = C::kUnits, HALF = NS / 2;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = a.L, E = a.E, F = a.L + a.E + 1;
-  double* colT = reinterpret_cast<double*>(smem_raw);  // [E][kES]: colT[e][j] = W[j][L+e]
-  double* bias = colT + E * kES;                       // [L][kES]: b_l[j]
-  double* bias2 = bias + L * kES;                      // [L][kES]: (1 - decay) b_l[j]
-  unsigned long long* mcnt = reinterpret_cast<unsigned long long*>(bias2 + L * kES);  // [3E+3]
-  for (int i = threadIdx.x; i < E * 64; i += blockDim.x) {
-    const int e = i / 64, j = i % 64;
-    colT[e * kES + half_off(j >> 5) + (j & 31)] = j < E ? a.Wt[(int64_t)j * F + L + e] : 0.0;
+  double2* colT = reinterpret_cast<double2*>(smem_raw);  // [E][TPS][NU]: W[j][L+e] pairs
+  double2* bias2 = colT + E * TPS * NU;                  // [L][TPS][NU]: (1 - decay) b_l
+  for (int i = threadIdx.x; i < E * TPS * NU; i += blockDim.x) {
+    const int e = i / (TPS * NU), j0 = NS * ((i / NU) % TPS) + 2 * (i % HALF);
+    colT[i] = make_double2(j0 < E ? a.Wt[(int64_t)j0 * F + L + e] : 0.0,
+                           j0 + 1 < E ? a.Wt[(int64_t)(j0 + 1) * F + L + e] : 0.0);
   }
-  for (int i = threadIdx.x; i < L * 64; i += blockDim.x) {
-    const int l = i / 64, j = i % 64;
-    const double b = j < E ? a.Wt[(int64_t)j * F + l] + a.Wt[(int64_t)j * F + L + E] : 0.0;
-    bias[l * kES + half_off(j >> 5) + (j & 31)] = b;
-    bias2[l * kES + half_off(j >> 5) + (j & 31)] = (1.0 - a.decay) * b;
+  for (int i = threadIdx.x; i < L * TPS * NU; i += blockDim.x) {
+    const int l = i / (TPS * NU), j0 = NS * ((i / NU) % TPS) + 2 * (i % HALF);
+    double b[2];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int j = j0 + c;
+      b[c] = j < E ? (1.0 - a.decay) * (a.Wt[(int64_t)j * F + l] + a.Wt[(int64_t)j * F + L + E])
+                   : 0.0;
+    }
+    bias2[i] = make_double2(b[0], b[1]);
   }
-  if (a.metrics)
-    for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x) mcnt[i] = 0;
   __syncthreads();
 
   const unsigned full = 0xffffffffu;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t sidx = g >> 1;  // stream
-  const int h = (int)(g & 1);   // which 32 experts
-  const int e0 = 32 * h;
-  const bool live = sidx < (int64_t)a.L * a.P;
-  const int p = live ? (int)(sidx / L) : 0;
-  const int l = live ? (int)(sidx % L) : 0;
-  const int64_t r0 = live ? a.row_off[p] : 0;
-  const int T = live ? (int)((a.row_off[p + 1] - r0) / L) : 0;
-  int Tw = T;  // warp-uniform trip count so ballots/shuffles see every lane
-#pragma unroll
-  for (int o = 16; o; o >>= 1) Tw = max(Tw, __shfl_xor_sync(full, Tw, o));
-
-  double z[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) z[j] = bias[l * kES + half_off(h) + j];
   const int lane = threadIdx.x & 31;
-  uint32_t tp_e = 0, fp_e = 0, fn_e = 0;  // packed counts of experts lane, lane + 32
-  uint32_t npos = 0, nexact = 0;
-  uint64_t nlabel = 0;
-  const uint64_t emask = E == 64 ? ~0ull : ((1ull << E) - 1);
-  const int k = a.budget < E ? a.budget : E;
+  const int q = lane % TPS;
+  const int e0 = NS * q;
+  const int rot = lane & 7;
+  const unsigned grp = ((1u << TPS) - 1) << (lane & ~(TPS - 1));
   const double NEG = -__longlong_as_double(0x7ff0000000000000LL);
+  const int k = a.budget < E ? a.budget : E;
+  const int64_t n_streams = (int64_t)a.L * a.P;
 
-  for (int t = 0; t < Tw; ++t) {
-    const bool valid = t < T;
-    const int64_t r = r0 + (int64_t)t * L + l;
-    const uint64_t tw = valid ? __ldg(a.truth + r) : 0ull;
-    uint64_t pm = 0;
-    if (a.threshold) {
-      uint32_t m = 0;
+  for (int64_t gbase = (int64_t)blockIdx.x * C::kStreams; gbase < n_streams;
+       gbase += (int64_t)gridDim.x * C::kStreams) {
+    const int64_t sidx = gbase + threadIdx.x / TPS;
+    const bool live = sidx < n_streams;
+    const int p = live ? (int)(sidx / L) : 0;
+    const int l = live ? (int)(sidx % L) : 0;
+    const int64_t r0 = live ? a.row_off[p] : 0;
+    const int T = live ? (int)((a.row_off[p + 1] - r0) / L) : 0;
+    int Tw = T;  // warp-uniform trip count so shuffles see every lane
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if ((FULL || e0 + j < E) && z[j] > 0.0) m |= 1u << j;
-      const uint32_t other = __shfl_xor_sync(full, m, 1);
-      pm = h ? ((uint64_t)m << 32 | other) : ((uint64_t)other << 32 | m);
-    } else {
-      uint32_t chosen = 0;
-      for (int it = 0; it < k; ++it) {
-        double best = NEG;
-        int bi = -1;
+    for (int o = 16; o; o >>= 1) Tw = max(Tw, __shfl_xor_sync(full, Tw, o));
+
+    double z[NS];  // slot s: expert slot_expert(s, q, rot); invalid experts (E < 64) = -inf
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const bool ok = (FULL || e0 + j < E) && !((chosen >> j) & 1u) && z[j] > best;
-          best = ok ? z[j] : best;
-          bi = ok ? j : bi;
-        }
-        const int gi = bi < 0 ? -1 : e0 + bi;
-        const double ob = __shfl_xor_sync(full, best, 1);
-        const int oi = __shfl_xor_sync(full, gi, 1);
-        const bool take_other = oi >= 0 && (gi < 0 || ob > best || (ob == best && oi < gi));
-        const int win = take_other ? oi : gi;
-        if (win >= e0 && win < e0 + 32) chosen |= 1u << (win - e0);
-        pm |= 1ull << win;
-      }
+    for (int s = 0; s < NS; ++s) {
+      const int ex = slot_expert<NS>(s, q, rot);
+      z[s] = (FULL || ex < E) ? a.Wt[(int64_t)ex * F + l] + a.Wt[(int64_t)ex * F + L + E] : NEG;
     }
-    pm &= valid ? ~0ull : 0ull;
-    if (valid) {
-      if (h == 0) a.pred[r] = pm;
-      if (a.logits) {
+    const double2* bcol = bias2 + (l * TPS + q) * NU + rot;
+
+    for (int t = 0; t < Tw; ++t) {
+      const bool valid = t < T;
+      const int64_t r = r0 + (int64_t)t * L + l;
+      const uint64_t tw = valid ? __ldg(a.truth + r) : 0ull;
+      uint64_t pm = 0;
+      if (a.threshold) {
+        uint32_t m = 0;  // slot mask -> expert mask of this part: rotate by 2 rot
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (e0 + j < E) a.logits[r * E + e0 + j] = z[j];
-      }
-    }
-    if (a.metrics) {
-      // lane 2i reports experts [0, 32), lane 2i+1 experts [32, 64) of its row
-      const bool m = valid && t >= a.warmup;
-      const uint64_t tpm = m ? (pm & tw) : 0, fpm = m ? (pm & ~tw) : 0, fnm = m ? (tw & ~pm) : 0;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const uint32_t b1 = __ballot_sync(full, (tpm >> (e0 + j)) & 1ull);
-        const uint32_t b2 = __ballot_sync(full, (fpm >> (e0 + j)) & 1ull);
-        const uint32_t b3 = __ballot_sync(full, (fnm >> (e0 + j)) & 1ull);
-        if (lane == j) {  // lane j owns experts j (low 16 bits) and j + 32 (high 16 bits)
-          tp_e += (uint32_t)__popc(b1 & 0x55555555u) | ((uint32_t)__popc(b1 & 0xAAAAAAAAu) << 16);
-          fp_e += (uint32_t)__popc(b2 & 0x55555555u) | ((uint32_t)__popc(b2 & 0xAAAAAAAAu) << 16);
-          fn_e += (uint32_t)__popc(b3 & 0x55555555u) | ((uint32_t)__popc(b3 & 0xAAAAAAAAu) << 16);
+        for (int s = 0; s < NS; ++s)
+          if (z[s] > 0.0) m |= 1u << s;
+        if (NS == 32) {
+          m = __funnelshift_l(m, m, 2 * rot);
+        } else {
+          m = ((m << (2 * rot)) | (m >> (NS - 2 * rot))) & ((1u << NS) - 1);
         }
-      }
-      const bool m0 = m && h == 0;
-      npos += m0;
-      nexact += m0 && pm == tw;
-      nlabel += m0 ? (uint64_t)(E - __popcll((pm ^ tw) & emask)) : 0;
-      if ((t & 1023) == 1023) {  // flush packed 16-bit counts before they overflow
-        const int j = lane;
-        {
-          if (j < E) {
-            atomicAdd(&mcnt[j], tp_e & 0xFFFFu);
-            atomicAdd(&mcnt[E + j], fp_e & 0xFFFFu);
-            atomicAdd(&mcnt[2 * E + j], fn_e & 0xFFFFu);
+        pm = (uint64_t)m << e0;
+#pragma unroll
+        for (int o = 1; o < TPS; o <<= 1) pm |= __shfl_xor_sync(full, pm, o);
+      } else {
+        uint32_t key[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) key[s] = order_key<NS>(z[s], s);
+        uint32_t kth = 0, bound = 0;
+        bool amb = false;
+        for (int it = 0; it <= k; ++it) {
+          uint32_t bk;
+          bool found;
+          if (it == 0) {
+            bk = key[0];
+#pragma unroll
+            for (int s = 1; s < NS; ++s) bk = max(bk, key[s]);
+            found = true;
+          } else {  // largest key below this lane's bound
+            const uint32_t bm1 = bound - 1u;
+            uint32_t tm = 0xffffffffu;
+#pragma unroll
+            for (int s = 0; s < NS; ++s) tm = min(tm, bm1 - key[s]);
+            found = bound != 0u && tm < bound;
+            bk = bm1 - tm;
           }
-          if (j + 32 < E) {
-            atomicAdd(&mcnt[j + 32], tp_e >> 16);
-            atomicAdd(&mcnt[E + j + 32], fp_e >> 16);
-            atomicAdd(&mcnt[2 * E + j + 32], fn_e >> 16);
+          uint32_t wk = bk;
+          bool wf = found;
+          int wq = q;
+#pragma unroll
+          for (int o = 1; o < TPS; o <<= 1) combine(wk, wf, wq, o);
+          if (it < k) {
+            const int wrot = ((lane & ~(TPS - 1)) | wq) & 7;
+            pm |= 1ull << slot_expert<NS>((int)(wk & (NS - 1)), wq, wrot);
+            kth = wk;
+            bound = wk + (q > wq ? 1u : 0u);
+          } else if (wf) {
+            amb = (kth & ~(uint32_t)(NS - 1)) - (wk & ~(uint32_t)(NS - 1)) <= (uint32_t)NS;
           }
         }
-        tp_e = fp_e = fn_e = 0;
-      }
-    }
-    if (valid) {  // update_history (learner.py:62-72), as a logit recurrence
-      const double2* b2 = reinterpret_cast<const double2*>(bias2 + l * kES + half_off(h));
+        if (amb) {  // exact fp64 passes (rare): ties to the lower expert id
+          pm = 0;
+          for (int it = 0; it < k; ++it) {
+            const int orot = opaque(rot);
+            double best = NEG;
+            int bi = 64;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const double2 v = b2[j];
-        z[2 * j] = fma(a.decay, z[2 * j], v.x);
-        z[2 * j + 1] = fma(a.decay, z[2 * j + 1], v.y);
-      }
-      uint64_t m = tw;
-      while (m) {
-        const int ex = __ffsll((long long)m) - 1;
-        m &= m - 1;
-        const double2* col = reinterpret_cast<const double2*>(colT + ex * kES + half_off(h));
+            for (int s = 0; s < NS; ++s) {
+              const int ex = slot_expert<NS>(s, q, orot);
+              const bool ok = (FULL || ex < E) && !((pm >> ex) & 1ull) &&
+                              (z[s] > best || (z[s] == best && ex < bi));
+              best = ok ? z[s] : best;
+              bi = ok ? ex : bi;
+            }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const double2 v = col[j];
-          z[2 * j] += v.x;
-          z[2 * j + 1] += v.y;
+            for (int o = 1; o < TPS; o <<= 1) {
+              const double ob = __shfl_xor_sync(grp, best, o);
+              const int oi = __shfl_xor_sync(grp, bi, o);
+              const bool take = oi < 64 && (bi == 64 || ob > best || (ob == best && oi < bi));
+              best = take ? ob : best;
+              bi = take ? oi : bi;
+            }
+            pm |= 1ull << bi;
+          }
+        }
+      }
+      if (valid) {
+        if (q == 0) a.pred[r] = pm;
+        if (a.logits) {
+          const int orot = opaque(rot);
+#pragma unroll
+          for (int s = 0; s < NS; ++s) {
+            const int ex = slot_expert<NS>(s, q, orot);
+            if (FULL || ex < E) a.logits[r * E + ex] = z[s];
+          }
+        }
+        // update_history (learner.py:62-72), as a logit recurrence
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) {
+          const double2 v = bcol[j];
+          z[2 * j] = fma(a.decay, z[2 * j], v.x);
+          z[2 * j + 1] = fma(a.decay, z[2 * j + 1], v.y);
+        }
+        uint64_t mm = tw;
+        while (mm) {
+          const int ex = __ffsll((long long)mm) - 1;
+          mm &= mm - 1;
+          const double2* col = colT + (ex * TPS + q) * NU + rot;
+#pragma unroll
+          for (int j = 0; j < HALF; ++j) {
+            const double2 v = col[j];
+            z[2 * j] += v.x;
+            z[2 * j + 1] += v.y;
+          }
         }
       }
     }
   }
+}
 
-  if (a.metrics) {
-    const int j = lane;
-    if (j < E) {
-      atomicAdd(&mcnt[j], (unsigned long long)(tp_e & 0xFFFFu));
-      atomicAdd(&mcnt[E + j], (unsigned long long)(fp_e & 0xFFFFu));
-      atomicAdd(&mcnt[2 * E + j], (unsigned long long)(fn_e & 0xFFFFu));
-    }
-    if (j + 32 < E) {
-      atomicAdd(&mcnt[j + 32], (unsigned long long)(tp_e >> 16));
-      atomicAdd(&mcnt[E + j + 32], (unsigned long long)(fp_e >> 16));
-      atomicAdd(&mcnt[2 * E + j + 32], (unsigned long long)(fn_e >> 16));
-    }
-    atomicAdd(&mcnt[3 * E], (unsigned long long)npos);
-    atomicAdd(&mcnt[3 * E + 1], (unsigned long long)nexact);
-    atomicAdd(&mcnt[3 * E + 2], (unsigned long long)nlabel);
-    __syncthreads();
-    for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x)
-      if (mcnt[i]) atomicAdd(reinterpret_cast<unsigned long long*>(a.metrics + i), mcnt[i]);
-  }
+template <int TPS>
+int launch_k3(const LinArgs& a, cudaStream_t s) {
+  using C = K3Cfg<TPS>;
+  const size_t smem = sizeof(double2) * (size_t)(a.E + a.L) * TPS * C::kUnits;
+  if ((int)smem > moeb::max_smem_per_block())
+    return moeb::fail(MOEB_ESMEM, "learned_linear tables need %zu B of shared memory", smem);
+  auto kern = a.E == 64 ? k_linear_predict<TPS, true> : k_linear_predict<TPS, false>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // persistent: at most 2 CTAs per SM, each looping over groups of kStreams streams
+  const int64_t groups = ((int64_t)a.L * a.P + C::kStreams - 1) / C::kStreams;
+  const int64_t blocks = groups < 2LL * moeb::num_sms() ? groups : 2LL * moeb::num_sms();
+  kern<<<(unsigned)blocks, C::kThreads, smem, s>>>(a);
+  return moeb::check_launch("k_linear_predict");
 }
 
 }  // namespace
@@ -231,15 +296,12 @@ extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_
   MOEB_REQUIRE(budget >= 1 && warmup_tokens >= 0, "bad budget/warmup");
   MOEB_REQUIRE(decay >= 0.0 && decay < 1.0, "decay must be in [0, 1)");
   LinArgs a{truth, prompt_row_off, n_prompts, L, E, weights, decay, budget,
-            threshold ? 1 : 0, warmup_tokens, pred, logits, metrics};
-  const size_t smem = sizeof(double) * ((size_t)E * kES + 2 * (size_t)L * kES) +
-                      sizeof(unsigned long long) * (3 * E + 3);
-  if ((int)smem > moeb::max_smem_per_block())
-    return moeb::fail(MOEB_ESMEM, "learned_linear tables need %zu B of shared memory", smem);
-  auto kern = E == 64 ? k_linear_predict<true> : k_linear_predict<false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t threads = 2 * (int64_t)L * n_prompts;  // two per (prompt, layer) stream
-  const int64_t blocks = (threads + kThreads - 1) / kThreads;
-  kern<<<(unsigned)blocks, kThreads, smem, moeb::as_stream(stream)>>>(a);
-  return moeb::check_launch("k_linear_predict");
+            threshold ? 1 : 0, warmup_tokens, pred, logits};
+  const char* env = getenv("MOEB_K3_TPS");  // tuning knob: threads per stream (2 or 4)
+  const int rc = (env && atoi(env) == 4) ? launch_k3<4>(a, moeb::as_stream(stream))
+                                         : launch_k3<2>(a, moeb::as_stream(stream));
+  if (rc != 0 || metrics == nullptr) return rc;
+  // K7 over the fresh masks (same stream): prediction metrics (metrics.py:12-79)
+  return moeb_metrics(pred, truth, prompt_row_off, n_prompts, L, E, warmup_tokens, metrics,
+                      stream);
 }

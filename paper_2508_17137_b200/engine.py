@@ -127,18 +127,23 @@ def _check_lengths(packed: PackedTraces, warmup: int) -> None:
 
 
 def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget: int,
-                 policy: str = "lru", want_per_prompt: bool = True, want_hits: bool = False):
+                 policy: str = "lru", want_per_prompt: bool = True, want_hits: bool = False,
+                 counters=None):
     """Run K1 for every (prediction stream, capacity) pair in one call.
 
     ``streams`` is a list of (masks | None, coverage | None, unbounded).
     Returns device tensors counters [n][C][4+3L], per_prompt [n][C][P][4] or
-    None, hit masks [n][C][rows][W] or None.
+    None, hit masks [n][C][rows][W] or None. ``counters`` (optional, int64
+    [n][C][4+3L]) is accumulated into instead of a fresh zero tensor.
     """
     shape = packed.shape
     L = shape.num_layers
     n, C, P = len(streams), len(capacities), packed.num_prompts
     dev = packed.device
-    counters = torch.zeros((n, C, 4 + 3 * L), dtype=torch.int64, device=dev)
+    if counters is None:
+        counters = torch.zeros((n, C, 4 + 3 * L), dtype=torch.int64, device=dev)
+    elif tuple(counters.shape) != (n, C, 4 + 3 * L) or counters.dtype != torch.int64:
+        raise ConfigError("counters must be int64 [streams][capacities][4+3L]")
     per_prompt = (torch.zeros((n, C, P, 4), dtype=torch.int64, device=dev)
                   if want_per_prompt else None)
     hits = (torch.zeros((n, C, packed.rows, shape.mask_words), dtype=torch.int64, device=dev)
@@ -178,6 +183,105 @@ def replay_traces(traces, predictor, config: ReplayConfig, jobs: int = 1, policy
     return SimReport.from_counters(
         config.shape, counters[0, 0].cpu().numpy(),
         None if pp is None else pp[0, 0].cpu().numpy(), packed.prompt_ids)
+
+
+class PipelinedReplay:
+    """Prediction + cache replay over prompt chunks on overlapping streams.
+
+    Prompts are independent (``engine.py:94-110`` fans them out to a process
+    pool), so a batch is cut into ``chunks`` row-balanced prompt ranges and
+    issued as a three-stage pipeline: [copy stream] host->device copy of the
+    chunk's truth rows (only when ``host_truth`` is given: pinned uint64 rows
+    of the whole batch), [predict stream] the predictor's masks (+ fused metric
+    counters), [replay stream] K1 for the chunk. Chunk c's replay runs while
+    chunk c+1 is predicted and chunk c+2 copied. All counters are integer sums
+    accumulated with atomics, so results are identical to one unchunked call.
+    The chunk views are built once (construction does host work that would
+    otherwise serialise the streams).
+    """
+
+    def __init__(self, packed: PackedTraces, chunks: int = 4):
+        self.packed = packed
+        P = packed.num_prompts
+        chunks = max(1, min(int(chunks), P))
+        targets = np.arange(1, chunks) * (packed.rows / chunks)
+        cuts = np.searchsorted(packed.row_off_host, targets)
+        bounds = sorted(set([0] + [int(c) for c in cuts] + [P]))
+        self.bounds = [(a, b) for a, b in zip(bounds[:-1], bounds[1:]) if b > a]
+        self.views = [packed.select(a, b) for a, b in self.bounds]
+        self._host_off = None
+        dev = packed.device
+        self.s_copy = torch.cuda.Stream(dev)
+        self.s_pred = torch.cuda.Stream(dev)
+        self.s_sim = torch.cuda.Stream(dev)
+
+    def host_offsets(self):
+        """Pinned host copies of each chunk's rebased row offsets (copied with
+        the truth rows when the batch comes from host memory)."""
+        if self._host_off is None:
+            self._host_off = [torch.from_numpy(np.ascontiguousarray(v.row_off_host)).pin_memory()
+                              for v in self.views]
+        return self._host_off
+
+    @property
+    def h2d_offset_bytes(self) -> int:
+        return sum(8 * (b - a + 1) for a, b in self.bounds)
+
+    def run(self, predictor, capacities, warmup: int, budget: int, policy: str = "lru",
+            metrics=None, host_truth=None, counters=None, timing=None):
+        """Enqueue the pipeline; returns counters [1][C][4+3L] (device, ordered
+        on the caller's current stream). ``metrics`` (int64 [3E+3]) receives the
+        fused prediction metrics when the predictor supports them. ``timing``
+        (a list) receives (stage, start_event, end_event, rows) per launch,
+        recorded on the launching stream."""
+        ev = (lambda: torch.cuda.Event(enable_timing=True)) if timing is not None else None
+        shape, packed = self.packed.shape, self.packed
+        main = torch.cuda.current_stream(packed.device)
+        if counters is None:
+            counters = torch.zeros((1, len(capacities), 4 + 3 * shape.num_layers),
+                                   dtype=torch.int64, device=packed.device)
+        for s in (self.s_copy, self.s_pred, self.s_sim):
+            s.wait_stream(main)
+        unbounded = bool(getattr(predictor, "unbounded_prefetch", False))
+        for ci, ((a, b), view) in enumerate(zip(self.bounds, self.views)):
+            if host_truth is not None:
+                r0, r1 = int(packed.row_off_host[a]), int(packed.row_off_host[b])
+                with torch.cuda.stream(self.s_copy):
+                    view.truth.copy_(host_truth[r0:r1], non_blocking=True)
+                    view.row_off.copy_(self.host_offsets()[ci],
+                                       non_blocking=True)
+                self.s_pred.wait_stream(self.s_copy)
+            with torch.cuda.stream(self.s_pred):
+                if getattr(predictor, "empty", False) and metrics is None:
+                    masks, cov = None, None
+                else:
+                    if ev:
+                        e0, e1 = ev(), ev()
+                        e0.record(self.s_pred)
+                    masks = predictor.predict_masks(view, budget, warmup, metrics=metrics)
+                    if ev:
+                        e1.record(self.s_pred)
+                        timing.append(("predict", e0, e1, view.rows))
+                    cov = predictor.coverage(view)
+            self.s_sim.wait_stream(self.s_pred)
+            for t in (masks, cov):
+                if t is not None:
+                    t.record_stream(self.s_sim)
+            with torch.cuda.stream(self.s_sim):
+                if ev:
+                    e2, e3 = ev(), ev()
+                    e2.record(self.s_sim)
+                cache_replay(view, [(masks, cov, unbounded)], capacities, warmup, budget,
+                             policy, want_per_prompt=False, counters=counters)
+                if ev:
+                    e3.record(self.s_sim)
+                    timing.append(("replay", e2, e3, view.rows))
+        main.wait_stream(self.s_sim)
+        main.wait_stream(self.s_pred)
+        counters.record_stream(self.s_sim)
+        if metrics is not None:
+            metrics.record_stream(self.s_pred)
+        return counters
 
 
 def replay_prompt(trace, predictor, config: ReplayConfig) -> SimReport:

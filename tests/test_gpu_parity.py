@@ -289,3 +289,70 @@ def test_c1_scale_vs_oracle(pkg, oracle):
             got, _, _ = pkg.cache_replay(packed, [(None if pm is None else masks, None, False)],
                                          [166], 8, 6, policy=("lru", "lfu")[pol])
             assert np.array_equal(got[0, 0].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 7])
+def test_pipelined_replay_matches_single_call(pkg, chunks):
+    """PipelinedReplay (predict || replay || H2D over prompt chunks) gives the
+    same counters and fused metrics as one unchunked predict + K1 call."""
+    shape = pkg.ModelShape(26, 64, 6)
+    packed = pkg.generate_packed(pkg.GeneratorConfig(40, 96, shape, 8, 0.9, 7))
+    w = np.random.default_rng(0).normal(0.0, 0.01, (64, 91))
+    model = pkg.LinearModel(shape, pkg.LearnerConfig(epochs=0), w, trained=True)
+    pred = pkg.make_predictor("learned_linear", shape, model=model)
+    vec = pkg.metrics.metric_vector(64, packed.device)
+    masks = pred.predict_masks(packed, 6, 8, metrics=vec)
+    want, _, _ = pkg.cache_replay(packed, [(masks, None, False)], [40, 166], 8, 6,
+                                  want_per_prompt=False)
+    pipe = pkg.PipelinedReplay(packed, chunks)
+    assert len(pipe.bounds) == chunks
+    vec2 = pkg.metrics.metric_vector(64, packed.device)
+    timing = []
+    got = pipe.run(pred, [40, 166], 8, 6, metrics=vec2, timing=timing)
+    assert torch.equal(got, want) and torch.equal(vec2, vec)
+    assert len(timing) == 2 * chunks
+    # from pinned host rows into a fresh device buffer
+    host = packed.truth.cpu().pin_memory()
+    dst = pkg.PackedTraces(shape, torch.zeros_like(packed.truth), torch.zeros_like(packed.row_off),
+                           packed.row_off_host, packed.prompt_ids)
+    pipe2 = pkg.PipelinedReplay(dst, chunks)
+    got2 = pipe2.run(pred, [40, 166], 8, 6, host_truth=host)
+    assert torch.equal(got2, want)
+    # LRU-only (no predictor launches) and LFU
+    lru = pkg.make_predictor("lru_only", shape)
+    want3, _, _ = pkg.cache_replay(packed, [(None, None, False)], [166], 8, 6, policy="lfu",
+                                   want_per_prompt=False)
+    assert torch.equal(pipe.run(lru, [166], 8, 6, policy="lfu"), want3)
+
+
+@pytest.mark.parametrize("L,E,budget,decay", [(5, 64, 6, 0.0), (3, 40, 5, 0.5), (4, 64, 1, 0.0),
+                                             (2, 33, 8, 0.5)])
+def test_learned_linear_exact_ties(pkg, oracle, L, E, budget, decay):
+    """Dyadic weights make logits exact in both the oracle and the kernel and
+    create many exact ties, so the kernel's key-based selection must fall
+    back to the exact fp64 passes (ties to the lower id) on every tied cut."""
+    rng = np.random.default_rng(L * 1000 + E)
+    shape = pkg.ModelShape(L, E, 6)
+    P, T = 24, 20
+    rows = P * T * L
+    truth = np.zeros(rows, dtype=np.uint64)
+    for r in range(rows):
+        for e in rng.choice(E, 6, replace=False):
+            truth[r] |= np.uint64(1) << np.uint64(e)
+    off = np.arange(P + 1, dtype=np.int64) * T * L
+    w = rng.integers(-2, 3, size=(E, L + E + 1)).astype(np.float64) * 0.25
+    packed = pkg.PackedTraces(shape, _dev(truth), torch.from_numpy(off).cuda(), off,
+                              np.arange(P, dtype=np.int64))
+    model = pkg.LinearModel(shape, pkg.LearnerConfig(epochs=0, decay=decay), w, trained=True)
+    for thr in (False, True):
+        pred = pkg.make_predictor("learned_linear", shape, model=model, threshold=thr)
+        masks = pred.predict_masks(packed, budget, 0)
+        want, logits = oracle.linear_predict(truth, off, L, E, w, decay, budget, threshold=thr,
+                                             want_logits=True)
+        got = _host(masks).reshape(-1)
+        want = want.reshape(-1)
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (thr, bad[:5], got[bad[:3]], want[bad[:3]])
+    # ties really occur at the top-k cut
+    srt = -np.sort(-logits, axis=1)
+    assert np.mean(srt[:, budget - 1] == srt[:, budget]) > 0.05
