@@ -335,11 +335,16 @@ def run_ours(args):
     dom = "k_cache_sim" if sim_ms >= lin_ms else "k_linear_predict"
     dom_ms = max(sim_ms, lin_ms)
     achieved = rows * bytes_per_row / (dom_ms / 1000.0) / 1e9
+    # DRAM bytes per launch from the committed `ncu --set full` capture of the
+    # same kernel on the same workload (profiles/traffic.json), scaled to this
+    # run's rows per launch when the chunking differs.
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            t = json.load(open(tpath)).get(dom)
+            if t:
+                traffic = t["dram_bytes"] * (rows / len(pipe.bounds)) / t["rows"]
         except Exception:
             traffic = None
 
@@ -385,7 +390,7 @@ def run_ours(args):
             msum = sum(a.elapsed_time(b) for a, b, _ in lst) / nt
             fl = sum(f for _, _, f in lst) / nt
             ker[name] = {"ms": msum, "tflops": fl / (msum / 1e3) / 1e12}
-        dom = max((k for k in ker if k.startswith("gemm")), key=lambda k: ker[k]["ms"])
+        tdom = max((k for k in ker if k.startswith("gemm")), key=lambda k: ker[k]["ms"])
         tot_flops = sum(sum(f for _, _, f in lst) for lst in timing.values()) / nt
         ct = cnt_t[0, 0].cpu().numpy()
         mct = m.MetricCounts.from_vector(vec_t.cpu().numpy(), E)
@@ -394,9 +399,9 @@ def run_ours(args):
             "predictor": "transformer 4x(d512,h8,ff2048), windows 512, fp16 operands / fp32 acc",
             "trace_tok_per_s": Pt * C2["tokens"] / (tms / 1e3), "ms_per_step": tms,
             "tflops_achieved": tot_flops / (tms / 1e3) / 1e12, "kernels": ker,
-            "roofline": {"bound": "tensor", "kernel": dom, "achieved": ker[dom]["tflops"],
+            "roofline": {"bound": "tensor", "kernel": tdom, "achieved": ker[tdom]["tflops"],
                          "peak": bf16_sus, "unit": "TFLOP/s",
-                         "frac": ker[dom]["tflops"] / bf16_sus,
+                         "frac": ker[tdom]["tflops"] / bf16_sus,
                          "peak_kind": f"{peak_kind} dense bf16/fp16 sustained"},
             "hit_rate_10pct": int(ct[1]) / int(ct[0]),
             "prediction": {"macro_f1": mct.macro_f1(), "position_accuracy": mct.position_accuracy,
