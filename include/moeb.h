@@ -257,6 +257,137 @@ int moeb_token_prefix_counts(const uint64_t* truth, const int64_t* prompt_row_of
                              const int64_t* query_off, int n_prompts, int L, int E,
                              int warmup_tokens, int32_t* out, void* stream);
 
+/*
+ * Trace ingestion: the reference's file formats parsed and
+ * emitted on device. Byte buffers are device copies of the file; they must be
+ * 16-byte aligned and readable up to the next multiple of 16 bytes.
+ *
+ * moeb_count_bytes / moeb_find_bytes -- ordered positions of every byte equal
+ *   to `value` (text.split("\n") in parse_trace_csv / parse_predictions,
+ *   traceio.py:58-61, :142). Blocks of MOEB_SCAN_CHUNK bytes;
+ *   block_offsets has ceil(n / MOEB_SCAN_CHUNK) + 1 entries: count_bytes
+ *   writes the exclusive block offsets and the total (also to *total), and
+ *   find_bytes writes positions[0 .. total).
+ */
+#define MOEB_SCAN_CHUNK 65536
+int moeb_count_bytes(const uint8_t* buf, int64_t n, int value, int64_t* block_offsets,
+                     int64_t* total, void* stream);
+int moeb_find_bytes(const uint8_t* buf, int64_t n, int value, const int64_t* block_offsets,
+                    int64_t* positions, void* stream);
+
+/* Line status codes of the device parsers (0 = record OK). */
+#define MOEB_LINE_OK 0
+#define MOEB_LINE_COLS 1          /* trace csv: not 6 columns */
+#define MOEB_LINE_INT_PROMPT 2    /* column prompt_id not an integer */
+#define MOEB_LINE_INT_TOKEN 3     /* column token_index not an integer */
+#define MOEB_LINE_INT_LAYER 4     /* column layer_id not an integer */
+#define MOEB_LINE_EMPTY_EXPERTS 5 /* empty expert_ids */
+#define MOEB_LINE_INT_EXPERT 6    /* an expert_ids part not an integer */
+#define MOEB_LINE_INT_TOKID 7     /* column token_id not an integer */
+#define MOEB_LINE_EMBED 8         /* bad embedding */
+#define MOEB_LINE_RANGE_NEG 16    /* TokenRecord.validate: negative prompt/token */
+#define MOEB_LINE_RANGE_LAYER 17  /* layer out of range */
+#define MOEB_LINE_RANGE_DUPEXP 18 /* duplicate expert ids */
+#define MOEB_LINE_RANGE_COUNT 19  /* not top_k expert ids */
+#define MOEB_LINE_RANGE_EXPERT 20 /* expert out of range */
+#define MOEB_LINE_SKIP 30         /* predictions: blank line (skipped) */
+#define MOEB_LINE_HOST 32         /* outside the device grammar (non-ASCII,
+                                     > int64, > 32 expert parts, general JSON):
+                                     the host parses this line itself */
+
+/*
+ * moeb_parse_trace_csv -- parse_trace_csv's per-line loop (traceio.py:64-103):
+ * data line i (0-based, file line i + 2) is segment first_segment + i of the
+ * newline split (segment j = [nl[j-1]+1, nl[j]) with nl[-1] = -1, the last
+ * one ending at n). Python int()/float() grammar (ASCII whitespace, sign,
+ * digit underscores; float inf/nan) and TokenRecord.validate (core.py:84-105)
+ * in the reference's check order. Per line: status (MOEB_LINE_*), key
+ * (prompt_id, token_index, layer_id), expert mask [W], token_id and
+ * has_embedding. flags |= 1 if any byte >= 0x80 (UTF-8 check on the host).
+ */
+int moeb_parse_trace_csv(const uint8_t* buf, int64_t n, const int64_t* nl, int64_t n_nl,
+                         int64_t first_segment, int64_t n_lines, int L, int E, int top_k,
+                         uint8_t* status, int64_t* prompt_id, int64_t* token_index,
+                         int32_t* layer_id, uint64_t* masks, int64_t* token_id,
+                         uint8_t* has_embedding, int32_t* flags, void* stream);
+
+/*
+ * moeb_parse_predictions -- parse_predictions' per-line loop
+ * (traceio.py:142-169) for lines 1..n_lines (segments 0..n_lines-1): blank
+ * lines -> MOEB_LINE_SKIP; objects of integer fields prompt_id, token_index,
+ * layer_id and an integer array experts (any key order, JSON whitespace) are
+ * parsed on device; the expert range check (list order) reports
+ * MOEB_LINE_RANGE_EXPERT, then the layer range check MOEB_LINE_RANGE_LAYER.
+ * Everything else is MOEB_LINE_HOST (json.loads on the host for that line).
+ */
+int moeb_parse_predictions(const uint8_t* buf, int64_t n, const int64_t* nl, int64_t n_nl,
+                           int64_t n_lines, int L, int E, uint8_t* status, int64_t* prompt_id,
+                           int64_t* token_index, int32_t* layer_id, uint64_t* masks,
+                           int32_t* flags, void* stream);
+
+/* First index i in [0, n) with status[i] != 0 and != skip_code (n if none) ->
+ * *out (device). */
+int moeb_first_status(const uint8_t* status, int64_t n, int skip_code, int64_t* out,
+                      void* stream);
+
+/* Key order check over rows [0, n) of (a, b, c) int64/int64/int32 keys whose
+ * status is 0 (other rows ignored, `status` nullable): out[0] = number of
+ * adjacent descents, out[1] = first index i whose key equals the previous
+ * counted key (n if none). Sorted input => out[1] is the first duplicate. */
+int moeb_keys_check(const int64_t* a, const int64_t* b, const int32_t* c, const uint8_t* status,
+                    int skip_code, int64_t n, int64_t* out, void* stream);
+
+/*
+ * Prompt grid of sorted, duplicate-free trace rows (PromptTrace.validate,
+ * core.py:128-149): starts[p] = first row of prompt p (rows where prompt_id
+ * changes; moeb_count_bytes/find_bytes over `flags` from moeb_prompt_flags),
+ * then moeb_check_grid: every prompt's rows must be exactly (t, l) for
+ * t < T_p, l < L; *bad_prompt = first failing prompt index (P if none).
+ */
+int moeb_prompt_flags(const int64_t* prompt_id, int64_t n, uint8_t* flags, void* stream);
+int moeb_check_grid(const int64_t* starts, int64_t n_prompts, int64_t n_rows,
+                    const int64_t* token_index, const int32_t* layer_id, int L,
+                    int64_t* bad_prompt, void* stream);
+
+/*
+ * External predictions joined onto packed traces (ExternalPredictor,
+ * predictors.py:222-242; engine.py:175-176): table rows sorted by (prompt_id,
+ * token_index, layer_id); for every trace row, pred = the table's mask and
+ * covered = 1, or pred = 0 and covered = 0 when the step is absent.
+ */
+int moeb_predictions_join(const int64_t* t_prompt, const int64_t* t_token, const int32_t* t_layer,
+                          const uint64_t* t_masks, int64_t n_table, const int64_t* prompt_ids,
+                          const int64_t* prompt_row_off, int n_prompts, int L, int E,
+                          uint64_t* pred, uint8_t* covered, void* stream);
+
+/*
+ * Canonical writers on device. Both first size every line (lens), then the
+ * caller runs moeb_exclusive_scan_i64 over lens (offsets, total), then writes.
+ * moeb_trace_csv_*: write_trace_csv (traceio.py:113-128) of packed traces
+ *   without embeddings: "prompt_id,token_index,layer_id,e1|e2|..,token_id,\n"
+ *   (token_ids per trace token, nullable -> 0); header by the caller.
+ * moeb_predictions_jsonl_*: write_predictions_jsonl (traceio.py:172-186) of a
+ *   table sorted by key: {"prompt_id":p,"token_index":t,"layer_id":l,
+ *   "experts":[...]}\n.
+ * moeb_exclusive_scan_i64: out[i] = sum(in[0..i)), out[n] = total; ws holds
+ *   ceil(n / 4096) + 1 int64.
+ */
+int moeb_trace_csv_lengths(const uint64_t* truth, const int64_t* prompt_ids,
+                           const int64_t* prompt_row_off, int n_prompts, int L, int E,
+                           const int32_t* token_ids, int64_t* lens, void* stream);
+int moeb_trace_csv_write(const uint64_t* truth, const int64_t* prompt_ids,
+                         const int64_t* prompt_row_off, int n_prompts, int L, int E,
+                         const int32_t* token_ids, const int64_t* offsets, uint8_t* out,
+                         void* stream);
+int moeb_predictions_jsonl_lengths(const int64_t* t_prompt, const int64_t* t_token,
+                                   const int32_t* t_layer, const uint64_t* t_masks, int64_t n,
+                                   int E, int64_t* lens, void* stream);
+int moeb_predictions_jsonl_write(const int64_t* t_prompt, const int64_t* t_token,
+                                 const int32_t* t_layer, const uint64_t* t_masks, int64_t n,
+                                 int E, const int64_t* offsets, uint8_t* out, void* stream);
+int moeb_exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* ws,
+                            void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,20 @@ _SIGS = {
     "moeb_eam_pack_queries": [P, I32, I32, P, P],
     "moeb_eam_rerank": [P, P, I32, P, P, P, I32, I32, I32, DBL, P, P, P, P],
     "moeb_token_prefix_counts": [P, P, P, I32, I32, I32, I32, P, P],
+    "moeb_count_bytes": [P, I64, I32, P, P, P],
+    "moeb_find_bytes": [P, I64, I32, P, P, P],
+    "moeb_parse_trace_csv": [P, I64, P, I64, I64, I64, I32, I32, I32, P, P, P, P, P, P, P, P, P],
+    "moeb_parse_predictions": [P, I64, P, I64, I64, I32, I32, P, P, P, P, P, P, P],
+    "moeb_first_status": [P, I64, I32, P, P],
+    "moeb_keys_check": [P, P, P, P, I32, I64, P, P],
+    "moeb_prompt_flags": [P, I64, P, P],
+    "moeb_check_grid": [P, I64, I64, P, P, I32, P, P],
+    "moeb_predictions_join": [P, P, P, P, I64, P, P, I32, I32, I32, P, P, P],
+    "moeb_trace_csv_lengths": [P, P, P, I32, I32, I32, P, P, P],
+    "moeb_trace_csv_write": [P, P, P, I32, I32, I32, P, P, P, P],
+    "moeb_predictions_jsonl_lengths": [P, P, P, P, I64, I32, P, P],
+    "moeb_predictions_jsonl_write": [P, P, P, P, I64, I32, P, P, P],
+    "moeb_exclusive_scan_i64": [P, I64, P, P, P],
     "moeb_version": [],
     "moeb_device_check": [],
 }

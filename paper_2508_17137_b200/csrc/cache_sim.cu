@@ -723,13 +723,13 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   // G lanes per simulation (32: one per warp; 16: two per warp). All
   // collectives below are restricted to the group's lanes (gmask), so the
   // two groups of a warp may diverge (fallback rows, different row counts).
-  static_assert(G == 16 || G == 32, "G must be 16 or 32");
+  static_assert(G == 8 || G == 16 || G == 32, "G must be 8, 16 or 32");
   extern __shared__ __align__(16) unsigned char smem[];
   const int L = a.L, E = a.E;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int hl = lane & (G - 1), gbase = lane - hl;
-  const unsigned gmask = G == 32 ? 0xffffffffu : (0xffffu << gbase);
-  const unsigned glow = G == 32 ? 0xffffffffu : 0xffffu;
+  const unsigned glow = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  const unsigned gmask = glow << gbase;
   unsigned int* bcnt = reinterpret_cast<unsigned int*>(smem);  // [3L] block counters
   for (int j = threadIdx.x; j < 3 * L; j += blockDim.x) bcnt[j] = 0;
   __syncthreads();
@@ -1070,6 +1070,9 @@ int launch_kernel(K k, const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
   return moeb::check_launch("k_cache_sim");
 }
 
+template <int W, int ES, int G>
+int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block);
+
 // LRU: warp-per-simulation kernel; E = 64 / 256 get shift-based key math.
 template <int W, int ES>
 int launch_lru(SimArgs a, cudaStream_t s) {
@@ -1077,8 +1080,17 @@ int launch_lru(SimArgs a, cudaStream_t s) {
   const int head = align16(4LL * 3 * a.L);
   a.off_c = head;
   // Two simulations per warp (16 lanes each) unless the state is so large
-  // that only one or two simulations fit a block.
-  constexpr int G = 16;
+  // that only one or two simulations fit a block. MOEB_K1_G (tuning knob):
+  // lanes per simulation, 8 / 16 / 32.
+  const char* env = getenv("MOEB_K1_G");
+  const int g = env ? atoi(env) : 16;
+  if (g == 8) return launch_lru_g<W, ES, 8>(a, s, head, max_block);
+  if (g == 32) return launch_lru_g<W, ES, 32>(a, s, head, max_block);
+  return launch_lru_g<W, ES, 16>(a, s, head, max_block);
+}
+
+template <int W, int ES, int G>
+int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
   int nw = 4;  // warps per block
   while (nw > 1 && head + (int64_t)nw * (32 / G) * a.sim_bytes > max_block) --nw;
   if (head + (int64_t)nw * (32 / G) * a.sim_bytes > max_block) {

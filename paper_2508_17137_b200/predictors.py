@@ -184,25 +184,15 @@ class ExternalPredictor(DevicePredictor):
         return (prompt_id, token_index, layer_id) in self.table
 
     def _build(self, packed: PackedTraces):
+        """Masks + coverage per trace row: the table (key-sorted device
+        arrays; a dict is packed once) joined onto the rows on device
+        (moeb_predictions_join)."""
+        from .traceio import PredictionTable, join_predictions
         key = (id(packed), packed.rows)
         if key not in self._cache:
-            L, W = self.shape.num_layers, self.shape.mask_words
-            rows = packed.rows
-            masks = np.zeros((rows, W), dtype=np.uint64)
-            cov = np.zeros(rows, dtype=np.uint8)
-            off = packed.row_off_host
-            for i, pid in enumerate(packed.prompt_ids):
-                pid = int(pid)
-                for r in range(int(off[i]), int(off[i + 1])):
-                    t, l = divmod(r - int(off[i]), L)
-                    s = self.table.get((pid, t, l))
-                    if s is None:
-                        continue
-                    cov[r] = 1
-                    for e in s:
-                        masks[r, e >> 6] |= np.uint64(1) << np.uint64(e & 63)
-            self._cache = {key: (torch.from_numpy(masks.view(np.int64)).to(packed.device),
-                                 torch.from_numpy(cov).to(packed.device))}
+            if not isinstance(self.table, PredictionTable):
+                self.table = PredictionTable.from_dict(self.table, self.shape, packed.device)
+            self._cache = {key: join_predictions(self.table, packed)}
         return self._cache[key]
 
     def predict_masks(self, packed, budget, warmup=0, metrics=None):

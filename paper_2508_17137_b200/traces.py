@@ -86,10 +86,27 @@ class PackedTraces:
         r0, r1 = int(self.row_off_host[lo]), int(self.row_off_host[hi])
         L = self.shape.num_layers
         off = self.row_off_host[lo:hi + 1] - r0
+        meta = {k: v for k, v in self.meta.items() if k not in ("embeddings", "row_token_ids")}
         return PackedTraces(
             self.shape, self.truth[r0:r1], torch.as_tensor(off, device=self.device),
             off, self.prompt_ids[lo:hi],
-            None if self.token_ids is None else self.token_ids[r0 // L:r1 // L], dict(self.meta))
+            None if self.token_ids is None else self.token_ids[r0 // L:r1 // L], meta)
+
+    def reorder(self, order) -> "PackedTraces":
+        """Prompts in the given order (a gather of whole prompts on device)."""
+        order = np.asarray(order, dtype=np.int64)
+        L = self.shape.num_layers
+        lens = np.diff(self.row_off_host)[order]
+        off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        idx = np.concatenate([np.arange(self.row_off_host[i], self.row_off_host[i + 1])
+                              for i in order]) if len(order) else np.zeros(0, np.int64)
+        idx_d = torch.from_numpy(idx).to(self.device)
+        tok = None
+        if self.token_ids is not None:
+            tok = self.token_ids[torch.div(idx_d[::L], L, rounding_mode="floor")]
+        return PackedTraces(self.shape, self.truth[idx_d].contiguous(),
+                            torch.from_numpy(off).to(self.device), off, self.prompt_ids[order],
+                            tok, {})
 
     def shard(self, rank: int, world: int) -> "PackedTraces":
         """Contiguous prompt range of this rank with ~equal row counts."""
@@ -100,28 +117,62 @@ class PackedTraces:
         bounds = [0] + [int(c) for c in cuts] + [self.num_prompts]
         return self.select(bounds[rank], bounds[rank + 1])
 
-    def unpack(self) -> list[PromptTrace]:
-        """Host PromptTrace objects (slow; for compatibility and small cases)."""
+    # A PackedTraces is also a read-only sequence of PromptTrace (the type the
+    # reference's parse_trace_csv / generate_synthetic return), materialised
+    # one prompt at a time.
+    def __len__(self) -> int:
+        return self.num_prompts
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            lo, hi, step = i.indices(self.num_prompts)
+            if step != 1:
+                return [self[k] for k in range(lo, hi, step)]
+            return self.select(lo, max(lo, hi))
+        if i < 0:
+            i += self.num_prompts
+        if not 0 <= i < self.num_prompts:
+            raise IndexError(i)
+        return self._prompt(i, *self._host_views())
+
+    def __iter__(self):
+        views = self._host_views()
+        for i in range(self.num_prompts):
+            yield self._prompt(i, *views)
+
+    def _host_views(self):
         truth = self.truth.cpu().numpy().view(np.uint64)
         toks = None if self.token_ids is None else self.token_ids.cpu().numpy()
+        rtok = self.meta.get("row_token_ids")
+        rtok = None if rtok is None else rtok.cpu().numpy()
+        emb = {}
+        if "embeddings" in self.meta:
+            from .traceio import row_embeddings
+            emb = row_embeddings(self)
+        return truth, toks, rtok, emb
+
+    def _prompt(self, i, truth, toks, rtok, emb) -> PromptTrace:
         L, E = self.shape.num_layers, self.shape.num_experts
-        out = []
-        for i, pid in enumerate(self.prompt_ids):
-            tr = PromptTrace(int(pid))
-            r0, r1 = int(self.row_off_host[i]), int(self.row_off_host[i + 1])
-            for r in range(r0, r1):
-                ids = []
-                for w, word in enumerate(truth[r]):
-                    word = int(word)
-                    while word:
-                        b = word & -word
-                        ids.append(w * 64 + b.bit_length() - 1)
-                        word ^= b
-                t, l = (r - r0) // L, (r - r0) % L
-                tr.records.append(TokenRecord(int(pid), t, l, tuple(e for e in ids if e < E),
-                                              0 if toks is None else int(toks[r // L])))
-            out.append(tr)
-        return out
+        pid = int(self.prompt_ids[i])
+        tr = PromptTrace(pid)
+        r0, r1 = int(self.row_off_host[i]), int(self.row_off_host[i + 1])
+        for r in range(r0, r1):
+            ids = []
+            for w, word in enumerate(truth[r]):
+                word = int(word)
+                while word:
+                    b = word & -word
+                    ids.append(w * 64 + b.bit_length() - 1)
+                    word ^= b
+            t, l = (r - r0) // L, (r - r0) % L
+            tid = int(rtok[r]) if rtok is not None else (0 if toks is None else int(toks[r // L]))
+            tr.records.append(TokenRecord(pid, t, l, tuple(e for e in ids if e < E), tid,
+                                          emb.get(r, ())))
+        return tr
+
+    def unpack(self) -> list[PromptTrace]:
+        """Host PromptTrace objects (slow; for compatibility and small cases)."""
+        return list(self)
 
 
 def _device(device):
