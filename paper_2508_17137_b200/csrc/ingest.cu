@@ -288,6 +288,69 @@ constexpr int kMaxParts = 32;
 // ---------------------------------------------------------------------------
 // Trace CSV lines (traceio.py:64-103 + TokenRecord.validate, core.py:84-105).
 // ---------------------------------------------------------------------------
+
+// Fast path for canonical lines -- unsigned decimal fields of <= 18 digits,
+// '|' only inside expert_ids, in-range expert ids, empty embedding -- in one
+// pass over the line's 16-byte vectors. Returns false when the line needs
+// the general path (which then decides the status); otherwise sets the
+// status (OK or the TokenRecord.validate error) and the record.
+template <int W>
+__device__ __forceinline__ bool fast_csv_line(const uint8_t* buf, int64_t s, int64_t e, int L,
+                                              int E, int top_k, int64_t* out_vals /*pid,tok,lay,tid*/,
+                                              uint64_t (&m)[W], uint8_t* st) {
+  uint64_t v = 0;
+  int nd = 0, f = 0, np = 0;
+  bool ok = true, dup = false;
+  uint64_t vals[5] = {0, 0, 0, 0, 0};
+  const uint4* vp = reinterpret_cast<const uint4*>(buf);
+  for (int64_t base = s & ~(int64_t)15; base < e && ok; base += 16) {
+    const uint4 q = __ldg(vp + (base >> 4));
+    const uint32_t words[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int64_t pos = base + k;
+      const uint32_t c = (words[k >> 2] >> ((k & 3) * 8)) & 0xffu;
+      const uint32_t d = c - '0';
+      const bool in = pos >= s && pos < e;
+      if (in && d < 10u) {
+        v = v * 10u + d;
+        ++nd;
+      } else if (in) {
+        // a separator: ',' ends field f, '|' ends one expert part (f == 3)
+        const bool sep_ok = (c == ',' && f < 5) || (c == '|' && f == 3);
+        ok = ok && sep_ok && nd > 0 && nd <= 18;
+        if (f == 3) {
+          ok = ok && v < (uint64_t)E;
+          const int ex = (int)(v & 255);
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            const uint64_t bit = (ex >> 6) == w ? (1ull << (ex & 63)) : 0ull;
+            dup |= (m[w] & bit) != 0;
+            m[w] |= bit;
+          }
+          ++np;
+        } else {
+          vals[f < 5 ? f : 4] = v;
+        }
+        f += c == ',' ? 1 : 0;
+        v = 0;
+        nd = 0;
+      }
+    }
+  }
+  // the line must end inside an empty embedding field
+  ok = ok && f == 5 && nd == 0;
+  if (!ok) return false;
+  out_vals[0] = (int64_t)vals[0];
+  out_vals[1] = (int64_t)vals[1];
+  out_vals[2] = (int64_t)vals[2];
+  out_vals[3] = (int64_t)vals[4];
+  if (vals[2] >= (uint64_t)L) *st = MOEB_LINE_RANGE_LAYER;
+  else if (dup) *st = MOEB_LINE_RANGE_DUPEXP;
+  else if (np != top_k) *st = MOEB_LINE_RANGE_COUNT;
+  else *st = MOEB_LINE_OK;
+  return true;
+}
 template <int W>
 __global__ void __launch_bounds__(kThreads) k_parse_trace_csv(
     const uint8_t* buf, int64_t n, const int64_t* nl, int64_t n_nl, int64_t first_seg,
@@ -298,8 +361,26 @@ __global__ void __launch_bounds__(kThreads) k_parse_trace_csv(
   if (i >= n_lines) return;
   int64_t s, e;
   segment(nl, n_nl, n, first_seg + i, &s, &e);
+  {
+    uint64_t fm[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) fm[w] = 0;
+    int64_t vals[4];
+    uint8_t fst;
+    if (fast_csv_line<W>(buf, s, e, L, E, top_k, vals, fm, &fst)) {
+      status[i] = fst;
+      prompt_id[i] = vals[0];
+      token_index[i] = vals[1];
+      layer_id[i] = (int32_t)vals[2];
+      token_id[i] = vals[3];
+      has_emb[i] = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) masks[i * W + w] = fst == MOEB_LINE_OK ? fm[w] : 0ull;
+      return;
+    }
+  }
   ByteReader rd(buf);
-  // one pass: field boundaries, non-ASCII
+  // general path: field boundaries, non-ASCII
   int64_t fb[7];
   fb[0] = s;
   int ncomma = 0;

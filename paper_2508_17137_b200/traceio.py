@@ -25,6 +25,7 @@ token_index and layer_id must fit int64 and token_id int32.
 from __future__ import annotations
 
 import json
+import warnings
 from collections.abc import Mapping
 
 import numpy as np
@@ -135,12 +136,17 @@ def _grid_error(pid: int, toks: np.ndarray, layers: np.ndarray, L: int) -> Range
 # ---------------------------------------------------------------------------
 
 def _upload(raw: bytes, dev) -> torch.Tensor:
-    """File bytes in HBM, padded to 16 bytes (the kernels read whole vectors)."""
+    """File bytes in HBM, padded to 16 bytes (the kernels read whole vectors).
+    One host->device copy straight from the bytes object (no host copies)."""
     n = len(raw)
-    host = torch.zeros(((n + 15) // 16) * 16 or 16, dtype=torch.uint8).pin_memory()
+    out = torch.empty(((n + 15) // 16) * 16 or 16, dtype=torch.uint8, device=dev)
     if n:
-        host[:n] = torch.frombuffer(bytearray(raw), dtype=torch.uint8)
-    return host.to(dev, non_blocking=True)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")  # read-only source buffer: only read here
+            src = torch.from_numpy(np.frombuffer(raw, dtype=np.uint8))
+        out[:n].copy_(src)
+    out[n:].zero_()
+    return out
 
 
 def _find_bytes(buf: torch.Tensor, n: int, value: int) -> torch.Tensor:
