@@ -388,6 +388,29 @@ int moeb_predictions_jsonl_write(const int64_t* t_prompt, const int64_t* t_token
 int moeb_exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t* ws,
                             void* stream);
 
+/*
+ * EAMC k-means on device (sketches.kmeans, sketches.py:62-139).
+ *  moeb_row_sqnorms    out[i] = (X[i] * X[i]).sum() with numpy's pairwise
+ *                      summation (bit-identical)
+ *  moeb_sqdist_argmin  per vector: first centroid minimising
+ *                      max((xn - 2 x.c) + cn, 0) (_squared_distances,
+ *                      sketches.py:62-69) and that distance (out_d2 nullable)
+ *  moeb_sqdist_update  k-means++: d2 = dist(x, c) (init) or minimum(d2, dist)
+ *                      for one centroid c with squared norm *cn (device)
+ *  moeb_cluster_means  centroids[j] = mean of the members of cluster j, members
+ *                      listed cluster by cluster in index order (members,
+ *                      offs [k+1]); empty clusters keep their centroid
+ * X [n][D], C [k][D] fp64 row-major.
+ */
+int moeb_row_sqnorms(const double* X, int64_t n, int64_t D, double* out, void* stream);
+int moeb_sqdist_argmin(const double* X, const double* xn, const double* C, const double* cn,
+                       int64_t n, int k, int64_t D, int64_t* out_idx, double* out_d2,
+                       void* stream);
+int moeb_sqdist_update(const double* X, const double* xn, const double* c, const double* cn,
+                       int64_t n, int64_t D, int init, double* d2, void* stream);
+int moeb_cluster_means(const double* X, const int64_t* members, const int64_t* offs, int k,
+                       int64_t D, double* centroids, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

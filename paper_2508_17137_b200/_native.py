@@ -69,6 +69,10 @@ _SIGS = {
     "moeb_predictions_jsonl_lengths": [P, P, P, P, I64, I32, P, P],
     "moeb_predictions_jsonl_write": [P, P, P, P, I64, I32, P, P, P],
     "moeb_exclusive_scan_i64": [P, I64, P, P, P],
+    "moeb_row_sqnorms": [P, I64, I64, P, P],
+    "moeb_sqdist_argmin": [P, P, P, P, I64, I32, I64, P, P, P],
+    "moeb_sqdist_update": [P, P, P, P, I64, I64, I32, P, P],
+    "moeb_cluster_means": [P, P, P, I32, I64, P, P],
     "moeb_version": [],
     "moeb_device_check": [],
 }

@@ -105,3 +105,45 @@ def load_model(path) -> LinearModel:
     if not np.isfinite(weights).all():
         raise ConfigError("model weights must be finite")
     return LinearModel(shape, config, weights, trained, losses)
+
+
+# Per-vector helpers of the reference's learner (learner.py:52-72, :158-182).
+# They score ONE feature vector on the host, exactly as the reference does;
+# whole traces go through K3 (moeb_linear_predict), never through these.
+
+def feature_vector(target_layer: int, layer_history: np.ndarray, shape: ModelShape) -> np.ndarray:
+    """[layer one-hot | decayed history for the target layer | 1.0] (learner.py:52-59)."""
+    f = np.zeros(shape.num_layers + shape.num_experts + 1, dtype=np.float64)
+    f[target_layer] = 1.0
+    f[shape.num_layers:shape.num_layers + shape.num_experts] = layer_history
+    f[-1] = 1.0
+    return f
+
+
+def update_history(history: np.ndarray, layer_id: int, expert_ids, decay: float) -> None:
+    """history[layer] = decay * history[layer] + firings (learner.py:62-72)."""
+    history[layer_id] *= decay
+    for e in expert_ids:
+        history[layer_id, e] += 1.0
+
+
+def predict_scores(model: LinearModel, features: np.ndarray) -> np.ndarray:
+    if not model.trained:
+        raise ConfigError("model is untrained")
+    return model.weights @ features
+
+
+def top_k_experts(scores: np.ndarray, k: int) -> frozenset[int]:
+    """The k highest-scoring experts, ties to the lower id (learner.py:164-169)."""
+    k = min(k, len(scores))
+    order = np.lexsort((np.arange(len(scores)), -np.asarray(scores)))
+    return frozenset(int(e) for e in order[:k])
+
+
+def predict_topk(model: LinearModel, features: np.ndarray, k: int,
+                 threshold: bool = False) -> frozenset[int]:
+    """Top-k experts by logit, or logit > 0 in threshold mode (learner.py:172-182)."""
+    scores = predict_scores(model, features)
+    if threshold:
+        return frozenset(int(e) for e in np.nonzero(scores > 0.0)[0])
+    return top_k_experts(scores, k)

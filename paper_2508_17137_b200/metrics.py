@@ -109,3 +109,54 @@ def label_accuracy(pred_sets, truth_sets, num_experts: int) -> float:
     if not truth_sets:
         return 0.0
     return _sets_counts(pred_sets, truth_sets, num_experts).label_accuracy
+
+
+@dataclass
+class ActivationReport:
+    """Exact activation counts per (layer, expert) plus per-prompt sparsity
+    (metrics.py:80-92)."""
+
+    layer_expert_counts: np.ndarray
+    prompt_ids: list[int]
+    prompt_layer_distinct: np.ndarray
+
+    @property
+    def total_activations(self) -> int:
+        return int(self.layer_expert_counts.sum())
+
+
+def activation_report(traces, shape) -> ActivationReport:
+    """metrics.activation_report (metrics.py:95-119) from the per-prompt
+    activation counts K8 (moeb_ream_counts) computes on device: layer totals
+    are their sum over prompts, distinct counts their per-layer support."""
+    from .sketches import ream_counts
+    from .traces import PackedTraces, pack_traces
+
+    packed = traces if isinstance(traces, PackedTraces) else pack_traces(traces, shape)
+    L, E = shape.num_layers, shape.num_experts
+    if packed.num_prompts == 0:
+        return ActivationReport(np.zeros((L, E), dtype=np.int64), [],
+                                np.zeros((0, L), dtype=np.int64))
+    counts = ream_counts(packed).view(packed.num_prompts, L, E)
+    totals = counts.sum(dim=0, dtype=torch.int64).cpu().numpy()
+    distinct = (counts > 0).sum(dim=2, dtype=torch.int64).cpu().numpy()
+    return ActivationReport(totals, [int(p) for p in packed.prompt_ids], distinct)
+
+
+def activation_report_csv(report: ActivationReport) -> bytes:
+    """metrics.activation_report_csv (metrics.py:122-128)."""
+    lines = ["layer_id,expert_id,count"]
+    counts = report.layer_expert_counts
+    for layer in range(counts.shape[0]):
+        for expert in range(counts.shape[1]):
+            lines.append(f"{layer},{expert},{counts[layer, expert]}")
+    return ("\n".join(lines) + "\n").encode("utf-8")
+
+
+def distinct_report_csv(report: ActivationReport) -> bytes:
+    """metrics.distinct_report_csv (metrics.py:131-136)."""
+    lines = ["prompt_id,layer_id,distinct_experts"]
+    for row, pid in enumerate(report.prompt_ids):
+        for layer in range(report.prompt_layer_distinct.shape[1]):
+            lines.append(f"{pid},{layer},{report.prompt_layer_distinct[row, layer]}")
+    return ("\n".join(lines) + "\n").encode("utf-8")

@@ -16,17 +16,33 @@ paper's predictor, transformer.py).
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 
 from . import _native as nat
-from .core import ConfigError, ModelShape
+from .core import ActivationMatrix, ConfigError, ModelShape
 from .learner import LinearModel
 from .sketches import SketchCollection, ream_counts
 from .traces import PackedTraces, pack_traces
 
 PREDICTOR_KINDS = ("oracle", "lru_only", "next_layer_all", "global_frequency", "eam_cosine",
                    "external", "learned_linear", "transformer")
+
+
+@dataclass
+class PredictionContext:
+    """One (token, layer) query of the reference's per-step protocol
+    (predictors.py:40-54). The device predictors here work on whole traces
+    (predict_masks); the type is kept for API compatibility."""
+
+    prompt_id: int
+    token_index: int
+    target_layer: int
+    partial_ream: ActivationMatrix
+    history: np.ndarray
+    budget: int
 
 
 def _empty(packed: PackedTraces) -> torch.Tensor:

@@ -2,16 +2,15 @@
 in the reference, :26-255).
 
 Sketches are row-normalised, layer-major flattened rEAMs. Building them from
-traces (counts + normalisation) and every match run on device; the raw
-sketches also stay on the host for JSON persistence. k-means EAMC
-construction (sketches.py:89-139) is the offline step before this path and is
-a DESIGN.md next component.
+traces (counts + normalisation), k-means EAMC construction
+(sketches.py:62-139; csrc/kmeans.cu) and every match run on device; the raw
+sketches also stay on the host for JSON persistence.
 """
 
 from __future__ import annotations
 
 import json
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -129,6 +128,113 @@ def normalize_counts(counts: torch.Tensor, shape: ModelShape, binarize: bool = F
     return out
 
 
+@dataclass
+class KMeansResult:
+    """sketches.KMeansResult (sketches.py:53-59)."""
+
+    centroids: np.ndarray
+    assignments: np.ndarray
+    objective: float
+    objective_history: list[float] = field(default_factory=list)
+    effective_k: int = 0
+
+
+def _sqnorms(X: torch.Tensor) -> torch.Tensor:
+    out = torch.empty(X.shape[0], dtype=torch.float64, device=X.device)
+    nat.call("moeb_row_sqnorms", nat.ptr(X), X.shape[0], X.shape[1], nat.ptr(out),
+             nat.stream_ptr())
+    return out
+
+
+def _assign(X, xn, C):
+    """First nearest centroid per vector and its squared distance (K9)."""
+    n, D = X.shape
+    cn = _sqnorms(C)
+    idx = torch.empty(n, dtype=torch.int64, device=X.device)
+    d2 = torch.empty(n, dtype=torch.float64, device=X.device)
+    nat.call("moeb_sqdist_argmin", nat.ptr(X), nat.ptr(xn), nat.ptr(C), nat.ptr(cn), n,
+             C.shape[0], D, nat.ptr(idx), nat.ptr(d2), nat.stream_ptr())
+    return idx, d2
+
+
+def _plusplus_init(X, xn, k: int, rng: np.random.Generator) -> torch.Tensor:
+    """sketches._plusplus_init (sketches.py:72-86): distances on device, the
+    seeded draws (rng.integers / rng.choice over d2 / total) on the host with
+    the reference's own numpy calls so the chosen indices follow its stream."""
+    n, D = X.shape
+    C = torch.empty((k, D), dtype=torch.float64, device=X.device)
+    d2 = torch.empty(n, dtype=torch.float64, device=X.device)
+    first = int(rng.integers(0, n))
+    C[0] = X[first]
+    for j in range(k):
+        if j > 0:
+            d2h = d2.cpu().numpy()
+            total = d2h.sum()
+            if total <= 0.0:
+                idx = int(rng.integers(0, n))
+            else:
+                idx = int(rng.choice(n, p=d2h / total))
+            C[j] = X[idx]
+            if j == k - 1:
+                break
+        cn = _sqnorms(C[j:j + 1])
+        nat.call("moeb_sqdist_update", nat.ptr(X), nat.ptr(xn), nat.ptr(C[j]), nat.ptr(cn), n,
+                 D, int(j == 0), nat.ptr(d2), nat.stream_ptr())
+    return C
+
+
+def kmeans(vectors, k: int, seed: int = 0, max_iters: int = 100, device=None) -> KMeansResult:
+    """sketches.kmeans (sketches.py:89-139): Lloyd's algorithm with seeded
+    k-means++ initialisation, on device. Assignment = fused distance GEMM +
+    argmin (K9); centroid update = per-cluster means in member index order
+    (bit-identical to numpy for identical assignments); empty clusters are
+    re-seeded from the farthest points (stable order). Returns numpy arrays
+    like the reference."""
+    if isinstance(vectors, torch.Tensor):
+        X = vectors.to(torch.float64)
+    else:
+        arr = np.asarray(vectors, dtype=np.float64)
+        if arr.ndim != 2 or arr.shape[0] < 1:
+            raise DimensionError("kmeans needs a non-empty 2-D array of vectors")
+        nat.load_library()
+        X = torch.from_numpy(np.ascontiguousarray(arr)).to(
+            device if device is not None else torch.device("cuda", torch.cuda.current_device()))
+    if X.dim() != 2 or X.shape[0] < 1:
+        raise DimensionError("kmeans needs a non-empty 2-D array of vectors")
+    X = X.contiguous()
+    n, D = X.shape
+    k = min(k, n)
+    if k < 1:
+        raise ConfigError(f"k must be >= 1, got {k}")
+    rng = np.random.default_rng(seed)
+    xn = _sqnorms(X)
+    C = _plusplus_init(X, xn, k, rng)
+    assignments = None
+    history: list[float] = []
+    for _ in range(max_iters):
+        idx, pd2 = _assign(X, xn, C)
+        counts = torch.bincount(idx, minlength=k)
+        empty = torch.nonzero(counts == 0).flatten().tolist()
+        if empty:
+            order = np.argsort(-pd2.cpu().numpy(), kind="stable")
+            for taken, j in enumerate(empty):
+                C[j] = X[int(order[taken])]
+            idx, pd2 = _assign(X, xn, C)
+        history.append(float(pd2.cpu().numpy().sum()))
+        if assignments is not None and torch.equal(idx, assignments):
+            break
+        assignments = idx
+        counts = torch.bincount(idx, minlength=k)
+        members = torch.argsort(idx, stable=True)
+        offs = torch.zeros(k + 1, dtype=torch.int64, device=X.device)
+        offs[1:] = torch.cumsum(counts, 0)
+        nat.call("moeb_cluster_means", nat.ptr(X), nat.ptr(members), nat.ptr(offs), k, D,
+                 nat.ptr(C), nat.stream_ptr())
+    idx, pd2 = _assign(X, xn, C)
+    objective = float(pd2.cpu().numpy().sum())
+    return KMeansResult(C.cpu().numpy(), idx.cpu().numpy(), objective, history, k)
+
+
 def build_eamc(matrices, config: EamcConfig, shape: ModelShape | None = None) -> SketchCollection:
     """Collection from rEAMs (sketches.py:200-216): ActivationMatrix list or
     PackedTraces (one rEAM per prompt). Recent mode keeps the last `capacity`."""
@@ -143,10 +249,12 @@ def build_eamc(matrices, config: EamcConfig, shape: ModelShape | None = None) ->
         shape = matrices[0].shape
         counts = torch.as_tensor(np.stack([m.counts for m in matrices]).reshape(len(matrices), -1)
                                  .astype(np.int32)).cuda()
-    if config.mode != "recent":
-        raise NotImplementedError("k-means EAMC construction is a DESIGN.md next component")
-    counts = counts[-config.capacity:]
-    return SketchCollection(normalize_counts(counts, shape, config.binarize), config, shape)
+    if config.mode == "recent":
+        counts = counts[-config.capacity:]
+        return SketchCollection(normalize_counts(counts, shape, config.binarize), config, shape)
+    vectors = normalize_counts(counts, shape, config.binarize)
+    result = kmeans(vectors, config.capacity, seed=config.seed, max_iters=config.kmeans_max_iters)
+    return SketchCollection(result.centroids, config, shape)
 
 
 def save_eamc(collection: SketchCollection, path) -> None:
