@@ -112,6 +112,20 @@ int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_row_off, in
                         int64_t* metrics, void* stream);
 
 /*
+ * Wide K3 for 64 < E <= 256 (DeepSeek-V3: 256 experts), same semantics as
+ * moeb_linear_predict. moeb_linear_prepare builds the fp64 tables once per
+ * (weights, decay): tables [moeb_linear_table_doubles(L, E)] = W_h transposed
+ * [E][E], start scores [L][E] (W[:, l] + bias), (1 - decay) * start [L][E].
+ */
+size_t moeb_linear_table_doubles(int L, int E);
+int moeb_linear_prepare(const double* weights, int L, int E, double decay, double* tables,
+                        void* stream);
+int moeb_linear_predict_wide(const uint64_t* truth, const int64_t* prompt_row_off,
+                             int n_prompts, int L, int E, const double* tables, double decay,
+                             int budget, int threshold, int warmup_tokens, uint64_t* pred,
+                             double* logits, int64_t* metrics, void* stream);
+
+/*
  * K2 -- mask head: logits -> top-k (ties to lower id) or logit > 0 masks.
  * Replaces top_k_experts / predict_topk (learner.py:164-181). fp32 logits.
  */

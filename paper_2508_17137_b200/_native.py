@@ -73,11 +73,13 @@ _SIGS = {
     "moeb_sqdist_argmin": [P, P, P, P, I64, I32, I64, P, P, P],
     "moeb_sqdist_update": [P, P, P, P, I64, I64, I32, P, P],
     "moeb_cluster_means": [P, P, P, I32, I64, P, P],
+    "moeb_linear_prepare": [P, I32, I32, DBL, P, P],
+    "moeb_linear_predict_wide": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P],
     "moeb_version": [],
     "moeb_device_check": [],
 }
 
-EXPORTS = tuple(_SIGS) + ("moeb_last_error",)
+EXPORTS = tuple(_SIGS) + ("moeb_last_error", "moeb_linear_table_doubles")
 
 
 def load_library(require_gpu: bool = True):
@@ -92,6 +94,8 @@ def load_library(require_gpu: bool = True):
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
+        lib.moeb_linear_table_doubles.argtypes = [I32, I32]
+        lib.moeb_linear_table_doubles.restype = ctypes.c_size_t
         lib.moeb_last_error.argtypes = []
         lib.moeb_last_error.restype = ctypes.c_char_p
         _lib = lib

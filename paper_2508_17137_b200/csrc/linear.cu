@@ -282,6 +282,130 @@ int launch_k3(const LinArgs& a, cudaStream_t s) {
   return moeb::check_launch("k_linear_predict");
 }
 
+// ---------------------------------------------------------------------------
+// Wide K3 (64 < E <= 256, e.g. DeepSeek-V3's 256 experts): the 64-expert
+// kernel's column tables would not fit shared memory, so the tables
+// (moeb_linear_prepare: W_h transposed, per-layer start scores and biases)
+// stay in L2 and one WARP owns one (prompt, layer) stream: lane i holds the
+// scores of experts i + 32 s, column reads are 256-byte coalesced rows of the
+// transposed W_h. Same fp64 recurrence; exact fp64 top-k passes (warp
+// argmax, ties to the lower id) or the threshold rule.
+// ---------------------------------------------------------------------------
+template <int NSW>
+__global__ void __launch_bounds__(256) k_linear_predict_wide(
+    const uint64_t* __restrict__ truth, const int64_t* __restrict__ row_off, int P, int L, int E,
+    const double* __restrict__ tab, double decay, int budget, int threshold,
+    uint64_t* __restrict__ pred, double* __restrict__ logits) {
+  constexpr int W = (NSW * 32 + 63) / 64;
+  const int lane = threadIdx.x & 31;
+  const int64_t stream = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (stream >= (int64_t)P * L) return;
+  const int p = (int)(stream / L), l = (int)(stream % L);
+  const double* colT = tab;                            // [E][E]
+  const double* z0 = tab + (int64_t)E * E;             // [L][E]
+  const double* bias = z0 + (int64_t)L * E;            // [L][E]
+  const double NEG = -__longlong_as_double(0x7ff0000000000000LL);
+  double z[NSW], b[NSW];
+#pragma unroll
+  for (int s = 0; s < NSW; ++s) {
+    const int ex = lane + 32 * s;
+    z[s] = ex < E ? z0[(int64_t)l * E + ex] : NEG;
+    b[s] = ex < E ? bias[(int64_t)l * E + ex] : 0.0;
+  }
+  const int64_t r0 = row_off[p];
+  const int T = (int)((row_off[p + 1] - r0) / L);
+  const int k = budget < E ? budget : E;
+  for (int t = 0; t < T; ++t) {
+    const int64_t r = r0 + (int64_t)t * L + l;
+    uint64_t pm[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) pm[w] = 0;
+    if (threshold) {
+#pragma unroll
+      for (int s = 0; s < NSW; ++s) {
+        const uint64_t bits = __ballot_sync(0xffffffffu, z[s] > 0.0);
+        pm[s >> 1] |= bits << (32 * (s & 1));
+      }
+    } else {
+      bool taken[NSW];
+#pragma unroll
+      for (int s = 0; s < NSW; ++s) taken[s] = false;
+      for (int it = 0; it < k; ++it) {
+        double best = NEG;
+        int bi = 1 << 20;
+#pragma unroll
+        for (int s = 0; s < NSW; ++s) {
+          const int ex = lane + 32 * s;
+          const bool ok = ex < E && !taken[s] && (z[s] > best || (z[s] == best && ex < bi));
+          best = ok ? z[s] : best;
+          bi = ok ? ex : bi;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          const bool take = ob > best || (ob == best && oi < bi);
+          best = take ? ob : best;
+          bi = take ? oi : bi;
+        }
+        if ((bi & 31) == lane) {
+#pragma unroll
+          for (int s = 0; s < NSW; ++s)
+            if (bi >> 5 == s) taken[s] = true;
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          if ((bi >> 6) == w) pm[w] |= 1ull << (bi & 63);
+      }
+    }
+    if (lane < W) {
+      uint64_t v = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        if (w == lane) v = pm[w];
+      pred[r * W + lane] = v;
+    }
+    if (logits) {
+#pragma unroll
+      for (int s = 0; s < NSW; ++s)
+        if (lane + 32 * s < E) logits[r * E + lane + 32 * s] = z[s];
+    }
+    // z <- decay z + (1 - decay) b_l + sum of the truth experts' W_h columns
+#pragma unroll
+    for (int s = 0; s < NSW; ++s) z[s] = fma(decay, z[s], b[s]);
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint64_t mm = __ldg(truth + r * W + w);
+      while (mm) {
+        const int ex = w * 64 + __ffsll((long long)mm) - 1;
+        mm &= mm - 1;
+        const double* col = colT + (int64_t)ex * E;
+#pragma unroll
+        for (int s = 0; s < NSW; ++s)
+          if (lane + 32 * s < E) z[s] += __ldg(col + lane + 32 * s);
+      }
+    }
+  }
+}
+
+__global__ void k_linear_prepare(const double* __restrict__ Wt, int L, int E, double decay,
+                                 double* tab) {
+  const int F = L + E + 1;
+  const int64_t n1 = (int64_t)E * E, n2 = (int64_t)L * E;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n1 + 2 * n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < n1) {
+      const int e = (int)(i / E), j = (int)(i % E);
+      tab[i] = Wt[(int64_t)j * F + L + e];
+    } else {
+      const int64_t q = (i - n1) % n2;
+      const int l = (int)(q / E), j = (int)(q % E);
+      const double zz = Wt[(int64_t)j * F + l] + Wt[(int64_t)j * F + L + E];
+      tab[i] = i < n1 + n2 ? zz : (1.0 - decay) * zz;
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_row_off,
@@ -292,7 +416,8 @@ extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_
   moeb::clear_error();
   MOEB_REQUIRE(truth && prompt_row_off && weights && pred, "null argument");
   MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && E >= 1 && E <= 64,
-               "learned_linear kernel supports E <= 64 (got L=%d E=%d)", L, E);
+               "moeb_linear_predict supports E <= 64 (got L=%d E=%d); use "
+               "moeb_linear_prepare + moeb_linear_predict_wide", L, E);
   MOEB_REQUIRE(budget >= 1 && warmup_tokens >= 0, "bad budget/warmup");
   MOEB_REQUIRE(decay >= 0.0 && decay < 1.0, "decay must be in [0, 1)");
   LinArgs a{truth, prompt_row_off, n_prompts, L, E, weights, decay, budget,
@@ -302,6 +427,52 @@ extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_
                                          : launch_k3<2>(a, moeb::as_stream(stream));
   if (rc != 0 || metrics == nullptr) return rc;
   // K7 over the fresh masks (same stream): prediction metrics (metrics.py:12-79)
+  return moeb_metrics(pred, truth, prompt_row_off, n_prompts, L, E, warmup_tokens, metrics,
+                      stream);
+}
+
+extern "C" size_t moeb_linear_table_doubles(int L, int E) {
+  return (size_t)E * E + 2 * (size_t)L * E;
+}
+
+extern "C" int moeb_linear_prepare(const double* weights, int L, int E, double decay,
+                                   double* tables, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(weights && tables && L >= 1 && E >= 1 && E <= 256, "bad arguments");
+  k_linear_prepare<<<256, 256, 0, moeb::as_stream(stream)>>>(weights, L, E, decay, tables);
+  return moeb::check_launch("k_linear_prepare");
+}
+
+extern "C" int moeb_linear_predict_wide(const uint64_t* truth, const int64_t* prompt_row_off,
+                                        int n_prompts, int L, int E, const double* tables,
+                                        double decay, int budget, int threshold,
+                                        int warmup_tokens, uint64_t* pred, double* logits,
+                                        int64_t* metrics, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(truth && prompt_row_off && tables && pred, "null argument");
+  MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && E >= 1 && E <= 256, "bad shape L=%d E=%d", L, E);
+  MOEB_REQUIRE(budget >= 1 && warmup_tokens >= 0, "bad budget/warmup");
+  MOEB_REQUIRE(decay >= 0.0 && decay < 1.0, "decay must be in [0, 1)");
+  cudaStream_t s = moeb::as_stream(stream);
+  const int64_t threads = (int64_t)n_prompts * L * 32;
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
+  const int nsw = (E + 31) / 32;
+#define MOEB_K3W(N)                                                                        \
+  case N:                                                                                  \
+    k_linear_predict_wide<N><<<blocks, 256, 0, s>>>(truth, prompt_row_off, n_prompts, L, E, \
+                                                    tables, decay, budget, threshold, pred, \
+                                                    logits);                                \
+    break;
+  switch (nsw) {
+    MOEB_K3W(1) MOEB_K3W(2) MOEB_K3W(3) MOEB_K3W(4) MOEB_K3W(5) MOEB_K3W(6) MOEB_K3W(7)
+    default:
+      k_linear_predict_wide<8><<<blocks, 256, 0, s>>>(truth, prompt_row_off, n_prompts, L, E,
+                                                      tables, decay, budget, threshold, pred,
+                                                      logits);
+  }
+#undef MOEB_K3W
+  int rc = moeb::check_launch("k_linear_predict_wide");
+  if (rc != 0 || metrics == nullptr) return rc;
   return moeb_metrics(pred, truth, prompt_row_off, n_prompts, L, E, warmup_tokens, metrics,
                       stream);
 }

@@ -244,9 +244,29 @@ class LearnedLinearPredictor(DevicePredictor):
                 np.ascontiguousarray(self.model.weights, dtype=np.float64)).to(device)
         return self._w[key]
 
+    def tables_on(self, device) -> torch.Tensor:
+        """Wide-kernel tables (moeb_linear_prepare) for E > 64."""
+        key = ("tab", str(device))
+        if key not in self._w:
+            s = self.shape
+            lib = nat.load_library()
+            n = lib.moeb_linear_table_doubles(s.num_layers, s.num_experts)
+            tab = torch.empty(n, dtype=torch.float64, device=device)
+            nat.call("moeb_linear_prepare", nat.ptr(self.weights_on(device)), s.num_layers,
+                     s.num_experts, float(self.history_decay), nat.ptr(tab), nat.stream_ptr())
+            self._w[key] = tab
+        return self._w[key]
+
     def predict_masks(self, packed, budget, warmup=0, metrics=None, logits=None):
         s = self.shape
         out = _empty(packed)
+        if s.num_experts > 64:
+            nat.call("moeb_linear_predict_wide", nat.ptr(packed.truth), nat.ptr(packed.row_off),
+                     packed.num_prompts, s.num_layers, s.num_experts,
+                     nat.ptr(self.tables_on(packed.device)), float(self.history_decay),
+                     int(budget), int(bool(self.threshold)), int(warmup), nat.ptr(out),
+                     nat.ptr(logits), nat.ptr(metrics), nat.stream_ptr())
+            return out
         nat.call("moeb_linear_predict", nat.ptr(packed.truth), nat.ptr(packed.row_off),
                  packed.num_prompts, s.num_layers, s.num_experts,
                  nat.ptr(self.weights_on(packed.device)), float(self.history_decay),

@@ -153,9 +153,7 @@ def test_cache_ops_random_vs_oracle(pkg, oracle):
 def test_learned_linear(pkg, oracle, name):
     c = load_case(name)
     L, E, _ = (int(x) for x in c["shape"])
-    if E > 64:
-        pytest.skip("learned_linear kernel supports E <= 64")
-    packed = _packed(pkg, c)
+    packed = _packed(pkg, c)  # E > 64 runs the wide kernel (moeb_linear_predict_wide)
     shape = packed.shape
     m = c["measured_rows"]
     model = pkg.LinearModel(shape, pkg.LearnerConfig(epochs=0, decay=float(c["decay"])),
@@ -234,8 +232,7 @@ def test_replay_traces_api(pkg, name):
     preds = {"lru_only": pkg.make_predictor("lru_only", shape),
              "oracle": pkg.make_predictor("oracle", shape, traces=packed),
              "next_layer_all": pkg.make_predictor("next_layer_all", shape)}
-    if shape.num_experts <= 64:
-        preds["learned_linear"] = pkg.make_predictor("learned_linear", shape, model=model)
+    preds["learned_linear"] = pkg.make_predictor("learned_linear", shape, model=model)
     for kind, pred in preds.items():
         for cap in c["capacities"]:
             cfg = pkg.ReplayConfig(shape, pkg.CacheConfig(capacity_entries=int(cap),
@@ -326,7 +323,8 @@ def test_pipelined_replay_matches_single_call(pkg, chunks):
 
 
 @pytest.mark.parametrize("L,E,budget,decay", [(5, 64, 6, 0.0), (3, 40, 5, 0.5), (4, 64, 1, 0.0),
-                                             (2, 33, 8, 0.5)])
+                                             (2, 33, 8, 0.5), (3, 256, 8, 0.0), (2, 100, 6, 0.5),
+                                             (2, 200, 1, 0.0)])
 def test_learned_linear_exact_ties(pkg, oracle, L, E, budget, decay):
     """Dyadic weights make logits exact in both the oracle and the kernel and
     create many exact ties, so the kernel's key-based selection must fall
@@ -335,10 +333,13 @@ def test_learned_linear_exact_ties(pkg, oracle, L, E, budget, decay):
     shape = pkg.ModelShape(L, E, 6)
     P, T = 24, 20
     rows = P * T * L
-    truth = np.zeros(rows, dtype=np.uint64)
+    W = (E + 63) // 64
+    truth = np.zeros((rows, W), dtype=np.uint64)
     for r in range(rows):
         for e in rng.choice(E, 6, replace=False):
-            truth[r] |= np.uint64(1) << np.uint64(e)
+            truth[r, e >> 6] |= np.uint64(1) << np.uint64(e & 63)
+    if W == 1:
+        truth = truth.reshape(-1)
     off = np.arange(P + 1, dtype=np.int64) * T * L
     w = rng.integers(-2, 3, size=(E, L + E + 1)).astype(np.float64) * 0.25
     packed = pkg.PackedTraces(shape, _dev(truth), torch.from_numpy(off).cuda(), off,
