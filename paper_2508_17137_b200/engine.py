@@ -284,6 +284,91 @@ class PipelinedReplay:
         return counters
 
 
+class StreamingReplay:
+    """Predict + replay over a sequence of host-resident batches of one prompt
+    geometry (same row offsets), double-buffered: batch i+1's host->device
+    copy runs on a copy stream while batch i is predicted and replayed on the
+    compute stream, and each batch's counters (plus fused prediction
+    metrics) go back to pinned host memory asynchronously. Throughput is
+    max(copy, compute) per batch instead of their sum.
+
+    ``run`` returns, per batch, pinned host tensors (counters [C][4+3L],
+    metrics [3E+3] or None), valid after ``torch.cuda.synchronize()`` (or the
+    returned event)."""
+
+    def __init__(self, shape: ModelShape, row_off_host: np.ndarray, prompt_ids, device=None,
+                 token_ids=None):
+        dev = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.shape = shape
+        rows = int(row_off_host[-1])
+        off_d = torch.from_numpy(np.ascontiguousarray(row_off_host, dtype=np.int64)).to(dev)
+        self.bufs = [PackedTraces(shape, torch.empty((rows, shape.mask_words), dtype=torch.int64,
+                                                     device=dev), off_d,
+                                  np.asarray(row_off_host, dtype=np.int64),
+                                  np.asarray(prompt_ids, dtype=np.int64), token_ids)
+                     for _ in range(2)]
+        self.s_copy = torch.cuda.Stream(dev)
+        self.s_comp = torch.cuda.Stream(dev)
+        self.device = dev
+
+    @property
+    def rows(self) -> int:
+        return self.bufs[0].rows
+
+    def run(self, predictor, capacities, warmup: int, budget: int, host_batches,
+            policy: str = "lru", metrics: bool = False, timing=None):
+        shape, dev = self.shape, self.device
+        L, E = shape.num_layers, shape.num_experts
+        main = torch.cuda.current_stream(dev)
+        self.s_copy.wait_stream(main)
+        self.s_comp.wait_stream(main)
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        freed = [None, None]
+        out = []
+        unbounded = bool(getattr(predictor, "unbounded_prefetch", False))
+        for i, hb in enumerate(host_batches):
+            b = i % 2
+            buf = self.bufs[b]
+            with torch.cuda.stream(self.s_copy):
+                if freed[b] is not None:
+                    self.s_copy.wait_event(freed[b])
+                buf.truth.copy_(hb, non_blocking=True)
+                copied[b].record(self.s_copy)
+            with torch.cuda.stream(self.s_comp):
+                self.s_comp.wait_event(copied[b])
+                if timing is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(self.s_comp)
+                vec = (torch.zeros(3 * E + 3, dtype=torch.int64, device=dev)
+                       if metrics else None)
+                if getattr(predictor, "empty", False) and vec is None:
+                    masks, cov = None, None
+                else:
+                    masks = predictor.predict_masks(buf, budget, warmup, metrics=vec)
+                    cov = predictor.coverage(buf)
+                cnt, _, _ = cache_replay(buf, [(masks, cov, unbounded)], capacities, warmup,
+                                         budget, policy, want_per_prompt=False)
+                ev = torch.cuda.Event()
+                ev.record(self.s_comp)
+                freed[b] = ev
+                c_h = torch.empty((len(capacities), 4 + 3 * L), dtype=torch.int64,
+                                  pin_memory=True)
+                c_h.copy_(cnt[0], non_blocking=True)
+                v_h = None
+                if vec is not None:
+                    v_h = torch.empty(3 * E + 3, dtype=torch.int64, pin_memory=True)
+                    v_h.copy_(vec, non_blocking=True)
+                if timing is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(self.s_comp)
+                    timing.append((e0, e1))
+                out.append((c_h, v_h))
+        main.wait_stream(self.s_comp)
+        main.wait_stream(self.s_copy)
+        return out
+
+
 def replay_prompt(trace, predictor, config: ReplayConfig) -> SimReport:
     return replay_traces([trace], predictor, config)
 

@@ -88,6 +88,21 @@ def c5(args):
         res[f"{pol}_only"] = {"sim_ms": sms, "trace_tok_per_s": toks / (sms / 1e3),
                               "hit_rate": int(c[1]) / int(c[0])}
         print(pol, res[f"{pol}_only"], flush=True)
+    # learned_linear on the V3 shape (wide K3, 256 experts) + LRU 10 %
+    w = np.random.default_rng(0).normal(0.0, 0.01, (256, 58 + 256 + 1))
+    lin = m.make_predictor("learned_linear", shape,
+                           model=m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True))
+    lin.predict_masks(packed.select(0, 8), 8, 8)
+    masks, pms = timed(lambda: lin.predict_masks(packed, 8, 8))
+    (cnt, _, _), sms = timed(lambda: m.cache_replay(packed, [(masks, None, False)], [cap], 8, 8,
+                                                    want_per_prompt=False))
+    c = cnt[0, 0].cpu().numpy()
+    res["learned_linear"] = {"predict_ms": pms, "sim_ms": sms,
+                             "trace_tok_per_s": toks / ((pms + sms) / 1e3),
+                             "hit_rate": int(c[1]) / int(c[0]),
+                             "prediction_hit_rate": int(c[2]) / int(c[0])}
+    print("learned_linear", res["learned_linear"], flush=True)
+    del masks
     if args.transformer:
         pred = m.make_predictor("transformer", shape,
                                 transformer=TR.TransformerWeights.random(58, 256, seed=0))
