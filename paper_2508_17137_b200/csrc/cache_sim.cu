@@ -718,6 +718,47 @@ __device__ __forceinline__ int rank_below(const uint64_t (&m)[W], int e) {
   return c;
 }
 
+// position of the n-th (0-based) set bit of a 64-bit word, n < popc(m):
+// halving steps with popcounts, branch-free
+__device__ __forceinline__ int nth_bit64(uint64_t m, int n) {
+  const uint32_t lo = (uint32_t)m;
+  const int cl = __popc(lo);
+  const bool up = n >= cl;
+  uint32_t x = up ? (uint32_t)(m >> 32) : lo;
+  int base = up ? 32 : 0;
+  n -= up ? cl : 0;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const int c = __popc(x & ((1u << w) - 1u));
+    const bool hi = n >= c;
+    x = hi ? x >> w : x;
+    base += hi ? w : 0;
+    n -= hi ? c : 0;
+  }
+  return base;
+}
+
+// n-th set bit (ascending expert order) of a W-word mask, n < popc
+template <int W>
+__device__ __forceinline__ int nth_bit(const uint64_t (&m)[W], int n) {
+  if (W == 1) return nth_bit64(m[0], n);
+  int w = 0;
+  uint64_t sel = m[0];
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    const int c = __popcll(m[j]);
+    if (w == j) {
+      if (n < c) {
+        sel = m[j];
+      } else {
+        n -= c;
+        ++w;
+      }
+    }
+  }
+  return w * 64 + nth_bit64(sel, n);
+}
+
 template <int W, int ES, int G>
 __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   // G lanes per simulation (32: one per warp; 16: two per warp). All
@@ -755,10 +796,6 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     const uint64_t* __restrict__ tr = a.truth + r0 * W;
     const uint64_t* __restrict__ pr = pred ? pred + r0 * W : nullptr;
     int tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
-    constexpr int kLC = 64 / G;  // per-layer counters for layers hl + G*j (L <= 64; else smem)
-    unsigned lck[kLC], lcc[kLC], lcp[kLC];
-#pragma unroll
-    for (int j = 0; j < kLC; ++j) lck[j] = lcc[j] = lcp[j] = 0;
     __syncwarp(gmask);
 
     uint64_t wt[W], wp[W], nt[W], np[W];  // current / next G-row windows
@@ -921,40 +958,20 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
           }
           st.tail = n;
         }
-        // append the row's keys: (K \ T) ascending, then T ascending
+        // append the row's keys: (K \ T) ascending, then T ascending -- lane
+        // i < ns writes the i-th key of that order (ns <= budget + top_k)
         uint64_t A[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) A[w] = K[w] & ~T[w];
         const int na = popc_w<W>(A);
-        if (W == 1) {
-#pragma unroll
-          for (int j = 0; j < 64 / G; ++j) {
-            const int ex = hl + G * j;
-            const uint64_t below = (1ull << ex) - 1;
-            const bool ina = (A[0] >> ex) & 1ull, int_ = (T[0] >> ex) & 1ull;
-            if (ex < E && (ina || int_)) {
-              const int rank = ina ? __popcll(A[0] & below) : na + __popcll(T[0] & below);
-              const uint32_t dst = st.tail + (uint32_t)rank;
-              const int key = st.key_of(l, ex);
-              q[dst & qmask] = (uint16_t)key;
-              pos_of[key] = (uint16_t)dst;
-            }
-          }
-        } else
-#pragma unroll
-        for (int j = 0; j < 64 * W / G; ++j) {
-          const int ex = hl + G * j;
-          if (ex < E) {
-            const uint64_t bit = 1ull << (ex & 63);
-            int slot2 = -1;
-            if (word_get<W>(A, ex >> 6) & bit) slot2 = rank_below<W>(A, ex);
-            else if (word_get<W>(T, ex >> 6) & bit) slot2 = na + rank_below<W>(T, ex);
-            if (slot2 >= 0) {
-              const uint32_t dst = st.tail + (uint32_t)slot2;
-              const int key = st.key_of(l, ex);
-              q[dst & qmask] = (uint16_t)key;
-              pos_of[key] = (uint16_t)dst;
-            }
+        for (int i0 = 0; i0 < ns; i0 += G) {
+          const int i = i0 + hl;
+          if (i < ns) {
+            const int ex = i < na ? nth_bit<W>(A, i) : nth_bit<W>(T, i - na);
+            const uint32_t dst = st.tail + (uint32_t)i;
+            const int key = st.key_of(l, ex);
+            q[dst & qmask] = (uint16_t)key;
+            pos_of[key] = (uint16_t)dst;
           }
         }
         st.tail += ns;
@@ -1013,15 +1030,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         tot_k += k;
         tot_ch += ch;
         tot_ph += ph;
-        if (L <= G * kLC) {
-#pragma unroll
-          for (int j = 0; j < kLC; ++j)
-            if (l == hl + G * j) {
-              lck[j] += k;
-              lcc[j] += ch;
-              lcp[j] += ph;
-            }
-        } else if (hl == 0) {
+        if (hl == 0) {  // per-layer counters: fire-and-forget shared-memory reductions
           atomicAdd(&bcnt[l], (unsigned)k);
           atomicAdd(&bcnt[L + l], (unsigned)ch);
           atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
@@ -1030,15 +1039,6 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       if (++l == L) {
         l = 0;
         ++t;
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < kLC; ++j) {
-      const int ll = hl + G * j;
-      if (ll < L) {
-        if (lck[j]) atomicAdd(&bcnt[ll], lck[j]);
-        if (lcc[j]) atomicAdd(&bcnt[L + ll], lcc[j]);
-        if (lcp[j]) atomicAdd(&bcnt[2 * L + ll], lcp[j]);
       }
     }
     int64_t* c = a.counters + pi * a.counters_stride;
