@@ -8,11 +8,24 @@
 // beyond the window); 8 warps x 16 queries = 128 queries per CTA; S = Q K^T
 // and O += P V with mma.sync m16n8k16 (fp32 accumulate), online softmax in
 // fp32 (exp2 form).
-// (Round-1 kernel: the tcgen05/TMEM attention is the DESIGN.md next step.)
+//
+// k_window_attention_tc (default) runs both products on the 5th-generation
+// tensor cores: S = Q K^T (M = 128 queries, N <= 256 keys per tcgen05.mma,
+// fp32 in tensor memory, the whole 512-key window in all 512 TMEM columns),
+// an exact two-pass softmax read back with tcgen05.ld (thread = query row),
+// unnormalised P = exp2(S - max) written 16-bit into 128-byte-swizzled shared
+// memory (the freed K buffer, 256 keys at a time) and O += P V with V as an
+// MN-major operand straight from its natural [key][d] layout; O (64 TMEM
+// columns, reusing S's first half) is scaled by 1/rowsum on the way out.
+// The mma.sync kernel above stays selectable (MOEB_ATTN=mma) as the
+// comparison baseline.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
+#include "tc_sm100.cuh"
 
 namespace {
 
@@ -249,6 +262,194 @@ __global__ void __launch_bounds__(256, 2) k_window_attention(const uint16_t* __r
   }
 }
 
+// ---------------------------------------------------------------------------
+// tcgen05 attention (one CTA = window x head x 128-query block, 8 warps: warp
+// w reads TMEM lane quarter w % 4 and the column half w / 4 of every 64-key
+// block; row max / row sum are combined through shared memory). CTAs of the
+// same (window, head) are adjacent in the 1-D grid so K/V stay in L2.
+// ---------------------------------------------------------------------------
+constexpr int TQ = 128;        // queries per CTA = TMEM lanes
+constexpr int TKMAX = 512;     // keys per window
+constexpr int kTcThreads = 256;
+
+// 128-byte swizzle of one 16-byte chunk (K-major rows of 64 16-bit elements)
+__device__ __forceinline__ uint32_t sw128(int row, int chunk) {
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// [rows][64] 16-bit rows from global (row stride ld elements) into a SW128
+// tile; rows >= n zero-filled
+__device__ __forceinline__ void load_sw128_async(unsigned char* tile, const uint16_t* src, int ld,
+                                                 int rows, int n) {
+  for (int i = threadIdx.x; i < rows * 8; i += kTcThreads) {
+    const int row = i >> 3, ch = i & 7;
+    const bool v = row < n;
+    cp_async16(smem_u32(tile + sw128(row, ch)), src + (int64_t)(v ? row : 0) * ld + ch * 8, v);
+  }
+}
+
+template <bool FP16>
+__global__ void __launch_bounds__(kTcThreads, 1) k_window_attention_tc(
+    const uint16_t* __restrict__ qkv, uint16_t* __restrict__ out,
+    const int64_t* __restrict__ win_start, const int32_t* __restrict__ win_len, int nqb) {
+  using namespace moeb::tc;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sQ = smem_raw;                 // [128][64]  16 KB
+  unsigned char* sK = sQ + TQ * 128;            // [512][64]  64 KB, later P (4 x [128][64])
+  unsigned char* sV = sK + TKMAX * 128;         // [512][64]  64 KB (MN-major B of P V)
+  float* red = reinterpret_cast<float*>(sV + TKMAX * 128);  // [2][128] row max / sum halves
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * TQ);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int qb = blockIdx.x % nqb;
+  const int head = (blockIdx.x / nqb) % 8;
+  const int w = blockIdx.x / (nqb * 8);
+  const int n = win_len[w];
+  if (qb * TQ >= n) return;
+  const int64_t r0 = win_start[w];
+  const int ld = 3 * 512;
+  const int nq = min(TQ, n - qb * TQ);
+  const int nkp = (n + 63) & ~63;  // keys padded to the 64-key blocks
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3, hh = warp >> 2;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  load_sw128_async(sQ, qkv + (r0 + qb * TQ) * ld + head * 64, ld, TQ, nq);
+  load_sw128_async(sK, qkv + r0 * ld + 512 + head * 64, ld, nkp, n);
+  load_sw128_async(sV, qkv + r0 * ld + 1024 + head * 64, ld, nkp, n);
+  cp_async_commit();
+  cp_async_wait<0>();
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int ab = FP16 ? 0 : 1;
+  uint32_t phase = 0;
+
+  // ---- S = Q K^T into TMEM columns [0, nkp) ----
+  if (threadIdx.x == 0) {
+    for (int nb = 0; nb < nkp; nb += 256) {
+      const int nn = min(256, nkp - nb);
+      const uint32_t idesc = umma_idesc_f16(TQ, nn, ab);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_f16_ss(tmem + nb, umma_desc_sw128(smem_u32(sQ) + k * 32),
+                   umma_desc_sw128(smem_u32(sK) + nb * 128 + k * 32), idesc, k > 0);
+    }
+    mma_commit(bar);
+  }
+  mbar_wait(bar, phase);
+  phase ^= 1;
+  tc_fence_after();
+
+  const int row = quarter * 32 + lane;                      // query row = TMEM lane
+  const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16) + hh * 32;
+  const float sl2 = 0.125f * 1.4426950408889634f;         // 1/sqrt(64) * log2(e)
+
+  // ---- pass 1: row max over the valid keys (this warp's column halves) ----
+  float mx = -INFINITY;
+  for (int c = 0; c < nkp; c += 128) {
+    uint32_t r0v[32], r1v[32];
+    tmem_ld32(trow + c, r0v);
+    const bool two = c + 64 < nkp;
+    if (two) tmem_ld32(trow + c + 64, r1v);
+    tmem_ld_wait();
+    const int k0 = c + hh * 32, k1 = c + 64 + hh * 32;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      if (k0 + j < n) mx = fmaxf(mx, __uint_as_float(r0v[j]));
+      if (two && k1 + j < n) mx = fmaxf(mx, __uint_as_float(r1v[j]));
+    }
+  }
+  red[hh * TQ + row] = mx;
+  __syncthreads();
+  mx = fmaxf(red[row], red[TQ + row]);
+  const float ms = mx * sl2;
+
+  // ---- pass 2 per 256-key half: P = exp2(S*sl2 - ms) -> smem, O += P V ----
+  float sum = 0.f;
+  unsigned char* sP = sK;
+  for (int h0 = 0; h0 < nkp; h0 += 256) {
+    const int hn = min(256, nkp - h0);
+    for (int c = 0; c < hn; c += 64) {
+      uint32_t rv[32];
+      tmem_ld32(trow + h0 + c, rv);
+      tmem_ld_wait();
+      unsigned char* blk = sP + (c >> 6) * (TQ * 128);
+      const int kb = h0 + c + hh * 32;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {  // 4 chunks of 8 keys
+        uint32_t pk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = q * 8 + u * 2;
+          const float x0 = kb + j < n ? exp2f(__uint_as_float(rv[j]) * sl2 - ms) : 0.f;
+          const float x1 = kb + j + 1 < n ? exp2f(__uint_as_float(rv[j + 1]) * sl2 - ms) : 0.f;
+          sum += x0 + x1;
+          pk[u] = pack2<FP16>(x0, x1);
+        }
+        *reinterpret_cast<uint4*>(blk + sw128(row, hh * 4 + q)) =
+            make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      // O (TMEM columns [0, 64), free once S's first half was read) += P V
+      const uint32_t idesc = umma_idesc_f16(TQ, 64, ab) | (1u << 16);  // B MN-major
+      for (int c = 0; c < hn; c += 64) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_f16_ss(tmem, umma_desc_sw128(smem_u32(sP) + (c >> 6) * (TQ * 128) + k * 32),
+                     umma_desc_sw128(smem_u32(sV) + (h0 + c + k * 16) * 128), idesc,
+                     (h0 | c | k) != 0);
+      }
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+  }
+
+  // ---- O / rowsum -> out (this warp's 32 of the 64 dims) ----
+  red[hh * TQ + row] = sum;  // max reads finished at the pass-2 barriers
+  __syncthreads();
+  sum = red[row] + red[TQ + row];
+  {
+    uint32_t o0[32];
+    tmem_ld32(trow, o0);
+    tmem_ld_wait();
+    const float inv = 1.f / sum;
+    if (row < nq) {
+      uint16_t* dst = out + (r0 + qb * TQ + row) * 512 + head * 64 + hh * 32;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = q * 8 + u * 2;
+          pk[u] = pack2<FP16>(__uint_as_float(o0[j]) * inv, __uint_as_float(o0[j + 1]) * inv);
+        }
+        reinterpret_cast<uint4*>(dst)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
 }  // namespace
 
 extern "C" int moeb_window_attention(const void* qkv, void* out, const int64_t* win_start,
@@ -260,6 +461,16 @@ extern "C" int moeb_window_attention(const void* qkv, void* out, const int64_t* 
   if (n_windows == 0) return MOEB_OK;
   dim3 grid((unsigned)n_windows, 8, (unsigned)((max_len + QB - 1) / QB));
   cudaStream_t s = moeb::as_stream(stream);
+  const char* env = getenv("MOEB_ATTN");  // "mma": the mma.sync baseline kernel
+  if (!(env && env[0] == 'm') && max_len <= TKMAX) {
+    const size_t smem = TQ * 128 + 2 * TKMAX * 128 + 2 * TQ * 4 + 64;
+    const int nqb = (max_len + TQ - 1) / TQ;
+    auto k = fp16 ? k_window_attention_tc<true> : k_window_attention_tc<false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<(unsigned)((int64_t)n_windows * 8 * nqb), kTcThreads, smem, s>>>(
+        static_cast<const uint16_t*>(qkv), static_cast<uint16_t*>(out), win_start, win_len, nqb);
+    return moeb::check_launch("k_window_attention_tc");
+  }
   if (fp16)
     k_window_attention<true><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(qkv),
                                                   static_cast<uint16_t*>(out), win_start, win_len);

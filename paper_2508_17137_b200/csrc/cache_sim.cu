@@ -49,6 +49,7 @@ struct SimArgs {
   const uint8_t* covered[MOEB_MAX_PREDS];
   uint32_t unbounded_bits;
   int n_preds;
+  int any_cov;
   const int64_t* row_off;
   int P, L, E, warmup, budget;
   int64_t cap;
@@ -759,7 +760,7 @@ __device__ __forceinline__ int nth_bit(const uint64_t (&m)[W], int n) {
   return w * 64 + nth_bit64(sel, n);
 }
 
-template <int W, int ES, int G>
+template <int W, int ES, int G, bool EXTRA>
 __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   // G lanes per simulation (32: one per warp; 16: two per warp). All
   // collectives below are restricted to the group's lanes (gmask), so the
@@ -787,10 +788,10 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     uint64_t* R = st.R;
     const uint32_t qmask = st.qmask;
     const uint64_t* __restrict__ pred = a.preds[pi];
-    const uint8_t* __restrict__ cov = a.covered[pi];
+    const uint8_t* __restrict__ cov = EXTRA ? a.covered[pi] : nullptr;
     const bool unbounded = (a.unbounded_bits >> pi) & 1u;
     const int limit = unbounded ? E : a.budget;
-    uint64_t* hits = a.hits ? a.hits + pi * a.hits_stride : nullptr;
+    uint64_t* hits = (EXTRA && a.hits) ? a.hits + pi * a.hits_stride : nullptr;
     const int64_t r0 = a.row_off[p];
     const int64_t nrows = a.row_off[p + 1] - r0;
     const uint64_t* __restrict__ tr = a.truth + r0 * W;
@@ -1014,7 +1015,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         }
         __syncwarp(gmask);
       }
-      if (hits && hl < W) {
+      if (EXTRA && hits && hl < W) {
         uint64_t v = 0;
 #pragma unroll
         for (int w = 0; w < W; ++w)
@@ -1026,7 +1027,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         int ph = 0;
 #pragma unroll
         for (int w = 0; w < W; ++w) ph += __popcll(T[w] & P[w]);  // FULL predicted set
-        if (cov && cov[r0 + i] == 0) ++tot_unc;                  // engine.py:175-176
+        if (EXTRA && cov && cov[r0 + i] == 0) ++tot_unc;         // engine.py:175-176
         tot_k += k;
         tot_ch += ch;
         tot_ph += ph;
@@ -1098,13 +1099,15 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
       return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
                         a.sim_bytes, max_block);
     const size_t smem1 = head + (size_t)a.sim_bytes;
-    auto k1 = k_cache_sim_warp<W, ES, 32>;
+    auto k1 = (a.hits || a.any_cov) ? k_cache_sim_warp<W, ES, 32, true>
+                                    : k_cache_sim_warp<W, ES, 32, false>;
     cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     k1<<<dim3((unsigned)a.P, (unsigned)a.n_preds), 32, smem1, s>>>(a);
     return moeb::check_launch("k_cache_sim_warp");
   }
   const size_t smem = head + (size_t)nw * (32 / G) * a.sim_bytes;
-  auto k = k_cache_sim_warp<W, ES, G>;
+  auto k = (a.hits || a.any_cov) ? k_cache_sim_warp<W, ES, G, true>
+                                 : k_cache_sim_warp<W, ES, G, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int spb = nw * (32 / G);
   const dim3 blocks((unsigned)((a.P + spb - 1) / spb), (unsigned)a.n_preds);
@@ -1162,6 +1165,7 @@ extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* pred
   for (int i = 0; i < n_preds; ++i) {
     a.preds[i] = preds ? preds[i] : nullptr;
     a.covered[i] = covered ? covered[i] : nullptr;
+    if (a.covered[i]) a.any_cov = 1;
     if (unbounded && unbounded[i]) a.unbounded_bits |= 1u << i;
   }
   a.row_off = prompt_row_off;

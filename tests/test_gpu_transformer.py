@@ -55,9 +55,12 @@ def test_gemm_epilogues(tr, fp16, M, N, K):
         torch.testing.assert_close(h16.float(), want, atol=5e-3 + q, rtol=q)
 
 
+@pytest.mark.parametrize("impl", ["tc", "mma"])
 @pytest.mark.parametrize("fp16", [True, False])
-def test_window_attention(tr, fp16):
+def test_window_attention(tr, fp16, impl, monkeypatch):
+    """tcgen05 kernel (default) and the mma.sync baseline (MOEB_ATTN=mma)."""
     from paper_2508_17137_b200 import _native as nat
+    monkeypatch.setenv("MOEB_ATTN", impl)
     dt = torch.float16 if fp16 else torch.bfloat16
     off = np.array([0, 700, 700 + 512, 700 + 512 + 37, 700 + 512 + 37 + 1100])
     ws, wl = tr.windows_of(off)
