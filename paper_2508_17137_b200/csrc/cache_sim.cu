@@ -779,7 +779,13 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   const int sims_per_block = nw * (32 / G);
   const int sl = wib * (32 / G) + lane / G;  // simulation within the block
   const int p = blockIdx.x * sims_per_block + sl;
-  if (p < a.P) {
+  const bool live = p < a.P;
+  constexpr unsigned FULL = 0xffffffffu;
+  // The whole warp runs the row loop to the longer of its groups' prompts
+  // (missing rows are all-zero no-op rows), so the common path's warp
+  // collectives can use the full mask: a dead or shorter group still takes
+  // part. Rare paths (scan, fallback, compaction) keep the group mask.
+  if (__any_sync(FULL, live)) {
     unsigned char* base = smem + a.off_c + (size_t)sl * a.sim_bytes;
     LruState<W, ES, false> st;
     st.init(base, a, L);  // every lane of the group holds the same state
@@ -792,8 +798,14 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     const bool unbounded = (a.unbounded_bits >> pi) & 1u;
     const int limit = unbounded ? E : a.budget;
     uint64_t* hits = (EXTRA && a.hits) ? a.hits + pi * a.hits_stride : nullptr;
-    const int64_t r0 = a.row_off[p];
-    const int64_t nrows = a.row_off[p + 1] - r0;
+    const int64_t r0 = live ? a.row_off[p] : 0;
+    const int64_t nrows = live ? a.row_off[p + 1] - r0 : 0;
+    int64_t nmax = nrows;
+#pragma unroll
+    for (int o = G; o < 32; o <<= 1) {
+      const int64_t other = __shfl_xor_sync(FULL, nmax, o);
+      nmax = other > nmax ? other : nmax;
+    }
     const uint64_t* __restrict__ tr = a.truth + r0 * W;
     const uint64_t* __restrict__ pr = pred ? pred + r0 * W : nullptr;
     int tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
@@ -806,7 +818,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       wp[w] = (pr && hl < nrows) ? __ldg(pr + (int64_t)hl * W + w) : 0ull;
     }
     int l = 0, t = 0;
-    for (int64_t i = 0; i < nrows; ++i) {
+    for (int64_t i = 0; i < nmax; ++i) {
       const int slot = (int)(i & (G - 1));
       if (slot == 0) {  // prefetch the next window
         const int64_t j = i + G + hl;
@@ -819,8 +831,8 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       uint64_t T[W], P[W], K[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        T[w] = __shfl_sync(gmask, wt[w], slot, G);
-        P[w] = __shfl_sync(gmask, wp[w], slot, G);
+        T[w] = __shfl_sync(FULL, wt[w], slot, G);
+        P[w] = __shfl_sync(FULL, wp[w], slot, G);
       }
       if (slot == G - 1) {
 #pragma unroll
@@ -852,36 +864,35 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       }
       const int e = st.count + m - st.cap > 0 ? st.count + m - st.cap : 0;
       bool fallback = (st.cap <= popc_w<W>(K)) || (e > st.count - refresh);
+      // first victim window: all lanes of the warp, converged (full-mask votes)
       uint32_t newhead = st.head;
       bool applied = false;
-      if (!fallback && e > 0) {  // common case: every victim in the first chunk
+      {
+        const bool want = !fallback && e > 0;
         const uint32_t idx = st.head + hl;
         const bool inr = (uint32_t)hl < st.tail - st.head;
         const int key = q[idx & qmask];
         const bool valid = inr && pos_of[key] == (uint16_t)idx;
-        const unsigned vb = (__ballot_sync(gmask, valid) >> gbase) & glow;
-        if (__popc(vb) >= e) {
-          const bool victim = valid && __popc(vb & ((1u << hl) - 1)) < e;
-          int vl = 0, ve = 0;
-          bool bad = false;
-          if (victim) {
-            vl = st.layer_of(key);
-            ve = st.expert_of(key, vl);
-            bad = vl == l && ((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull);
-          }
-          if (__any_sync(gmask, bad)) {
-            fallback = true;
-          } else {
-            if (victim) {
-              pos_of[key] = (uint16_t)(idx + 0x8000u);
-              atomicAnd(reinterpret_cast<unsigned int*>(R + vl * W + (ve >> 6)) + ((ve >> 5) & 1),
-                        ~(1u << (ve & 31)));
-            }
-            const unsigned vict = (__ballot_sync(gmask, victim) >> gbase) & glow;
-            newhead = st.head + (32 - __clz(vict));
-            applied = true;
-          }
+        const unsigned vb = (__ballot_sync(FULL, valid) >> gbase) & glow;
+        const bool ok1 = want && __popc(vb) >= e;
+        const bool victim = ok1 && valid && __popc(vb & ((1u << hl) - 1)) < e;
+        int vl = 0, ve = 0;
+        bool bad = false;
+        if (victim) {
+          vl = st.layer_of(key);
+          ve = st.expert_of(key, vl);
+          bad = vl == l && ((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull);
         }
+        const bool anybad = ((__ballot_sync(FULL, bad) >> gbase) & glow) != 0u;
+        if (ok1 && anybad) fallback = true;
+        applied = ok1 && !anybad;
+        if (applied && victim) {
+          pos_of[key] = (uint16_t)(idx + 0x8000u);
+          atomicAnd(reinterpret_cast<unsigned int*>(R + vl * W + (ve >> 6)) + ((ve >> 5) & 1),
+                    ~(1u << (ve & 31)));
+        }
+        const unsigned vict = (__ballot_sync(FULL, applied && victim) >> gbase) & glow;
+        if (applied) newhead = st.head + (32 - __clz(vict));
       }
       if (!fallback && e > 0 && !applied) {  // scan: find the e-th valid entry, check interplay
         int found = 0;
@@ -1015,7 +1026,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         }
         __syncwarp(gmask);
       }
-      if (EXTRA && hits && hl < W) {
+      if (EXTRA && hits && hl < W && i < nrows) {
         uint64_t v = 0;
 #pragma unroll
         for (int w = 0; w < W; ++w)
@@ -1027,7 +1038,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         int ph = 0;
 #pragma unroll
         for (int w = 0; w < W; ++w) ph += __popcll(T[w] & P[w]);  // FULL predicted set
-        if (EXTRA && cov && cov[r0 + i] == 0) ++tot_unc;         // engine.py:175-176
+        if (EXTRA && cov && i < nrows && cov[r0 + i] == 0) ++tot_unc;  // engine.py:175-176
         tot_k += k;
         tot_ch += ch;
         tot_ph += ph;
@@ -1043,7 +1054,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       }
     }
     int64_t* c = a.counters + pi * a.counters_stride;
-    if (hl == 0) {
+    if (hl == 0 && live) {
       atomicAdd(reinterpret_cast<unsigned long long*>(c + 0), (unsigned long long)tot_k);
       atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot_ch);
       atomicAdd(reinterpret_cast<unsigned long long*>(c + 2), (unsigned long long)tot_ph);

@@ -357,3 +357,39 @@ def test_learned_linear_exact_ties(pkg, oracle, L, E, budget, decay):
     # ties really occur at the top-k cut
     srt = -np.sort(-logits, axis=1)
     assert np.mean(srt[:, budget - 1] == srt[:, budget]) > 0.05
+
+
+@pytest.mark.parametrize("G", ["16", "32", "8"])
+def test_ragged_prompts(pkg, oracle, G, monkeypatch):
+    """Prompts of different lengths share warps (K1 pads the shorter group
+    with no-op rows): counters, per-prompt counters and hit masks vs the C
+    oracle, for every lane-group width."""
+    monkeypatch.setenv("MOEB_K1_G", G)
+    shape = pkg.ModelShape(26, 64, 6)
+    full = pkg.generate_packed(pkg.GeneratorConfig(37, 40, shape, 8, 0.9, 5))
+    L = 26
+    truth_all = full.truth.cpu().numpy().view(np.uint64).reshape(-1)
+    rows, off = [], [0]
+    for p in range(37):
+        T = 9 + (p * 7) % 31
+        r0 = int(full.row_off_host[p])
+        rows.append(truth_all[r0:r0 + T * L])
+        off.append(off[-1] + T * L)
+    truth = np.concatenate(rows)
+    off = np.array(off, dtype=np.int64)
+    packed = pkg.PackedTraces(shape, _dev(truth), torch.from_numpy(off).cuda(), off,
+                              np.arange(37, dtype=np.int64))
+    w = np.random.default_rng(1).normal(0.0, 0.01, (64, 91))
+    model = pkg.LinearModel(shape, pkg.LearnerConfig(epochs=0), w, trained=True)
+    masks = pkg.make_predictor("learned_linear", shape, model=model).predict_masks(packed, 6, 8)
+    caps = [3, 40, 166, 700]
+    for pm in (masks, None):
+        counters, pp, hits = pkg.cache_replay(packed, [(pm, None, False)], caps, 8, 6,
+                                              want_hits=True)
+        pred_h = np.zeros_like(truth) if pm is None else _host(pm).reshape(-1)
+        for j, cap in enumerate(caps):
+            want, wpp, whits = oracle.cache_sim(truth, pred_h, off, 26, 64, 8, cap, 6,
+                                                want_hits=True)
+            assert np.array_equal(counters[0, j].cpu().numpy(), want), (G, cap)
+            assert np.array_equal(pp[0, j].cpu().numpy().reshape(-1), np.asarray(wpp).reshape(-1))
+            assert np.array_equal(_host(hits[0, j]).reshape(-1), np.asarray(whits).reshape(-1))
