@@ -979,7 +979,11 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         for (int i0 = 0; i0 < ns; i0 += G) {
           const int i = i0 + hl;
           if (i < ns) {
-            const int ex = i < na ? nth_bit<W>(A, i) : nth_bit<W>(T, i - na);
+            const bool in_a = i < na;  // select the mask first: one n-th-bit search
+            uint64_t M[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) M[w] = in_a ? A[w] : T[w];
+            const int ex = nth_bit<W>(M, in_a ? i : i - na);
             const uint32_t dst = st.tail + (uint32_t)i;
             const int key = st.key_of(l, ex);
             q[dst & qmask] = (uint16_t)key;
