@@ -168,7 +168,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     cores = os.cpu_count() or 1
-    n_sample = max(cores, 32)  # one prompt (363 tokens) per worker, at least 32
+    n_sample = max(16 * cores, 256)  # ~10 s of the reference's predict + replay per step
     try:
         _import_reference()
     except Exception as exc:  # pragma: no cover
@@ -450,7 +450,7 @@ def run_ours(args):
     cpu_base = None
     if rank == 0 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        n_sample = max(cores, 32)
+        n_sample = max(16 * cores, 256)  # ~10 s of reference work (bounded C2 sample)
         try:
             v, dt, _ = time_reference(n_sample, cores)
             cpu_base = {"value": v, "unit": "trace tokens/s", "cores": cores, "kind": "reference",
