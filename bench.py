@@ -218,8 +218,16 @@ def run_ours(args):
 
     world, rank, local = _dist()
     if world > 1:
+        # MOEB_BENCH_ONE_DEVICE=1 + MOEB_BENCH_DIST_BACKEND=gloo run every rank
+        # on cuda:0 (a check of the multi-rank code path on a single-GPU box)
+        if os.environ.get("MOEB_BENCH_ONE_DEVICE") == "1":
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("MOEB_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
