@@ -1078,6 +1078,284 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     if (bcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bcnt[j]);
 }
 
+// ---------------------------------------------------------------------------
+// K1 LFU, warp per simulation. Same semantics and op stream as LfuState (one
+// access at a time, bit-exact with the thread-per-simulation kernel and its
+// oracle), but the eviction argmin is warp-parallel: lane i owns the slots
+// i, i + 32, ... of the slot array and keeps the minimum (value, slot) of
+// its slots in registers; a victim is a 5-step shuffle argmin over the 32
+// lane minima, and only the lane owning a changed slot rescans its slots.
+// Values are pin << 63 | freq << 32 | clock (unique clock: no ties).
+// ---------------------------------------------------------------------------
+template <int W, bool EXTRA>
+__global__ void __launch_bounds__(128) k_cache_sim_lfu_warp(const SimArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr unsigned FULL = 0xffffffffu;
+  const int L = a.L, E = a.E;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned int* bcnt = reinterpret_cast<unsigned int*>(smem);  // [3L] block counters
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x) bcnt[j] = 0;
+  __syncthreads();
+  const int pi = blockIdx.y;
+  const int p = blockIdx.x * nw + wib;
+  if (p < a.P) {
+    unsigned char* base = smem + a.off_c + (size_t)wib * a.sim_bytes;
+    uint16_t* slot_of = reinterpret_cast<uint16_t*>(base);
+    uint64_t* Rs = reinterpret_cast<uint64_t*>(base + a.off_r);
+    uint64_t* vals = reinterpret_cast<uint64_t*>(base + a.off_q);
+    uint16_t* skeys = reinterpret_cast<uint16_t*>(base + a.off_q + 8 * a.cap);
+    for (int j = lane; j < L * W; j += 32) Rs[j] = 0;
+    const int cap = (int)a.cap;
+    int count = 0, npins = 0, cur = 0;
+    uint32_t clock = 1;
+    uint64_t Rl[W], Pm[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) Rl[w] = Pm[w] = 0;
+    uint64_t mv = ~0ull;  // this lane's minimum slot value, and its slot
+    int ms = -1;
+    __syncwarp();
+
+    auto rescan = [&]() {  // owner lane: minimum over its slots < count
+      uint64_t best = ~0ull;
+      int bs = -1;
+      for (int sl = lane; sl < count; sl += 32) {
+        const uint64_t v = vals[sl];
+        if (v < best) {
+          best = v;
+          bs = sl;
+        }
+      }
+      mv = best;
+      ms = bs;
+    };
+    auto focus = [&](int l) {
+      if (l == cur) return;
+      __syncwarp();
+      if (lane < W) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          if (w == lane) v = Rl[w];
+        Rs[cur * W + lane] = v;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int w = 0; w < W; ++w) Rl[w] = Rs[l * W + w];
+      cur = l;
+    };
+    // slot for a new key: a fresh one or the evicted victim's (make_room)
+    auto make_room = [&]() -> int {
+      if (count < cap) return count++;
+      uint64_t bv = mv;
+      int bsl = ms;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t ov = __shfl_xor_sync(FULL, bv, o);
+        const int os = __shfl_xor_sync(FULL, bsl, o);
+        if (ov < bv) {
+          bv = ov;
+          bsl = os;
+        }
+      }
+      const uint32_t vk = skeys[bsl];
+      const int vl = (int)(vk >> 8), vex = (int)(vk & 0xFFu);
+      const uint64_t bit = 1ull << (vex & 63);
+      if (vl == cur) {
+        word_clear<W>(Rl, vex >> 6, bit);
+      } else if (lane == 0) {
+        Rs[vl * W + (vex >> 6)] &= ~bit;
+      }
+      return bsl;
+    };
+    auto place = [&](int sl, uint64_t v, int key, int ex) {  // write a slot (owner lane)
+      if ((sl & 31) == lane) {
+        vals[sl] = v;
+        skeys[sl] = (uint16_t)((cur << 8) | ex);
+        if (sl == ms) {
+          __threadfence_block();
+          rescan();
+        } else if (v < mv) {
+          mv = v;
+          ms = sl;
+        }
+      }
+      if (lane == 0) slot_of[key] = (uint16_t)sl;
+    };
+    auto update = [&](int sl, uint64_t v) {  // change a resident slot's value
+      if ((sl & 31) == lane) {
+        vals[sl] = v;
+        if (sl == ms) rescan();
+        else if (v < mv) {
+          mv = v;
+          ms = sl;
+        }
+      }
+    };
+
+    const uint64_t* __restrict__ pred = a.preds[pi];
+    const uint8_t* __restrict__ cov = EXTRA ? a.covered[pi] : nullptr;
+    const bool unbounded = (a.unbounded_bits >> pi) & 1u;
+    const int limit = unbounded ? E : a.budget;
+    uint64_t* hits = (EXTRA && a.hits) ? a.hits + pi * a.hits_stride : nullptr;
+    const int64_t r0 = a.row_off[p];
+    const int64_t nrows = a.row_off[p + 1] - r0;
+    int64_t tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
+    int l = 0, t = 0;
+    uint64_t tw = 0, pw = 0;  // row words held by lane w (coalesced reads)
+    for (int64_t i = 0; i < nrows; ++i) {
+      if (lane < W) {
+        tw = __ldg(a.truth + (r0 + i) * W + lane);
+        pw = pred ? __ldg(pred + (r0 + i) * W + lane) : 0ull;
+      }
+      uint64_t T[W], P[W], K[W], Hm[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        T[w] = __shfl_sync(FULL, tw, w);
+        P[w] = __shfl_sync(FULL, pw, w);
+        Hm[w] = 0;
+      }
+      const bool measured = t >= a.warmup;
+      if (measured) {
+        // begin_step (cache.py:102-104): unpin the previous step's keys
+        MOEB_FOR_EACH_BIT(W, Pm, ex, {
+          const int sl = slot_of[cur * E + ex];
+          __syncwarp();
+          if ((sl & 31) == lane) {
+            const uint64_t v = vals[sl] & ~kPin;
+            vals[sl] = v;
+            if (v < mv) {
+              mv = v;
+              ms = sl;
+            }
+          }
+        })
+#pragma unroll
+        for (int w = 0; w < W; ++w) Pm[w] = 0;
+        npins = 0;
+      }
+      focus(l);
+      int npk = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        K[w] = measured ? P[w] : 0ull;
+        npk += __popcll(K[w]);
+      }
+      if (limit <= 0) {
+#pragma unroll
+        for (int w = 0; w < W; ++w) K[w] = 0;
+      } else if (npk > limit) {
+        keep_lowest<W>(K, limit);
+      }
+      // prefetch(sorted(pred)[:limit]) (cache.py:126-154)
+      MOEB_FOR_EACH_BIT(W, K, ex, {
+        const int key = l * E + ex;
+        const uint64_t bit = 1ull << (ex & 63);
+        __syncwarp();
+        if (word_get<W>(Rl, ex >> 6) & bit) {
+          const int sl = slot_of[key];
+          const uint64_t v = vals[sl];
+          __syncwarp();
+          update(sl, kPin | (v & 0x7FFFFFFF00000000ull) | clock++);
+          if (!(v & kPin)) {
+            word_or<W>(Pm, ex >> 6, bit);
+            ++npins;
+          }
+        } else if (!(count >= cap && count <= npins)) {
+          const int sl = make_room();
+          __syncwarp();
+          place(sl, kPin | clock++, key, ex);
+          word_or<W>(Rl, ex >> 6, bit);
+          word_or<W>(Pm, ex >> 6, bit);
+          ++npins;
+        }
+      })
+      // touch every truth expert ascending (cache.py:106-124)
+      int ch = 0;
+      MOEB_FOR_EACH_BIT(W, T, ex, {
+        const int key = l * E + ex;
+        const uint64_t bit = 1ull << (ex & 63);
+        __syncwarp();
+        if (word_get<W>(Rl, ex >> 6) & bit) {
+          const int sl = slot_of[key];
+          const uint64_t v = vals[sl];
+          __syncwarp();
+          const uint64_t freq = ((v & ~kPin) >> 32) + 1;
+          update(sl, (v & kPin) | (freq << 32) | clock++);
+          ++ch;
+          word_or<W>(Hm, ex >> 6, bit);
+        } else if (!(count >= cap && count <= npins)) {
+          const int sl = make_room();
+          __syncwarp();
+          place(sl, (1ull << 32) | clock++, key, ex);
+          word_or<W>(Rl, ex >> 6, bit);
+        }
+      })
+      if (EXTRA && hits && lane < W) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          if (w == lane) v = Hm[w];
+        hits[(r0 + i) * W + lane] = v;
+      }
+      if (measured) {
+        const int k = popc_w<W>(T);
+        int ph = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) ph += __popcll(T[w] & P[w]);
+        if (EXTRA && cov && cov[r0 + i] == 0) ++tot_unc;
+        tot_k += k;
+        tot_ch += ch;
+        tot_ph += ph;
+        if (lane == 0) {
+          atomicAdd(&bcnt[l], (unsigned)k);
+          atomicAdd(&bcnt[L + l], (unsigned)ch);
+          atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
+        }
+      }
+      if (++l == L) {
+        l = 0;
+        ++t;
+      }
+    }
+    int64_t* c = a.counters + pi * a.counters_stride;
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(c + 0), (unsigned long long)tot_k);
+      atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot_ch);
+      atomicAdd(reinterpret_cast<unsigned long long*>(c + 2), (unsigned long long)tot_ph);
+      if (tot_unc) atomicAdd(reinterpret_cast<unsigned long long*>(c + 3), (unsigned long long)tot_unc);
+      if (a.per_prompt) {
+        int64_t* pp = a.per_prompt + pi * a.per_prompt_stride + 4 * (int64_t)p;
+        pp[0] += tot_k;
+        pp[1] += tot_ch;
+        pp[2] += tot_ph;
+        pp[3] += tot_unc;
+      }
+    }
+  }
+  __syncthreads();
+  int64_t* c = a.counters + pi * a.counters_stride;
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x)
+    if (bcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bcnt[j]);
+}
+
+template <int W>
+int launch_lfu_warp(SimArgs a, cudaStream_t s) {
+  const int max_block = moeb::max_smem_per_block();
+  const int head = align16(4LL * 3 * a.L);
+  a.off_c = head;
+  int nw = 4;
+  while (nw > 1 && head + (int64_t)nw * a.sim_bytes > max_block) --nw;
+  if (head + (int64_t)nw * a.sim_bytes > max_block)
+    return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
+                      a.sim_bytes, max_block);
+  const size_t smem = head + (size_t)nw * a.sim_bytes;
+  auto k = (a.hits || a.any_cov) ? k_cache_sim_lfu_warp<W, true> : k_cache_sim_lfu_warp<W, false>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const dim3 blocks((unsigned)((a.P + nw - 1) / nw), (unsigned)a.n_preds);
+  k<<<blocks, 32 * nw, smem, s>>>(a);
+  return moeb::check_launch("k_cache_sim_lfu_warp");
+}
+
 template <class K>
 int launch_kernel(K k, const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1143,8 +1421,11 @@ int launch_sim(SimArgs a, int policy, cudaStream_t s) {
     return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
                       a.sim_bytes, max_block);
   const size_t smem = head + (size_t)tpb * a.sim_bytes;
-  if (policy == MOEB_POLICY_LFU)
+  if (policy == MOEB_POLICY_LFU) {
+    const char* env = getenv("MOEB_LFU_KERNEL");  // "thread": the thread-per-simulation kernel
+    if (!(env && env[0] == 't')) return launch_lfu_warp<W>(a, s);
     return launch_kernel(k_cache_sim<W, LfuState<W, false>>, a, tpb, smem, s);
+  }
   if (W == 1 && a.E == 64) return launch_lru<1, 6>(a, s);
   if (W == 4 && a.E == 256) return launch_lru<4, 8>(a, s);
   return launch_lru<W, -1>(a, s);

@@ -85,9 +85,12 @@ def test_cache_sim_null_stream_is_lru_only(pkg):
         assert np.array_equal(_host(hits[0, j]), c[f"hits_lru_only_c{cap}"])
 
 
+@pytest.mark.parametrize("kernel", ["warp", "thread"])
 @pytest.mark.parametrize("name", CASES)
-def test_lfu_matches_oracle(pkg, oracle, name):
-    """LFU (builder-defined) vs its C oracle restatement."""
+def test_lfu_matches_oracle(pkg, oracle, name, kernel, monkeypatch):
+    """LFU (builder-defined) vs its C oracle restatement: the warp-per-
+    simulation kernel (default) and the thread-per-simulation one."""
+    monkeypatch.setenv("MOEB_LFU_KERNEL", kernel)
     c = load_case(name)
     packed = _packed(pkg, c)
     L, E, _ = (int(x) for x in c["shape"])
