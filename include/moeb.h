@@ -229,11 +229,13 @@ int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int 
  * K5 -- windowed multi-head attention of the transformer predictor: qkv
  * [rows][1536] 16-bit (q | k | v, 8 heads x 64), windows (start row, length
  * <= max_len) of consecutive rows, bidirectional with key padding;
- * out [rows][512] 16-bit.
+ * out [rows][512] 16-bit; rows = the valid rows of qkv (TMA bounds: key
+ * chunks past a window's end read the following rows, which must be finite,
+ * or zeros past `rows`).
  */
 int moeb_window_attention(const void* qkv, void* out, const int64_t* win_start,
-                          const int32_t* win_len, int n_windows, int max_len, int fp16,
-                          void* stream);
+                          const int32_t* win_len, int n_windows, int max_len, int64_t rows,
+                          int fp16, void* stream);
 
 /* Transformer input rows: out32[r] = ptok[token_ids[r / L]] + play[r % L]
  * (factorised input projection), out16 = 16-bit copy. Rows of 512. */

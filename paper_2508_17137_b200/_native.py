@@ -48,7 +48,7 @@ _SIGS = {
     "moeb_match_queries": [P, I32, I32, P, I32, P, P, P],
     "moeb_gemm": [P, I32, P, I32, I32, I32, I32, I32, I32, P, P, P, I32, P, P,
                   ctypes.c_float, P],
-    "moeb_window_attention": [P, P, P, P, I32, I32, I32, P],
+    "moeb_window_attention": [P, P, P, P, I32, I32, I64, I32, P],
     "moeb_embed_rows": [P, P, P, I32, I64, P, P, I32, P],
     "moeb_to16": [P, P, I64, I32, P],
     "moeb_eam_pack_library": [P, I32, I32, I32, P, P, P],

@@ -22,6 +22,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cuda.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -450,21 +452,287 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_window_attention_tc(
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised tcgen05 attention (default): one CTA = (window, head,
+// 128-query block), two CTAs per SM (97 KB shared memory, 256 TMEM columns
+// each). Keys stream in 64-key chunks through a 3-stage TMA ring;
+//   warp 0   TMA producer: Q (2 boxes), then K chunks (pass 1), then K + V
+//            chunks (pass 2)
+//   warp 1   MMA issuer: S_c = Q K_c^T into one of two 64-column TMEM
+//            buffers; in pass 2 also O += P_c V_c (V MN-major from its
+//            natural layout) into 64 more columns
+//   warps 2-9 softmax: two warps per TMEM lane quarter, 32 keys each; pass 1
+//            row max, pass 2 P = exp2(S - max) (16-bit, SW128 shared memory,
+//            two buffers) and the row sum; final O / sum
+// Exact two-pass softmax (S recomputed: the MMAs are cheap, TMEM holds only
+// two S chunks); every hand-off is an mbarrier (TMA complete_tx,
+// tcgen05.commit, or 8 softmax-warp arrivals).
+// ---------------------------------------------------------------------------
+constexpr int FA_CK = 64;      // keys per chunk
+constexpr int FA_NST = 3;      // ring stages (K 8 KB + V 8 KB each)
+constexpr int FA_THREADS = 320;
+
+struct FaSmem {
+  static constexpr int Q = 0;                         // 16 KB
+  static constexpr int RING = 16384;                  // FA_NST x 16 KB
+  static constexpr int P = RING + FA_NST * 16384;     // 2 x 16 KB
+  static constexpr int RED = P + 2 * 16384;           // 4 x 128 floats
+  static constexpr int BAR = RED + 4 * 128 * 4;       // 17 mbarriers
+  static constexpr int SLOT = BAR + 8 * 24;
+  static constexpr int BYTES = SLOT + 16;
+};
+
+template <bool FP16>
+__global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
+    const __grid_constant__ CUtensorMap tm, uint16_t* __restrict__ out,
+    const int64_t* __restrict__ win_start, const int32_t* __restrict__ win_len, int nqb) {
+  using namespace moeb::tc;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* sQ = smem_raw + FaSmem::Q;
+  unsigned char* ring = smem_raw + FaSmem::RING;
+  unsigned char* sP = smem_raw + FaSmem::P;
+  float* red = reinterpret_cast<float*>(smem_raw + FaSmem::RED);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + FaSmem::BAR);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;             // [FA_NST]
+  uint64_t* kv_empty = kv_full + FA_NST;    // [FA_NST]
+  uint64_t* s_full = kv_empty + FA_NST;     // [2]
+  uint64_t* s_empty = s_full + 2;           // [2]
+  uint64_t* p_full = s_empty + 2;           // [2]
+  uint64_t* p_empty = p_full + 2;           // [2]
+  uint64_t* o_full = p_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + FaSmem::SLOT);
+
+  const int qb = blockIdx.x % nqb;
+  const int head = (blockIdx.x / nqb) % 8;
+  const int w = blockIdx.x / (nqb * 8);
+  const int n = win_len[w];
+  if (qb * TQ >= n) return;
+  const int r0 = (int)win_start[w];
+  const int nq = min(TQ, n - qb * TQ);
+  const int nch = (n + FA_CK - 1) / FA_CK;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < FA_NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 8);
+      mbar_init(&p_full[b], 8);
+      mbar_init(&p_empty[b], 1);
+    }
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;  // S buffers at +0 / +64, O at +128
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer =====
+      mbar_expect_tx(q_full, TQ * 128);
+      tma_load_2d(sQ, &tm, q_full, head * 64, r0 + qb * TQ);
+      tma_load_2d(sQ + 64 * 128, &tm, q_full, head * 64, r0 + qb * TQ + 64);
+      for (int g = 0; g < 2 * nch; ++g) {
+        const int c = g < nch ? g : g - nch;
+        const bool v = g >= nch;
+        const int st = g % FA_NST;
+        mbar_wait(&kv_empty[st], ((g / FA_NST) & 1) ^ 1);
+        unsigned char* stg = ring + st * 16384;
+        mbar_expect_tx(&kv_full[st], v ? 16384 : 8192);
+        tma_load_2d(stg, &tm, &kv_full[st], 512 + head * 64, r0 + c * FA_CK);
+        if (v) tma_load_2d(stg + 8192, &tm, &kv_full[st], 1024 + head * 64, r0 + c * FA_CK);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ===== MMA issuer =====
+      const int ab = FP16 ? 0 : 1;
+      const uint32_t idesc_s = umma_idesc_f16(TQ, FA_CK, ab);
+      const uint32_t idesc_o = umma_idesc_f16(TQ, 64, ab) | (1u << 16);  // V MN-major
+      int s_use = 0;
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int g) {
+        const int st = g % FA_NST;
+        mbar_wait(&kv_full[st], (g / FA_NST) & 1);
+        const int b = s_use & 1;
+        mbar_wait(&s_empty[b], ((s_use >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t kb = smem_u32(ring + st * 16384);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_f16_ss(tmem + b * 64, umma_desc_sw128(smem_u32(sQ) + k * 32),
+                     umma_desc_sw128(kb + k * 32), idesc_s, k > 0);
+        mma_commit(&s_full[b]);
+        if (g < nch) mma_commit(&kv_empty[st]);  // pass 1: K chunk consumed
+        ++s_use;
+      };
+      for (int g = 0; g < nch; ++g) issue_s(g);
+      issue_s(nch);
+      for (int c = 0; c < nch; ++c) {
+        const int g = nch + c;
+        if (c + 1 < nch) issue_s(g + 1);
+        mbar_wait(&p_full[c & 1], (c >> 1) & 1);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(ring + (g % FA_NST) * 16384 + 8192);
+        const uint32_t pb = smem_u32(sP + (c & 1) * 16384);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_f16_ss(tmem + 128, umma_desc_sw128(pb + k * 32), umma_desc_sw128(vb + k * 2048),
+                     idesc_o, (c | k) != 0);
+        mma_commit(&p_empty[c & 1]);
+        mma_commit(&kv_empty[g % FA_NST]);  // pass 2: K + V chunk consumed
+      }
+      mma_commit(o_full);
+    }
+  } else {
+    // ===== softmax warps 2..9 =====
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + half * 32;
+    const float sl2 = 0.125f * 1.4426950408889634f;
+    int s_use = 0;
+    float mx = -INFINITY;
+    for (int c = 0; c < nch; ++c) {  // pass 1: row max
+      const int b = s_use & 1;
+      mbar_wait(&s_full[b], (s_use >> 1) & 1);
+      tc_fence_after();
+      uint32_t r[32];
+      tmem_ld32(tq + b * 64, r);
+      tmem_ld_wait();
+      const int k0 = c * FA_CK + half * 32;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (k0 + j < n) mx = fmaxf(mx, __uint_as_float(r[j]));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);
+      ++s_use;
+    }
+    red[half * TQ + row] = mx;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    mx = fmaxf(red[row], red[TQ + row]);
+    const float ms = mx * sl2;
+    float sum = 0.f;
+    for (int c = 0; c < nch; ++c) {  // pass 2: P and row sum
+      const int b = s_use & 1;
+      mbar_wait(&s_full[b], (s_use >> 1) & 1);
+      tc_fence_after();
+      uint32_t r[32];
+      tmem_ld32(tq + b * 64, r);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[b]);
+      ++s_use;
+      const int k0 = c * FA_CK + half * 32;
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        const float x0 = k0 + j < n ? exp2f(__uint_as_float(r[j]) * sl2 - ms) : 0.f;
+        const float x1 = k0 + j + 1 < n ? exp2f(__uint_as_float(r[j + 1]) * sl2 - ms) : 0.f;
+        sum += x0 + x1;
+        pk[j >> 1] = pack2<FP16>(x0, x1);
+      }
+      const int pb = c & 1;
+      if (c >= 2) mbar_wait(&p_empty[pb], ((c >> 1) - 1) & 1);  // PV of chunk c - 2 done
+      unsigned char* dst = sP + pb * 16384;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        *reinterpret_cast<uint4*>(dst + sw128(row, half * 4 + q)) =
+            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[pb]);
+    }
+    red[2 * TQ + half * TQ + row] = sum;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    sum = red[2 * TQ + row] + red[3 * TQ + row];
+    mbar_wait(o_full, 0);
+    tc_fence_after();
+    uint32_t o[32];
+    tmem_ld32(tq + 128, o);
+    tmem_ld_wait();
+    const float inv = 1.f / sum;
+    if (row < nq) {
+      uint16_t* dst = out + ((int64_t)r0 + qb * TQ + row) * 512 + head * 64 + half * 32;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = q * 8 + u * 2;
+          pk[u] = pack2<FP16>(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
+        }
+        reinterpret_cast<uint4*>(dst)[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// qkv [rows][1536] 16-bit, 64 x 64 boxes, 128-byte swizzle
+int qkv_map(CUtensorMap* m, const void* qkv, int64_t rows, bool fp16) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return moeb::fail(MOEB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  cuuint64_t dims[2] = {1536, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {1536 * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(qkv), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return moeb::fail(MOEB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return MOEB_OK;
+}
+
 }  // namespace
 
 extern "C" int moeb_window_attention(const void* qkv, void* out, const int64_t* win_start,
-                                     const int32_t* win_len, int n_windows, int max_len, int fp16,
-                                     void* stream) {
+                                     const int32_t* win_len, int n_windows, int max_len,
+                                     int64_t rows, int fp16, void* stream) {
   moeb::clear_error();
   MOEB_REQUIRE(qkv && out && win_start && win_len, "null argument");
-  MOEB_REQUIRE(n_windows >= 0 && max_len >= 1 && max_len <= 4096, "bad window arguments");
+  MOEB_REQUIRE(n_windows >= 0 && max_len >= 1 && max_len <= 4096 && rows >= 1,
+               "bad window arguments");
   if (n_windows == 0) return MOEB_OK;
   dim3 grid((unsigned)n_windows, 8, (unsigned)((max_len + QB - 1) / QB));
   cudaStream_t s = moeb::as_stream(stream);
-  const char* env = getenv("MOEB_ATTN");  // "mma": the mma.sync baseline kernel
-  if (!(env && env[0] == 'm') && max_len <= TKMAX) {
+  const char* env = getenv("MOEB_ATTN");  // "mma": mma.sync baseline, "tc1": one-pass tcgen05
+  const char mode = env ? env[0] : 'f';
+  const int nqb = (max_len + TQ - 1) / TQ;
+  if (mode == 'f' && max_len <= TKMAX && rows < (1ll << 31)) {
+    CUtensorMap tm;
+    if (int rc = qkv_map(&tm, qkv, rows, fp16 != 0)) return rc;
+    auto k = fp16 ? k_window_attention_fa<true> : k_window_attention_fa<false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FaSmem::BYTES);
+    k<<<(unsigned)((int64_t)n_windows * 8 * nqb), FA_THREADS, FaSmem::BYTES, s>>>(
+        tm, static_cast<uint16_t*>(out), win_start, win_len, nqb);
+    return moeb::check_launch("k_window_attention_fa");
+  }
+  if (mode == 't' && max_len <= TKMAX) {
     const size_t smem = TQ * 128 + 2 * TKMAX * 128 + 2 * TQ * 4 + 64;
-    const int nqb = (max_len + TQ - 1) / TQ;
     auto k = fp16 ? k_window_attention_tc<true> : k_window_attention_tc<false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)((int64_t)n_windows * 8 * nqb), kTcThreads, smem, s>>>(

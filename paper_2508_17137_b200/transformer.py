@@ -202,7 +202,8 @@ class TransformerPredictor:
                 timed("gemm_qkv", 2.0 * M * 3 * D_MODEL * D_MODEL, gemm, h16, lay["qkv"], M,
                       3 * D_MODEL, D_MODEL, EPI_BIAS, bias=lay["qkv_b"], out16=qkv, fp16=W.fp16)
                 timed("attention", att_flops, nat.call, "moeb_window_attention", nat.ptr(qkv),
-                      nat.ptr(att), nat.ptr(ws_d), nat.ptr(wl_d), len(ws), WINDOW, int(W.fp16),
+                      nat.ptr(att), nat.ptr(ws_d), nat.ptr(wl_d), len(ws), WINDOW, M,
+                      int(W.fp16),
                       nat.stream_ptr())
                 timed("gemm_out_ln", 2.0 * M * D_MODEL * D_MODEL, gemm, att, lay["o"], M, D_MODEL,
                       D_MODEL, EPI_RESID_LN, bias=lay["o_b"], out32=h32, out16=h16,

@@ -55,10 +55,11 @@ def test_gemm_epilogues(tr, fp16, M, N, K):
         torch.testing.assert_close(h16.float(), want, atol=5e-3 + q, rtol=q)
 
 
-@pytest.mark.parametrize("impl", ["tc", "mma"])
+@pytest.mark.parametrize("impl", ["fa", "tc1", "mma"])
 @pytest.mark.parametrize("fp16", [True, False])
 def test_window_attention(tr, fp16, impl, monkeypatch):
-    """tcgen05 kernel (default) and the mma.sync baseline (MOEB_ATTN=mma)."""
+    """warp-specialised tcgen05 kernel (default), the one-pass tcgen05 kernel
+    (MOEB_ATTN=tc1) and the mma.sync baseline (MOEB_ATTN=mma)."""
     from paper_2508_17137_b200 import _native as nat
     monkeypatch.setenv("MOEB_ATTN", impl)
     dt = torch.float16 if fp16 else torch.bfloat16
@@ -70,7 +71,7 @@ def test_window_attention(tr, fp16, impl, monkeypatch):
     out = torch.zeros(rows, 512, device="cuda", dtype=dt)
     ws_d, wl_d = torch.from_numpy(ws).cuda(), torch.from_numpy(wl).cuda()  # keep alive
     nat.call("moeb_window_attention", nat.ptr(qkv), nat.ptr(out), nat.ptr(ws_d), nat.ptr(wl_d),
-             len(ws), 512, int(fp16), nat.stream_ptr())
+             len(ws), 512, rows, int(fp16), nat.stream_ptr())
     x = qkv.float()
     for s, n in zip(ws, wl):
         q = x[s:s + n, :512].view(n, 8, 64).transpose(0, 1)
