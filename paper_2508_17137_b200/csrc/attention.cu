@@ -468,6 +468,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_window_attention_tc(
 // two S chunks); every hand-off is an mbarrier (TMA complete_tx,
 // tcgen05.commit, or 8 softmax-warp arrivals).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ float ex2_ftz(float x) {  // one MUFU.EX2
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 constexpr int FA_CK = 64;      // keys per chunk
 constexpr int FA_NST = 3;      // ring stages (K 8 KB + V 8 KB each)
 constexpr int FA_THREADS = 320;
@@ -607,9 +613,14 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
       tmem_ld32(tq + b * 64, r);
       tmem_ld_wait();
       const int k0 = c * FA_CK + half * 32;
+      if (k0 + 32 <= n) {  // full chunk: no key mask
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (k0 + j < n) mx = fmaxf(mx, __uint_as_float(r[j]));
+        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(r[j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (k0 + j < n) mx = fmaxf(mx, __uint_as_float(r[j]));
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_empty[b]);
@@ -633,12 +644,23 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
       ++s_use;
       const int k0 = c * FA_CK + half * 32;
       uint32_t pk[16];
+      if (k0 + 32 <= n) {  // full chunk: no key mask
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const float x0 = k0 + j < n ? exp2f(__uint_as_float(r[j]) * sl2 - ms) : 0.f;
-        const float x1 = k0 + j + 1 < n ? exp2f(__uint_as_float(r[j + 1]) * sl2 - ms) : 0.f;
-        sum += x0 + x1;
-        pk[j >> 1] = pack2<FP16>(x0, x1);
+        for (int j = 0; j < 32; j += 2) {
+          const float x0 = ex2_ftz(fmaf(__uint_as_float(r[j]), sl2, -ms));
+          const float x1 = ex2_ftz(fmaf(__uint_as_float(r[j + 1]), sl2, -ms));
+          sum += x0 + x1;
+          pk[j >> 1] = pack2<FP16>(x0, x1);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float x0 = k0 + j < n ? ex2_ftz(fmaf(__uint_as_float(r[j]), sl2, -ms)) : 0.f;
+          const float x1 =
+              k0 + j + 1 < n ? ex2_ftz(fmaf(__uint_as_float(r[j + 1]), sl2, -ms)) : 0.f;
+          sum += x0 + x1;
+          pk[j >> 1] = pack2<FP16>(x0, x1);
+        }
       }
       const int pb = c & 1;
       if (c >= 2) mbar_wait(&p_empty[pb], ((c >> 1) - 1) & 1);  // PV of chunk c - 2 done
