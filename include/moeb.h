@@ -219,6 +219,8 @@ int moeb_match_queries(const double* queries, int M, int D, const double* unit_t
  *    ln_eps) in place, out16 = 16-bit copy (post-norm encoder sublayer)
  *  5 ROW-MAX (N % 256 == 0): out32 [M][N/256] = max of each 256-column tile
  *    of each row, out16 (as int32) = its first argmax column (m-fastest raster)
+ *  6 RESID_ADD: out32 += C + bias (fp32 residual stream, in place; the
+ *    post-norm LayerNorm then runs as moeb_layernorm_rows)
  * K % 64 == 0, N % 64 == 0.
  */
 int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K, int fp16,
@@ -241,6 +243,10 @@ int moeb_window_attention(const void* qkv, void* out, const int64_t* win_start,
  * (factorised input projection), out16 = 16-bit copy. Rows of 512. */
 int moeb_embed_rows(const float* ptok, const float* play, const int32_t* token_ids, int L,
                     int64_t rows, float* out32, void* out16, int fp16, void* stream);
+/* Post-norm LayerNorm of 512-wide rows: x32 = LN(x32; w, b, eps) in place,
+ * out16 = 16-bit copy (the next GEMM's operand). */
+int moeb_layernorm_rows(float* x32, void* out16, const float* w, const float* b, int64_t rows,
+                        float eps, int fp16, void* stream);
 /* fp32 -> 16-bit (fp16 or bf16) conversion (weight packing). */
 int moeb_to16(const float* x, void* y, int64_t n, int fp16, void* stream);
 

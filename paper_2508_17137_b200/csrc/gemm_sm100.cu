@@ -33,7 +33,8 @@ enum : int {
   EPI_BIAS_RELU = 2,
   EPI_BIAS_GELU = 3,
   EPI_RESID_LN = 4,
-  EPI_ROWMAX = 5  // per (row, N-tile): max value (out32) and first argmax column (out16 as int32)
+  EPI_ROWMAX = 5,  // per (row, N-tile): max value (out32) and first argmax column (out16 as int32)
+  EPI_RESID_ADD = 6  // out32 += C + bias (fp32 residual stream, in place; LN runs separately)
 };
 
 struct GemmArgs {
@@ -307,6 +308,14 @@ __global__ void __launch_bounds__(320, 1)
           for (int q = 0; q < 8; ++q)
             bb[q] = g.bias ? __ldg(reinterpret_cast<const float4*>(g.bias + col) + q)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (EPI == EPI_RESID_ADD && rv) {  // residual row chunk, loaded under the TMEM load
+            const float4* res = reinterpret_cast<const float4*>(g.out32 + (int64_t)row * g.N + col);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 x = res[q];
+              bb[q] = make_float4(bb[q].x + x.x, bb[q].y + x.y, bb[q].z + x.z, bb[q].w + x.w);
+            }
+          }
           tmem_ld_wait();
           if (!rv) continue;
           float v[32];
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(320, 1)
             if (EPI == EPI_BIAS_RELU) v[j] = fmaxf(v[j], 0.f);
             if (EPI == EPI_BIAS_GELU) v[j] = gelu_erf(v[j]);
           }
-          if (EPI == EPI_F32) {
+          if (EPI == EPI_F32 || EPI == EPI_RESID_ADD) {
             float4* o = reinterpret_cast<float4*>(g.out32 + (int64_t)row * g.N + col);
 #pragma unroll
             for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -424,7 +433,7 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
   moeb::clear_error();
   MOEB_REQUIRE(A && B && M >= 1 && N >= 1 && K >= 1, "bad GEMM arguments");
   MOEB_REQUIRE(K % BK == 0, "K must be a multiple of %d (got %d)", BK, K);
-  MOEB_REQUIRE(epi >= EPI_F32 && epi <= EPI_ROWMAX, "unknown epilogue %d", epi);
+  MOEB_REQUIRE(epi >= EPI_F32 && epi <= EPI_RESID_ADD, "unknown epilogue %d", epi);
   int bn;
   if (epi == EPI_RESID_LN) {
     MOEB_REQUIRE(N == 512, "LayerNorm epilogue needs N == 512");
@@ -433,7 +442,8 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
   } else {
     bn = N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : N % 64 == 0 ? 64 : 0;
     MOEB_REQUIRE(bn, "N must be a multiple of 64 (got %d)", N);
-    MOEB_REQUIRE(epi == EPI_F32 ? out32 != nullptr : out16 != nullptr, "missing output");
+    MOEB_REQUIRE((epi == EPI_F32 || epi == EPI_RESID_ADD) ? out32 != nullptr : out16 != nullptr,
+                 "missing output");
     MOEB_REQUIRE(epi != EPI_ROWMAX || (out32 && bn == 256), "row-max epilogue needs N % 256 == 0");
   }
   CUtensorMap ta, tb;
@@ -446,6 +456,7 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
     case EPI_BIAS: return fp16 ? dispatch<EPI_BIAS, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS, false>(ta, tb, g, bn, s);
     case EPI_BIAS_RELU: return fp16 ? dispatch<EPI_BIAS_RELU, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS_RELU, false>(ta, tb, g, bn, s);
     case EPI_BIAS_GELU: return fp16 ? dispatch<EPI_BIAS_GELU, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS_GELU, false>(ta, tb, g, bn, s);
+    case EPI_RESID_ADD: return fp16 ? dispatch<EPI_RESID_ADD, true>(ta, tb, g, bn, s) : dispatch<EPI_RESID_ADD, false>(ta, tb, g, bn, s);
     case EPI_ROWMAX: return fp16 ? launch_gemm<256, 4, EPI_ROWMAX, true>(ta, tb, g, s) : launch_gemm<256, 4, EPI_ROWMAX, false>(ta, tb, g, s);
     default: return fp16 ? launch_gemm<512, 2, EPI_RESID_LN, true>(ta, tb, g, s) : launch_gemm<512, 2, EPI_RESID_LN, false>(ta, tb, g, s);
   }

@@ -57,7 +57,80 @@ __global__ void k_to16(const float* __restrict__ x, uint16_t* __restrict__ y, in
                 : __bfloat16_as_ushort(__float2bfloat16_rn(x[i]));
 }
 
+// Post-norm LayerNorm of the residual stream, one warp per 512-wide row:
+// two-pass mean / variance in registers, y = (x - mean) rsqrt(var + eps) w + b
+// written back in fp32 (in place) and as the 16-bit GEMM operand.
+template <bool FP16>
+__global__ void __launch_bounds__(256) k_layernorm_rows(float* __restrict__ x32,
+                                                        uint16_t* __restrict__ out16,
+                                                        const float* __restrict__ w,
+                                                        const float* __restrict__ b,
+                                                        int64_t rows, float eps) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  float4* xr = reinterpret_cast<float4*>(x32 + r * 512);
+  float4 v[4];
+  float s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // lane owns columns [128 q + 4 lane, +4)
+    v[q] = xr[q * 32 + lane];
+    s += (v[q].x + v[q].y) + (v[q].z + v[q].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s * (1.f / 512.f);
+  float s2 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float a0 = v[q].x - mean, a1 = v[q].y - mean, a2 = v[q].z - mean, a3 = v[q].w - mean;
+    s2 += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  const float rstd = rsqrtf(s2 * (1.f / 512.f) + eps);
+  const float4* w4 = reinterpret_cast<const float4*>(w);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  uint2* o16 = reinterpret_cast<uint2*>(out16 + r * 512);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 ww = __ldg(w4 + q * 32 + lane), bb = __ldg(b4 + q * 32 + lane);
+    const float4 y = make_float4((v[q].x - mean) * rstd * ww.x + bb.x,
+                                 (v[q].y - mean) * rstd * ww.y + bb.y,
+                                 (v[q].z - mean) * rstd * ww.z + bb.z,
+                                 (v[q].w - mean) * rstd * ww.w + bb.w);
+    xr[q * 32 + lane] = y;
+    uint32_t p0, p1;
+    if (FP16) {
+      const __half2 h0 = __floats2half2_rn(y.x, y.y), h1 = __floats2half2_rn(y.z, y.w);
+      p0 = *reinterpret_cast<const uint32_t*>(&h0);
+      p1 = *reinterpret_cast<const uint32_t*>(&h1);
+    } else {
+      const __nv_bfloat162 h0 = __floats2bfloat162_rn(y.x, y.y), h1 = __floats2bfloat162_rn(y.z, y.w);
+      p0 = *reinterpret_cast<const uint32_t*>(&h0);
+      p1 = *reinterpret_cast<const uint32_t*>(&h1);
+    }
+    o16[q * 32 + lane] = make_uint2(p0, p1);
+  }
+}
+
 }  // namespace
+
+extern "C" int moeb_layernorm_rows(float* x32, void* out16, const float* w, const float* b,
+                                   int64_t rows, float eps, int fp16, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(x32 && out16 && w && b && rows >= 0, "bad args");
+  if (rows == 0) return MOEB_OK;
+  const unsigned blocks = (unsigned)((rows * 32 + 255) / 256);
+  cudaStream_t s = moeb::as_stream(stream);
+  if (fp16)
+    k_layernorm_rows<true><<<blocks, 256, 0, s>>>(x32, static_cast<uint16_t*>(out16), w, b, rows,
+                                                  eps);
+  else
+    k_layernorm_rows<false><<<blocks, 256, 0, s>>>(x32, static_cast<uint16_t*>(out16), w, b,
+                                                   rows, eps);
+  return moeb::check_launch("k_layernorm_rows");
+}
 
 extern "C" int moeb_embed_rows(const float* ptok, const float* play, const int32_t* token_ids,
                                int L, int64_t rows, float* out32, void* out16, int fp16,

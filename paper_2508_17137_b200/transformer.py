@@ -35,6 +35,7 @@ VOCAB, D_TOK, D_LAYER, D_MODEL, N_HEAD, D_FF, N_LAYERS, D_HEAD_MLP = (
 WINDOW = 512
 LN_EPS = 1e-5
 EPI_F32, EPI_BIAS, EPI_BIAS_RELU, EPI_BIAS_GELU, EPI_RESID_LN = range(5)
+EPI_RESID_ADD = 6
 
 
 def init_state(num_layers: int, num_experts: int, seed: int = 0) -> dict:
@@ -115,6 +116,12 @@ class TransformerWeights:
                device=None):
         return cls(init_state(num_layers, num_experts, seed), num_layers, num_experts, fp16,
                    device)
+
+
+def layernorm(x32, x16, w, b, rows, fp16, eps=1e-5):
+    """Post-norm LayerNorm of the first `rows` rows (moeb_layernorm_rows)."""
+    nat.call("moeb_layernorm_rows", nat.ptr(x32), nat.ptr(x16), nat.ptr(w), nat.ptr(b), rows,
+             float(eps), int(bool(fp16)), nat.stream_ptr())
 
 
 def windows_of(row_off_host: np.ndarray, window: int = WINDOW):
@@ -205,14 +212,17 @@ class TransformerPredictor:
                       nat.ptr(att), nat.ptr(ws_d), nat.ptr(wl_d), len(ws), WINDOW, M,
                       int(W.fp16),
                       nat.stream_ptr())
-                timed("gemm_out_ln", 2.0 * M * D_MODEL * D_MODEL, gemm, att, lay["o"], M, D_MODEL,
-                      D_MODEL, EPI_RESID_LN, bias=lay["o_b"], out32=h32, out16=h16,
-                      ln=(lay["n1_w"], lay["n1_b"]), fp16=W.fp16)
+                # residual add fused into the GEMM epilogue (fp32 stream, two
+                # TMEM accumulators so epilogue and mainloop overlap), then a
+                # streaming LayerNorm kernel over the rows
+                timed("gemm_out", 2.0 * M * D_MODEL * D_MODEL, gemm, att, lay["o"], M, D_MODEL,
+                      D_MODEL, EPI_RESID_ADD, bias=lay["o_b"], out32=h32, fp16=W.fp16)
+                timed("layernorm", 0.0, layernorm, h32, h16, lay["n1_w"], lay["n1_b"], M, W.fp16)
                 timed("gemm_ffn1", 2.0 * M * D_FF * D_MODEL, gemm, h16, lay["f1"], M, D_FF,
                       D_MODEL, EPI_BIAS_RELU, bias=lay["f1_b"], out16=ff, fp16=W.fp16)
-                timed("gemm_ffn2_ln", 2.0 * M * D_MODEL * D_FF, gemm, ff, lay["f2"], M, D_MODEL,
-                      D_FF, EPI_RESID_LN, bias=lay["f2_b"], out32=h32, out16=h16,
-                      ln=(lay["n2_w"], lay["n2_b"]), fp16=W.fp16)
+                timed("gemm_ffn2", 2.0 * M * D_MODEL * D_FF, gemm, ff, lay["f2"], M, D_MODEL,
+                      D_FF, EPI_RESID_ADD, bias=lay["f2_b"], out32=h32, fp16=W.fp16)
+                timed("layernorm", 0.0, layernorm, h32, h16, lay["n2_w"], lay["n2_b"], M, W.fp16)
             timed("gemm_head", 2.0 * M * (D_HEAD_MLP * D_MODEL + E * D_HEAD_MLP), self._head,
                   h16, y, out[r0:r0 + M], M)
         return out
