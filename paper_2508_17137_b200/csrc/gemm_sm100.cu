@@ -50,6 +50,7 @@ struct GemmArgs {
 };
 
 constexpr int BM = 128;
+constexpr int kBiasMax = 4096;  // bias entries staged in shared memory
 constexpr int BK = 64;  // 64 16-bit elements = one 128-byte swizzle row
 
 __device__ __forceinline__ uint16_t to16(float x, bool fp16) {
@@ -88,6 +89,13 @@ __global__ void __launch_bounds__(320, 1)
   // per-epilogue-warp 32 x 33 fp32 transpose tiles (LayerNorm epilogue),
   // then the pair-exchange area (8 warps x 32 lanes x 8 bytes)
   float* tbuf = reinterpret_cast<float*>(tmem_base_smem + 4);
+  // bias staged once per CTA (N <= kBiasMax): epilogue reads are smem broadcasts
+  float* sbias = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(tbuf + (EPI == EPI_RESID_LN ? 8 * 32 * 33 : 0) + 8 * 32 * 2) +
+       15) & ~uintptr_t(15));
+  const bool bias_smem = g.bias != nullptr && g.N <= kBiasMax;
+  if (bias_smem)
+    for (int i = threadIdx.x; i < g.N; i += blockDim.x) sbias[i] = __ldg(g.bias + i);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_m = (g.M + BM - 1) / BM, tiles_n = g.N / BN;
@@ -227,7 +235,8 @@ __global__ void __launch_bounds__(320, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const float x = __uint_as_float(r[j]) + __ldg(g.bias + c0 + j) + T[lane * 33 + j];
+            const float x = __uint_as_float(r[j]) + (bias_smem ? sbias[c0 + j] : __ldg(g.bias + c0 + j)) +
+                            T[lane * 33 + j];
             r[j] = __float_as_uint(x);
             s1 += x;
             s2 += x * x;
@@ -306,8 +315,9 @@ __global__ void __launch_bounds__(320, 1)
           float4 bb[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            bb[q] = g.bias ? __ldg(reinterpret_cast<const float4*>(g.bias + col) + q)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            bb[q] = bias_smem ? reinterpret_cast<const float4*>(sbias + col)[q]
+                    : g.bias  ? __ldg(reinterpret_cast<const float4*>(g.bias + col) + q)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
           if (EPI == EPI_RESID_ADD && rv) {  // residual row chunk, loaded under the TMEM load
             const float4* res = reinterpret_cast<const float4*>(g.out32 + (int64_t)row * g.N + col);
 #pragma unroll
@@ -406,7 +416,8 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
-                      (EPI == EPI_RESID_LN ? 8 * 32 * 33 * sizeof(float) : 0) + 8 * 32 * 8;
+                      (EPI == EPI_RESID_LN ? 8 * 32 * 33 * sizeof(float) : 0) + 8 * 32 * 8 +
+                      kBiasMax * sizeof(float) + 16;
   auto k = k_gemm<BN, STAGES, EPI, FP16>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
