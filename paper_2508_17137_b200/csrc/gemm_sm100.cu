@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(320, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const GemmArgs g) {
   constexpr int ACC = BN <= 256 ? 2 : 1;           // TMEM accumulator buffers
+  constexpr bool kTbuf = EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD;  // 32x33 transposes
   constexpr uint32_t TMEM_COLS = BN * ACC <= 32 ? 32 : BN * ACC;
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(320, 1)
   float* tbuf = reinterpret_cast<float*>(tmem_base_smem + 4);
   // bias staged once per CTA (N <= kBiasMax): epilogue reads are smem broadcasts
   float* sbias = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(tbuf + (EPI == EPI_RESID_LN ? 8 * 32 * 33 : 0) + 8 * 32 * 2) +
+      (reinterpret_cast<uintptr_t>(tbuf + (kTbuf ? 8 * 32 * 33 : 0) + 8 * 32 * 2) +
        15) & ~uintptr_t(15));
   const bool bias_smem = g.bias != nullptr && g.N <= kBiasMax;
   if (bias_smem)
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(320, 1)
     const int half = ew >> 2;
     constexpr int HC = BN / 2;  // columns per epilogue warp
     const int cb = half * HC;
-    float2* xch = reinterpret_cast<float2*>(tbuf + (EPI == EPI_RESID_LN ? 8 * 32 * 33 : 0));
+    float2* xch = reinterpret_cast<float2*>(tbuf + (kTbuf ? 8 * 32 * 33 : 0));
     auto pair_sync = [&]() {  // the two warps sharing this lane quarter
       asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
     };
@@ -307,6 +308,35 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
         pair_sync();
+      } else if (EPI == EPI_RESID_ADD) {
+        // out32 += acc + bias with coalesced residual I/O: each 32 x 32
+        // accumulator chunk goes through a padded shared-memory transpose and
+        // lanes walk columns (the 32 residual loads are issued under the
+        // TMEM load)
+        float* T = tbuf + ew * (32 * 33);
+        const int rowbase = tm * BM + quarter * 32;
+        for (int c0 = cb; c0 < cb + HC; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(t0 + c0, r);
+          const int col = tn * BN + c0 + lane;
+          const float bl = bias_smem ? sbias[col] : (g.bias ? __ldg(g.bias + col) : 0.f);
+          float res[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int rr = rowbase + i;
+            res[i] = rr < g.M ? g.out32[(int64_t)rr * g.N + col] : 0.f;
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int rr = rowbase + i;
+            if (rr < g.M) g.out32[(int64_t)rr * g.N + col] = res[i] + (T[i * 33 + lane] + bl);
+          }
+          __syncwarp();
+        }
       } else {
         for (int c0 = cb; c0 < cb + HC; c0 += 32) {
           uint32_t r[32];
@@ -416,7 +446,9 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
-                      (EPI == EPI_RESID_LN ? 8 * 32 * 33 * sizeof(float) : 0) + 8 * 32 * 8 +
+                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD) ? 8 * 32 * 33 * sizeof(float)
+                                                                     : 0) +
+                      8 * 32 * 8 +
                       kBiasMax * sizeof(float) + 16;
   auto k = k_gemm<BN, STAGES, EPI, FP16>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -430,7 +462,10 @@ template <int EPI, bool FP16>
 int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn,
              cudaStream_t s) {
   if (bn == 512) return launch_gemm<512, 2, EPI, FP16>(ta, tb, g, s);
-  if (bn == 256) return launch_gemm<256, 4, EPI, FP16>(ta, tb, g, s);
+  if (bn == 256) {
+    if (EPI == EPI_RESID_ADD) return launch_gemm<256, 3, EPI, FP16>(ta, tb, g, s);  // + transposes
+    return launch_gemm<256, 4, EPI, FP16>(ta, tb, g, s);
+  }
   if (bn == 128) return launch_gemm<128, 6, EPI, FP16>(ta, tb, g, s);
   return launch_gemm<64, 8, EPI, FP16>(ta, tb, g, s);
 }

@@ -42,6 +42,11 @@ def test_gemm_epilogues(tr, fp16, M, N, K):
         out16 = torch.empty(M, N, device="cuda", dtype=dt)
         tr.gemm(a, b, M, N, K, epi, bias=bias, out16=out16, fp16=fp16)
         torch.testing.assert_close(out16.float(), fn(ref), atol=tol + q, rtol=q)
+    if N % 256 == 0:  # fp32 residual add (transformer post-norm sublayers)
+        resid = torch.randn(M, N, device="cuda", generator=g)
+        h = resid.clone()
+        tr.gemm(a, b, M, N, K, tr.EPI_RESID_ADD, bias=bias, out32=h, fp16=fp16)
+        torch.testing.assert_close(h, resid + ref, atol=tol, rtol=1e-3)
     if N == 512:
         resid = torch.randn(M, N, device="cuda", generator=g)
         lw = 1 + 0.1 * torch.randn(N, device="cuda", generator=g)
@@ -51,6 +56,13 @@ def test_gemm_epilogues(tr, fp16, M, N, K):
         h16 = torch.empty(M, N, device="cuda", dtype=dt)
         tr.gemm(a, b, M, N, K, tr.EPI_RESID_LN, bias=bias, out32=h32, out16=h16, ln=(lw, lb),
                 fp16=fp16)
+        torch.testing.assert_close(h32, want, atol=5e-3, rtol=1e-3)
+        torch.testing.assert_close(h16.float(), want, atol=5e-3 + q, rtol=q)
+        # split form: residual-add GEMM + LayerNorm kernel
+        h32 = resid.clone()
+        tr.gemm(a, b, M, N, K, tr.EPI_RESID_ADD, bias=bias, out32=h32, fp16=fp16)
+        h16 = torch.empty(M, N, device="cuda", dtype=dt)
+        tr.layernorm(h32, h16, lw, lb, M, fp16)
         torch.testing.assert_close(h32, want, atol=5e-3, rtol=1e-3)
         torch.testing.assert_close(h16.float(), want, atol=5e-3 + q, rtol=q)
 
