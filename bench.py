@@ -34,6 +34,16 @@ BUDGET = 6
 WARMUP_TOKENS = 8
 
 
+def _config(P, rows, cap, world):
+    """The workload description both arms report (BASELINE configs[1], C2)."""
+    return {"workload": f"C2: {P} prompts x {C2['tokens']} tokens per GPU, "
+                        "DeepSeek-V2-Lite 26 MoE layers x 64 experts top-6",
+            "rows_per_gpu": rows, "predictor": "learned_linear (random init, seed 0)",
+            "capacity_entries": cap, "prefetch_budget": BUDGET,
+            "warmup_tokens": WARMUP_TOKENS, "parallelism": f"prompt-sharded x{world}",
+            "l2": "inputs (528 MB/GPU) larger than L2"}
+
+
 def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -192,9 +202,10 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1000.0 * elapsed / max(1, args.steps),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator)",
-        "config": {"workload": "C2 sample: DeepSeek-V2-Lite 26x64 top-6, 363-token prompts",
-                   "capacity_fraction": CAP_FRACTION, "prefetch_budget": BUDGET,
-                   "warmup_tokens": WARMUP_TOKENS, "predictor": "learned_linear"},
+        "config": dict(_config(C2["prompts"], C2["prompts"] * C2["tokens"] * C2["layers"], 166,
+                               world),
+                       sampled=f"each step replays {n_sample} of the {C2['prompts']} prompts "
+                               "(bounded CPU sample, see cpu_baseline)"),
         "cpu_baseline": {"value": value, "unit": "trace tokens/s", "cores": cores,
                          "kind": "reference", "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "trace tokens/s", "h2d_bytes_per_step": 0,
@@ -476,12 +487,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int64+f64",
             "data": "synthetic (reference generator, bit-identical, generated on device)",
-            "config": {"workload": f"C2: {P} prompts x {C2['tokens']} tokens per GPU, "
-                                   "DeepSeek-V2-Lite 26 MoE layers x 64 experts top-6",
-                       "rows_per_gpu": rows, "predictor": "learned_linear (random init, seed 0)",
-                       "capacity_entries": cap, "prefetch_budget": BUDGET,
-                       "warmup_tokens": WARMUP_TOKENS, "parallelism": f"prompt-sharded x{world}",
-                       "l2": "inputs (528 MB/GPU) larger than L2"},
+            "config": _config(P, rows, cap, world),
             "e2e": {"value": e2e_value, "unit": "trace tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             # per chunk: K3 (k_linear_predict) + K7 (k_metrics64) + K1 (k_cache_sim_warp)
