@@ -91,9 +91,10 @@ __global__ void __launch_bounds__(320, 1)
   // then the pair-exchange area (8 warps x 32 lanes x 8 bytes)
   float* tbuf = reinterpret_cast<float*>(tmem_base_smem + 4);
   // bias staged once per CTA (N <= kBiasMax): epilogue reads are smem broadcasts
-  float* sbias = reinterpret_cast<float*>(
-      (reinterpret_cast<uintptr_t>(tbuf + (kTbuf ? 8 * 32 * 33 : 0) + 8 * 32 * 2) +
-       15) & ~uintptr_t(15));
+  // (offset arithmetic on the shared window keeps LDS, not generic loads)
+  float* sbias0 = tbuf + (kTbuf ? 8 * 32 * 33 : 0) + 8 * 32 * 2;
+  const uint32_t mis = smem_u32(sbias0) & 15u;
+  float* sbias = sbias0 + (mis ? (16u - mis) / 4u : 0u);
   const bool bias_smem = g.bias != nullptr && g.N <= kBiasMax;
   if (bias_smem)
     for (int i = threadIdx.x; i < g.N; i += blockDim.x) sbias[i] = __ldg(g.bias + i);
