@@ -126,6 +126,20 @@ int moeb_linear_predict_wide(const uint64_t* truth, const int64_t* prompt_row_of
                              double* logits, int64_t* metrics, void* stream);
 
 /*
+ * learned_linear training (learner.train, learner.py:75-155).
+ * moeb_linear_features: hist [rows][E] fp64 = the decayed history of the
+ *   row's layer before the row (training_pairs' feature block), bit-identical.
+ * moeb_linear_sgd_epoch: per-example SGD over the rows in `order` (the
+ *   host's rng.permutation), weights [E][L+E+1] fp64 updated in place;
+ *   *loss_total = sum over examples of the example's mean BCE.
+ */
+int moeb_linear_features(const uint64_t* truth, const int64_t* prompt_row_off, int n_prompts,
+                         int L, int E, double decay, double* hist, void* stream);
+int moeb_linear_sgd_epoch(double* weights, const double* hist, const uint64_t* truth,
+                          const int64_t* order, int64_t n, int L, int E, double learning_rate,
+                          double* loss_total, void* stream);
+
+/*
  * K2 -- mask head: logits -> top-k (ties to lower id) or logit > 0 masks.
  * Replaces top_k_experts / predict_topk (learner.py:164-181). fp32 logits.
  */

@@ -76,6 +76,8 @@ _SIGS = {
     "moeb_cluster_means": [P, P, P, I32, I64, P, P],
     "moeb_linear_prepare": [P, I32, I32, DBL, P, P],
     "moeb_linear_predict_wide": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P],
+    "moeb_linear_features": [P, P, I32, I32, I32, DBL, P, P],
+    "moeb_linear_sgd_epoch": [P, P, P, P, I64, I32, I32, DBL, P, P],
     "moeb_version": [],
     "moeb_device_check": [],
 }

@@ -1,11 +1,9 @@
 """Linear learned predictor model container (learner.py:22-224 in the reference).
 
 Inference over whole traces is the device kernel moeb_linear_predict
-(predictors.LearnedLinearPredictor). Training with epochs > 0 (the reference's
-per-example SGD, learner.py:116-155) is the step before this hot path and is
-listed as a next component in DESIGN.md; ``train`` here reproduces the
-reference's seeded initialisation exactly (epochs = 0 returns it, marked
-trained, as the reference does).
+(predictors.LearnedLinearPredictor); training (the reference's per-example
+SGD, learner.py:116-155) runs as moeb_linear_features + one
+moeb_linear_sgd_epoch launch per epoch (csrc/learner.cu).
 """
 
 from __future__ import annotations
@@ -56,15 +54,61 @@ def init_weights(shape: ModelShape, seed: int) -> np.ndarray:
     return rng.normal(0.0, 0.01, size=(shape.num_experts, shape.num_layers + shape.num_experts + 1))
 
 
+_EARLY_STOP_DELTA = 1e-5
+_EARLY_STOP_PATIENCE = 3
+
+
 def train(traces, shape: ModelShape, config: LearnerConfig = LearnerConfig()) -> LinearModel:
-    """Seeded model. epochs = 0: the reference's random init, marked trained."""
+    """learner.train (learner.py:116-155): per-example SGD over seeded-shuffled
+    (token, layer) steps with patience-3 early stop, on device.
+
+    The features (decayed histories, bit-identical to training_pairs) come
+    from moeb_linear_features; each epoch is one moeb_linear_sgd_epoch launch
+    in the permutation the reference's rng draws (same seed, same call
+    sequence: normal() init, then permutation() per epoch). epochs = 0
+    returns the seeded initialisation, marked trained."""
+    import torch
+
+    from . import _native as nat
+    from .traces import PackedTraces, pack_traces
+
     if traces is not None and hasattr(traces, "__len__") and len(traces) == 0:
         raise ConfigError("cannot train on an empty trace list")
-    if config.epochs > 0:
-        raise NotImplementedError(
-            "SGD training (learner.py:116-155) is not part of this hot path; "
-            "use epochs=0 (seeded init) or load_model() with trained weights")
-    return LinearModel(shape, config, init_weights(shape, config.seed), trained=True)
+    if traces is None and config.epochs > 0:  # None: the seeded init only (epochs = 0)
+        raise ConfigError("cannot train on an empty trace list")
+    rng = np.random.default_rng(config.seed)
+    L, E = shape.num_layers, shape.num_experts
+    weights = rng.normal(0.0, 0.01, size=(E, L + E + 1))
+    if config.epochs == 0:
+        return LinearModel(shape, config, weights, trained=True)
+    packed = traces if isinstance(traces, PackedTraces) else pack_traces(traces, shape)
+    n = packed.rows
+    if n == 0:
+        raise ConfigError("no training examples: traces are empty")
+    dev = packed.device
+    hist = torch.empty((n, E), dtype=torch.float64, device=dev)
+    nat.call("moeb_linear_features", nat.ptr(packed.truth), nat.ptr(packed.row_off),
+             packed.num_prompts, L, E, float(config.decay), nat.ptr(hist), nat.stream_ptr())
+    w_d = torch.from_numpy(np.ascontiguousarray(weights)).to(dev)
+    loss_d = torch.zeros(1, dtype=torch.float64, device=dev)
+    losses: list[float] = []
+    best = np.inf
+    stalls = 0
+    for _ in range(config.epochs):
+        order = torch.from_numpy(rng.permutation(n).astype(np.int64)).to(dev)
+        nat.call("moeb_linear_sgd_epoch", nat.ptr(w_d), nat.ptr(hist), nat.ptr(packed.truth),
+                 nat.ptr(order), n, L, E, float(config.learning_rate), nat.ptr(loss_d),
+                 nat.stream_ptr())
+        epoch_loss = float(loss_d.item()) / n
+        losses.append(epoch_loss)
+        if best - epoch_loss < _EARLY_STOP_DELTA:
+            stalls += 1
+            if stalls >= _EARLY_STOP_PATIENCE:
+                break
+        else:
+            stalls = 0
+        best = min(best, epoch_loss)
+    return LinearModel(shape, config, w_d.cpu().numpy(), trained=True, loss_history=losses)
 
 
 def save_model(model: LinearModel, path) -> None:
