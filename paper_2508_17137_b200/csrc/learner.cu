@@ -92,37 +92,60 @@ __global__ void k_linear_sgd_epoch(double* __restrict__ Wg, const double* __rest
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int F = L + E + 1;
   const int W = (E + 63) / 64;
-  double* hs = reinterpret_cast<double*>(smem_raw);  // [E] features of the example
-  double* terms = hs + E;                             // [E] loss terms
-  double* Ws = terms + E;                             // [E][F] (w_smem)
+  double* hbuf = reinterpret_cast<double*>(smem_raw);  // [2][E] features (double-buffered)
+  double* terms = hbuf + 2 * E;                        // [E] loss terms
+  double* Ws = terms + E;                              // [E][F] (w_smem)
   double* Wt = w_smem ? Ws : Wg;
   const int j = threadIdx.x;
   if (w_smem)
     for (int i = j; i < E * F; i += blockDim.x) Ws[i] = Wg[i];
   __syncthreads();
   double total = 0.0;
+  if (j < E) hbuf[j] = hist[order[0] * E + j];
+  int64_t rn = n > 1 ? order[1] : 0;
   for (int64_t it = 0; it < n; ++it) {
     const int64_t r = order[it];
     const int l = (int)(r % L);
-    if (j < E) hs[j] = hist[r * E + j];
+    double* hs = hbuf + (it & 1) * E;
+    // the next example's features, loaded under this example's work
+    const double hn = (j < E && it + 1 < n) ? hist[rn * E + j] : 0.0;
+    rn = it + 2 < n ? order[it + 2] : 0;
     __syncthreads();
     double z = 0.0, t = 0.0, term = 0.0;
     double* wr = Wt + (int64_t)j * F;
     if (j < E) {
-      // z = W_j . f, f = [onehot(l) | h | 1], in feature order
-      for (int k = 0; k < L + E + 1; ++k) {
-        double fk;
-        if (k < L) fk = k == l ? 1.0 : 0.0;
-        else if (k < L + E) fk = hs[k - L];
-        else fk = 1.0;
-        if (fk != 0.0) z = fma(wr[k], fk, z);
+      // z = W_j . f, f = [onehot(l) | h | 1], non-zero features in order
+      z = wr[l];
+      for (int e = 0; e < E; ++e) {
+        const double fk = hs[e];
+        if (fk != 0.0) z = fma(wr[L + e], fk, z);
       }
+      z = __dadd_rn(z, wr[L + E]);
       t = ((truth[r * W + (j >> 6)] >> (j & 63)) & 1ull) ? 1.0 : 0.0;
       term = __dsub_rn(logaddexp0(z), __dmul_rn(t, z));
       terms[j] = term;
     }
     __syncthreads();
-    if (j == 0) total = __dadd_rn(total, pairwise_sum(terms, E) / (double)E);
+    if (j < 32) {  // numpy's pairwise mean of the E terms (same tree, warp 0)
+      double part;
+      if (E <= 128 && E >= 8) {
+        // r[q] = a[q] + a[q+8] + ... sequentially, q < 8; tail added last
+        double acc = 0.0;
+        const int nb = E - (E % 8);
+        if (j < 8) {
+          acc = terms[j];
+          for (int i = 8 + j; i < nb; i += 8) acc = __dadd_rn(acc, terms[i]);
+        }
+        const double s1 = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));  // r0+r1, ...
+        const double s2 = __dadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, 2));
+        double res = __dadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, 4));
+        for (int i = nb; i < E; ++i) res = __dadd_rn(res, terms[i]);
+        part = res;
+      } else {
+        part = j == 0 ? pairwise_sum(terms, E) : 0.0;
+      }
+      if (j == 0) total = __dadd_rn(total, part / (double)E);
+    }
     if (j < E) {
       const double sig = 1.0 / (1.0 + exp(-z));
       const double g = (sig - t) / (double)E;
@@ -134,8 +157,9 @@ __global__ void k_linear_sgd_epoch(double* __restrict__ Wg, const double* __rest
       }
       wr[L + E] = __dsub_rn(wr[L + E], __dmul_rn(lr, __dmul_rn(g, 1.0)));
     }
-    __syncthreads();  // hs is rewritten by the next example
+    if (j < E) hbuf[((it + 1) & 1) * E + j] = hn;  // other buffer: no reader this round
   }
+  __syncthreads();  // every row's last update lands before the copy-out
   if (w_smem)
     for (int i = j; i < E * F; i += blockDim.x) Wg[i] = Ws[i];
   if (j == 0) *loss_total = total;
@@ -162,7 +186,7 @@ extern "C" int moeb_linear_sgd_epoch(double* weights, const double* hist, const 
   MOEB_REQUIRE(weights && hist && truth && order && loss_total && n >= 1, "null argument");
   MOEB_REQUIRE(L >= 1 && E >= 1 && E <= 256, "unsupported shape L=%d E=%d", L, E);
   const int F = L + E + 1;
-  size_t smem = sizeof(double) * (size_t)(2 * E);
+  size_t smem = sizeof(double) * (size_t)(3 * E);  // features [2][E], loss terms [E]
   const size_t wbytes = sizeof(double) * (size_t)E * F;
   const int w_smem = smem + wbytes <= (size_t)moeb::max_smem_per_block() ? 1 : 0;
   if (w_smem) smem += wbytes;
