@@ -448,3 +448,70 @@ def sweep(traces, predictor_factory, predictor_kind: str, capacities, shape: Mod
     return [SweepPoint(f, predictor_kind,
                        SimReport.from_counters(shape, counters[0, j], pp[0, j], packed.prompt_ids))
             for j, f in enumerate(capacities)]
+
+
+# ---------------------------------------------------------------------------
+# CSV reports of the device counters (engine.py:58-59, 309-383), formatted
+# exactly as the reference does.
+# ---------------------------------------------------------------------------
+
+def format_rate(rate) -> str:
+    return "n/a" if rate is None else repr(rate)
+
+
+def sweep_csv(points) -> bytes:
+    out = ["capacity_fraction,predictor,cache_hit_rate,prediction_hit_rate,measured_accesses\n"]
+    for p in points:
+        out.append(f"{repr(p.capacity_fraction)},{p.predictor_kind},"
+                   f"{format_rate(p.report.cache_hit_rate)},"
+                   f"{format_rate(p.report.prediction_hit_rate)},"
+                   f"{p.report.measured_accesses}\n")
+    return "".join(out).encode("utf-8")
+
+
+def sweep_layers_csv(points) -> bytes:
+    out = ["capacity_fraction,predictor,layer_id,measured_accesses,"
+           "cache_hits,cache_hit_rate,prediction_hits,prediction_hit_rate\n"]
+    for p in points:
+        r = p.report
+        for layer in range(r.shape.num_layers):
+            acc, ch = int(r.layer_accesses[layer]), int(r.layer_cache_hits[layer])
+            ph = int(r.layer_prediction_hits[layer])
+            out.append(f"{repr(p.capacity_fraction)},{p.predictor_kind},{layer},"
+                       f"{acc},{ch},{format_rate(_rate(ch, acc))},"
+                       f"{ph},{format_rate(_rate(ph, acc))}\n")
+    return "".join(out).encode("utf-8")
+
+
+def report_summary_csv(report: SimReport, predictor_kind: str, capacity_entries: int) -> bytes:
+    return ("predictor,capacity_entries,measured_accesses,cache_hits,"
+            "cache_hit_rate,prediction_opportunities,prediction_hits,"
+            "prediction_hit_rate,uncovered_queries\n"
+            f"{predictor_kind},{capacity_entries},{report.measured_accesses},"
+            f"{report.cache_hits},{format_rate(report.cache_hit_rate)},"
+            f"{report.prediction_opportunities},{report.prediction_hits},"
+            f"{format_rate(report.prediction_hit_rate)},{report.uncovered_queries}\n"
+            ).encode("utf-8")
+
+
+def report_layers_csv(report: SimReport) -> bytes:
+    out = ["layer_id,measured_accesses,cache_hits,cache_hit_rate,"
+           "prediction_hits,prediction_hit_rate\n"]
+    for layer in range(report.shape.num_layers):
+        acc, ch = int(report.layer_accesses[layer]), int(report.layer_cache_hits[layer])
+        ph = int(report.layer_prediction_hits[layer])
+        out.append(f"{layer},{acc},{ch},{format_rate(_rate(ch, acc))},"
+                   f"{ph},{format_rate(_rate(ph, acc))}\n")
+    return "".join(out).encode("utf-8")
+
+
+def report_prompts_csv(report: SimReport) -> bytes:
+    out = ["prompt_id,measured_accesses,cache_hits,cache_hit_rate,"
+           "prediction_hits,prediction_hit_rate\n"]
+    for pid in sorted(report.per_prompt):
+        c = report.per_prompt[pid]
+        out.append(f"{pid},{c.measured_accesses},{c.cache_hits},"
+                   f"{format_rate(_rate(c.cache_hits, c.measured_accesses))},"
+                   f"{c.prediction_hits},"
+                   f"{format_rate(_rate(c.prediction_hits, c.prediction_opportunities))}\n")
+    return "".join(out).encode("utf-8")
