@@ -17,6 +17,7 @@
 // Two TMEM accumulators (when BN <= 256) let the epilogue of tile i overlap
 // the mainloop of tile i+1.
 #include <cuda.h>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -62,18 +63,27 @@ __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
 }
 
-template <int BN, int STAGES, int EPI, bool FP16>
+// PAIR: a cluster of two CTAs on one TPC computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (M = 256): each CTA loads its 128 rows of A and
+// half of the BN rows of B (the 2-SM TMA completes on the leader's barrier),
+// the leader issues the MMAs and multicasts their completion; each CTA's
+// epilogue drains its own 128 accumulator rows. Per-SM operand traffic per
+// output tile drops from (A + B) to (A + B / 2).
+template <int BN, int STAGES, int EPI, bool FP16, bool PAIR = false>
 __global__ void __launch_bounds__(320, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const GemmArgs g) {
   constexpr int ACC = BN <= 256 ? 2 : 1;           // TMEM accumulator buffers
   constexpr bool kTbuf = EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD;  // 32x33 transposes
   constexpr uint32_t TMEM_COLS = BN * ACC <= 32 ? 32 : BN * ACC;
+  constexpr int BROWS = PAIR ? BN / 2 : BN;        // B rows held by this CTA
+  constexpr int TM = PAIR ? 2 * BM : BM;            // output rows per tile
   constexpr int A_BYTES = BM * BK * 2;
-  constexpr int B_BYTES = BN * BK * 2;
-  constexpr int BOX_N = BN < 256 ? BN : 256;        // TMA box rows for B
+  constexpr int B_BYTES = BROWS * BK * 2;
+  constexpr int BOX_N = BROWS < 256 ? BROWS : 256;  // TMA box rows for B
   constexpr int UMMA_N = BN < 256 ? BN : 256;
-  constexpr uint32_t IDESC = umma_idesc_f16(BM, UMMA_N, FP16 ? 0 : 1);
+  constexpr uint32_t IDESC = umma_idesc_f16(TM, UMMA_N, FP16 ? 0 : 1);
+  static_assert(!PAIR || BN <= 256, "pair tiles use one accumulator per N <= 256");
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // The dynamic shared-memory window starts 1024-byte aligned (no static
@@ -100,9 +110,13 @@ __global__ void __launch_bounds__(320, 1)
     for (int i = threadIdx.x; i < g.N; i += blockDim.x) sbias[i] = __ldg(g.bias + i);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles_m = (g.M + BM - 1) / BM, tiles_n = g.N / BN;
+  const int tiles_m = (g.M + TM - 1) / TM, tiles_n = g.N / BN;
   const int num_tiles = tiles_m * tiles_n;
   const int nk = g.K / BK;
+  const int rank = PAIR ? (int)cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int tile0 = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+  const int tstride = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -113,13 +127,17 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int b = 0; b < ACC; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 8);  // one arrive per epilogue warp
+      mbar_init(&tempty[b], PAIR ? 16 : 8);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_base_smem);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair<TMEM_COLS>(tmem_base_smem);
+    else tmem_alloc<TMEM_COLS>(tmem_base_smem);
+  }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_smem;
 
@@ -128,19 +146,30 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < num_tiles; tile += tstride) {
         // n-fastest raster: consecutive CTAs share the A tile in L2 (m-fastest
         // when B is the large streamed operand)
         const int tn = g.raster_m ? tile / tiles_m : tile % tiles_n;
         const int tm = g.raster_m ? tile % tiles_m : tile / tiles_n;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (PAIR) {
+            // both CTAs' bytes complete on the leader's barrier
+            if (leader) mbar_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+            tma_load_2d_pair(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK,
+                             tm * TM + rank * BM);
+#pragma unroll
+            for (int j = 0; j < BROWS / BOX_N; ++j)
+              tma_load_2d_pair(sB + stage * B_BYTES + j * BOX_N * 128, &tmB, &full[stage],
+                               kb * BK, tn * BN + rank * BROWS + j * BOX_N);
+          } else {
           mbar_expect_tx(&full[stage], A_BYTES + B_BYTES);
           tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, tm * BM);
 #pragma unroll
           for (int j = 0; j < BN / BOX_N; ++j)
             tma_load_2d(sB + stage * B_BYTES + j * BOX_N * 128, &tmB, &full[stage], kb * BK,
                         tn * BN + j * BOX_N);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -149,13 +178,13 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer =====
-    if (lane == 0) {
+    // ===== MMA issuer (the leader CTA of a pair) =====
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < num_tiles; tile += tstride) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this buffer
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -170,16 +199,21 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
             for (int j = 0; j < BN / UMMA_N; ++j) {
               const uint64_t bd = umma_desc_sw128(b0 + j * UMMA_N * 128 + k * 32);
-              mma_f16_ss(d_tmem + j * UMMA_N, ad, bd, IDESC, (kb | k) != 0);
+              if (PAIR) mma_f16_ss_pair(d_tmem + j * UMMA_N, ad, bd, IDESC, (kb | k) != 0);
+              else mma_f16_ss(d_tmem + j * UMMA_N, ad, bd, IDESC, (kb | k) != 0);
             }
           }
-          mma_commit(&empty[stage]);  // frees the smem stage when these MMAs finish
+          // frees the smem stage (of both CTAs) when these MMAs finish
+          if (PAIR) mma_commit_pair(&empty[stage], 3);
+          else mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+        // accumulator ready for the epilogue(s)
+        if (PAIR) mma_commit_pair(&tfull[acc], 3);
+        else mma_commit(&tfull[acc]);
         if (++acc == ACC) {
           acc = 0;
           acc_phase ^= 1;
@@ -200,12 +234,12 @@ __global__ void __launch_bounds__(320, 1)
     };
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+    for (int tile = tile0; tile < num_tiles; tile += tstride) {
       const int tn = g.raster_m ? tile / tiles_m : tile % tiles_n;
       const int tm = g.raster_m ? tile % tiles_m : tile / tiles_n;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = tm * BM + quarter * 32 + lane;
+      const int row = tm * TM + rank * BM + quarter * 32 + lane;
       const bool rv = row < g.M;
       const uint32_t t0 = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
       if (EPI == EPI_RESID_LN) {
@@ -315,7 +349,7 @@ __global__ void __launch_bounds__(320, 1)
         // lanes walk columns (the 32 residual loads are issued under the
         // TMEM load)
         float* T = tbuf + ew * (32 * 33);
-        const int rowbase = tm * BM + quarter * 32;
+        const int rowbase = tm * TM + rank * BM + quarter * 32;
         for (int c0 = cb; c0 < cb + HC; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
@@ -392,7 +426,10 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if (PAIR && !leader) mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA waits
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == ACC) {
         acc = 0;
         acc_phase ^= 1;
@@ -402,7 +439,12 @@ __global__ void __launch_bounds__(320, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem_base);
+  if (PAIR) {
+    cluster_sync();  // both CTAs done with TMEM and each other's barriers
+    if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+  } else if (warp == 1) {
+    tmem_dealloc<TMEM_COLS>(tmem_base);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -443,6 +485,36 @@ int make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld, int box_r
 }
 
 template <int BN, int STAGES, int EPI, bool FP16>
+int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
+                     cudaStream_t s) {
+  constexpr int ACC = BN <= 256 ? 2 : 1;
+  const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + (BN / 2) * BK * 2) +
+                      8 * (2 * STAGES + 2 * ACC) + 16 +
+                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD) ? 8 * 32 * 33 * sizeof(float)
+                                                                     : 0) +
+                      8 * 32 * 8 + kBiasMax * sizeof(float) + 16;
+  auto k = k_gemm<BN, STAGES, EPI, FP16, true>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * (g.N / BN);
+  const int pairs = tiles < moeb::num_sms() / 2 ? tiles : moeb::num_sms() / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, k, ta, tb, g) != cudaSuccess)
+    return moeb::check_launch("k_gemm (pair launch)");
+  return moeb::check_launch("k_gemm (pair)");
+}
+
+template <int BN, int STAGES, int EPI, bool FP16>
 int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
@@ -459,11 +531,21 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
   return moeb::check_launch("k_gemm");
 }
 
+// MOEB_GEMM_PAIR=0 disables the 2-SM tiles (single-CTA M = 128 tiles)
+bool pair_mode() {
+  const char* e = getenv("MOEB_GEMM_PAIR");
+  return !(e && e[0] == '0');
+}
+
 template <int EPI, bool FP16>
 int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn,
              cudaStream_t s) {
   if (bn == 512) return launch_gemm<512, 2, EPI, FP16>(ta, tb, g, s);
   if (bn == 256) {
+    if (pair_mode()) {  // 2-SM tiles (M = 256): B tile split across the CTA pair
+      if (EPI == EPI_RESID_ADD) return launch_gemm_pair<256, 4, EPI, FP16>(ta, tb, g, s);
+      return launch_gemm_pair<256, 5, EPI, FP16>(ta, tb, g, s);
+    }
     if (EPI == EPI_RESID_ADD) return launch_gemm<256, 3, EPI, FP16>(ta, tb, g, s);  // + transposes
     return launch_gemm<256, 4, EPI, FP16>(ta, tb, g, s);
   }
@@ -495,7 +577,9 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
   }
   CUtensorMap ta, tb;
   if (int rc = make_map(&ta, A, M, K, lda, BM, fp16)) return rc;
-  if (int rc = make_map(&tb, B, N, K, ldb, bn < 256 ? bn : 256, fp16)) return rc;
+  // pair tiles (dispatch, N-tile 256) load half of the B tile per CTA
+  const bool pair_b = bn == 256 && epi != EPI_RESID_LN && epi != EPI_ROWMAX && pair_mode();
+  if (int rc = make_map(&tb, B, N, K, ldb, pair_b ? 128 : (bn < 256 ? bn : 256), fp16)) return rc;
   GemmArgs g{M, N, K, bias, out32, out16, ld16, ln_w, ln_b, ln_eps, epi == EPI_ROWMAX ? 1 : 0};
   cudaStream_t s = moeb::as_stream(stream);
   switch (epi) {
