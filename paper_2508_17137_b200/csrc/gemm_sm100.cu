@@ -18,6 +18,7 @@
 // the mainloop of tile i+1.
 #include <cuda.h>
 #include <cstdlib>
+#include <cstring>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -72,7 +73,7 @@ __device__ __forceinline__ float gelu_erf(float x) {
 template <int BN, int STAGES, int EPI, bool FP16, bool PAIR = false>
 __global__ void __launch_bounds__(320, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const GemmArgs g) {
+           const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
   constexpr int ACC = BN <= 256 ? 2 : 1;           // TMEM accumulator buffers
   constexpr bool kTbuf = EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD;  // 32x33 transposes
   constexpr uint32_t TMEM_COLS = BN * ACC <= 32 ? 32 : BN * ACC;
@@ -106,6 +107,11 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t mis = smem_u32(sbias0) & 15u;
   float* sbias = sbias0 + (mis ? (16u - mis) / 4u : 0u);
   const bool bias_smem = g.bias != nullptr && g.N <= kBiasMax;
+  // 16-bit output staging for TMA stores: per epilogue warp two [32][32] boxes
+  constexpr bool kTmaOut =
+      PAIR && (EPI == EPI_BIAS || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS_GELU);
+  unsigned char* stg0 = reinterpret_cast<unsigned char*>(sbias + kBiasMax);
+  unsigned char* sstage = stg0 + ((128u - (smem_u32(stg0) & 127u)) & 127u);
   if (bias_smem)
     for (int i = threadIdx.x; i < g.N; i += blockDim.x) sbias[i] = __ldg(g.bias + i);
 
@@ -373,6 +379,7 @@ __global__ void __launch_bounds__(320, 1)
           __syncwarp();
         }
       } else {
+        unsigned char* wstage = sstage + ew * 4096;  // this warp's two 2 KB boxes
         for (int c0 = cb; c0 < cb + HC; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
@@ -392,7 +399,7 @@ __global__ void __launch_bounds__(320, 1)
             }
           }
           tmem_ld_wait();
-          if (!rv) continue;
+          if (!kTmaOut && !rv) continue;
           float v[32];
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -410,6 +417,29 @@ __global__ void __launch_bounds__(320, 1)
             float4* o = reinterpret_cast<float4*>(g.out32 + (int64_t)row * g.N + col);
 #pragma unroll
             for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else if (kTmaOut) {
+            // stage [32 rows][32 cols] 16-bit, then one TMA store per warp
+            // (rows past M are clipped by the tensor map)
+            const int buf = (c0 >> 5) & 1;
+            unsigned char* box = wstage + buf * 2048;
+            if (c0 - cb >= 64) {  // the box written two chunks ago has been read
+              if (lane == 0) bulk_wait_read<1>();
+              __syncwarp();
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint32_t w[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                w[u] = to16(v[8 * q + 2 * u], FP16) | ((uint32_t)to16(v[8 * q + 2 * u + 1], FP16) << 16);
+              *reinterpret_cast<uint4*>(box + lane * 64 + q * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmC, box, col, tm * TM + rank * BM + quarter * 32);
+              bulk_commit();
+            }
           } else {
             uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(g.out16) +
                                                 (int64_t)row * g.ld16 + col);
@@ -426,6 +456,10 @@ __global__ void __launch_bounds__(320, 1)
       }
       tc_fence_before();
       __syncwarp();
+      if (kTmaOut) {  // the next tile reuses this warp's staging boxes
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+      }
       if (lane == 0) {
         if (PAIR && !leader) mbar_arrive_cluster(&tempty[acc], 0);  // the leader's MMA waits
         else mbar_arrive(&tempty[acc]);
@@ -437,6 +471,7 @@ __global__ void __launch_bounds__(320, 1)
     }
   }
 
+  if (kTmaOut && warp >= 2 && lane == 0) bulk_wait<0>();  // stores complete before exit
   tc_fence_before();
   __syncthreads();
   if (PAIR) {
@@ -484,15 +519,34 @@ int make_map(CUtensorMap* m, const void* ptr, int rows, int K, int ld, int box_r
   return MOEB_OK;
 }
 
+// 16-bit output [rows][ld] (N columns), 32 x 32 boxes, no swizzle (TMA store)
+int make_out_map(CUtensorMap* m, const void* ptr, int rows, int N, int ld, bool fp16) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return moeb::fail(MOEB_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, fp16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return moeb::fail(MOEB_ECUDA, "cuTensorMapEncodeTiled (out) failed (%d)", (int)r);
+  return MOEB_OK;
+}
+
 template <int BN, int STAGES, int EPI, bool FP16>
-int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
-                     cudaStream_t s) {
+int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                     const GemmArgs& g, cudaStream_t s) {
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + (BN / 2) * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
                       ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD) ? 8 * 32 * 33 * sizeof(float)
                                                                      : 0) +
-                      8 * 32 * 8 + kBiasMax * sizeof(float) + 16;
+                      8 * 32 * 8 + kBiasMax * sizeof(float) + 16 +
+                      ((EPI == EPI_BIAS || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS_GELU)
+                           ? 8 * 4096 + 128
+                           : 0);
   auto k = k_gemm<BN, STAGES, EPI, FP16, true>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = ((g.M + 2 * BM - 1) / (2 * BM)) * (g.N / BN);
@@ -509,13 +563,14 @@ int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArg
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, k, ta, tb, g) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, k, ta, tb, tc, g) != cudaSuccess)
     return moeb::check_launch("k_gemm (pair launch)");
   return moeb::check_launch("k_gemm (pair)");
 }
 
 template <int BN, int STAGES, int EPI, bool FP16>
-int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, cudaStream_t s) {
+int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                const GemmArgs& g, cudaStream_t s) {
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
@@ -527,7 +582,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g,
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
   const int grid = tiles < moeb::num_sms() ? tiles : moeb::num_sms();
-  k<<<grid, 320, smem, s>>>(ta, tb, g);
+  k<<<grid, 320, smem, s>>>(ta, tb, tc, g);
   return moeb::check_launch("k_gemm");
 }
 
@@ -538,19 +593,20 @@ bool pair_mode() {
 }
 
 template <int EPI, bool FP16>
-int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& g, int bn,
+int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+             const GemmArgs& g, int bn,
              cudaStream_t s) {
-  if (bn == 512) return launch_gemm<512, 2, EPI, FP16>(ta, tb, g, s);
+  if (bn == 512) return launch_gemm<512, 2, EPI, FP16>(ta, tb, tc, g, s);
   if (bn == 256) {
     if (pair_mode()) {  // 2-SM tiles (M = 256): B tile split across the CTA pair
-      if (EPI == EPI_RESID_ADD) return launch_gemm_pair<256, 4, EPI, FP16>(ta, tb, g, s);
-      return launch_gemm_pair<256, 5, EPI, FP16>(ta, tb, g, s);
+      if (EPI == EPI_RESID_ADD) return launch_gemm_pair<256, 4, EPI, FP16>(ta, tb, tc, g, s);
+      return launch_gemm_pair<256, 5, EPI, FP16>(ta, tb, tc, g, s);
     }
-    if (EPI == EPI_RESID_ADD) return launch_gemm<256, 3, EPI, FP16>(ta, tb, g, s);  // + transposes
-    return launch_gemm<256, 4, EPI, FP16>(ta, tb, g, s);
+    if (EPI == EPI_RESID_ADD) return launch_gemm<256, 3, EPI, FP16>(ta, tb, tc, g, s);  // + transposes
+    return launch_gemm<256, 4, EPI, FP16>(ta, tb, tc, g, s);
   }
-  if (bn == 128) return launch_gemm<128, 6, EPI, FP16>(ta, tb, g, s);
-  return launch_gemm<64, 8, EPI, FP16>(ta, tb, g, s);
+  if (bn == 128) return launch_gemm<128, 6, EPI, FP16>(ta, tb, tc, g, s);
+  return launch_gemm<64, 8, EPI, FP16>(ta, tb, tc, g, s);
 }
 
 }  // namespace
@@ -575,20 +631,25 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
                  "missing output");
     MOEB_REQUIRE(epi != EPI_ROWMAX || (out32 && bn == 256), "row-max epilogue needs N % 256 == 0");
   }
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc;
   if (int rc = make_map(&ta, A, M, K, lda, BM, fp16)) return rc;
+  memset(&tc, 0, sizeof(tc));
+  const bool tma_out = epi >= EPI_BIAS && epi <= EPI_BIAS_GELU && bn == 256 && pair_mode();
+  if (tma_out) {  // 16-bit output tile stores by TMA (32 x 32 boxes)
+    if (int rc = make_out_map(&tc, out16, M, N, ld16, fp16)) return rc;
+  }
   // pair tiles (dispatch, N-tile 256) load half of the B tile per CTA
   const bool pair_b = bn == 256 && epi != EPI_RESID_LN && epi != EPI_ROWMAX && pair_mode();
   if (int rc = make_map(&tb, B, N, K, ldb, pair_b ? 128 : (bn < 256 ? bn : 256), fp16)) return rc;
   GemmArgs g{M, N, K, bias, out32, out16, ld16, ln_w, ln_b, ln_eps, epi == EPI_ROWMAX ? 1 : 0};
   cudaStream_t s = moeb::as_stream(stream);
   switch (epi) {
-    case EPI_F32: return fp16 ? dispatch<EPI_F32, true>(ta, tb, g, bn, s) : dispatch<EPI_F32, false>(ta, tb, g, bn, s);
-    case EPI_BIAS: return fp16 ? dispatch<EPI_BIAS, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS, false>(ta, tb, g, bn, s);
-    case EPI_BIAS_RELU: return fp16 ? dispatch<EPI_BIAS_RELU, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS_RELU, false>(ta, tb, g, bn, s);
-    case EPI_BIAS_GELU: return fp16 ? dispatch<EPI_BIAS_GELU, true>(ta, tb, g, bn, s) : dispatch<EPI_BIAS_GELU, false>(ta, tb, g, bn, s);
-    case EPI_RESID_ADD: return fp16 ? dispatch<EPI_RESID_ADD, true>(ta, tb, g, bn, s) : dispatch<EPI_RESID_ADD, false>(ta, tb, g, bn, s);
-    case EPI_ROWMAX: return fp16 ? launch_gemm<256, 4, EPI_ROWMAX, true>(ta, tb, g, s) : launch_gemm<256, 4, EPI_ROWMAX, false>(ta, tb, g, s);
-    default: return fp16 ? launch_gemm<512, 2, EPI_RESID_LN, true>(ta, tb, g, s) : launch_gemm<512, 2, EPI_RESID_LN, false>(ta, tb, g, s);
+    case EPI_F32: return fp16 ? dispatch<EPI_F32, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_F32, false>(ta, tb, tc, g, bn, s);
+    case EPI_BIAS: return fp16 ? dispatch<EPI_BIAS, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_BIAS, false>(ta, tb, tc, g, bn, s);
+    case EPI_BIAS_RELU: return fp16 ? dispatch<EPI_BIAS_RELU, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_BIAS_RELU, false>(ta, tb, tc, g, bn, s);
+    case EPI_BIAS_GELU: return fp16 ? dispatch<EPI_BIAS_GELU, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_BIAS_GELU, false>(ta, tb, tc, g, bn, s);
+    case EPI_RESID_ADD: return fp16 ? dispatch<EPI_RESID_ADD, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_RESID_ADD, false>(ta, tb, tc, g, bn, s);
+    case EPI_ROWMAX: return fp16 ? launch_gemm<256, 4, EPI_ROWMAX, true>(ta, tb, tc, g, s) : launch_gemm<256, 4, EPI_ROWMAX, false>(ta, tb, tc, g, s);
+    default: return fp16 ? launch_gemm<512, 2, EPI_RESID_LN, true>(ta, tb, tc, g, s) : launch_gemm<512, 2, EPI_RESID_LN, false>(ta, tb, tc, g, s);
   }
 }
