@@ -17,7 +17,7 @@ cap() {  # regex name skip
 cap "k_cache_sim_warp" k1 1
 cap "k_linear_predict" k3 1
 cap "k_window_attention_fa" attn 2
-cap "k_gemm<.int.256, .int.4, .int.2," gemm_ffn1 2
+cap "k_gemm<.int.256, .int.5, .int.2," gemm_ffn1 2
 cap "k_gemm<.int.256, .int.4, .int.6," gemm_resid 2
 cap "k_layernorm_rows" layernorm 2
 ls gpurun_out | grep $TAG
