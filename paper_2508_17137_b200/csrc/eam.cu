@@ -29,6 +29,7 @@
 namespace {
 
 constexpr int kSPT = 8;  // sketches per thread
+constexpr int kMaxK = 8;  // experts per row gathered together (more: sequential loop)
 
 __global__ void k_eam_norms(const double* __restrict__ sk, int S, int D, double* __restrict__ unit_t) {
   const int s = blockIdx.x;
@@ -151,13 +152,42 @@ __global__ void __launch_bounds__(256) k_eam_predict(
 #pragma unroll
       for (int w = 0; w < W; ++w) pred[r * W + w] = 0;
     }
-    // accumulate the row into the partial rEAM (core.py:182-194)
+    // accumulate the row into the partial rEAM (core.py:182-194). The
+    // row's experts are listed first so that all gathers are in flight
+    // together (one L2 round trip per row instead of one per expert); the
+    // sum keeps ascending expert order.
+    int exl[kMaxK];
+    int nk = 0;
+    if (W == 1) {  // registers: peel the lowest set bits in an unrolled sequence
+      uint64_t mm = tw[0];
+      nk = __popcll(mm);
+#pragma unroll
+      for (int i = 0; i < kMaxK; ++i) {
+        exl[i] = __ffsll((long long)mm) - 1;
+        mm &= mm - 1;
+      }
+    } else {
+      MOEB_FOR_EACH_BIT(W, tw, ex, {
+        if (nk < kMaxK) exl[nk] = ex;
+        ++nk;
+      })
+    }
 #pragma unroll
     for (int j = 0; j < kSPT; ++j) {
       const int s = tid + j * nt;
       if (s < S) {
         double g = 0.0;
-        MOEB_FOR_EACH_BIT(W, tw, ex, { g += __ldg(unit_t + (int64_t)(l * E + ex) * S + s); })
+        if (nk <= kMaxK) {
+          double gv[kMaxK];
+#pragma unroll
+          for (int i = 0; i < kMaxK; ++i)
+            gv[i] = i < nk ? __ldg(unit_t + (int64_t)(l * E + exl[i]) * S + s) : 0.0;
+#pragma unroll
+          for (int i = 0; i < kMaxK; ++i)
+            if (i < nk) g += gv[i];
+        } else {
+          MOEB_FOR_EACH_BIT(W, tw, ex, { g += __ldg(unit_t + (int64_t)(l * E + ex) * S + s); })
+        }
         const double dold = d[l * S + s];
         const double dnew = dold + g;
         d[l * S + s] = dnew;
