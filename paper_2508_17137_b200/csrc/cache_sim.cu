@@ -772,8 +772,13 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   const int hl = lane & (G - 1), gbase = lane - hl;
   const unsigned glow = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
   const unsigned gmask = glow << gbase;
-  unsigned int* bcnt = reinterpret_cast<unsigned int*>(smem);  // [3L] block counters
-  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x) bcnt[j] = 0;
+  // block per-layer counters: [L] u64 (activations | cache hits << 32), [L] u32 prediction hits
+  unsigned long long* bkc = reinterpret_cast<unsigned long long*>(smem);
+  unsigned int* bph = reinterpret_cast<unsigned int*>(bkc + L);
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    bkc[j] = 0;
+    bph[j] = 0;
+  }
   __syncthreads();
   const int pi = blockIdx.y;
   const int sims_per_block = nw * (32 / G);
@@ -848,22 +853,27 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         K[w] = measured ? P[w] : 0ull;
         npk += __popcll(K[w]);
       }
-      if (npk > limit) keep_lowest<W>(K, limit);
+      if (npk > limit) {
+        keep_lowest<W>(K, limit);
+        npk = limit;  // = popc(K)
+      }
       uint64_t Rl[W], S[W], Hm[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         Rl[w] = R[l * W + w];
         S[w] = K[w] | T[w];
       }
-      int m = 0, refresh = 0;
+      // inserts m = |K \ R| + |T \ (R | K)| = |S \ R|; refreshed = |S & R| = ns - m
+      int m = 0, ns = 0;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        m += __popcll(K[w] & ~Rl[w]) + __popcll(T[w] & ~(Rl[w] | K[w]));
-        refresh += __popcll(S[w] & Rl[w]);
+        m += __popcll(S[w] & ~Rl[w]);
+        ns += __popcll(S[w]);
         Hm[w] = T[w] & (Rl[w] | K[w]);
       }
+      const int refresh = ns - m;
       const int e = st.count + m - st.cap > 0 ? st.count + m - st.cap : 0;
-      bool fallback = (st.cap <= popc_w<W>(K)) || (e > st.count - refresh);
+      bool fallback = (st.cap <= npk) || (e > st.count - refresh);
       // first victim window: all lanes of the warp, converged (full-mask votes)
       uint32_t newhead = st.head;
       bool applied = false;
@@ -948,7 +958,6 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         }
         st.head = newhead;
         st.count += m - e;
-        const int ns = popc_w<W>(S);
         if (st.tail - st.head + (uint32_t)ns > qmask + 1) {  // group compaction
           __syncwarp(gmask);
           uint32_t n = st.head;
@@ -1047,9 +1056,8 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         tot_ch += ch;
         tot_ph += ph;
         if (hl == 0) {  // per-layer counters: fire-and-forget shared-memory reductions
-          atomicAdd(&bcnt[l], (unsigned)k);
-          atomicAdd(&bcnt[L + l], (unsigned)ch);
-          atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
+          atomicAdd(&bkc[l], (unsigned long long)k | ((unsigned long long)ch << 32));
+          atomicAdd(&bph[l], (unsigned)ph);
         }
       }
       if (++l == L) {
@@ -1074,8 +1082,12 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   }
   __syncthreads();
   int64_t* c = a.counters + pi * a.counters_stride;
-  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x)
-    if (bcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bcnt[j]);
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    const unsigned long long kc = bkc[j];
+    if (kc & 0xffffffffull) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), kc & 0xffffffffull);
+    if (kc >> 32) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + L + j), kc >> 32);
+    if (bph[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + 2 * L + j), (unsigned long long)bph[j]);
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -50,6 +50,11 @@ __device__ __forceinline__ void vc_drain(uint64_t (&va)[kPlanes], uint64_t (&vb)
   for (int i = 0; i < kPlanes; ++i) va[i] = vb[i] = vc[i] = 0;
 }
 
+// Row-balanced: the trace's rows are split into equal ranges of 32-row chunks,
+// one range per warp (prompt lengths do not matter), and every lane keeps
+// four chunk loads in flight. A row is measured if it lies at or past its
+// prompt's warm-up rows; each lane tracks its prompt boundary incrementally.
+constexpr int kMetDepth = 4;
 __global__ void __launch_bounds__(256) k_metrics64(const uint64_t* __restrict__ pred,
                                                    const uint64_t* __restrict__ truth,
                                                    const int64_t* __restrict__ row_off, int P,
@@ -58,25 +63,56 @@ __global__ void __launch_bounds__(256) k_metrics64(const uint64_t* __restrict__ 
   for (int i = threadIdx.x; i < 3 * E + 3; i += blockDim.x) scnt[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t rbeg = row_off[0], rend = row_off[P];
+  const int64_t chunks = (rend - rbeg + 31) >> 5;
+  const int64_t c0 = chunks * w / nw, c1 = chunks * (w + 1) / nw;
+  const int64_t skip = (int64_t)warmup * L;
   uint64_t va[kPlanes], vb[kPlanes], vc[kPlanes];
 #pragma unroll
   for (int i = 0; i < kPlanes; ++i) va[i] = vb[i] = vc[i] = 0;
   uint32_t tp[2] = {0, 0}, fp[2] = {0, 0}, fn[2] = {0, 0};
   uint64_t npos = 0, nexact = 0, nlabel = 0;
   int pending = 0;  // rows per lane since the last drain (warp-uniform)
-  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P; p += warps) {
-    const int64_t r0 = row_off[p] + (int64_t)warmup * L, r1 = row_off[p + 1];
-    for (int64_t base = r0; base < r1; base += 32) {
-      const int64_t r = base + lane;
-      const bool m = r < r1;
-      const uint64_t pw = m ? __ldg(pred + r) : 0ull, tw = m ? __ldg(truth + r) : 0ull;
-      vc_add(va, pw & tw);
-      vc_add(vb, pw & ~tw);
-      vc_add(vc, tw & ~pw);
+  // this lane's prompt: the last p with row_off[p] <= first row
+  int pl = 0;
+  {
+    const int64_t r = rbeg + c0 * 32 + lane;
+    int lo = 0, hi = P - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (row_off[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    pl = lo;
+  }
+  int64_t mstart = row_off[pl] + skip, nb = row_off[pl + 1];
+  for (int64_t c = c0; c < c1; c += kMetDepth) {
+    uint64_t pw[kMetDepth], tw[kMetDepth];
+#pragma unroll
+    for (int u = 0; u < kMetDepth; ++u) {
+      const int64_t r = rbeg + (c + u) * 32 + lane;
+      const bool in = c + u < c1 && r < rend;
+      pw[u] = in ? __ldg(pred + r) : 0ull;
+      tw[u] = in ? __ldg(truth + r) : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < kMetDepth; ++u) {
+      const int64_t r = rbeg + (c + u) * 32 + lane;
+      const bool in = c + u < c1 && r < rend;
+      while (in && r >= nb) {  // crossed into the next prompt(s)
+        ++pl;
+        mstart = nb + skip;
+        nb = row_off[pl + 1];
+      }
+      const bool m = in && r >= mstart;
+      const uint64_t p = m ? pw[u] : 0ull, t = m ? tw[u] : 0ull;
+      vc_add(va, p & t);
+      vc_add(vb, p & ~t);
+      vc_add(vc, t & ~p);
       npos += m;
-      nexact += m && pw == tw;
-      nlabel += m ? (uint64_t)(E - __popcll(pw ^ tw)) : 0;
+      nexact += m && p == t;
+      nlabel += m ? (uint64_t)(E - __popcll(p ^ t)) : 0;
       if (++pending == (1 << kPlanes) - 1) {
         vc_drain(va, vb, vc, lane, tp, fp, fn);
         pending = 0;
@@ -289,9 +325,8 @@ extern "C" int moeb_metrics(const uint64_t* pred, const uint64_t* truth,
   const int W = moeb::words_for(E);
   const int threads = 256;
   cudaStream_t s = moeb::as_stream(stream);
-  if (W == 1) {  // persistent bit-sliced kernel: 4 CTAs per SM at most
-    int blocks = (int)((n_prompts + 7) / 8);
-    blocks = blocks < 4 * moeb::num_sms() ? blocks : 4 * moeb::num_sms();
+  if (W == 1) {  // persistent bit-sliced kernel: 4 CTAs per SM, equal row ranges per warp
+    const int blocks = 4 * moeb::num_sms();
     k_metrics64<<<blocks, threads, 0, s>>>(pred, truth, prompt_row_off, n_prompts, L, E,
                                            warmup_tokens, metrics);
     return moeb::check_launch("k_metrics64");
