@@ -344,6 +344,16 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms2 = float(t.item())
     e2e_value = tokens_per_rank * world / (ms2 / 1000.0) * args.steps
+    if os.environ.get("MOEB_E2E_DEBUG"):  # per-batch compute spans of one more e2e run
+        tl = []
+        s3 = ev()
+        s3.record(stream)
+        sr.run(pred, [cap], WARMUP_TOKENS, BUDGET, [truth_host] * args.steps, metrics=True,
+               timing=tl)
+        torch.cuda.synchronize()
+        print("e2e batches (start ms, compute ms):",
+              [(round(s3.elapsed_time(a), 2), round(a.elapsed_time(b), 2)) for a, b in tl],
+              file=sys.stderr)
     if world == 1:
         assert np.array_equal(res2[-1][0].numpy().reshape(-1), counters.cpu().numpy().reshape(-1))
 

@@ -290,14 +290,17 @@ class StreamingReplay:
     copy runs on a copy stream while batch i is predicted and replayed on the
     compute stream, and each batch's counters (plus fused prediction
     metrics) go back to pinned host memory asynchronously. Throughput is
-    max(copy, compute) per batch instead of their sum.
+    max(copy, compute) per batch instead of their sum. The first batch has no
+    compute to hide its copy behind, so it is copied in ``first_chunks``
+    row-balanced prompt ranges and the predictor starts on each range as it
+    lands (the replay needs the whole batch's masks).
 
     ``run`` returns, per batch, pinned host tensors (counters [C][4+3L],
     metrics [3E+3] or None), valid after ``torch.cuda.synchronize()`` (or the
     returned event)."""
 
     def __init__(self, shape: ModelShape, row_off_host: np.ndarray, prompt_ids, device=None,
-                 token_ids=None):
+                 token_ids=None, first_chunks: int = 4):
         dev = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self.shape = shape
@@ -311,6 +314,11 @@ class StreamingReplay:
         self.s_copy = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev)
         self.device = dev
+        P = len(prompt_ids)
+        n = max(1, min(int(first_chunks), P))
+        cuts = np.searchsorted(self.bufs[0].row_off_host, np.arange(1, n) * (rows / n))
+        b = sorted(set([0] + [int(c) for c in cuts] + [P]))
+        self.first_views = [self.bufs[0].select(lo, hi) for lo, hi in zip(b[:-1], b[1:]) if hi > lo]
 
     @property
     def rows(self) -> int:
@@ -330,20 +338,41 @@ class StreamingReplay:
         for i, hb in enumerate(host_batches):
             b = i % 2
             buf = self.bufs[b]
+            empty = getattr(predictor, "empty", False) and not metrics
+            split = i == 0 and len(self.first_views) > 1 and not empty
+            parts = []
             with torch.cuda.stream(self.s_copy):
                 if freed[b] is not None:
                     self.s_copy.wait_event(freed[b])
-                buf.truth.copy_(hb, non_blocking=True)
+                if split:  # first batch: copy range by range, predict as each lands
+                    r0 = 0
+                    for v in self.first_views:
+                        r1 = r0 + v.rows
+                        v.truth.copy_(hb[r0:r1], non_blocking=True)
+                        e = torch.cuda.Event()
+                        e.record(self.s_copy)
+                        parts.append(e)
+                        r0 = r1
+                else:
+                    buf.truth.copy_(hb, non_blocking=True)
                 copied[b].record(self.s_copy)
             with torch.cuda.stream(self.s_comp):
-                self.s_comp.wait_event(copied[b])
+                if not split:
+                    self.s_comp.wait_event(copied[b])
                 if timing is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(self.s_comp)
                 vec = (torch.zeros(3 * E + 3, dtype=torch.int64, device=dev)
                        if metrics else None)
-                if getattr(predictor, "empty", False) and vec is None:
+                if empty:
                     masks, cov = None, None
+                elif split:
+                    pieces = []
+                    for v, e in zip(self.first_views, parts):
+                        self.s_comp.wait_event(e)
+                        pieces.append(predictor.predict_masks(v, budget, warmup, metrics=vec))
+                    masks = torch.cat(pieces)
+                    cov = predictor.coverage(buf)
                 else:
                     masks = predictor.predict_masks(buf, budget, warmup, metrics=vec)
                     cov = predictor.coverage(buf)
