@@ -213,7 +213,8 @@ class PipelinedReplay:
         dev = packed.device
         self.s_copy = torch.cuda.Stream(dev)
         self.s_pred = torch.cuda.Stream(dev)
-        self.s_sim = torch.cuda.Stream(dev)
+        self.s_sim = torch.cuda.Stream(dev, priority=-1)
+        self.s_met = torch.cuda.Stream(dev, priority=0)
 
     def host_offsets(self):
         """Pinned host copies of each chunk's rebased row offsets (copied with
@@ -240,7 +241,7 @@ class PipelinedReplay:
         if counters is None:
             counters = torch.zeros((1, len(capacities), 4 + 3 * shape.num_layers),
                                    dtype=torch.int64, device=packed.device)
-        for s in (self.s_copy, self.s_pred, self.s_sim):
+        for s in (self.s_copy, self.s_pred, self.s_sim, self.s_met):
             s.wait_stream(main)
         unbounded = bool(getattr(predictor, "unbounded_prefetch", False))
         for ci, ((a, b), view) in enumerate(zip(self.bounds, self.views)):
@@ -258,12 +259,14 @@ class PipelinedReplay:
                     if ev:
                         e0, e1 = ev(), ev()
                         e0.record(self.s_pred)
-                    masks = predictor.predict_masks(view, budget, warmup, metrics=metrics)
+                    masks = predictor.predict_masks(view, budget, warmup)
                     if ev:
                         e1.record(self.s_pred)
                         timing.append(("predict", e0, e1, view.rows))
                     cov = predictor.coverage(view)
-            self.s_sim.wait_stream(self.s_pred)
+            masks_ready = torch.cuda.Event()
+            masks_ready.record(self.s_pred)
+            self.s_sim.wait_event(masks_ready)
             for t in (masks, cov):
                 if t is not None:
                     t.record_stream(self.s_sim)
@@ -276,12 +279,28 @@ class PipelinedReplay:
                 if ev:
                     e3.record(self.s_sim)
                     timing.append(("replay", e2, e3, view.rows))
+            if metrics is not None and masks is not None:
+                _overlapped_metrics(self.s_met, masks_ready, masks, view, warmup, metrics)
         main.wait_stream(self.s_sim)
         main.wait_stream(self.s_pred)
+        main.wait_stream(self.s_met)
         counters.record_stream(self.s_sim)
         if metrics is not None:
-            metrics.record_stream(self.s_pred)
+            metrics.record_stream(self.s_met)
         return counters
+
+
+def _overlapped_metrics(s_met, masks_ready, masks, view, warmup, out):
+    """K7 on a low-priority stream, issued after the replay (K1) launch on the
+    high-priority one: K1's blocks are placed first (one resident wave), and
+    the HBM-streaming metrics pass fills the resources they leave free
+    instead of running between the predictor and the replay."""
+    s_met.wait_event(masks_ready)
+    masks.record_stream(s_met)
+    view.truth.record_stream(s_met)
+    with torch.cuda.stream(s_met):
+        mask_metrics(masks, view.truth, view.row_off, view.shape.num_layers,
+                     view.shape.num_experts, warmup, out=out)
 
 
 class StreamingReplay:
@@ -312,7 +331,8 @@ class StreamingReplay:
                                   np.asarray(prompt_ids, dtype=np.int64), token_ids)
                      for _ in range(2)]
         self.s_copy = torch.cuda.Stream(dev)
-        self.s_comp = torch.cuda.Stream(dev)
+        self.s_comp = torch.cuda.Stream(dev, priority=-1)
+        self.s_met = torch.cuda.Stream(dev, priority=0)
         self.device = dev
         P = len(prompt_ids)
         n = max(1, min(int(first_chunks), P))
@@ -331,6 +351,7 @@ class StreamingReplay:
         main = torch.cuda.current_stream(dev)
         self.s_copy.wait_stream(main)
         self.s_comp.wait_stream(main)
+        self.s_met.wait_stream(main)
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         freed = [None, None]
         out = []
@@ -370,15 +391,22 @@ class StreamingReplay:
                     pieces = []
                     for v, e in zip(self.first_views, parts):
                         self.s_comp.wait_event(e)
-                        pieces.append(predictor.predict_masks(v, budget, warmup, metrics=vec))
+                        pieces.append(predictor.predict_masks(v, budget, warmup))
                     masks = torch.cat(pieces)
                     cov = predictor.coverage(buf)
                 else:
-                    masks = predictor.predict_masks(buf, budget, warmup, metrics=vec)
+                    masks = predictor.predict_masks(buf, budget, warmup)
                     cov = predictor.coverage(buf)
+                masks_ready = torch.cuda.Event()
+                masks_ready.record(self.s_comp)
                 cnt, _, _ = cache_replay(buf, [(masks, cov, unbounded)], capacities, warmup,
                                          budget, policy, want_per_prompt=False)
                 ev = torch.cuda.Event()
+                if vec is not None and masks is not None:
+                    _overlapped_metrics(self.s_met, masks_ready, masks, buf, warmup, vec)
+                    # the metrics run beside the replay; both end before the
+                    # buffer is refilled or the vector read back
+                    self.s_comp.wait_stream(self.s_met)
                 ev.record(self.s_comp)
                 freed[b] = ev
                 c_h = torch.empty((len(capacities), 4 + 3 * L), dtype=torch.int64,
@@ -395,6 +423,7 @@ class StreamingReplay:
                 out.append((c_h, v_h))
         main.wait_stream(self.s_comp)
         main.wait_stream(self.s_copy)
+        main.wait_stream(self.s_met)
         return out
 
 
