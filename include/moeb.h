@@ -77,6 +77,7 @@ int moeb_device_check(void);
  *                   measured_accesses, cache_hits, prediction_hits, uncovered
  *  hit_masks        [n_preds][n_caps][rows][W] (nullable): bit e set iff the
  *                   touch of truth expert e hit (warm-up rows included)
+ *  Limit: every prompt has fewer than 2^31 - 64 rows (the caller checks).
  */
 int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* preds,
                    const uint8_t* const* covered, const int32_t* unbounded, int n_preds,

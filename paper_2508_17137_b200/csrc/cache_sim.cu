@@ -772,13 +772,8 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   const int hl = lane & (G - 1), gbase = lane - hl;
   const unsigned glow = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
   const unsigned gmask = glow << gbase;
-  // block per-layer counters: [L] u64 (activations | cache hits << 32), [L] u32 prediction hits
-  unsigned long long* bkc = reinterpret_cast<unsigned long long*>(smem);
-  unsigned int* bph = reinterpret_cast<unsigned int*>(bkc + L);
-  for (int j = threadIdx.x; j < L; j += blockDim.x) {
-    bkc[j] = 0;
-    bph[j] = 0;
-  }
+  unsigned int* bcnt = reinterpret_cast<unsigned int*>(smem);  // [3L] block counters
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x) bcnt[j] = 0;
   __syncthreads();
   const int pi = blockIdx.y;
   const int sims_per_block = nw * (32 / G);
@@ -804,13 +799,11 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     const int limit = unbounded ? E : a.budget;
     uint64_t* hits = (EXTRA && a.hits) ? a.hits + pi * a.hits_stride : nullptr;
     const int64_t r0 = live ? a.row_off[p] : 0;
-    const int64_t nrows = live ? a.row_off[p + 1] - r0 : 0;
-    int64_t nmax = nrows;
+    // rows per prompt < 2^31 - 64 (checked by the host wrapper): 32-bit row loop
+    const int nrows = live ? (int)(a.row_off[p + 1] - r0) : 0;
+    int nmax = nrows;
 #pragma unroll
-    for (int o = G; o < 32; o <<= 1) {
-      const int64_t other = __shfl_xor_sync(FULL, nmax, o);
-      nmax = other > nmax ? other : nmax;
-    }
+    for (int o = G; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(FULL, nmax, o));
     const uint64_t* __restrict__ tr = a.truth + r0 * W;
     const uint64_t* __restrict__ pr = pred ? pred + r0 * W : nullptr;
     int tot_k = 0, tot_ch = 0, tot_ph = 0, tot_unc = 0;
@@ -823,14 +816,14 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       wp[w] = (pr && hl < nrows) ? __ldg(pr + (int64_t)hl * W + w) : 0ull;
     }
     int l = 0, t = 0;
-    for (int64_t i = 0; i < nmax; ++i) {
-      const int slot = (int)(i & (G - 1));
+    for (int i = 0; i < nmax; ++i) {
+      const int slot = i & (G - 1);
       if (slot == 0) {  // prefetch the next window
-        const int64_t j = i + G + hl;
+        const int j = i + G + hl;
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-          nt[w] = j < nrows ? __ldg(tr + j * W + w) : 0ull;
-          np[w] = (pr && j < nrows) ? __ldg(pr + j * W + w) : 0ull;
+          nt[w] = j < nrows ? __ldg(tr + (int64_t)j * W + w) : 0ull;
+          np[w] = (pr && j < nrows) ? __ldg(pr + (int64_t)j * W + w) : 0ull;
         }
       }
       uint64_t T[W], P[W], K[W];
@@ -1056,8 +1049,9 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         tot_ch += ch;
         tot_ph += ph;
         if (hl == 0) {  // per-layer counters: fire-and-forget shared-memory reductions
-          atomicAdd(&bkc[l], (unsigned long long)k | ((unsigned long long)ch << 32));
-          atomicAdd(&bph[l], (unsigned)ph);
+          atomicAdd(&bcnt[l], (unsigned)k);  // native 32-bit shared atomics (a
+          atomicAdd(&bcnt[L + l], (unsigned)ch);  // 64-bit one is a CAS loop)
+          atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
         }
       }
       if (++l == L) {
@@ -1082,12 +1076,8 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   }
   __syncthreads();
   int64_t* c = a.counters + pi * a.counters_stride;
-  for (int j = threadIdx.x; j < L; j += blockDim.x) {
-    const unsigned long long kc = bkc[j];
-    if (kc & 0xffffffffull) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), kc & 0xffffffffull);
-    if (kc >> 32) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + L + j), kc >> 32);
-    if (bph[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + 2 * L + j), (unsigned long long)bph[j]);
-  }
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x)
+    if (bcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bcnt[j]);
 }
 
 // ---------------------------------------------------------------------------

@@ -17,7 +17,7 @@ import torch
 
 from . import _native as nat
 from .cache import POLICIES, CacheConfig
-from .core import ConfigError, ModelShape
+from .core import ConfigError, ModelShape, RangeError
 from .metrics import MetricCounts, mask_metrics, metric_vector
 from .traces import PackedTraces, pack_traces
 
@@ -140,6 +140,8 @@ def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget:
     L = shape.num_layers
     n, C, P = len(streams), len(capacities), packed.num_prompts
     dev = packed.device
+    if P and int(np.max(np.diff(packed.row_off_host))) >= 2**31 - 64:
+        raise RangeError("a prompt has >= 2^31 - 64 trace rows (cache replay limit)")
     if counters is None:
         counters = torch.zeros((n, C, 4 + 3 * L), dtype=torch.int64, device=dev)
     elif tuple(counters.shape) != (n, C, 4 + 3 * L) or counters.dtype != torch.int64:
