@@ -871,24 +871,22 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
       uint32_t newhead = st.head;
       bool applied = false;
       {
-        const bool want = !fallback && e > 0;
+        // branch-free (bitwise &, unconditional key decode): the vote chain
+        // below is the row's critical path
+        const bool want = !fallback & (e > 0);
         const uint32_t idx = st.head + hl;
         const bool inr = (uint32_t)hl < st.tail - st.head;
         const int key = q[idx & qmask];
         const bool valid = inr && pos_of[key] == (uint16_t)idx;
         const unsigned vb = (__ballot_sync(FULL, valid) >> gbase) & glow;
-        const bool ok1 = want && __popc(vb) >= e;
-        const bool victim = ok1 && valid && __popc(vb & ((1u << hl) - 1)) < e;
-        int vl = 0, ve = 0;
-        bool bad = false;
-        if (victim) {
-          vl = st.layer_of(key);
-          ve = st.expert_of(key, vl);
-          bad = vl == l && ((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull);
-        }
+        const bool ok1 = want & (__popc(vb) >= e);
+        const bool victim = ok1 & valid & (__popc(vb & ((1u << hl) - 1)) < e);
+        const int vl = st.layer_of(key);
+        const int ve = st.expert_of(key, vl);
+        const bool bad = victim & (vl == l) & (((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull) != 0);
         const bool anybad = ((__ballot_sync(FULL, bad) >> gbase) & glow) != 0u;
-        if (ok1 && anybad) fallback = true;
-        applied = ok1 && !anybad;
+        if (ok1 & anybad) fallback = true;
+        applied = ok1 & !anybad;
         if (applied && victim) {
           pos_of[key] = (uint16_t)(idx + 0x8000u);
           atomicAnd(reinterpret_cast<unsigned int*>(R + vl * W + (ve >> 6)) + ((ve >> 5) & 1),
@@ -993,13 +991,16 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
           }
         }
         st.tail += ns;
-        __syncwarp(gmask);
+        // R_l |= S as shared atomics: on this path no victim is in S, so the
+        // victims' atomicAnd and this OR commute and need no barrier between
         if (hl < W) {
           uint64_t v = 0;
 #pragma unroll
           for (int w = 0; w < W; ++w)
-            if (w == hl) v = R[l * W + w] | S[w];
-          R[l * W + hl] = v;
+            if (w == hl) v = S[w];
+          unsigned int* rw = reinterpret_cast<unsigned int*>(R + l * W + hl);
+          if ((uint32_t)v) atomicOr(rw, (uint32_t)v);
+          if ((uint32_t)(v >> 32)) atomicOr(rw + 1, (uint32_t)(v >> 32));
         }
         __syncwarp(gmask);
         ch = popc_w<W>(Hm);
