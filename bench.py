@@ -80,7 +80,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "20"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -329,7 +329,10 @@ def run_ours(args):
             return buf.cpu()
         return res
 
-    e2e_run(max(1, args.warmup))
+    # warm-up with as many batches as the timed run, so the pinned host
+    # buffers the batches read back into come from the caching host allocator
+    # (a cudaHostAlloc inside the timed region stalls the pipeline)
+    e2e_run(max(args.steps, args.warmup))
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()

@@ -357,6 +357,12 @@ class StreamingReplay:
         copied = [torch.cuda.Event(), torch.cuda.Event()]
         freed = [None, None]
         out = []
+        host_batches = list(host_batches)
+        # every batch's pinned read-back buffers up front, before any work is
+        # enqueued (a host allocation between launches would stall the pipeline)
+        outs = [(torch.empty((len(capacities), 4 + 3 * L), dtype=torch.int64, pin_memory=True),
+                 torch.empty(3 * E + 3, dtype=torch.int64, pin_memory=True) if metrics else None)
+                for _ in host_batches]
         unbounded = bool(getattr(predictor, "unbounded_prefetch", False))
         for i, hb in enumerate(host_batches):
             b = i % 2
@@ -411,12 +417,9 @@ class StreamingReplay:
                     self.s_comp.wait_stream(self.s_met)
                 ev.record(self.s_comp)
                 freed[b] = ev
-                c_h = torch.empty((len(capacities), 4 + 3 * L), dtype=torch.int64,
-                                  pin_memory=True)
+                c_h, v_h = outs[i]
                 c_h.copy_(cnt[0], non_blocking=True)
-                v_h = None
                 if vec is not None:
-                    v_h = torch.empty(3 * E + 3, dtype=torch.int64, pin_memory=True)
                     v_h.copy_(vec, non_blocking=True)
                 if timing is not None:
                     e1 = torch.cuda.Event(enable_timing=True)
