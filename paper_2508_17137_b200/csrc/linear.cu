@@ -196,8 +196,19 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
           uint32_t wk = bk;
           bool wf = found;
           int wq = q;
+          if (TPS == 2) {
+            // one shuffle: real keys are >= 0x000fffe0 (order_key of -inf),
+            // so 0 encodes "none found", and the partner's part is q ^ 1
+            const uint32_t kk = found ? bk : 0u;
+            const uint32_t ok = __shfl_xor_sync(0xffffffffu, kk, 1);
+            const bool take = ok > kk || (ok == kk && q == 1);
+            wk = take ? ok : kk;
+            wq = take ? (q ^ 1) : q;
+            wf = wk != 0u;
+          } else {
 #pragma unroll
-          for (int o = 1; o < TPS; o <<= 1) combine(wk, wf, wq, o);
+            for (int o = 1; o < TPS; o <<= 1) combine(wk, wf, wq, o);
+          }
           if (it < k) {
             const int wrot = ((lane & ~(TPS - 1)) | wq) & 7;
             pm |= 1ull << slot_expert<NS>((int)(wk & (NS - 1)), wq, wrot);
