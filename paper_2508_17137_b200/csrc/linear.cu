@@ -97,7 +97,9 @@ __device__ __forceinline__ void combine(uint32_t& k, bool& f, int& q, int o) {
   q = take ? oq : q;
 }
 
-template <int TPS, bool FULL>  // FULL: E == 64, no per-expert bounds checks
+// FULL: E == 64, no per-expert bounds checks. KT > 0: the budget is KT
+// (compile-time: the k + 1 selection passes unroll into straight-line code)
+template <int TPS, bool FULL, int KT>
 __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(const LinArgs a) {
   using C = K3Cfg<TPS>;
   constexpr int NS = C::NS, NU = C::kUnits, HALF = NS / 2;
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
   const int rot = lane & 7;
   const unsigned grp = ((1u << TPS) - 1) << (lane & ~(TPS - 1));
   const double NEG = -__longlong_as_double(0x7ff0000000000000LL);
-  const int k = a.budget < E ? a.budget : E;
+  const int k = KT > 0 ? KT : (a.budget < E ? a.budget : E);
   const int64_t n_streams = (int64_t)a.L * a.P;
 
   for (int64_t gbase = (int64_t)blockIdx.x * C::kStreams; gbase < n_streams;
@@ -177,7 +179,8 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
         for (int s = 0; s < NS; ++s) key[s] = order_key<NS>(z[s], s);
         uint32_t kth = 0, bound = 0;
         bool amb = false;
-        for (int it = 0; it <= k; ++it) {
+#pragma unroll
+        for (int it = 0; it <= (KT > 0 ? KT : k); ++it) {
           uint32_t bk;
           bool found;
           if (it == 0) {
@@ -284,7 +287,11 @@ int launch_k3(const LinArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(double2) * (size_t)(a.E + a.L) * TPS * C::kUnits;
   if ((int)smem > moeb::max_smem_per_block())
     return moeb::fail(MOEB_ESMEM, "learned_linear tables need %zu B of shared memory", smem);
-  auto kern = a.E == 64 ? k_linear_predict<TPS, true> : k_linear_predict<TPS, false>;
+  const int kb = a.budget < a.E ? a.budget : a.E;
+  auto kern = a.E == 64 ? (kb == 6 ? k_linear_predict<TPS, true, 6>
+                                   : kb == 8 ? k_linear_predict<TPS, true, 8>
+                                             : k_linear_predict<TPS, true, 0>)
+                        : k_linear_predict<TPS, false, 0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   // persistent: at most 2 CTAs per SM, each looping over groups of kStreams streams
   const int64_t groups = ((int64_t)a.L * a.P + C::kStreams - 1) / C::kStreams;
