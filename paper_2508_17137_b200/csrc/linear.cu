@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
   const int L = a.L, E = a.E, F = a.L + a.E + 1;
   double2* colT = reinterpret_cast<double2*>(smem_raw);  // [E][TPS][NU]: W[j][L+e] pairs
   double2* bias2 = colT + E * TPS * NU;                  // [L][TPS][NU]: (1 - decay) b_l
+  double2* zcol = bias2 + L * TPS * NU;                  // [TPS][NU] zeros (odd pair tail)
   for (int i = threadIdx.x; i < E * TPS * NU; i += blockDim.x) {
     const int e = i / (TPS * NU), j0 = NS * ((i / NU) % TPS) + 2 * (i % HALF);
     colT[i] = make_double2(j0 < E ? a.Wt[(int64_t)j0 * F + L + e] : 0.0,
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
     }
     bias2[i] = make_double2(b[0], b[1]);
   }
+  for (int i = threadIdx.x; i < TPS * NU; i += blockDim.x) zcol[i] = make_double2(0.0, 0.0);
   __syncthreads();
 
   const unsigned full = 0xffffffffu;
@@ -264,16 +266,24 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
           z[2 * j] = fma(a.decay, z[2 * j], v.x);
           z[2 * j + 1] = fma(a.decay, z[2 * j + 1], v.y);
         }
+        // two fired experts per trip (ascending, so the additions round
+        // exactly as one at a time); an odd last one pairs with a zero column
         uint64_t mm = tw;
         while (mm) {
-          const int ex = __ffsll((long long)mm) - 1;
+          const int ex0 = __ffsll((long long)mm) - 1;
           mm &= mm - 1;
-          const double2* col = colT + (ex * TPS + q) * NU + rot;
+          const double2* c0 = colT + (ex0 * TPS + q) * NU + rot;
+          const double2* c1 = zcol + q * NU + rot;
+          if (mm) {
+            const int ex1 = __ffsll((long long)mm) - 1;
+            mm &= mm - 1;
+            c1 = colT + (ex1 * TPS + q) * NU + rot;
+          }
 #pragma unroll
           for (int j = 0; j < HALF; ++j) {
-            const double2 v = col[j];
-            z[2 * j] += v.x;
-            z[2 * j + 1] += v.y;
+            const double2 v0 = c0[j], v1 = c1[j];
+            z[2 * j] = (z[2 * j] + v0.x) + v1.x;
+            z[2 * j + 1] = (z[2 * j + 1] + v0.y) + v1.y;
           }
         }
       }
@@ -284,7 +294,7 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
 template <int TPS>
 int launch_k3(const LinArgs& a, cudaStream_t s) {
   using C = K3Cfg<TPS>;
-  const size_t smem = sizeof(double2) * (size_t)(a.E + a.L) * TPS * C::kUnits;
+  const size_t smem = sizeof(double2) * (size_t)(a.E + a.L + 1) * TPS * C::kUnits;
   if ((int)smem > moeb::max_smem_per_block())
     return moeb::fail(MOEB_ESMEM, "learned_linear tables need %zu B of shared memory", smem);
   const int kb = a.budget < a.E ? a.budget : a.E;
