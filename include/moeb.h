@@ -87,6 +87,21 @@ int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* preds,
                    void* stream);
 
 /*
+ * moeb_cache_sim with the cache-independent counters supplied by the caller:
+ * given_counts [n_preds][2 + 2L] = measured accesses, prediction hits, then
+ * per layer of each (e.g. from moeb_linear_predict_counts over the same rows
+ * and warm-up). The fast LRU kernel then skips computing them and adds these
+ * instead; every other kernel (LFU, coverage / hit-mask outputs, per-prompt
+ * counters) ignores them. Results are identical to moeb_cache_sim's.
+ */
+int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* const* preds,
+                           const uint8_t* const* covered, const int32_t* unbounded, int n_preds,
+                           const int64_t* prompt_row_off, int n_prompts, int L, int E,
+                           int warmup_tokens, const int64_t* capacities, int n_caps, int budget,
+                           int policy, int64_t* counters, int64_t* per_prompt,
+                           uint64_t* hit_masks, const int64_t* given_counts, void* stream);
+
+/*
  * ExpertCache op stream (cache.py:58-154) for one cache, executed on device:
  * ops[i] = 0 begin_step, 1 touch(keys[i]), 2 prefetch([keys[i]]).
  * results[i] = touch hit / prefetch inserted. keys = layer*E + expert.
@@ -111,6 +126,13 @@ int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_row_off, in
                         int L, int E, const double* weights, double decay, int budget,
                         int threshold, int warmup_tokens, uint64_t* pred, double* logits,
                         int64_t* metrics, void* stream);
+/* moeb_linear_predict that also accumulates, over rows with token >= warmup,
+ * counts [2 + 2L] += sum |truth|, sum |truth & pred|, then the same per layer
+ * (the replay's measured accesses and prediction hits, engine.py:175-200). */
+int moeb_linear_predict_counts(const uint64_t* truth, const int64_t* prompt_row_off,
+                               int n_prompts, int L, int E, const double* weights, double decay,
+                               int budget, int threshold, int warmup_tokens, uint64_t* pred,
+                               double* logits, int64_t* metrics, int64_t* counts, void* stream);
 
 /*
  * Wide K3 for 64 < E <= 256 (DeepSeek-V3: 256 experts), same semantics as

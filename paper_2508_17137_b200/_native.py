@@ -35,8 +35,11 @@ I32, I64, DBL = ctypes.c_int, ctypes.c_int64, ctypes.c_double
 
 _SIGS = {
     "moeb_cache_sim": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P, P],
+    "moeb_cache_sim_counted": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P,
+                               P, P],
     "moeb_cache_ops": [P, P, I64, I32, I32, I64, I32, P, P],
     "moeb_linear_predict": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P],
+    "moeb_linear_predict_counts": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P, P],
     "moeb_mask_head": [P, I64, I32, I32, I32, P, P],
     "moeb_metrics": [P, P, P, I32, I32, I32, I32, P, P],
     "moeb_policy_masks": [I32, P, I64, I32, I32, I32, P, P, P],

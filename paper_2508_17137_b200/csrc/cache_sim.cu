@@ -60,6 +60,9 @@ struct SimArgs {
   int64_t per_prompt_stride;
   uint64_t* hits;
   int64_t hits_stride;
+  // nullable [n_preds][2 + 2L]: measured accesses / prediction hits (total,
+  // per layer) computed upstream; used by the fast LRU kernel only
+  const int64_t* given;
   // per-simulation shared-memory layout (bytes)
   int off_r, off_q, off_k, off_c, sim_bytes;
   uint32_t magic;  // layer_of(key) = (key * magic) >> 22
@@ -760,7 +763,9 @@ __device__ __forceinline__ int nth_bit(const uint64_t (&m)[W], int n) {
   return w * 64 + nth_bit64(sel, n);
 }
 
-template <int W, int ES, int G, bool EXTRA>
+// KPH = false: the measured-access / prediction-hit counters are not
+// computed here (they do not depend on the cache); block 0 adds a.given
+template <int W, int ES, int G, bool EXTRA, bool KPH = true>
 __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   // G lanes per simulation (32: one per warp; 16: two per warp). All
   // collectives below are restricted to the group's lanes (gmask), so the
@@ -1041,18 +1046,20 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         hits[(r0 + i) * W + hl] = v;
       }
       if (measured) {
-        const int k = popc_w<W>(T);
-        int ph = 0;
+        int k = 0, ph = 0;
+        if (KPH) {
+          k = popc_w<W>(T);
 #pragma unroll
-        for (int w = 0; w < W; ++w) ph += __popcll(T[w] & P[w]);  // FULL predicted set
+          for (int w = 0; w < W; ++w) ph += __popcll(T[w] & P[w]);  // FULL predicted set
+        }
         if (EXTRA && cov && i < nrows && cov[r0 + i] == 0) ++tot_unc;  // engine.py:175-176
         tot_k += k;
         tot_ch += ch;
         tot_ph += ph;
         if (hl == 0) {  // per-layer counters: fire-and-forget shared-memory reductions
-          atomicAdd(&bcnt[l], (unsigned)k);  // native 32-bit shared atomics (a
-          atomicAdd(&bcnt[L + l], (unsigned)ch);  // 64-bit one is a CAS loop)
-          atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
+          if (KPH) atomicAdd(&bcnt[l], (unsigned)k);  // native 32-bit shared atomics (a
+          atomicAdd(&bcnt[L + l], (unsigned)ch);      // 64-bit one is a CAS loop)
+          if (KPH) atomicAdd(&bcnt[2 * L + l], (unsigned)ph);
         }
       }
       if (++l == L) {
@@ -1079,6 +1086,13 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   int64_t* c = a.counters + pi * a.counters_stride;
   for (int j = threadIdx.x; j < 3 * L; j += blockDim.x)
     if (bcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bcnt[j]);
+  if (!KPH && blockIdx.x == 0) {  // the upstream counts, once per prediction stream
+    const int64_t* g = a.given + (int64_t)pi * (2 + 2 * L);
+    for (int j = threadIdx.x; j < 2 + 2 * L; j += blockDim.x) {
+      const int idx = j == 0 ? 0 : j == 1 ? 2 : j < 2 + L ? 4 + (j - 2) : 4 + 2 * L + (j - 2 - L);
+      if (g[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + idx), (unsigned long long)g[j]);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1403,7 +1417,8 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
   }
   const size_t smem = head + (size_t)nw * (32 / G) * a.sim_bytes;
   auto k = (a.hits || a.any_cov) ? k_cache_sim_warp<W, ES, G, true>
-                                 : k_cache_sim_warp<W, ES, G, false>;
+           : (a.given && !a.per_prompt) ? k_cache_sim_warp<W, ES, G, false, false>
+                                        : k_cache_sim_warp<W, ES, G, false>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int spb = nw * (32 / G);
   const dim3 blocks((unsigned)((a.P + spb - 1) / spb), (unsigned)a.n_preds);
@@ -1442,6 +1457,18 @@ extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* pred
                               int E, int warmup_tokens, const int64_t* capacities, int n_caps,
                               int budget, int policy, int64_t* counters, int64_t* per_prompt,
                               uint64_t* hit_masks, void* stream) {
+  return moeb_cache_sim_counted(truth, preds, covered, unbounded, n_preds, prompt_row_off,
+                                n_prompts, L, E, warmup_tokens, capacities, n_caps, budget,
+                                policy, counters, per_prompt, hit_masks, nullptr, stream);
+}
+
+extern "C" int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* const* preds,
+                                      const uint8_t* const* covered, const int32_t* unbounded,
+                                      int n_preds, const int64_t* prompt_row_off, int n_prompts,
+                                      int L, int E, int warmup_tokens, const int64_t* capacities,
+                                      int n_caps, int budget, int policy, int64_t* counters,
+                                      int64_t* per_prompt, uint64_t* hit_masks,
+                                      const int64_t* given_counts, void* stream) {
   moeb::clear_error();
   MOEB_REQUIRE(truth && prompt_row_off && counters && capacities, "null argument");
   MOEB_REQUIRE(n_preds >= 1 && n_preds <= MOEB_MAX_PREDS, "n_preds must be in [1, %d]",
@@ -1474,6 +1501,7 @@ extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* pred
   a.warmup = warmup_tokens;
   a.budget = budget;
   a.rows = rows;
+  a.given = given_counts;
   const int nc = 4 + 3 * L;
   cudaStream_t s = moeb::as_stream(stream);
   for (int c = 0; c < n_caps; ++c) {

@@ -55,6 +55,7 @@ struct LinArgs {
   int budget, threshold, warmup;
   uint64_t* pred;
   double* logits;
+  int64_t* counts;  // nullable [2 + 2L]: measured accesses, prediction hits, per layer of each
 };
 
 template <int TPS>
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
       z[s] = (FULL || ex < E) ? a.Wt[(int64_t)ex * F + l] + a.Wt[(int64_t)ex * F + L + E] : NEG;
     }
     const double2* bcol = bias2 + (l * TPS + q) * NU + rot;
+    int acc_k = 0, acc_ph = 0;
 
     for (int t = 0; t < Tw; ++t) {
       const bool valid = t < T;
@@ -250,7 +252,13 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
         }
       }
       if (valid) {
-        if (q == 0) a.pred[r] = pm;
+        if (q == 0) {
+          a.pred[r] = pm;
+          if (t >= a.warmup) {  // the replay's access / prediction-hit counters
+            acc_k += __popcll(tw);
+            acc_ph += __popcll(tw & pm);
+          }
+        }
         if (a.logits) {
           const int orot = opaque(rot);
 #pragma unroll
@@ -287,6 +295,13 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
           }
         }
       }
+    }
+    if (a.counts && q == 0 && live && (acc_k | acc_ph)) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + 0), (unsigned long long)acc_k);
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + 1), (unsigned long long)acc_ph);
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + 2 + l), (unsigned long long)acc_k);
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.counts + 2 + L + l),
+                (unsigned long long)acc_ph);
     }
   }
 }
@@ -441,6 +456,16 @@ extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_
                                    double decay, int budget, int threshold, int warmup_tokens,
                                    uint64_t* pred, double* logits, int64_t* metrics,
                                    void* stream) {
+  return moeb_linear_predict_counts(truth, prompt_row_off, n_prompts, L, E, weights, decay,
+                                    budget, threshold, warmup_tokens, pred, logits, metrics,
+                                    nullptr, stream);
+}
+
+extern "C" int moeb_linear_predict_counts(const uint64_t* truth, const int64_t* prompt_row_off,
+                                          int n_prompts, int L, int E, const double* weights,
+                                          double decay, int budget, int threshold,
+                                          int warmup_tokens, uint64_t* pred, double* logits,
+                                          int64_t* metrics, int64_t* counts, void* stream) {
   moeb::clear_error();
   MOEB_REQUIRE(truth && prompt_row_off && weights && pred, "null argument");
   MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && E >= 1 && E <= 64,
@@ -449,7 +474,7 @@ extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_
   MOEB_REQUIRE(budget >= 1 && warmup_tokens >= 0, "bad budget/warmup");
   MOEB_REQUIRE(decay >= 0.0 && decay < 1.0, "decay must be in [0, 1)");
   LinArgs a{truth, prompt_row_off, n_prompts, L, E, weights, decay, budget,
-            threshold ? 1 : 0, warmup_tokens, pred, logits};
+            threshold ? 1 : 0, warmup_tokens, pred, logits, counts};
   const char* env = getenv("MOEB_K3_TPS");  // tuning knob: threads per stream (2 or 4)
   const int rc = (env && atoi(env) == 4) ? launch_k3<4>(a, moeb::as_stream(stream))
                                          : launch_k3<2>(a, moeb::as_stream(stream));

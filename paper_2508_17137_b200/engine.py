@@ -128,13 +128,16 @@ def _check_lengths(packed: PackedTraces, warmup: int) -> None:
 
 def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget: int,
                  policy: str = "lru", want_per_prompt: bool = True, want_hits: bool = False,
-                 counters=None):
+                 counters=None, given_counts=None):
     """Run K1 for every (prediction stream, capacity) pair in one call.
 
     ``streams`` is a list of (masks | None, coverage | None, unbounded).
     Returns device tensors counters [n][C][4+3L], per_prompt [n][C][P][4] or
     None, hit masks [n][C][rows][W] or None. ``counters`` (optional, int64
     [n][C][4+3L]) is accumulated into instead of a fresh zero tensor.
+    ``given_counts`` (optional, int64 [n][2+2L], e.g. from the learned_linear
+    predictor's fused counts) supplies the cache-independent counters so the
+    replay kernel skips them (moeb_cache_sim_counted); results are identical.
     """
     shape = packed.shape
     L = shape.num_layers
@@ -152,7 +155,7 @@ def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget:
             if want_hits else None)
     for lo in range(0, n, 16):
         chunk = streams[lo:lo + 16]
-        nat.call("moeb_cache_sim", nat.ptr(packed.truth),
+        nat.call("moeb_cache_sim_counted", nat.ptr(packed.truth),
                  nat.ptr_array([m for m, _, _ in chunk]),
                  nat.ptr_array([c for _, c, _ in chunk]),
                  nat.i32_array([int(bool(u)) for _, _, u in chunk]), len(chunk),
@@ -160,7 +163,9 @@ def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget:
                  nat.i64_array(capacities), C, int(budget), POLICIES[policy],
                  nat.ptr(counters[lo:lo + 16]),
                  nat.ptr(None if per_prompt is None else per_prompt[lo:lo + 16]),
-                 nat.ptr(None if hits is None else hits[lo:lo + 16]), nat.stream_ptr())
+                 nat.ptr(None if hits is None else hits[lo:lo + 16]),
+                 nat.ptr(None if given_counts is None else given_counts[lo:lo + 16]),
+                 nat.stream_ptr())
     return counters, per_prompt, hits
 
 
@@ -255,13 +260,15 @@ class PipelinedReplay:
                                        non_blocking=True)
                 self.s_pred.wait_stream(self.s_copy)
             with torch.cuda.stream(self.s_pred):
+                gc = None
                 if getattr(predictor, "empty", False) and metrics is None:
                     masks, cov = None, None
                 else:
                     if ev:
                         e0, e1 = ev(), ev()
                         e0.record(self.s_pred)
-                    masks = predictor.predict_masks(view, budget, warmup)
+                    gc = _counts_buffer(predictor, shape, packed.device)
+                    masks = predictor.predict_masks(view, budget, warmup, **_counts_kw(gc))
                     if ev:
                         e1.record(self.s_pred)
                         timing.append(("predict", e0, e1, view.rows))
@@ -269,7 +276,7 @@ class PipelinedReplay:
             masks_ready = torch.cuda.Event()
             masks_ready.record(self.s_pred)
             self.s_sim.wait_event(masks_ready)
-            for t in (masks, cov):
+            for t in (masks, cov, gc):
                 if t is not None:
                     t.record_stream(self.s_sim)
             with torch.cuda.stream(self.s_sim):
@@ -277,7 +284,7 @@ class PipelinedReplay:
                     e2, e3 = ev(), ev()
                     e2.record(self.s_sim)
                 cache_replay(view, [(masks, cov, unbounded)], capacities, warmup, budget,
-                             policy, want_per_prompt=False, counters=counters)
+                             policy, want_per_prompt=False, counters=counters, given_counts=gc)
                 if ev:
                     e3.record(self.s_sim)
                     timing.append(("replay", e2, e3, view.rows))
@@ -290,6 +297,18 @@ class PipelinedReplay:
         if metrics is not None:
             metrics.record_stream(self.s_met)
         return counters
+
+
+def _counts_buffer(predictor, shape, device):
+    """[1][2+2L] zeros when the predictor fuses the replay's cache-independent
+    counters (measured accesses, prediction hits) into its kernel, else None."""
+    if not getattr(predictor, "supports_counts", False):
+        return None
+    return torch.zeros((1, 2 + 2 * shape.num_layers), dtype=torch.int64, device=device)
+
+
+def _counts_kw(gc):
+    return {} if gc is None else {"counts": gc[0]}
 
 
 def _overlapped_metrics(s_met, masks_ready, masks, view, warmup, out):
@@ -393,22 +412,25 @@ class StreamingReplay:
                     e0.record(self.s_comp)
                 vec = (torch.zeros(3 * E + 3, dtype=torch.int64, device=dev)
                        if metrics else None)
+                gc = None
                 if empty:
                     masks, cov = None, None
                 elif split:
+                    gc = _counts_buffer(predictor, shape, dev)
                     pieces = []
                     for v, e in zip(self.first_views, parts):
                         self.s_comp.wait_event(e)
-                        pieces.append(predictor.predict_masks(v, budget, warmup))
+                        pieces.append(predictor.predict_masks(v, budget, warmup, **_counts_kw(gc)))
                     masks = torch.cat(pieces)
                     cov = predictor.coverage(buf)
                 else:
-                    masks = predictor.predict_masks(buf, budget, warmup)
+                    gc = _counts_buffer(predictor, shape, dev)
+                    masks = predictor.predict_masks(buf, budget, warmup, **_counts_kw(gc))
                     cov = predictor.coverage(buf)
                 masks_ready = torch.cuda.Event()
                 masks_ready.record(self.s_comp)
                 cnt, _, _ = cache_replay(buf, [(masks, cov, unbounded)], capacities, warmup,
-                                         budget, policy, want_per_prompt=False)
+                                         budget, policy, want_per_prompt=False, given_counts=gc)
                 ev = torch.cuda.Event()
                 if vec is not None and masks is not None:
                     _overlapped_metrics(self.s_met, masks_ready, masks, buf, warmup, vec)

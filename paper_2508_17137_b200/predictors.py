@@ -257,9 +257,17 @@ class LearnedLinearPredictor(DevicePredictor):
             self._w[key] = tab
         return self._w[key]
 
-    def predict_masks(self, packed, budget, warmup=0, metrics=None, logits=None):
+    @property
+    def supports_counts(self) -> bool:
+        """predict_masks(counts=...) fills the replay's cache-independent
+        counters (E <= 64 kernel only)."""
+        return self.shape.num_experts <= 64
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None, logits=None, counts=None):
         s = self.shape
         out = _empty(packed)
+        if counts is not None and s.num_experts > 64:
+            raise ConfigError("fused replay counts need E <= 64")
         if s.num_experts > 64:
             nat.call("moeb_linear_predict_wide", nat.ptr(packed.truth), nat.ptr(packed.row_off),
                      packed.num_prompts, s.num_layers, s.num_experts,
@@ -267,11 +275,11 @@ class LearnedLinearPredictor(DevicePredictor):
                      int(budget), int(bool(self.threshold)), int(warmup), nat.ptr(out),
                      nat.ptr(logits), nat.ptr(metrics), nat.stream_ptr())
             return out
-        nat.call("moeb_linear_predict", nat.ptr(packed.truth), nat.ptr(packed.row_off),
+        nat.call("moeb_linear_predict_counts", nat.ptr(packed.truth), nat.ptr(packed.row_off),
                  packed.num_prompts, s.num_layers, s.num_experts,
                  nat.ptr(self.weights_on(packed.device)), float(self.history_decay),
                  int(budget), int(bool(self.threshold)), int(warmup), nat.ptr(out),
-                 nat.ptr(logits), nat.ptr(metrics), nat.stream_ptr())
+                 nat.ptr(logits), nat.ptr(metrics), nat.ptr(counts), nat.stream_ptr())
         return out
 
 
