@@ -61,7 +61,7 @@ struct LinArgs {
 template <int TPS>
 struct K3Cfg {
   static constexpr int NS = 64 / TPS;                    // experts (slots) per thread
-  static constexpr int kThreads = TPS == 2 ? 192 : 256;  // 2 CTAs per SM
+  static constexpr int kThreads = 256;  // 2 CTAs per SM (<= 128 registers, no spills)
   static constexpr int kStreams = kThreads / TPS;
   static constexpr int kUnits = NS;                      // 16-byte units per (column, part)
 };
