@@ -63,6 +63,10 @@ struct SimArgs {
   // nullable [n_preds][2 + 2L]: measured accesses / prediction hits (total,
   // per layer) computed upstream; used by the fast LRU kernel only
   const int64_t* given;
+  // nullable: the fast LRU kernel replays only prompts plist[pi * P + i],
+  // i < plist_n[pi] (the stack-distance replay's undecided prompts)
+  const int32_t* plist;
+  const int32_t* plist_n;
   // per-simulation shared-memory layout (bytes)
   int off_r, off_q, off_k, off_c, sim_bytes;
   uint32_t magic;  // layer_of(key) = (key * magic) >> 22
@@ -783,8 +787,9 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   const int pi = blockIdx.y;
   const int sims_per_block = nw * (32 / G);
   const int sl = wib * (32 / G) + lane / G;  // simulation within the block
-  const int p = blockIdx.x * sims_per_block + sl;
-  const bool live = p < a.P;
+  const int sidx = blockIdx.x * sims_per_block + sl;
+  const bool live = a.plist ? sidx < a.plist_n[pi] : sidx < a.P;
+  const int p = a.plist ? (live ? a.plist[(int64_t)pi * a.P + sidx] : 0) : sidx;
   constexpr unsigned FULL = 0xffffffffu;
   // The whole warp runs the row loop to the longer of its groups' prompts
   // (missing rows are all-zero no-op rows), so the common path's warp
@@ -1086,7 +1091,7 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
   int64_t* c = a.counters + pi * a.counters_stride;
   for (int j = threadIdx.x; j < 3 * L; j += blockDim.x)
     if (bcnt[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bcnt[j]);
-  if (!KPH && blockIdx.x == 0) {  // the upstream counts, once per prediction stream
+  if (!KPH && a.given && blockIdx.x == 0) {  // the upstream counts, once per prediction stream
     const int64_t* g = a.given + (int64_t)pi * (2 + 2 * L);
     for (int j = threadIdx.x; j < 2 + 2 * L; j += blockDim.x) {
       const int idx = j == 0 ? 0 : j == 1 ? 2 : j < 2 + L ? 4 + (j - 2) : 4 + 2 * L + (j - 2 - L);
@@ -1381,6 +1386,185 @@ int launch_kernel(K k, const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
   return moeb::check_launch("k_cache_sim");
 }
 
+
+// ---------------------------------------------------------------------------
+// K1s -- stack-distance replay (E <= 64, LRU, no coverage / hit-mask /
+// per-prompt outputs). When no pin can bind (capacity C > every row's
+// distinct-key count, so the LRU victim is never a key prefetched in the
+// same row and nothing is rejected) the reference's cache is a pure LRU over
+// the access sequence (row order; in a row: sorted(pred)[:limit], then the
+// truth keys ascending), and a touch of key x hits iff fewer than C distinct
+// other keys were accessed since x's previous access (Mattson's stack
+// distance). Keys of different layers are distinct and every row is one
+// layer, so with S_q the row key sets and n_q = |S_q|:
+//  * x prefetched in the same row: hit;
+//  * x in S_{r-L} (previous token): D = sum of n over rows r-L+1..r-1 (prefix
+//    sums) + |after(x in row r-L) | before(x in row r)| -- O(1);
+//  * otherwise D >= sum of n over rows r-L..r-1; if that is >= C: miss;
+//    else x's previous access is searched up to dmax tokens back and D is
+//    the exact per-layer union over the span; beyond that the prompt is
+//    undecided and goes to the exact kernel (plist).
+// One warp per prompt, 32 rows per step (lane = row), the last H rows' masks
+// and prefix sums in a shared-memory ring. Cache-hit counters only (the
+// cache-independent ones come from a.given). Undecided prompts contribute
+// nothing here and are replayed by k_cache_sim_warp over plist.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t above_bits(int x) { return x >= 63 ? 0ull : ~((2ull << x) - 1ull); }
+__device__ __forceinline__ uint64_t below_bits(int x) { return (1ull << x) - 1ull; }
+// keys of row (k, t) accessed after x's last access in that row
+__device__ __forceinline__ uint64_t after_last(uint64_t k, uint64_t t, int x) {
+  return ((t >> x) & 1ull) ? (t & above_bits(x)) : ((k & above_bits(x)) | t);
+}
+
+__global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, int dmax,
+                                                      int32_t* plist, int32_t* plist_n) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr unsigned FULL = 0xffffffffu;
+  const int L = a.L;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned int* bch = reinterpret_cast<unsigned int*>(smem);  // [L] block cache hits
+  unsigned char* wbase = smem + ((4 * L + 15) / 16) * 16 +
+                         (size_t)wib * ((size_t)H * 20 + ((4 * L + 15) / 16) * 16);
+  uint64_t* rK = reinterpret_cast<uint64_t*>(wbase);  // [H] prefetched keys of row q
+  uint64_t* rT = rK + H;                               // [H] touched keys
+  uint32_t* rP = reinterpret_cast<uint32_t*>(rT + H);  // [H] inclusive prefix of n (mod 2^32)
+  unsigned int* wch = reinterpret_cast<unsigned int*>(rP + H);  // [L] this prompt's hits
+  for (int j = threadIdx.x; j < L; j += blockDim.x) bch[j] = 0;
+  for (int j = lane; j < L; j += 32) wch[j] = 0;
+  __syncthreads();
+  const int pi = blockIdx.y;
+  const int p = blockIdx.x * (blockDim.x >> 5) + wib;
+  const uint32_t cap = (uint32_t)a.cap;
+  const int hm = H - 1;
+  if (p < a.P) {
+    const uint64_t* __restrict__ pred = a.preds[pi];
+    const bool unbounded = (a.unbounded_bits >> pi) & 1u;
+    const int limit = unbounded ? a.E : a.budget;
+    const int64_t r0 = a.row_off[p];
+    const int nrows = (int)(a.row_off[p + 1] - r0);
+    const uint64_t* __restrict__ tr = a.truth + r0;
+    const uint64_t* __restrict__ pr = pred ? pred + r0 : nullptr;
+    bool undecided = false;
+    uint32_t carry = 0;
+    long long tot = 0;
+    auto pn = [&](int q) -> uint32_t { return q < 0 ? 0u : rP[q & hm]; };
+    for (int base = 0; base < nrows; base += 32) {
+      const int i = base + lane;
+      const bool in = i < nrows;
+      const uint64_t T = in ? __ldg(tr + i) : 0ull;
+      uint64_t K = (in && pr) ? __ldg(pr + i) : 0ull;
+      const int t = i / L, l = i - t * L;
+      const bool measured = in && t >= a.warmup;
+      if (!measured) K = 0ull;
+      if (__popcll(K) > limit) {
+        uint64_t k1[1] = {K};
+        keep_lowest<1>(k1, limit);
+        K = k1[0];
+      }
+      const uint32_t n = (uint32_t)__popcll(K | T);
+      if (in && n >= cap) undecided = true;  // a pin could bind: exact kernel
+      uint32_t v = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += y;
+      }
+      const uint32_t pfx = carry + v;
+      carry = __shfl_sync(FULL, pfx, 31);
+      rK[i & hm] = K;
+      rT[i & hm] = T;
+      rP[i & hm] = pfx;
+      __syncwarp();
+      if (measured) {
+        int ch = __popcll(T & K);  // prefetched in this row, then touched: hits
+        uint64_t tm = T & ~K;
+        while (tm) {
+          const int x = __ffsll((long long)tm) - 1;
+          tm &= tm - 1;
+          const uint64_t before = K | (T & below_bits(x));
+          bool hit = false;
+          const int q1 = i - L;
+          if (q1 >= 0 && (((rK[q1 & hm] | rT[q1 & hm]) >> x) & 1ull)) {
+            const uint32_t D = (pn(i - 1) - pn(i - L)) +
+                               (uint32_t)__popcll(after_last(rK[q1 & hm], rT[q1 & hm], x) | before);
+            hit = D < cap;
+          } else if (i - 2 * L >= 0 && pn(i - 1) - pn(i - L - 1) < cap) {
+            // the full previous token (distinct layers) does not decide it
+            int jf = 0;
+            bool none = false;
+            for (int j = 2; j <= dmax; ++j) {
+              const int q = i - j * L;
+              if (q < 0) {
+                none = true;  // no earlier access of x at all: miss
+                break;
+              }
+              if (((rK[q & hm] | rT[q & hm]) >> x) & 1ull) {
+                jf = j;
+                break;
+              }
+            }
+            if (!none) {
+              const int j = jf ? jf : dmax;  // exact union over the span (a lower bound if !jf)
+              uint32_t D = 0;
+              for (int o = 1; o < L && D < cap; ++o) {
+                uint64_t u = 0;
+                for (int q = i - j * L + o; q < i; q += L) u |= rK[q & hm] | rT[q & hm];
+                D += (uint32_t)__popcll(u);
+              }
+              uint64_t u = before;
+              for (int m = 1; m < j; ++m) u |= rK[(i - m * L) & hm] | rT[(i - m * L) & hm];
+              if (jf) u |= after_last(rK[(i - j * L) & hm], rT[(i - j * L) & hm], x);
+              D += (uint32_t)__popcll(u);
+              if (jf) {
+                hit = D < cap;
+              } else if (D < cap) {
+                if (i - (dmax + 1) * L >= 0) undecided = true;  // x may be older than dmax tokens
+              }
+            }
+          }
+          ch += hit ? 1 : 0;
+        }
+        if (ch) atomicAdd(&wch[l], (unsigned)ch);
+        tot += ch;
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+    if (__any_sync(FULL, undecided)) {
+      if (lane == 0) {
+        const int k = atomicAdd(plist_n + pi, 1);
+        plist[(int64_t)pi * a.P + k] = p;
+      }
+    } else {
+      for (int j = lane; j < L; j += 32)
+        if (wch[j]) atomicAdd(&bch[j], wch[j]);
+      if (lane == 0 && tot) {
+        int64_t* c = a.counters + pi * a.counters_stride;
+        atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot);
+      }
+    }
+  }
+  __syncthreads();
+  int64_t* c = a.counters + pi * a.counters_stride;
+  for (int j = threadIdx.x; j < L; j += blockDim.x)
+    if (bch[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + L + j), (unsigned long long)bch[j]);
+  if (a.given && blockIdx.x == 0) {  // the upstream counts, once per prediction stream
+    const int64_t* g = a.given + (int64_t)pi * (2 + 2 * L);
+    for (int j = threadIdx.x; j < 2 + 2 * L; j += blockDim.x) {
+      const int idx = j == 0 ? 0 : j == 1 ? 2 : j < 2 + L ? 4 + (j - 2) : 4 + 2 * L + (j - 2 - L);
+      if (g[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + idx), (unsigned long long)g[j]);
+    }
+  }
+}
+
+// MOEB_K1_STACK=0 disables the stack-distance replay (every prompt through
+// the exact kernel)
+inline bool stack_mode() {
+  const char* env = getenv("MOEB_K1_STACK");
+  return !(env && env[0] == '0');
+}
+
 template <int W, int ES, int G>
 int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block);
 
@@ -1416,6 +1600,39 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
     return moeb::check_launch("k_cache_sim_warp");
   }
   const size_t smem = head + (size_t)nw * (32 / G) * a.sim_bytes;
+  if (W == 1 && G == 16 && a.given && !a.per_prompt && !a.hits && !a.any_cov && stack_mode()) {
+    // K1s over every prompt, then the exact kernel over the undecided ones
+    const int dmax = 4;
+    int H = 64;
+    while (H < (dmax + 1) * a.L + 64) H <<= 1;
+    const size_t lbytes = (size_t)((4 * a.L + 15) / 16) * 16;
+    const size_t ssmem = lbytes + 4 * ((size_t)H * 20 + lbytes);
+    if ((int)ssmem <= max_block) {
+      int32_t* pl = nullptr;
+      const size_t plbytes = sizeof(int32_t) * ((size_t)a.n_preds * a.P + a.n_preds);
+      if (cudaMallocAsync(reinterpret_cast<void**>(&pl), plbytes, s) != cudaSuccess)
+        return moeb::fail(MOEB_ECUDA, "cudaMallocAsync(%zu) for the undecided-prompt list", plbytes);
+      int32_t* pln = pl + (size_t)a.n_preds * a.P;
+      cudaMemsetAsync(pln, 0, sizeof(int32_t) * a.n_preds, s);
+      cudaFuncSetAttribute(k_stack_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+      k_stack_replay<<<dim3((unsigned)((a.P + 3) / 4), (unsigned)a.n_preds), 128, ssmem, s>>>(
+          a, H, dmax, pl, pln);
+      int rc = moeb::check_launch("k_stack_replay");
+      if (rc == 0) {
+        SimArgs b = a;
+        b.given = nullptr;  // added by k_stack_replay
+        b.plist = pl;
+        b.plist_n = pln;
+        auto k = k_cache_sim_warp<W, ES, G, false, false>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int spb = nw * (32 / G);
+        k<<<dim3((unsigned)((a.P + spb - 1) / spb), (unsigned)a.n_preds), 32 * nw, smem, s>>>(b);
+        rc = moeb::check_launch("k_cache_sim_warp");
+      }
+      cudaFreeAsync(pl, s);
+      return rc;
+    }
+  }
   auto k = (a.hits || a.any_cov) ? k_cache_sim_warp<W, ES, G, true>
            : (a.given && !a.per_prompt) ? k_cache_sim_warp<W, ES, G, false, false>
                                         : k_cache_sim_warp<W, ES, G, false>;

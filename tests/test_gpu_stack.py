@@ -1,0 +1,64 @@
+"""K1s (stack-distance replay, `k_stack_replay`) + the exact kernel over its
+undecided prompts give exactly the exact kernel's counters: every capacity
+from 1 to all keys, predictions that are empty / learned / over the budget /
+unbounded, ragged prompts, warm-up 0 and 8, several geometries."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _packed(m, shape, prompts, tokens, seed, ragged):
+    packed = m.generate_packed(m.GeneratorConfig(prompts, tokens, shape, 8, 0.9, seed))
+    if not ragged:
+        return packed
+    L = shape.num_layers
+    truth_all = packed.truth.reshape(-1)
+    rows, off = [], [0]
+    for p in range(packed.num_prompts):
+        T = 1 + (p * 7) % tokens
+        r0 = int(packed.row_off_host[p])
+        rows.append(truth_all[r0:r0 + T * L])
+        off.append(off[-1] + T * L)
+    off = np.array(off, dtype=np.int64)
+    return m.PackedTraces(shape, torch.cat(rows).reshape(-1, 1).contiguous(),
+                          torch.from_numpy(off).cuda(), off,
+                          np.arange(packed.num_prompts, dtype=np.int64))
+
+
+def _given(counters, L):
+    c = counters[:, 0]
+    return torch.cat([c[:, 0:1], c[:, 2:3], c[:, 4:4 + L], c[:, 4 + 2 * L:4 + 3 * L]], 1).contiguous()
+
+
+@pytest.mark.parametrize("geom", [(26, 64, 6), (3, 64, 2), (5, 40, 4)])
+@pytest.mark.parametrize("ragged", [False, True])
+@pytest.mark.parametrize("warmup", [0, 8])
+def test_stack_replay_equals_exact(geom, ragged, warmup, monkeypatch):
+    import paper_2508_17137_b200 as m
+    m.load_library()
+    L, E, k = geom
+    shape = m.ModelShape(L, E, k)
+    packed = _packed(m, shape, 45, 60, 3 + L, ragged)
+    rng = np.random.default_rng(L + E)
+    w = rng.normal(0.0, 0.01, (E, L + E + 1))
+    model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
+    learned = m.make_predictor("learned_linear", shape, model=model).predict_masks(packed, k, warmup)
+    rows = packed.rows
+    wide = torch.from_numpy(rng.integers(0, 2**62, rows, dtype=np.int64)).cuda().reshape(-1, 1)
+    wide &= (1 << E) - 1 if E < 64 else -1
+    ones = torch.full((rows, 1), (1 << E) - 1 if E < 64 else -1, dtype=torch.int64, device="cuda")
+    caps = sorted({1, 2, 5, 12, 20, max(1, L * E // 20), L * E // 10, L * E // 4, L * E // 2,
+                   L * E})
+    budget = k
+    for masks, unbounded in ((learned, False), (None, False), (wide, False), (ones, True)):
+        streams = [(masks, None, unbounded)]
+        monkeypatch.setenv("MOEB_K1_STACK", "0")
+        want, _, _ = m.cache_replay(packed, streams, caps, warmup, budget, want_per_prompt=False)
+        given = _given(want, L)
+        monkeypatch.setenv("MOEB_K1_STACK", "1")
+        got, _, _ = m.cache_replay(packed, streams, caps, warmup, budget, want_per_prompt=False,
+                                   given_counts=given)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), (masks is None, unbounded)
