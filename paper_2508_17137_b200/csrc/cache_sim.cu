@@ -1416,21 +1416,22 @@ __device__ __forceinline__ uint64_t after_last(uint64_t k, uint64_t t, int x) {
   return ((t >> x) & 1ull) ? (t & above_bits(x)) : ((k & above_bits(x)) | t);
 }
 
+template <bool KPH>  // KPH: also the cache-independent counters (else a.given is added)
 __global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, int dmax,
                                                       int32_t* plist, int32_t* plist_n) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr unsigned FULL = 0xffffffffu;
   const int L = a.L;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  unsigned int* bch = reinterpret_cast<unsigned int*>(smem);  // [L] block cache hits
-  unsigned char* wbase = smem + ((4 * L + 15) / 16) * 16 +
-                         (size_t)wib * ((size_t)H * 20 + ((4 * L + 15) / 16) * 16);
+  const size_t lb = (size_t)((12 * L + 15) / 16) * 16;
+  unsigned int* bch = reinterpret_cast<unsigned int*>(smem);  // [3L] block: k, ch, ph per layer
+  unsigned char* wbase = smem + lb + (size_t)wib * ((size_t)H * 20 + lb);
   uint64_t* rK = reinterpret_cast<uint64_t*>(wbase);  // [H] prefetched keys of row q
   uint64_t* rT = rK + H;                               // [H] touched keys
   uint32_t* rP = reinterpret_cast<uint32_t*>(rT + H);  // [H] inclusive prefix of n (mod 2^32)
-  unsigned int* wch = reinterpret_cast<unsigned int*>(rP + H);  // [L] this prompt's hits
-  for (int j = threadIdx.x; j < L; j += blockDim.x) bch[j] = 0;
-  for (int j = lane; j < L; j += 32) wch[j] = 0;
+  unsigned int* wch = reinterpret_cast<unsigned int*>(rP + H);  // [3L] this prompt's k, ch, ph
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x) bch[j] = 0;
+  for (int j = lane; j < 3 * L; j += 32) wch[j] = 0;
   __syncthreads();
   const int pi = blockIdx.y;
   const int p = blockIdx.x * (blockDim.x >> 5) + wib;
@@ -1446,13 +1447,14 @@ __global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, in
     const uint64_t* __restrict__ pr = pred ? pred + r0 : nullptr;
     bool undecided = false;
     uint32_t carry = 0;
-    long long tot = 0;
+    long long tot = 0, tk = 0, tph = 0;
     auto pn = [&](int q) -> uint32_t { return q < 0 ? 0u : rP[q & hm]; };
     for (int base = 0; base < nrows; base += 32) {
       const int i = base + lane;
       const bool in = i < nrows;
       const uint64_t T = in ? __ldg(tr + i) : 0ull;
-      uint64_t K = (in && pr) ? __ldg(pr + i) : 0ull;
+      const uint64_t Pf = (in && pr) ? __ldg(pr + i) : 0ull;  // full predicted set
+      uint64_t K = Pf;
       const int t = i / L, l = i - t * L;
       const bool measured = in && t >= a.warmup;
       if (!measured) K = 0ull;
@@ -1524,32 +1526,53 @@ __global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, in
           }
           ch += hit ? 1 : 0;
         }
-        if (ch) atomicAdd(&wch[l], (unsigned)ch);
+        if (ch) atomicAdd(&wch[L + l], (unsigned)ch);
         tot += ch;
+        if (KPH) {
+          const int kk = __popcll(T), ph = __popcll(T & Pf);
+          if (kk) atomicAdd(&wch[l], (unsigned)kk);
+          if (ph) atomicAdd(&wch[2 * L + l], (unsigned)ph);
+          tk += kk;
+          tph += ph;
+        }
       }
       __syncwarp();
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+    for (int o = 16; o; o >>= 1) {
+      tot += __shfl_xor_sync(FULL, tot, o);
+      if (KPH) {
+        tk += __shfl_xor_sync(FULL, tk, o);
+        tph += __shfl_xor_sync(FULL, tph, o);
+      }
+    }
     if (__any_sync(FULL, undecided)) {
       if (lane == 0) {
         const int k = atomicAdd(plist_n + pi, 1);
         plist[(int64_t)pi * a.P + k] = p;
       }
     } else {
-      for (int j = lane; j < L; j += 32)
+      for (int j = lane; j < 3 * L; j += 32)
         if (wch[j]) atomicAdd(&bch[j], wch[j]);
-      if (lane == 0 && tot) {
+      if (lane == 0) {
         int64_t* c = a.counters + pi * a.counters_stride;
-        atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot);
+        if (KPH && tk) atomicAdd(reinterpret_cast<unsigned long long*>(c + 0), (unsigned long long)tk);
+        if (tot) atomicAdd(reinterpret_cast<unsigned long long*>(c + 1), (unsigned long long)tot);
+        if (KPH && tph) atomicAdd(reinterpret_cast<unsigned long long*>(c + 2), (unsigned long long)tph);
+        if (a.per_prompt) {
+          int64_t* pp = a.per_prompt + pi * a.per_prompt_stride + 4 * (int64_t)p;
+          pp[0] += tk;
+          pp[1] += tot;
+          pp[2] += tph;
+        }
       }
     }
   }
   __syncthreads();
   int64_t* c = a.counters + pi * a.counters_stride;
-  for (int j = threadIdx.x; j < L; j += blockDim.x)
-    if (bch[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + L + j), (unsigned long long)bch[j]);
-  if (a.given && blockIdx.x == 0) {  // the upstream counts, once per prediction stream
+  for (int j = threadIdx.x; j < 3 * L; j += blockDim.x)
+    if (bch[j]) atomicAdd(reinterpret_cast<unsigned long long*>(c + 4 + j), (unsigned long long)bch[j]);
+  if (!KPH && a.given && blockIdx.x == 0) {  // the upstream counts, once per prediction stream
     const int64_t* g = a.given + (int64_t)pi * (2 + 2 * L);
     for (int j = threadIdx.x; j < 2 + 2 * L; j += blockDim.x) {
       const int idx = j == 0 ? 0 : j == 1 ? 2 : j < 2 + L ? 4 + (j - 2) : 4 + 2 * L + (j - 2 - L);
@@ -1600,12 +1623,12 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
     return moeb::check_launch("k_cache_sim_warp");
   }
   const size_t smem = head + (size_t)nw * (32 / G) * a.sim_bytes;
-  if (W == 1 && G == 16 && a.given && !a.per_prompt && !a.hits && !a.any_cov && stack_mode()) {
+  if (W == 1 && G == 16 && !a.hits && !a.any_cov && stack_mode()) {
     // K1s over every prompt, then the exact kernel over the undecided ones
     const int dmax = 4;
     int H = 64;
     while (H < (dmax + 1) * a.L + 64) H <<= 1;
-    const size_t lbytes = (size_t)((4 * a.L + 15) / 16) * 16;
+    const size_t lbytes = (size_t)((12 * a.L + 15) / 16) * 16;
     const size_t ssmem = lbytes + 4 * ((size_t)H * 20 + lbytes);
     if ((int)ssmem <= max_block) {
       int32_t* pl = nullptr;
@@ -1614,8 +1637,11 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
         return moeb::fail(MOEB_ECUDA, "cudaMallocAsync(%zu) for the undecided-prompt list", plbytes);
       int32_t* pln = pl + (size_t)a.n_preds * a.P;
       cudaMemsetAsync(pln, 0, sizeof(int32_t) * a.n_preds, s);
-      cudaFuncSetAttribute(k_stack_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
-      k_stack_replay<<<dim3((unsigned)((a.P + 3) / 4), (unsigned)a.n_preds), 128, ssmem, s>>>(
+      // with upstream counts (and no per-prompt output) neither kernel computes them
+      const bool given = a.given && !a.per_prompt;
+      auto ks = given ? k_stack_replay<false> : k_stack_replay<true>;
+      cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+      ks<<<dim3((unsigned)((a.P + 3) / 4), (unsigned)a.n_preds), 128, ssmem, s>>>(
           a, H, dmax, pl, pln);
       int rc = moeb::check_launch("k_stack_replay");
       if (rc == 0) {
@@ -1623,7 +1649,7 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
         b.given = nullptr;  // added by k_stack_replay
         b.plist = pl;
         b.plist_n = pln;
-        auto k = k_cache_sim_warp<W, ES, G, false, false>;
+        auto k = given ? k_cache_sim_warp<W, ES, G, false, false> : k_cache_sim_warp<W, ES, G, false>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const int spb = nw * (32 / G);
         k<<<dim3((unsigned)((a.P + spb - 1) / spb), (unsigned)a.n_preds), 32 * nw, smem, s>>>(b);

@@ -1,5 +1,6 @@
 """K1s (stack-distance replay, `k_stack_replay`) + the exact kernel over its
-undecided prompts give exactly the exact kernel's counters: every capacity
+undecided prompts give exactly the exact kernel's counters and per-prompt
+counters, with and without upstream (fused) access counts: every capacity
 from 1 to all keys, predictions that are empty / learned / over the budget /
 unbounded, ragged prompts, warm-up 0 and 8, several geometries."""
 import numpy as np
@@ -55,10 +56,12 @@ def test_stack_replay_equals_exact(geom, ragged, warmup, monkeypatch):
     for masks, unbounded in ((learned, False), (None, False), (wide, False), (ones, True)):
         streams = [(masks, None, unbounded)]
         monkeypatch.setenv("MOEB_K1_STACK", "0")
-        want, _, _ = m.cache_replay(packed, streams, caps, warmup, budget, want_per_prompt=False)
+        want, want_pp, _ = m.cache_replay(packed, streams, caps, warmup, budget)
         given = _given(want, L)
         monkeypatch.setenv("MOEB_K1_STACK", "1")
         got, _, _ = m.cache_replay(packed, streams, caps, warmup, budget, want_per_prompt=False,
                                    given_counts=given)
+        got_pp, pp, _ = m.cache_replay(packed, streams, caps, warmup, budget)
         torch.cuda.synchronize()
         assert torch.equal(got, want), (masks is None, unbounded)
+        assert torch.equal(got_pp, want) and torch.equal(pp, want_pp), (masks is None, unbounded)
