@@ -503,8 +503,9 @@ def run_ours(args):
             "config": _config(P, rows, cap, world),
             "e2e": {"value": e2e_value, "unit": "trace tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            # per chunk: K3 (k_linear_predict) + K7 (k_metrics64) + K1 (k_cache_sim_warp)
-            "gpu_launches": 3 * len(pipe.bounds) * args.steps,
+            # per chunk: K3 (k_linear_predict) + K7 (k_metrics64) + K1s (k_stack_replay)
+            # + K1 (k_cache_sim_warp over the prompts K1s left undecided)
+            "gpu_launches": 4 * len(pipe.bounds) * args.steps,
             "pipeline": {"chunks": len(pipe.bounds), "streams": "predict || replay (|| H2D in e2e)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
