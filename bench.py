@@ -311,13 +311,19 @@ def run_ours(args):
     mc = m.MetricCounts.from_vector(vec.cpu().numpy(), E)
 
     # --- end to end through the public API with host buffers ---
-    # StreamingReplay: every step copies its 528 MB of pinned host trace rows
-    # to the device (copy stream, double-buffered so step i+1's copy overlaps
+    # StreamingReplay: every step copies its pinned host trace rows (396 MB of
+    # expert ids, or 528 MB of masks with --e2e-format masks) to the device (copy stream, double-buffered so step i+1's copy overlaps
     # step i's compute) and reads its counters + metrics back to pinned host
     # memory; all inside the timed region.
-    truth_host = packed.truth.cpu().pin_memory()
+    # Host batches in the compact wire format: each row's k expert ids as u8
+    # (the reference trace's own representation, 6 B/row instead of an 8-byte
+    # mask), decoded into masks on the device after the copy.
+    if args.e2e_format == "ids":
+        truth_host = m.masks_to_ids(packed.truth, C2["top_k"]).cpu().pin_memory()
+    else:
+        truth_host = packed.truth.cpu().pin_memory()
     sr = m.StreamingReplay(shape, packed.row_off_host, packed.prompt_ids, dev)
-    h2d = truth_host.numel() * 8
+    h2d = truth_host.numel() * truth_host.element_size()
     d2h = (4 + 3 * L) * 8 + (3 * E + 3) * 8
 
     def e2e_run(n):
@@ -502,7 +508,9 @@ def run_ours(args):
             "data": "synthetic (reference generator, bit-identical, generated on device)",
             "config": _config(P, rows, cap, world),
             "e2e": {"value": e2e_value, "unit": "trace tokens/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "host_format": ("u8 expert ids [rows][6], decoded on device (k_ids_to_masks)"
+                                    if args.e2e_format == "ids" else "int64 mask rows")},
             # per chunk: K3 (k_linear_predict) + K7 (k_metrics64) + K1s (k_stack_replay)
             # + K1 (k_cache_sim_warp over the prompts K1s left undecided)
             "gpu_launches": 4 * len(pipe.bounds) * args.steps,
@@ -535,6 +543,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--prompts", type=int, default=C2["prompts"])
+    ap.add_argument("--e2e-format", choices=["ids", "masks"], default="ids",
+                    help="host batch format of the end-to-end run: u8 expert ids (6 B/row, "
+                         "decoded on device) or the 8-byte mask rows")
     ap.add_argument("--chunks", type=int, default=1,
                     help="prompt chunks pipelined across the predict / replay streams")
     ap.add_argument("--no-cpu-baseline", action="store_true")

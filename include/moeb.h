@@ -180,6 +180,18 @@ int moeb_metrics(const uint64_t* pred, const uint64_t* truth, const int64_t* pro
                  void* stream);
 
 /*
+ * Compact trace rows (the host->device wire format of StreamingReplay): k
+ * expert ids per row, u8, ascending, 0xff = none, E <= 64 (a row of the
+ * reference trace is its sorted expert-id tuple, core.py:64-90).
+ *  moeb_ids_to_masks: ids [rows][k] -> masks [rows]; *bad = 1 if an id >= E
+ *  moeb_masks_to_ids: masks [rows] -> ids [rows][k]; *bad = 1 if a row has > k
+ */
+int moeb_ids_to_masks(const uint8_t* ids, int64_t rows, int k, int E, uint64_t* masks, int* bad,
+                      void* stream);
+int moeb_masks_to_ids(const uint64_t* masks, int64_t rows, int k, uint8_t* ids, int* bad,
+                      void* stream);
+
+/*
  * Rule-based predictors as mask tables (predictors.py:57-139).
  *  kind 0 lru_only (empty), 1 oracle (truth truncated to the `budget` lowest
  *  ids, :80-81), 2 next_layer_all (all E), 3 per-layer table

@@ -40,6 +40,8 @@ _SIGS = {
     "moeb_cache_ops": [P, P, I64, I32, I32, I64, I32, P, P],
     "moeb_linear_predict": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P],
     "moeb_linear_predict_counts": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P, P],
+    "moeb_ids_to_masks": [P, I64, I32, I32, P, P, P],
+    "moeb_masks_to_ids": [P, I64, I32, P, P, P],
     "moeb_mask_head": [P, I64, I32, I32, I32, P, P],
     "moeb_metrics": [P, P, P, I32, I32, I32, I32, P, P],
     "moeb_policy_masks": [I32, P, I64, I32, I32, I32, P, P, P],

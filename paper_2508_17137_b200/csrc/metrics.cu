@@ -381,3 +381,65 @@ extern "C" int moeb_policy_masks(int kind, const uint64_t* truth, int64_t rows, 
   }
   return moeb::check_launch("k_policy_masks");
 }
+
+// Compact trace rows for host->device transfer: k expert ids per row (u8,
+// ascending, 0xff = none; E <= 64) <-> one-word expert masks. A row of the
+// reference trace is its sorted expert-id tuple (core.py:64-90), so the ids
+// are the natural wire format: k bytes per row instead of an 8-byte mask.
+namespace {
+__global__ void k_ids_to_masks(const uint8_t* __restrict__ ids, int64_t rows, int k, int E,
+                               uint64_t* __restrict__ masks, int* __restrict__ bad) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t m = 0;
+    for (int j = 0; j < k; ++j) {
+      const int e = ids[r * k + j];
+      if (e == 0xff) continue;
+      if (e >= E) {
+        atomicExch(bad, 1);
+        continue;
+      }
+      m |= 1ull << e;
+    }
+    masks[r] = m;
+  }
+}
+
+__global__ void k_masks_to_ids(const uint64_t* __restrict__ masks, int64_t rows, int k,
+                               uint8_t* __restrict__ ids, int* __restrict__ bad) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t m = masks[r];
+    if (__popcll(m) > k) atomicExch(bad, 1);
+    for (int j = 0; j < k; ++j) {
+      int e = 0xff;
+      if (m) {
+        e = __ffsll((long long)m) - 1;
+        m &= m - 1;
+      }
+      ids[r * k + j] = (uint8_t)e;
+    }
+  }
+}
+}  // namespace
+
+extern "C" int moeb_ids_to_masks(const uint8_t* ids, int64_t rows, int k, int E, uint64_t* masks,
+                                 int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(ids && masks && bad && rows >= 0 && k >= 1 && k <= 64 && E >= 1 && E <= 64,
+               "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_ids_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(ids, rows, k, E, masks, bad);
+  return moeb::check_launch("k_ids_to_masks");
+}
+
+extern "C" int moeb_masks_to_ids(const uint64_t* masks, int64_t rows, int k, uint8_t* ids, int* bad,
+                                 void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(ids && masks && bad && rows >= 0 && k >= 1 && k <= 64, "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_masks_to_ids<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, ids, bad);
+  return moeb::check_launch("k_masks_to_ids");
+}

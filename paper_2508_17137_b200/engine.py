@@ -19,7 +19,7 @@ from . import _native as nat
 from .cache import POLICIES, CacheConfig
 from .core import ConfigError, ModelShape, RangeError
 from .metrics import MetricCounts, mask_metrics, metric_vector
-from .traces import PackedTraces, pack_traces
+from .traces import PackedTraces, ids_to_masks, pack_traces
 
 
 @dataclass(frozen=True)
@@ -335,6 +335,11 @@ class StreamingReplay:
     row-balanced prompt ranges and the predictor starts on each range as it
     lands (the replay needs the whole batch's masks).
 
+    A host batch is either the int64 mask rows [rows][W] or, for E <= 64, the
+    compact wire format ``masks_to_ids`` produces (u8 [rows][k] expert ids,
+    k / 8 of the bytes for k = 6): the ids are copied and decoded into masks on
+    the copy stream (``ids_bad`` turns 1 if an id was >= E).
+
     ``run`` returns, per batch, pinned host tensors (counters [C][4+3L],
     metrics [3E+3] or None), valid after ``torch.cuda.synchronize()`` (or the
     returned event)."""
@@ -351,6 +356,8 @@ class StreamingReplay:
                                   np.asarray(row_off_host, dtype=np.int64),
                                   np.asarray(prompt_ids, dtype=np.int64), token_ids)
                      for _ in range(2)]
+        self.ids_bufs = [None, None]  # device staging for compact (id) batches
+        self.ids_bad = torch.zeros(1, dtype=torch.int32, device=dev)
         self.s_copy = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev, priority=-1)
         self.s_met = torch.cuda.Stream(dev, priority=0)
@@ -389,20 +396,34 @@ class StreamingReplay:
             empty = getattr(predictor, "empty", False) and not metrics
             split = i == 0 and len(self.first_views) > 1 and not empty
             parts = []
+            compact = hb.dtype == torch.uint8  # [rows][k] expert ids, decoded on device
             with torch.cuda.stream(self.s_copy):
                 if freed[b] is not None:
                     self.s_copy.wait_event(freed[b])
+                if compact:
+                    ib = self.ids_bufs[b]
+                    if ib is None or ib.shape != hb.shape:
+                        ib = self.ids_bufs[b] = torch.empty(hb.shape, dtype=torch.uint8,
+                                                            device=dev)
+
+                def land(dst, r0, r1):
+                    if compact:
+                        ib[r0:r1].copy_(hb[r0:r1], non_blocking=True)
+                        ids_to_masks(ib[r0:r1], E, dst, self.ids_bad)
+                    else:
+                        dst.copy_(hb[r0:r1], non_blocking=True)
+
                 if split:  # first batch: copy range by range, predict as each lands
                     r0 = 0
                     for v in self.first_views:
                         r1 = r0 + v.rows
-                        v.truth.copy_(hb[r0:r1], non_blocking=True)
+                        land(v.truth, r0, r1)
                         e = torch.cuda.Event()
                         e.record(self.s_copy)
                         parts.append(e)
                         r0 = r1
                 else:
-                    buf.truth.copy_(hb, non_blocking=True)
+                    land(buf.truth, 0, buf.rows)
                 copied[b].record(self.s_copy)
             with torch.cuda.stream(self.s_comp):
                 if not split:

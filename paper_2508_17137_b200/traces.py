@@ -269,3 +269,24 @@ def generate_packed(config: GeneratorConfig, device=None) -> PackedTraces:
 def generate_synthetic(config: GeneratorConfig) -> list[PromptTrace]:
     """traceio.generate_synthetic (traceio.py:277-283), computed on device."""
     return generate_packed(config).unpack()
+
+
+def masks_to_ids(truth: torch.Tensor, k: int) -> torch.Tensor:
+    """One-word expert masks [rows] (or [rows][1]) -> the compact wire format:
+    k expert ids per row, u8, ascending, 0xff padding (moeb_masks_to_ids)."""
+    t = truth.reshape(-1).contiguous()
+    ids = torch.empty((t.numel(), int(k)), dtype=torch.uint8, device=t.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=t.device)
+    nat.call("moeb_masks_to_ids", nat.ptr(t), t.numel(), int(k), nat.ptr(ids), nat.ptr(bad),
+             nat.stream_ptr())
+    if int(bad.item()):
+        raise RangeError(f"a row has more than {k} experts")
+    return ids
+
+
+def ids_to_masks(ids: torch.Tensor, num_experts: int, out: torch.Tensor, bad: torch.Tensor):
+    """Device decode of the compact rows into masks (moeb_ids_to_masks); bad[0]
+    is set to 1 (asynchronously) if an id is >= num_experts."""
+    nat.call("moeb_ids_to_masks", nat.ptr(ids), ids.shape[0], ids.shape[1], int(num_experts),
+             nat.ptr(out), nat.ptr(bad), nat.stream_ptr())
+    return out
