@@ -1588,6 +1588,22 @@ inline bool stack_mode() {
   return !(env && env[0] == '0');
 }
 
+// The undecided-prompt list comes from the stream-ordered allocator; keep its
+// freed blocks in the device's default pool (release threshold = max) so a
+// synchronize between calls does not hand them back to the driver and make
+// the next call map fresh memory.
+inline void keep_pool_memory() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 template <int W, int ES, int G>
 int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block);
 
@@ -1631,6 +1647,7 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
     const size_t lbytes = (size_t)((12 * a.L + 15) / 16) * 16;
     const size_t ssmem = lbytes + 4 * ((size_t)H * 20 + lbytes);
     if ((int)ssmem <= max_block) {
+      keep_pool_memory();
       int32_t* pl = nullptr;
       const size_t plbytes = sizeof(int32_t) * ((size_t)a.n_preds * a.P + a.n_preds);
       if (cudaMallocAsync(reinterpret_cast<void**>(&pl), plbytes, s) != cudaSuccess)

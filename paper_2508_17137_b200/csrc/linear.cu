@@ -187,16 +187,20 @@ __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(cons
         for (int it = 0; it <= (KT > 0 ? KT : k); ++it) {
           uint32_t bk;
           bool found;
+          // four independent partial reductions: a dependency chain of NS/4 + 2
+          // instead of NS (the passes are latency-bound)
           if (it == 0) {
-            bk = key[0];
+            uint32_t b4[4] = {key[0], key[1], key[2], key[3]};
 #pragma unroll
-            for (int s = 1; s < NS; ++s) bk = max(bk, key[s]);
+            for (int s = 4; s < NS; ++s) b4[s & 3] = max(b4[s & 3], key[s]);
+            bk = max(max(b4[0], b4[1]), max(b4[2], b4[3]));
             found = true;
           } else {  // largest key below this lane's bound
             const uint32_t bm1 = bound - 1u;
-            uint32_t tm = 0xffffffffu;
+            uint32_t t4[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
 #pragma unroll
-            for (int s = 0; s < NS; ++s) tm = min(tm, bm1 - key[s]);
+            for (int s = 0; s < NS; ++s) t4[s & 3] = min(t4[s & 3], bm1 - key[s]);
+            const uint32_t tm = min(min(t4[0], t4[1]), min(t4[2], t4[3]));
             found = bound != 0u && tm < bound;
             bk = bm1 - tm;
           }
