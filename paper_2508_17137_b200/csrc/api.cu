@@ -1,7 +1,10 @@
 // Error reporting, version and device checks for the C ABI (include/moeb.h).
 #include <cstdarg>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <string>
+#include <utility>
 
 #include "common.cuh"
 
@@ -46,6 +49,21 @@ static int device_attr(cudaDeviceAttr attr) {
 int max_smem_per_block() { return device_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin); }
 int max_smem_per_sm() { return device_attr(cudaDevAttrMaxSharedMemoryPerMultiprocessor); }
 int num_sms() { return device_attr(cudaDevAttrMultiProcessorCount); }
+
+// cudaFuncSetAttribute costs tens of microseconds of host time per call;
+// remember the largest dynamic shared memory already granted per (device,
+// kernel) and only call it to raise the limit.
+bool smem_attr_needed(const void* f, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> granted;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  int& g = granted[{dev, f}];
+  if (bytes <= g) return false;
+  g = bytes;
+  return true;
+}
 
 }  // namespace moeb
 

@@ -1372,7 +1372,7 @@ int launch_lfu_warp(SimArgs a, cudaStream_t s) {
                       a.sim_bytes, max_block);
   const size_t smem = head + (size_t)nw * a.sim_bytes;
   auto k = (a.hits || a.any_cov) ? k_cache_sim_lfu_warp<W, true> : k_cache_sim_lfu_warp<W, false>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  moeb::set_smem(k, (int)smem);
   const dim3 blocks((unsigned)((a.P + nw - 1) / nw), (unsigned)a.n_preds);
   k<<<blocks, 32 * nw, smem, s>>>(a);
   return moeb::check_launch("k_cache_sim_lfu_warp");
@@ -1380,7 +1380,7 @@ int launch_lfu_warp(SimArgs a, cudaStream_t s) {
 
 template <class K>
 int launch_kernel(K k, const SimArgs& a, int tpb, size_t smem, cudaStream_t s) {
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  moeb::set_smem(k, (int)smem);
   const dim3 blocks((unsigned)((a.P + tpb - 1) / tpb), (unsigned)a.n_preds);
   k<<<blocks, tpb, smem, s>>>(a);
   return moeb::check_launch("k_cache_sim");
@@ -1634,7 +1634,7 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
     const size_t smem1 = head + (size_t)a.sim_bytes;
     auto k1 = (a.hits || a.any_cov) ? k_cache_sim_warp<W, ES, 32, true>
                                     : k_cache_sim_warp<W, ES, 32, false>;
-    cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+    moeb::set_smem(k1, (int)smem1);
     k1<<<dim3((unsigned)a.P, (unsigned)a.n_preds), 32, smem1, s>>>(a);
     return moeb::check_launch("k_cache_sim_warp");
   }
@@ -1657,7 +1657,7 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
       // with upstream counts (and no per-prompt output) neither kernel computes them
       const bool given = a.given && !a.per_prompt;
       auto ks = given ? k_stack_replay<false> : k_stack_replay<true>;
-      cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+      moeb::set_smem(ks, (int)ssmem);
       ks<<<dim3((unsigned)((a.P + 3) / 4), (unsigned)a.n_preds), 128, ssmem, s>>>(
           a, H, dmax, pl, pln);
       int rc = moeb::check_launch("k_stack_replay");
@@ -1667,7 +1667,7 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
         b.plist = pl;
         b.plist_n = pln;
         auto k = given ? k_cache_sim_warp<W, ES, G, false, false> : k_cache_sim_warp<W, ES, G, false>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        moeb::set_smem(k, (int)smem);
         const int spb = nw * (32 / G);
         k<<<dim3((unsigned)((a.P + spb - 1) / spb), (unsigned)a.n_preds), 32 * nw, smem, s>>>(b);
         rc = moeb::check_launch("k_cache_sim_warp");
@@ -1679,7 +1679,7 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
   auto k = (a.hits || a.any_cov) ? k_cache_sim_warp<W, ES, G, true>
            : (a.given && !a.per_prompt) ? k_cache_sim_warp<W, ES, G, false, false>
                                         : k_cache_sim_warp<W, ES, G, false>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  moeb::set_smem(k, (int)smem);
   const int spb = nw * (32 / G);
   const dim3 blocks((unsigned)((a.P + spb - 1) / spb), (unsigned)a.n_preds);
   k<<<blocks, 32 * nw, smem, s>>>(a);
@@ -1793,11 +1793,11 @@ static int launch_ops(SimArgs& a, int policy, const int32_t* ops, const int32_t*
     return moeb::fail(MOEB_ESMEM, "cache state %zu B exceeds shared memory", smem);
   if (policy == MOEB_POLICY_LRU) {
     auto k = k_cache_ops<W, LruState<W, -1, true>>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    moeb::set_smem(k, (int)smem);
     k<<<1, 32, smem, s>>>(a, ops, keys, n, results);
   } else {
     auto k = k_cache_ops<W, LfuState<W, true>>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    moeb::set_smem(k, (int)smem);
     k<<<1, 32, smem, s>>>(a, ops, keys, n, results);
   }
   return moeb::check_launch("k_cache_ops");

@@ -24,6 +24,15 @@ int max_smem_per_block();
 int max_smem_per_sm();
 int num_sms();
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when it raises the
+// kernel's limit on this device (the call itself costs host time per launch)
+bool smem_attr_needed(const void* f, int bytes);
+template <class F>
+inline void set_smem(F* f, int bytes) {
+  if (smem_attr_needed(reinterpret_cast<const void*>(f), bytes))
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 }  // namespace moeb
 
 #define MOEB_REQUIRE(cond, ...)                       \

@@ -321,7 +321,7 @@ int launch_k3(const LinArgs& a, cudaStream_t s) {
                                    : kb == 8 ? k_linear_predict<TPS, true, 8>
                                              : k_linear_predict<TPS, true, 0>)
                         : k_linear_predict<TPS, false, 0>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  moeb::set_smem(kern, (int)smem);
   // persistent: at most 2 CTAs per SM, each looping over groups of kStreams streams
   const int64_t groups = ((int64_t)a.L * a.P + C::kStreams - 1) / C::kStreams;
   const int64_t blocks = groups < 2LL * moeb::num_sms() ? groups : 2LL * moeb::num_sms();
