@@ -891,9 +891,17 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
         const unsigned vb = (__ballot_sync(FULL, valid) >> gbase) & glow;
         const bool ok1 = want & (__popc(vb) >= e);
         const bool victim = ok1 & valid & (__popc(vb & ((1u << hl) - 1)) < e);
-        const int vl = st.layer_of(key);
-        const int ve = st.expert_of(key, vl);
-        const bool bad = victim & (vl == l) & (((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull) != 0);
+        int vl = 0, ve = 0;
+        bool bad = false;
+        if (W == 1) {  // one mask word: decode unconditionally
+          vl = st.layer_of(key);
+          ve = st.expert_of(key, vl);
+          bad = victim & (vl == l) & (((S[0] >> (ve & 63)) & 1ull) != 0);
+        } else if (victim) {
+          vl = st.layer_of(key);
+          ve = st.expert_of(key, vl);
+          bad = vl == l && ((word_get<W>(S, ve >> 6) >> (ve & 63)) & 1ull);
+        }
         const bool anybad = ((__ballot_sync(FULL, bad) >> gbase) & glow) != 0u;
         if (ok1 & anybad) fallback = true;
         applied = ok1 & !anybad;
@@ -1001,16 +1009,23 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
           }
         }
         st.tail += ns;
-        // R_l |= S as shared atomics: on this path no victim is in S, so the
-        // victims' atomicAnd and this OR commute and need no barrier between
-        if (hl < W) {
-          uint64_t v = 0;
+        if (W == 1) {
+          // R_l |= S as shared atomics: on this path no victim is in S, so the
+          // victims' atomicAnd and this OR commute and need no barrier between
+          if (hl == 0) {
+            unsigned int* rw = reinterpret_cast<unsigned int*>(R + l);
+            if ((uint32_t)S[0]) atomicOr(rw, (uint32_t)S[0]);
+            if ((uint32_t)(S[0] >> 32)) atomicOr(rw + 1, (uint32_t)(S[0] >> 32));
+          }
+        } else {
+          __syncwarp(gmask);
+          if (hl < W) {
+            uint64_t v = 0;
 #pragma unroll
-          for (int w = 0; w < W; ++w)
-            if (w == hl) v = S[w];
-          unsigned int* rw = reinterpret_cast<unsigned int*>(R + l * W + hl);
-          if ((uint32_t)v) atomicOr(rw, (uint32_t)v);
-          if ((uint32_t)(v >> 32)) atomicOr(rw + 1, (uint32_t)(v >> 32));
+            for (int w = 0; w < W; ++w)
+              if (w == hl) v = R[l * W + w] | S[w];
+            R[l * W + hl] = v;
+          }
         }
         __syncwarp(gmask);
         ch = popc_w<W>(Hm);
@@ -1536,6 +1551,8 @@ __global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, in
           tph += ph;
         }
       }
+      // an undecided prompt goes to the exact kernel anyway: stop here
+      if (__any_sync(FULL, undecided)) break;
       __syncwarp();
     }
 #pragma unroll
@@ -1639,7 +1656,13 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
     return moeb::check_launch("k_cache_sim_warp");
   }
   const size_t smem = head + (size_t)nw * (32 / G) * a.sim_bytes;
-  if (W == 1 && G == 16 && !a.hits && !a.any_cov && stack_mode()) {
+  // K1s pays off when rows carry predictions: without them (lru_only) a row
+  // is just the top-k truth keys, one token's keys (L * k) can stay below
+  // the capacity, and too many touches need the span unions; the exact
+  // kernel is cheap for those rows anyway.
+  bool all_pred = true;
+  for (int i = 0; i < a.n_preds; ++i) all_pred = all_pred && a.preds[i] != nullptr;
+  if (W == 1 && G == 16 && !a.hits && !a.any_cov && all_pred && stack_mode()) {
     // K1s over every prompt, then the exact kernel over the undecided ones
     const int dmax = 4;
     int H = 64;
