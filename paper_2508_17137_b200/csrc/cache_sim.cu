@@ -1494,7 +1494,10 @@ __global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, in
       __syncwarp();
       if (measured) {
         int ch = __popcll(T & K);  // prefetched in this row, then touched: hits
-        uint64_t tm = T & ~K;
+        // every other touch misses when even the L-1 rows since the previous
+        // token of this layer hold >= C keys (D >= that sum for d = 1 and for
+        // d >= 2), or when there is no previous token: skip the per-key work
+        uint64_t tm = (i < L || pn(i - 1) - pn(i - L) >= cap) ? 0ull : (T & ~K);
         while (tm) {
           const int x = __ffsll((long long)tm) - 1;
           tm &= tm - 1;
