@@ -65,3 +65,31 @@ def test_stack_replay_equals_exact(geom, ragged, warmup, monkeypatch):
         torch.cuda.synchronize()
         assert torch.equal(got, want), (masks is None, unbounded)
         assert torch.equal(got_pp, want) and torch.equal(pp, want_pp), (masks is None, unbounded)
+
+
+def test_stack_replay_several_streams(monkeypatch):
+    """Several prediction streams in one call (blockIdx.y): per-stream lists
+    of undecided prompts and per-stream upstream counts."""
+    import paper_2508_17137_b200 as m
+    m.load_library()
+    shape = m.ModelShape(26, 64, 6)
+    L = 26
+    packed = _packed(m, shape, 70, 50, 9, True)
+    w = np.random.default_rng(4).normal(0.0, 0.01, (64, 91))
+    model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
+    learned = m.make_predictor("learned_linear", shape, model=model).predict_masks(packed, 6, 8)
+    oracle = packed.truth.clone()
+    rng = np.random.default_rng(5)
+    noise = torch.from_numpy(rng.integers(0, 2**62, packed.rows, dtype=np.int64)).cuda()
+    streams = [(learned, None, False), (oracle, None, False), (noise.reshape(-1, 1), None, False)]
+    caps = [3, 83, 166, 400, 1000]
+    monkeypatch.setenv("MOEB_K1_STACK", "0")
+    want, want_pp, _ = m.cache_replay(packed, streams, caps, 8, 6)
+    given = torch.stack([_given(want[i:i + 1], L)[0] for i in range(3)])
+    monkeypatch.setenv("MOEB_K1_STACK", "1")
+    got, _, _ = m.cache_replay(packed, streams, caps, 8, 6, want_per_prompt=False,
+                               given_counts=given)
+    got_pp, pp, _ = m.cache_replay(packed, streams, caps, 8, 6)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    assert torch.equal(got_pp, want) and torch.equal(pp, want_pp)
