@@ -1461,6 +1461,7 @@ __global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, in
     const uint64_t* __restrict__ tr = a.truth + r0;
     const uint64_t* __restrict__ pr = pred ? pred + r0 : nullptr;
     bool undecided = false;
+    int unions = 0;  // span-union evaluations by this lane (bounded: see below)
     uint32_t carry = 0;
     long long tot = 0, tk = 0, tph = 0;
     auto pn = [&](int q) -> uint32_t { return q < 0 ? 0u : rP[q & hm]; };
@@ -1522,6 +1523,12 @@ __global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, in
                 jf = j;
                 break;
               }
+            }
+            // a prompt that keeps needing span unions (large capacities) is
+            // cheaper in the exact kernel: give up on it after a few
+            if (!none && ++unions > 8) {
+              undecided = true;
+              none = true;
             }
             if (!none) {
               const int j = jf ? jf : dmax;  // exact union over the span (a lower bound if !jf)
