@@ -12,11 +12,10 @@
 namespace {
 
 // E <= 64 (one mask word): bit-sliced ("vertical") counters. Each lane owns
-// one row per iteration and adds its TP / FP / FN masks into 6 bit-planes
-// each (carry-save, 2 ops per plane); every 63 rows per lane the planes are
-// drained into per-expert counts with ballot+popc per (expert, plane). That
-// is ~5 warp instructions per row instead of ~22 for per-row ballots.
-constexpr int kPlanes = 6;
+// one row per iteration and adds its TP / FP / FN masks into 8 bit-planes
+// each (carry-save, 2 ops per plane); every 255 rows per lane the planes are
+// drained into per-expert counts with ballot+popc per (expert, plane).
+constexpr int kPlanes = 8;
 __device__ __forceinline__ void vc_add(uint64_t (&v)[kPlanes], uint64_t x) {
 #pragma unroll
   for (int i = 0; i < kPlanes; ++i) {
