@@ -274,6 +274,11 @@ def run_ours(args):
         return counters, vec
 
     # --- warm-up ---
+    # The clock sampler (an nvidia-smi process) starts before the warm-up so
+    # its NVML start-up is over before the timed region; it keeps sampling
+    # through the timed region.
+    clocks = ClockSampler(torch.cuda.current_device()).__enter__()
+    time.sleep(1.0)
     for _ in range(args.warmup):
         counters, vec = step()
     torch.cuda.synchronize()
@@ -281,7 +286,7 @@ def run_ours(args):
     # --- timed region: device clock, max over ranks ---
     hbm, bf16, bf16_sus, peak_kind = _peaks()
     timing = []
-    with ClockSampler(torch.cuda.current_device()) as clocks:
+    try:
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -293,6 +298,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+    finally:
+        clocks.__exit__(None, None, None)
     ms = start.elapsed_time(end)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
