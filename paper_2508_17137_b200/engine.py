@@ -399,7 +399,9 @@ class StreamingReplay:
             compact = hb.dtype == torch.uint8  # [rows][k] expert ids, decoded on device
             with torch.cuda.stream(self.s_copy):
                 if freed[b] is not None:
-                    self.s_copy.wait_event(freed[b])
+                    for e in freed[b]:
+                        if e is not None:
+                            self.s_copy.wait_event(e)
                 if compact:
                     ib = self.ids_bufs[b]
                     if ib is None or ib.shape != hb.shape:
@@ -453,17 +455,21 @@ class StreamingReplay:
                 cnt, _, _ = cache_replay(buf, [(masks, cov, unbounded)], capacities, warmup,
                                          budget, policy, want_per_prompt=False, given_counts=gc)
                 ev = torch.cuda.Event()
-                if vec is not None and masks is not None:
-                    _overlapped_metrics(self.s_met, masks_ready, masks, buf, warmup, vec)
-                    # the metrics run beside the replay; both end before the
-                    # buffer is refilled or the vector read back
-                    self.s_comp.wait_stream(self.s_met)
                 ev.record(self.s_comp)
-                freed[b] = ev
                 c_h, v_h = outs[i]
                 c_h.copy_(cnt[0], non_blocking=True)
+                met_ev = None
                 if vec is not None:
-                    v_h.copy_(vec, non_blocking=True)
+                    # the metrics pass runs on its own (low-priority) stream and
+                    # is not waited for by the next batch's predictor, only by
+                    # the refill of this batch's buffer and its read-back
+                    _overlapped_metrics(self.s_met, masks_ready, masks, buf, warmup, vec)
+                    vec.record_stream(self.s_met)
+                    with torch.cuda.stream(self.s_met):
+                        v_h.copy_(vec, non_blocking=True)
+                        met_ev = torch.cuda.Event()
+                        met_ev.record(self.s_met)
+                freed[b] = (ev, met_ev)
                 if timing is not None:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(self.s_comp)
