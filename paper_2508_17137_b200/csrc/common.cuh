@@ -29,8 +29,12 @@ int num_sms();
 bool smem_attr_needed(const void* f, int bytes);
 template <class F>
 inline void set_smem(F* f, int bytes) {
-  if (smem_attr_needed(reinterpret_cast<const void*>(f), bytes))
+  if (smem_attr_needed(reinterpret_cast<const void*>(f), bytes)) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    // these kernels size their grids for full shared-memory residency
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+  }
 }
 
 }  // namespace moeb
