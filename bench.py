@@ -102,14 +102,14 @@ class ClockSampler:
         try:
             for line in open(self.path):
                 f = [x.strip() for x in line.split(",")]
-                if len(f) < 9:
+                if len(f) < 8:
                     continue
                 try:
                     sm.append(float(f[1]))
                     smax = float(f[2])
                 except ValueError:
                     continue
-                for n, v in zip(names, f[5:9]):
+                for n, v in zip(names, f[-4:]):
                     if v.lower() == "active":
                         reasons.add(n)
         except Exception:
