@@ -73,6 +73,7 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.path = None
+        self.out = None
 
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
@@ -80,10 +81,11 @@ class ClockSampler:
         if os.environ.get("MOEB_BENCH_NO_CLOCKS") == "1":  # diagnosis only
             return self
         try:
+            self.out = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                stdout=self.out, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
         return self
@@ -95,6 +97,10 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.proc = None
+        if self.out is not None:
+            self.out.close()
+            self.out = None
 
     def summary(self):
         sm, smax, reasons = [], None, set()
@@ -571,6 +577,16 @@ def main():
     ap.add_argument("--transformer-prompts", type=int, default=700,
                     help="C2 prompts replayed with the transformer predictor (0: skip)")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        # --gpus N without a torchrun environment: relaunch as N ranks on this node
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={29500 + os.getpid() % 1000}", os.path.abspath(__file__)]
+        os.execv(sys.executable, cmd + sys.argv[1:])
+    if world and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

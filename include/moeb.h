@@ -11,8 +11,13 @@
  *
  * Conventions
  *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
- *    unless the parameter says "host". The caller owns all memory; the
- *    library allocates nothing and holds no global mutable state.
+ *    unless the parameter says "host". The caller owns all memory: the
+ *    library allocates no device or host memory. Scratch space comes from a
+ *    caller-provided workspace sized by the matching *_workspace_bytes()
+ *    query. Process-wide state is limited to idempotent caches (per-(device,
+ *    kernel) function attributes already set, the cuTensorMapEncodeTiled
+ *    entry point) and constant tables uploaded once (the generator's PCG64
+ *    jump tables); no call's result depends on another call.
  *  - `stream` is a cudaStream_t passed as void*. Calls are stream-ordered and
  *    asynchronous; they return after enqueueing.
  *  - Return 0 on success, a nonzero MOEB_E* code on failure; a thread-local
@@ -77,14 +82,20 @@ int moeb_device_check(void);
  *                   measured_accesses, cache_hits, prediction_hits, uncovered
  *  hit_masks        [n_preds][n_caps][rows][W] (nullable): bit e set iff the
  *                   touch of truth expert e hit (warm-up rows included)
+ *  rows             host: prompt_row_off[n_prompts] (total trace rows)
+ *  workspace        [workspace_bytes] scratch, >= moeb_cache_sim_workspace_bytes
+ *                   (n_preds, n_prompts) for the stack-distance replay K1s (its
+ *                   undecided-prompt list); NULL / smaller -> every prompt is
+ *                   replayed by the exact kernel (same results, slower)
  *  Limit: every prompt has fewer than 2^31 - 64 rows (the caller checks).
  */
+size_t moeb_cache_sim_workspace_bytes(int n_preds, int n_prompts);
 int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* preds,
                    const uint8_t* const* covered, const int32_t* unbounded, int n_preds,
                    const int64_t* prompt_row_off, int n_prompts, int L, int E,
                    int warmup_tokens, const int64_t* capacities, int n_caps, int budget,
                    int policy, int64_t* counters, int64_t* per_prompt, uint64_t* hit_masks,
-                   void* stream);
+                   int64_t rows, void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * moeb_cache_sim with the cache-independent counters supplied by the caller:
@@ -99,7 +110,8 @@ int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* const* preds,
                            const int64_t* prompt_row_off, int n_prompts, int L, int E,
                            int warmup_tokens, const int64_t* capacities, int n_caps, int budget,
                            int policy, int64_t* counters, int64_t* per_prompt,
-                           uint64_t* hit_masks, const int64_t* given_counts, void* stream);
+                           uint64_t* hit_masks, const int64_t* given_counts, int64_t rows,
+                           void* workspace, size_t workspace_bytes, void* stream);
 
 /*
  * ExpertCache op stream (cache.py:58-154) for one cache, executed on device:
@@ -428,8 +440,8 @@ int moeb_check_grid(const int64_t* starts, int64_t n_prompts, int64_t n_rows,
  */
 int moeb_predictions_join(const int64_t* t_prompt, const int64_t* t_token, const int32_t* t_layer,
                           const uint64_t* t_masks, int64_t n_table, const int64_t* prompt_ids,
-                          const int64_t* prompt_row_off, int n_prompts, int L, int E,
-                          uint64_t* pred, uint8_t* covered, void* stream);
+                          const int64_t* prompt_row_off, int n_prompts, int64_t rows, int L,
+                          int E, uint64_t* pred, uint8_t* covered, void* stream);
 
 /*
  * Canonical writers on device. Both first size every line (lens), then the
@@ -444,11 +456,11 @@ int moeb_predictions_join(const int64_t* t_prompt, const int64_t* t_token, const
  *   ceil(n / 4096) + 1 int64.
  */
 int moeb_trace_csv_lengths(const uint64_t* truth, const int64_t* prompt_ids,
-                           const int64_t* prompt_row_off, int n_prompts, int L, int E,
-                           const int32_t* token_ids, int64_t* lens, void* stream);
+                           const int64_t* prompt_row_off, int n_prompts, int64_t rows, int L,
+                           int E, const int32_t* token_ids, int64_t* lens, void* stream);
 int moeb_trace_csv_write(const uint64_t* truth, const int64_t* prompt_ids,
-                         const int64_t* prompt_row_off, int n_prompts, int L, int E,
-                         const int32_t* token_ids, const int64_t* offsets, uint8_t* out,
+                         const int64_t* prompt_row_off, int n_prompts, int64_t rows, int L,
+                         int E, const int32_t* token_ids, const int64_t* offsets, uint8_t* out,
                          void* stream);
 int moeb_predictions_jsonl_lengths(const int64_t* t_prompt, const int64_t* t_token,
                                    const int32_t* t_layer, const uint64_t* t_masks, int64_t n,

@@ -34,9 +34,10 @@ P = ctypes.c_void_p
 I32, I64, DBL = ctypes.c_int, ctypes.c_int64, ctypes.c_double
 
 _SIGS = {
-    "moeb_cache_sim": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P, P],
+    "moeb_cache_sim": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P, I64, P,
+                       ctypes.c_size_t, P],
     "moeb_cache_sim_counted": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P,
-                               P, P],
+                               P, I64, P, ctypes.c_size_t, P],
     "moeb_cache_ops": [P, P, I64, I32, I32, I64, I32, P, P],
     "moeb_linear_predict": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P],
     "moeb_linear_predict_counts": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P, P],
@@ -69,9 +70,9 @@ _SIGS = {
     "moeb_keys_check": [P, P, P, P, I32, I64, P, P],
     "moeb_prompt_flags": [P, I64, P, P],
     "moeb_check_grid": [P, I64, I64, P, P, I32, P, P],
-    "moeb_predictions_join": [P, P, P, P, I64, P, P, I32, I32, I32, P, P, P],
-    "moeb_trace_csv_lengths": [P, P, P, I32, I32, I32, P, P, P],
-    "moeb_trace_csv_write": [P, P, P, I32, I32, I32, P, P, P, P],
+    "moeb_predictions_join": [P, P, P, P, I64, P, P, I32, I64, I32, I32, P, P, P],
+    "moeb_trace_csv_lengths": [P, P, P, I32, I64, I32, I32, P, P, P],
+    "moeb_trace_csv_write": [P, P, P, I32, I64, I32, I32, P, P, P, P],
     "moeb_predictions_jsonl_lengths": [P, P, P, P, I64, I32, P, P],
     "moeb_predictions_jsonl_write": [P, P, P, P, I64, I32, P, P, P],
     "moeb_exclusive_scan_i64": [P, I64, P, P, P],
@@ -87,7 +88,12 @@ _SIGS = {
     "moeb_device_check": [],
 }
 
-EXPORTS = tuple(_SIGS) + ("moeb_last_error", "moeb_linear_table_doubles")
+SIZE_QUERIES = {
+    "moeb_linear_table_doubles": [I32, I32],
+    "moeb_cache_sim_workspace_bytes": [I32, I32],
+}
+
+EXPORTS = tuple(_SIGS) + ("moeb_last_error",) + tuple(SIZE_QUERIES)
 
 
 def load_library(require_gpu: bool = True):
@@ -102,8 +108,10 @@ def load_library(require_gpu: bool = True):
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
-        lib.moeb_linear_table_doubles.argtypes = [I32, I32]
-        lib.moeb_linear_table_doubles.restype = ctypes.c_size_t
+        for name, args in SIZE_QUERIES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_size_t
         lib.moeb_last_error.argtypes = []
         lib.moeb_last_error.restype = ctypes.c_char_p
         _lib = lib
@@ -123,6 +131,14 @@ def call(name: str, *args) -> None:
     rc = getattr(lib, name)(*args)
     if rc != 0:
         raise NativeError(name, rc, lib.moeb_last_error().decode())
+
+
+def workspace(nbytes: int, device) -> torch.Tensor | None:
+    """Caller-owned scratch for an entry point that takes (workspace,
+    workspace_bytes); the library itself never allocates."""
+    if nbytes <= 0:
+        return None
+    return torch.empty(int(nbytes), dtype=torch.uint8, device=device)
 
 
 def ptr(t):

@@ -67,6 +67,9 @@ struct SimArgs {
   // i < plist_n[pi] (the stack-distance replay's undecided prompts)
   const int32_t* plist;
   const int32_t* plist_n;
+  // caller workspace (moeb_cache_sim_workspace_bytes), host-side use only
+  void* ws;
+  size_t ws_bytes;
   // per-simulation shared-memory layout (bytes)
   int off_r, off_q, off_k, off_c, sim_bytes;
   uint32_t magic;  // layer_of(key) = (key * magic) >> 22
@@ -1615,22 +1618,6 @@ inline bool stack_mode() {
   return !(env && env[0] == '0');
 }
 
-// The undecided-prompt list comes from the stream-ordered allocator; keep its
-// freed blocks in the device's default pool (release threshold = max) so a
-// synchronize between calls does not hand them back to the driver and make
-// the next call map fresh memory.
-inline void keep_pool_memory() {
-  static bool done[64] = {};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[dev] = true;
-}
-
 template <int W, int ES, int G>
 int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block);
 
@@ -1679,14 +1666,15 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
     while (H < (dmax + 1) * a.L + 64) H <<= 1;
     const size_t lbytes = (size_t)((12 * a.L + 15) / 16) * 16;
     const size_t ssmem = lbytes + 4 * ((size_t)H * 20 + lbytes);
-    if ((int)ssmem <= max_block) {
-      keep_pool_memory();
-      int32_t* pl = nullptr;
-      const size_t plbytes = sizeof(int32_t) * ((size_t)a.n_preds * a.P + a.n_preds);
-      if (cudaMallocAsync(reinterpret_cast<void**>(&pl), plbytes, s) != cudaSuccess)
-        return moeb::fail(MOEB_ECUDA, "cudaMallocAsync(%zu) for the undecided-prompt list", plbytes);
+    // the undecided-prompt list lives in the caller's workspace
+    // (moeb_cache_sim_workspace_bytes); without one every prompt takes the
+    // exact kernel below
+    const size_t plbytes = sizeof(int32_t) * ((size_t)a.n_preds * a.P + a.n_preds);
+    if ((int)ssmem <= max_block && a.ws && a.ws_bytes >= plbytes) {
+      int32_t* pl = reinterpret_cast<int32_t*>(a.ws);
       int32_t* pln = pl + (size_t)a.n_preds * a.P;
-      cudaMemsetAsync(pln, 0, sizeof(int32_t) * a.n_preds, s);
+      if (cudaMemsetAsync(pln, 0, sizeof(int32_t) * a.n_preds, s) != cudaSuccess)
+        return moeb::fail(MOEB_ECUDA, "clearing the undecided-prompt count");
       // with upstream counts (and no per-prompt output) neither kernel computes them
       const bool given = a.given && !a.per_prompt;
       auto ks = given ? k_stack_replay<false> : k_stack_replay<true>;
@@ -1705,7 +1693,6 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
         k<<<dim3((unsigned)((a.P + spb - 1) / spb), (unsigned)a.n_preds), 32 * nw, smem, s>>>(b);
         rc = moeb::check_launch("k_cache_sim_warp");
       }
-      cudaFreeAsync(pl, s);
       return rc;
     }
   }
@@ -1744,15 +1731,22 @@ int launch_sim(SimArgs a, int policy, cudaStream_t s) {
 
 }  // namespace
 
+extern "C" size_t moeb_cache_sim_workspace_bytes(int n_preds, int n_prompts) {
+  if (n_preds < 1 || n_prompts < 1) return 0;
+  return sizeof(int32_t) * ((size_t)n_preds * n_prompts + n_preds);
+}
+
 extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* preds,
                               const uint8_t* const* covered, const int32_t* unbounded,
                               int n_preds, const int64_t* prompt_row_off, int n_prompts, int L,
                               int E, int warmup_tokens, const int64_t* capacities, int n_caps,
                               int budget, int policy, int64_t* counters, int64_t* per_prompt,
-                              uint64_t* hit_masks, void* stream) {
+                              uint64_t* hit_masks, int64_t rows, void* workspace,
+                              size_t workspace_bytes, void* stream) {
   return moeb_cache_sim_counted(truth, preds, covered, unbounded, n_preds, prompt_row_off,
                                 n_prompts, L, E, warmup_tokens, capacities, n_caps, budget,
-                                policy, counters, per_prompt, hit_masks, nullptr, stream);
+                                policy, counters, per_prompt, hit_masks, nullptr, rows,
+                                workspace, workspace_bytes, stream);
 }
 
 extern "C" int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* const* preds,
@@ -1761,7 +1755,8 @@ extern "C" int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* con
                                       int L, int E, int warmup_tokens, const int64_t* capacities,
                                       int n_caps, int budget, int policy, int64_t* counters,
                                       int64_t* per_prompt, uint64_t* hit_masks,
-                                      const int64_t* given_counts, void* stream) {
+                                      const int64_t* given_counts, int64_t rows, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
   moeb::clear_error();
   MOEB_REQUIRE(truth && prompt_row_off && counters && capacities, "null argument");
   MOEB_REQUIRE(n_preds >= 1 && n_preds <= MOEB_MAX_PREDS, "n_preds must be in [1, %d]",
@@ -1771,13 +1766,8 @@ extern "C" int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* con
   MOEB_REQUIRE(warmup_tokens >= 0 && budget >= 1, "bad warmup/budget");
   MOEB_REQUIRE(policy == MOEB_POLICY_LRU || policy == MOEB_POLICY_LFU, "unknown policy %d",
                policy);
+  MOEB_REQUIRE(rows >= 0, "rows must be >= 0");
   const int W = moeb::words_for(E);
-  int64_t rows = 0;
-  if (hit_masks) {
-    if (cudaMemcpy(&rows, prompt_row_off + n_prompts, sizeof(int64_t),
-                   cudaMemcpyDeviceToHost) != cudaSuccess)
-      return moeb::fail(MOEB_ECUDA, "reading prompt_row_off");
-  }
   SimArgs a{};
   a.truth = truth;
   a.n_preds = n_preds;
@@ -1795,6 +1785,8 @@ extern "C" int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* con
   a.budget = budget;
   a.rows = rows;
   a.given = given_counts;
+  a.ws = workspace;
+  a.ws_bytes = workspace ? workspace_bytes : 0;
   const int nc = 4 + 3 * L;
   cudaStream_t s = moeb::as_stream(stream);
   for (int c = 0; c < n_caps; ++c) {

@@ -694,6 +694,12 @@ __global__ void __launch_bounds__(kThreads) k_parse_predictions(
 // ---------------------------------------------------------------------------
 // Reductions over parsed lines.
 // ---------------------------------------------------------------------------
+// out[0] = v0, out[1] = v1 (n = 1 or 2): a stream-ordered initialisation
+// (instead of an async copy from a host stack variable)
+__global__ void k_fill_i64(int64_t* out, int n, int64_t v0, int64_t v1) {
+  if (threadIdx.x < n) out[threadIdx.x] = threadIdx.x == 0 ? v0 : v1;
+}
+
 __global__ void k_first_status(const uint8_t* status, int64_t n, int skip, int64_t* out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1021,9 +1027,7 @@ int moeb_first_status(const uint8_t* status, int64_t n, int skip_code, int64_t* 
   moeb::clear_error();
   MOEB_REQUIRE(out && (n == 0 || status), "null argument");
   cudaStream_t s = moeb::as_stream(stream);
-  const int64_t init = n;
-  if (cudaMemcpyAsync(out, &init, sizeof(int64_t), cudaMemcpyHostToDevice, s) != cudaSuccess)
-    return moeb::fail(MOEB_ECUDA, "init");
+  k_fill_i64<<<1, 32, 0, s>>>(out, 1, n, 0);
   if (n > 0) k_first_status<<<blocks_for(n), kThreads, 0, s>>>(status, n, skip_code, out);
   return moeb::check_launch("k_first_status");
 }
@@ -1034,9 +1038,7 @@ int moeb_keys_check(const int64_t* a, const int64_t* b, const int32_t* c, const 
   MOEB_REQUIRE(out && (n == 0 || (a && b && c)), "null argument");
   (void)skip_code;
   cudaStream_t s = moeb::as_stream(stream);
-  const int64_t init[2] = {0, n};
-  if (cudaMemcpyAsync(out, init, sizeof(init), cudaMemcpyHostToDevice, s) != cudaSuccess)
-    return moeb::fail(MOEB_ECUDA, "init");
+  k_fill_i64<<<1, 32, 0, s>>>(out, 2, 0, n);
   if (n > 0) k_keys_check<<<blocks_for(n), kThreads, 0, s>>>(a, b, c, status, skip_code, n, out);
   return moeb::check_launch("k_keys_check");
 }
@@ -1054,9 +1056,7 @@ int moeb_check_grid(const int64_t* starts, int64_t n_prompts, int64_t n_rows,
   moeb::clear_error();
   MOEB_REQUIRE(bad_prompt && L >= 1, "bad argument");
   cudaStream_t s = moeb::as_stream(stream);
-  if (cudaMemcpyAsync(bad_prompt, &n_prompts, sizeof(int64_t), cudaMemcpyHostToDevice, s) !=
-      cudaSuccess)
-    return moeb::fail(MOEB_ECUDA, "init");
+  k_fill_i64<<<1, 32, 0, s>>>(bad_prompt, 1, n_prompts, 0);
   if (n_rows > 0 && n_prompts > 0)
     k_check_grid<<<blocks_for(n_rows), kThreads, 0, s>>>(starts, n_prompts, n_rows, token_index,
                                                          layer_id, L, bad_prompt);
@@ -1065,15 +1065,11 @@ int moeb_check_grid(const int64_t* starts, int64_t n_prompts, int64_t n_rows,
 
 int moeb_predictions_join(const int64_t* t_prompt, const int64_t* t_token, const int32_t* t_layer,
                           const uint64_t* t_masks, int64_t n_table, const int64_t* prompt_ids,
-                          const int64_t* prompt_row_off, int n_prompts, int L, int E,
-                          uint64_t* pred, uint8_t* covered, void* stream) {
+                          const int64_t* prompt_row_off, int n_prompts, int64_t rows, int L,
+                          int E, uint64_t* pred, uint8_t* covered, void* stream) {
   moeb::clear_error();
   MOEB_REQUIRE(prompt_ids && prompt_row_off && pred && covered && n_prompts >= 1, "null argument");
-  MOEB_REQUIRE(L >= 1 && E >= 1 && E <= 256, "unsupported shape");
-  int64_t rows = 0;
-  if (cudaMemcpy(&rows, prompt_row_off + n_prompts, sizeof(int64_t), cudaMemcpyDeviceToHost) !=
-      cudaSuccess)
-    return moeb::fail(MOEB_ECUDA, "reading prompt_row_off");
+  MOEB_REQUIRE(L >= 1 && E >= 1 && E <= 256 && rows >= 0, "unsupported shape");
   if (rows == 0) return MOEB_OK;
   cudaStream_t s = moeb::as_stream(stream);
   const int W = moeb::words_for(E);
@@ -1084,15 +1080,12 @@ int moeb_predictions_join(const int64_t* t_prompt, const int64_t* t_token, const
 }
 
 static int trace_csv(const uint64_t* truth, const int64_t* pids, const int64_t* row_off, int P,
-                     int L, int E, const int32_t* tokid, int64_t* lens, const int64_t* offs,
-                     uint8_t* out, bool write, void* stream) {
+                     int64_t rows, int L, int E, const int32_t* tokid, int64_t* lens,
+                     const int64_t* offs, uint8_t* out, bool write, void* stream) {
   moeb::clear_error();
   MOEB_REQUIRE(truth && pids && row_off && P >= 1 && (write ? (offs && out) : lens != nullptr),
                "null argument");
-  MOEB_REQUIRE(L >= 1 && E >= 1 && E <= 256, "unsupported shape");
-  int64_t rows = 0;
-  if (cudaMemcpy(&rows, row_off + P, sizeof(int64_t), cudaMemcpyDeviceToHost) != cudaSuccess)
-    return moeb::fail(MOEB_ECUDA, "reading prompt_row_off");
+  MOEB_REQUIRE(L >= 1 && E >= 1 && E <= 256 && rows >= 0, "unsupported shape");
   if (rows == 0) return MOEB_OK;
   cudaStream_t s = moeb::as_stream(stream);
   const int W = moeb::words_for(E);
@@ -1107,17 +1100,17 @@ static int trace_csv(const uint64_t* truth, const int64_t* pids, const int64_t* 
 }
 
 int moeb_trace_csv_lengths(const uint64_t* truth, const int64_t* prompt_ids,
-                           const int64_t* prompt_row_off, int n_prompts, int L, int E,
-                           const int32_t* token_ids, int64_t* lens, void* stream) {
-  return trace_csv(truth, prompt_ids, prompt_row_off, n_prompts, L, E, token_ids, lens, nullptr,
-                   nullptr, false, stream);
+                           const int64_t* prompt_row_off, int n_prompts, int64_t rows, int L,
+                           int E, const int32_t* token_ids, int64_t* lens, void* stream) {
+  return trace_csv(truth, prompt_ids, prompt_row_off, n_prompts, rows, L, E, token_ids, lens,
+                   nullptr, nullptr, false, stream);
 }
 
 int moeb_trace_csv_write(const uint64_t* truth, const int64_t* prompt_ids,
-                         const int64_t* prompt_row_off, int n_prompts, int L, int E,
-                         const int32_t* token_ids, const int64_t* offsets, uint8_t* out,
+                         const int64_t* prompt_row_off, int n_prompts, int64_t rows, int L,
+                         int E, const int32_t* token_ids, const int64_t* offsets, uint8_t* out,
                          void* stream) {
-  return trace_csv(truth, prompt_ids, prompt_row_off, n_prompts, L, E, token_ids, nullptr,
+  return trace_csv(truth, prompt_ids, prompt_row_off, n_prompts, rows, L, E, token_ids, nullptr,
                    offsets, out, true, stream);
 }
 
@@ -1161,10 +1154,8 @@ int moeb_exclusive_scan_i64(const int64_t* in, int64_t n, int64_t* out, int64_t*
   cudaStream_t s = moeb::as_stream(stream);
   const int64_t nb = (n + kThreads * 16 - 1) / (kThreads * 16);
   if (nb == 0) {
-    const int64_t z = 0;
-    if (cudaMemcpyAsync(out, &z, sizeof(z), cudaMemcpyHostToDevice, s) != cudaSuccess)
-      return moeb::fail(MOEB_ECUDA, "init");
-    return MOEB_OK;
+    k_fill_i64<<<1, 32, 0, s>>>(out, 1, 0, 0);
+    return moeb::check_launch("k_fill_i64");
   }
   k_block_sums<<<(unsigned)nb, kThreads, 0, s>>>(in, n, ws);
   k_scan_inplace<<<1, kThreads, 0, s>>>(ws, nb, nullptr);

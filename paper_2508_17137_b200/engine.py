@@ -153,6 +153,9 @@ def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget:
                   if want_per_prompt else None)
     hits = (torch.zeros((n, C, packed.rows, shape.mask_words), dtype=torch.int64, device=dev)
             if want_hits else None)
+    lib = nat.load_library()
+    ws_bytes = lib.moeb_cache_sim_workspace_bytes(min(n, 16), P)
+    ws = nat.workspace(ws_bytes, dev)
     for lo in range(0, n, 16):
         chunk = streams[lo:lo + 16]
         nat.call("moeb_cache_sim_counted", nat.ptr(packed.truth),
@@ -165,7 +168,7 @@ def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget:
                  nat.ptr(None if per_prompt is None else per_prompt[lo:lo + 16]),
                  nat.ptr(None if hits is None else hits[lo:lo + 16]),
                  nat.ptr(None if given_counts is None else given_counts[lo:lo + 16]),
-                 nat.stream_ptr())
+                 packed.rows, nat.ptr(ws), ws_bytes, nat.stream_ptr())
     return counters, per_prompt, hits
 
 

@@ -193,23 +193,34 @@ class ExternalPredictor(DevicePredictor):
 
     def __init__(self, table: dict, shape: ModelShape):
         self.shape = shape
-        self.table = table
-        self._cache = {}
+        self.table = table      # as given: a dict (reference form) or a PredictionTable
+        self._tables = {}       # device -> PredictionTable
+        self._last = None       # (packed, (masks, coverage)) of the last join
 
     def covers(self, prompt_id: int, token_index: int, layer_id: int) -> bool:
         return (prompt_id, token_index, layer_id) in self.table
 
+    def _table_on(self, device):
+        from .traceio import PredictionTable
+        if isinstance(self.table, PredictionTable) and self.table.prompt_id.device == device:
+            return self.table
+        key = str(device)
+        if key not in self._tables:
+            self._tables[key] = (self.table.to(device) if isinstance(self.table, PredictionTable)
+                                 else PredictionTable.from_dict(self.table, self.shape, device))
+        return self._tables[key]
+
     def _build(self, packed: PackedTraces):
         """Masks + coverage per trace row: the table (key-sorted device
-        arrays; a dict is packed once) joined onto the rows on device
-        (moeb_predictions_join)."""
-        from .traceio import PredictionTable, join_predictions
-        key = (id(packed), packed.rows)
-        if key not in self._cache:
-            if not isinstance(self.table, PredictionTable):
-                self.table = PredictionTable.from_dict(self.table, self.shape, packed.device)
-            self._cache = {key: join_predictions(self.table, packed)}
-        return self._cache[key]
+        arrays, one copy per device) joined onto the rows on device
+        (moeb_predictions_join). The last join is reused only for the very
+        same PackedTraces object (predict_masks + coverage of one replay)."""
+        from .traceio import join_predictions
+        if self._last is not None and self._last[0] is packed:
+            return self._last[1]
+        res = join_predictions(self._table_on(packed.device), packed)
+        self._last = (packed, res)
+        return res
 
     def predict_masks(self, packed, budget, warmup=0, metrics=None):
         return self._build(packed)[0]

@@ -432,8 +432,8 @@ def write_trace_csv(traces) -> bytes:
     lens = torch.empty(packed.rows, dtype=torch.int64, device=dev)
     tok = packed.token_ids.contiguous() if packed.token_ids is not None else None
     nat.call("moeb_trace_csv_lengths", nat.ptr(packed.truth), nat.ptr(pid_d),
-             nat.ptr(packed.row_off), packed.num_prompts, L, E, nat.ptr(tok), nat.ptr(lens),
-             nat.stream_ptr())
+             nat.ptr(packed.row_off), packed.num_prompts, packed.rows, L, E, nat.ptr(tok),
+             nat.ptr(lens), nat.stream_ptr())
     offs = _scan(lens)
     head = (TRACE_HEADER + "\n").encode()
     total = int(offs[-1].item())
@@ -441,8 +441,8 @@ def write_trace_csv(traces) -> bytes:
     out[:len(head)] = torch.frombuffer(bytearray(head), dtype=torch.uint8).to(dev)
     body = out[len(head):]
     nat.call("moeb_trace_csv_write", nat.ptr(packed.truth), nat.ptr(pid_d),
-             nat.ptr(packed.row_off), packed.num_prompts, L, E, nat.ptr(tok), nat.ptr(offs),
-             nat.ptr(body), nat.stream_ptr())
+             nat.ptr(packed.row_off), packed.num_prompts, packed.rows, L, E, nat.ptr(tok),
+             nat.ptr(offs), nat.ptr(body), nat.stream_ptr())
     return out.cpu().numpy().tobytes()
 
 
@@ -477,6 +477,12 @@ class PredictionTable(Mapping):
         t = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a)).to(dev, dt)  # noqa: E731
         return cls(shape, t(k[:, 0], torch.int64), t(k[:, 1], torch.int64),
                    t(k[:, 2], torch.int32), t(m.view(np.int64), torch.int64))
+
+    def to(self, device) -> "PredictionTable":
+        """The same table on another device."""
+        dev = _device(device)
+        return PredictionTable(self.shape, self.prompt_id.to(dev), self.token_index.to(dev),
+                               self.layer_id.to(dev), self.masks.to(dev))
 
     def _h(self):
         if self._host is None:
@@ -653,6 +659,6 @@ def join_predictions(table: PredictionTable, packed: PackedTraces):
     n = len(table)
     nat.call("moeb_predictions_join", nat.ptr(table.prompt_id), nat.ptr(table.token_index),
              nat.ptr(table.layer_id), nat.ptr(tm), n, nat.ptr(pids), nat.ptr(packed.row_off),
-             packed.num_prompts, packed.shape.num_layers, packed.shape.num_experts,
-             nat.ptr(pred), nat.ptr(cov), nat.stream_ptr())
+             packed.num_prompts, packed.rows, packed.shape.num_layers,
+             packed.shape.num_experts, nat.ptr(pred), nat.ptr(cov), nat.stream_ptr())
     return pred, cov

@@ -203,10 +203,12 @@ def pack_traces(traces, shape: ModelShape, device=None) -> PackedTraces:
             if rec.token_index != j // L or rec.layer_id != j % L:
                 raise RangeError(f"prompt {tr.prompt_id}: records not a complete (token, layer) "
                                  f"grid at position {j}")
+            # the reference's own record check (core.py:84-104): exactly top_k
+            # distinct in-range ids -- a bitmask row cannot carry a duplicate
+            # id, so such a record is rejected instead of silently collapsed
+            rec.validate(shape)
             m = [0] * W
             for e in rec.expert_ids:
-                if not 0 <= e < shape.num_experts:
-                    raise RangeError(f"expert {e} out of range [0, {shape.num_experts})")
                 m[e >> 6] |= 1 << (e & 63)
             rows.append(m)
             if j % L == 0:
