@@ -139,12 +139,30 @@ int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_row_off, in
                         int threshold, int warmup_tokens, uint64_t* pred, double* logits,
                         int64_t* metrics, void* stream);
 /* moeb_linear_predict that also accumulates, over rows with token >= warmup,
- * counts [2 + 2L] += sum |truth|, sum |truth & pred|, then the same per layer
- * (the replay's measured accesses and prediction hits, engine.py:175-200). */
+ * counts [2 + 2L] (nullable) += sum |truth|, sum |truth & pred|, then the
+ * same per layer (the replay's measured accesses and prediction hits,
+ * engine.py:175-200).
+ *  top_k       experts per trace row (ModelShape.top_k; rows are validated
+ *              to hold exactly top_k, core.py:84-104). Only sizes the fast
+ *              path's error bound; a row with more ids is still exact (its
+ *              stream falls back to fp64). 0 = unknown (bound for E).
+ *  rows        host: prompt_row_off[n_prompts]
+ *  workspace   >= moeb_linear_workspace_bytes(rows, L, E) enables K3t (E =
+ *              64, L <= 32, budget <= 16, logits == NULL): tensor-core
+ *              column sums and fp32 scores with a rigorous error bound, the
+ *              rows it cannot decide re-evaluated in fp64 -- masks identical
+ *              to the fp64 kernel's. NULL -> the fp64 kernel. */
+size_t moeb_linear_workspace_bytes(int64_t rows, int L, int E);
+/* Diagnostics: out[0] (device int64) = the number of rows the last K3t call
+ * on this workspace re-evaluated in fp64 (> list capacity: the whole call
+ * was redone by the fp64 kernel). */
+int moeb_linear_ambiguous_rows(const void* workspace, int L, int64_t* out, void* stream);
 int moeb_linear_predict_counts(const uint64_t* truth, const int64_t* prompt_row_off,
                                int n_prompts, int L, int E, const double* weights, double decay,
-                               int budget, int threshold, int warmup_tokens, uint64_t* pred,
-                               double* logits, int64_t* metrics, int64_t* counts, void* stream);
+                               int budget, int threshold, int warmup_tokens, int top_k,
+                               uint64_t* pred, double* logits, int64_t* metrics, int64_t* counts,
+                               int64_t rows, void* workspace, size_t workspace_bytes,
+                               void* stream);
 
 /*
  * Wide K3 for 64 < E <= 256 (DeepSeek-V3: 256 experts), same semantics as

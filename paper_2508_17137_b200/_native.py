@@ -40,7 +40,8 @@ _SIGS = {
                                P, I64, P, ctypes.c_size_t, P],
     "moeb_cache_ops": [P, P, I64, I32, I32, I64, I32, P, P],
     "moeb_linear_predict": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P],
-    "moeb_linear_predict_counts": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P, P],
+    "moeb_linear_predict_counts": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, I32, P, P, P, P,
+                                   I64, P, ctypes.c_size_t, P],
     "moeb_ids_to_masks": [P, I64, I32, I32, P, P, P],
     "moeb_masks_to_ids": [P, I64, I32, P, P, P],
     "moeb_mask_head": [P, I64, I32, I32, I32, P, P],
@@ -81,6 +82,7 @@ _SIGS = {
     "moeb_sqdist_update": [P, P, P, P, I64, I64, I32, P, P],
     "moeb_cluster_means": [P, P, P, I32, I64, P, P],
     "moeb_linear_prepare": [P, I32, I32, DBL, P, P],
+    "moeb_linear_ambiguous_rows": [P, I32, P, P],
     "moeb_linear_predict_wide": [P, P, I32, I32, I32, P, DBL, I32, I32, I32, P, P, P, P],
     "moeb_linear_features": [P, P, I32, I32, I32, DBL, P, P],
     "moeb_linear_sgd_epoch": [P, P, P, P, I64, I32, I32, DBL, P, P],
@@ -91,6 +93,7 @@ _SIGS = {
 SIZE_QUERIES = {
     "moeb_linear_table_doubles": [I32, I32],
     "moeb_cache_sim_workspace_bytes": [I32, I32],
+    "moeb_linear_workspace_bytes": [I64, I32, I32],
 }
 
 EXPORTS = tuple(_SIGS) + ("moeb_last_error",) + tuple(SIZE_QUERIES)

@@ -56,6 +56,8 @@ struct LinArgs {
   uint64_t* pred;
   double* logits;
   int64_t* counts;  // nullable [2 + 2L]: measured accesses, prediction hits, per layer of each
+  const int* gate;  // nullable: run only if *gate > gate_cap (K3t's list overflowed)
+  int gate_cap;
 };
 
 template <int TPS>
@@ -104,6 +106,7 @@ template <int TPS, bool FULL, int KT>
 __global__ void __launch_bounds__(K3Cfg<TPS>::kThreads, 2) k_linear_predict(const LinArgs a) {
   using C = K3Cfg<TPS>;
   constexpr int NS = C::NS, NU = C::kUnits, HALF = NS / 2;
+  if (a.gate && *a.gate <= a.gate_cap) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = a.L, E = a.E, F = a.L + a.E + 1;
   double2* colT = reinterpret_cast<double2*>(smem_raw);  // [E][TPS][NU]: W[j][L+e] pairs
@@ -455,21 +458,58 @@ __global__ void k_linear_prepare(const double* __restrict__ Wt, int L, int E, do
 
 }  // namespace
 
+namespace moeb {
+size_t linear_tc_workspace_bytes(int64_t rows, int L);
+size_t linear_tc_min_workspace(int L);
+bool linear_tc_eligible(int L, int E, int budget, const double* logits);
+int linear_tc_launch(const uint64_t* truth, const int64_t* row_off, int P, int64_t rows, int L,
+                     const double* W, double decay, int budget, int threshold, int warmup,
+                     int kmax, uint64_t* pred, int64_t* counts, void* workspace,
+                     size_t ws_bytes, cudaStream_t s);
+
+int launch_linear_fp64_gated(const uint64_t* truth, const int64_t* row_off, int P, int L, int E,
+                             const double* W, double decay, int budget, int threshold, int warmup,
+                             uint64_t* pred, int64_t* counts, const int* gate, int gate_cap,
+                             cudaStream_t s) {
+  LinArgs a{truth, row_off, P, L, E, W, decay, budget, threshold ? 1 : 0, warmup, pred, nullptr,
+            counts, gate, gate_cap};
+  return launch_k3<2>(a, s);
+}
+}  // namespace moeb
+
+namespace moeb {
+int linear_tc_ambiguous(const void* workspace, int L, int64_t* out, cudaStream_t s);
+}
+
+extern "C" int moeb_linear_ambiguous_rows(const void* workspace, int L, int64_t* out,
+                                          void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(workspace && out && L >= 1 && L <= 32, "bad argument");
+  return moeb::linear_tc_ambiguous(workspace, L, out, moeb::as_stream(stream));
+}
+
+extern "C" size_t moeb_linear_workspace_bytes(int64_t rows, int L, int E) {
+  if (E != 64 || L < 1 || L > 32) return 0;
+  return moeb::linear_tc_workspace_bytes(rows, L);
+}
+
 extern "C" int moeb_linear_predict(const uint64_t* truth, const int64_t* prompt_row_off,
                                    int n_prompts, int L, int E, const double* weights,
                                    double decay, int budget, int threshold, int warmup_tokens,
                                    uint64_t* pred, double* logits, int64_t* metrics,
                                    void* stream) {
   return moeb_linear_predict_counts(truth, prompt_row_off, n_prompts, L, E, weights, decay,
-                                    budget, threshold, warmup_tokens, pred, logits, metrics,
-                                    nullptr, stream);
+                                    budget, threshold, warmup_tokens, 0, pred, logits, metrics,
+                                    nullptr, 0, nullptr, 0, stream);
 }
 
 extern "C" int moeb_linear_predict_counts(const uint64_t* truth, const int64_t* prompt_row_off,
                                           int n_prompts, int L, int E, const double* weights,
                                           double decay, int budget, int threshold,
-                                          int warmup_tokens, uint64_t* pred, double* logits,
-                                          int64_t* metrics, int64_t* counts, void* stream) {
+                                          int warmup_tokens, int top_k, uint64_t* pred,
+                                          double* logits, int64_t* metrics, int64_t* counts,
+                                          int64_t rows, void* workspace, size_t workspace_bytes,
+                                          void* stream) {
   moeb::clear_error();
   MOEB_REQUIRE(truth && prompt_row_off && weights && pred, "null argument");
   MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && E >= 1 && E <= 64,
@@ -477,11 +517,21 @@ extern "C" int moeb_linear_predict_counts(const uint64_t* truth, const int64_t* 
                "moeb_linear_prepare + moeb_linear_predict_wide", L, E);
   MOEB_REQUIRE(budget >= 1 && warmup_tokens >= 0, "bad budget/warmup");
   MOEB_REQUIRE(decay >= 0.0 && decay < 1.0, "decay must be in [0, 1)");
-  LinArgs a{truth, prompt_row_off, n_prompts, L, E, weights, decay, budget,
-            threshold ? 1 : 0, warmup_tokens, pred, logits, counts};
-  const char* env = getenv("MOEB_K3_TPS");  // tuning knob: threads per stream (2 or 4)
-  const int rc = (env && atoi(env) == 4) ? launch_k3<4>(a, moeb::as_stream(stream))
-                                         : launch_k3<2>(a, moeb::as_stream(stream));
+  cudaStream_t s = moeb::as_stream(stream);
+  int rc;
+  if (workspace && moeb::linear_tc_eligible(L, E, budget, logits) &&
+      workspace_bytes >= moeb::linear_tc_min_workspace(L)) {
+    // K3t: tensor-core column sums, fp32 scores + exact fp64 re-evaluation
+    // of the rows the fp32 bound cannot decide
+    rc = moeb::linear_tc_launch(truth, prompt_row_off, n_prompts, rows, L, weights, decay, budget,
+                                threshold ? 1 : 0, warmup_tokens, top_k, pred, counts, workspace,
+                                workspace_bytes, s);
+  } else {
+    LinArgs a{truth, prompt_row_off, n_prompts, L, E, weights, decay, budget,
+              threshold ? 1 : 0, warmup_tokens, pred, logits, counts, nullptr, 0};
+    const char* env = getenv("MOEB_K3_TPS");  // tuning knob: threads per stream (2 or 4)
+    rc = (env && atoi(env) == 4) ? launch_k3<4>(a, s) : launch_k3<2>(a, s);
+  }
   if (rc != 0 || metrics == nullptr) return rc;
   // K7 over the fresh masks (same stream): prediction metrics (metrics.py:12-79)
   return moeb_metrics(pred, truth, prompt_row_off, n_prompts, L, E, warmup_tokens, metrics,

@@ -268,6 +268,17 @@ class LearnedLinearPredictor(DevicePredictor):
             self._w[key] = tab
         return self._w[key]
 
+    def ambiguous_rows(self) -> int | None:
+        """Rows of the last predict_masks call that the tensor-core kernel
+        (K3t) handed to the exact fp64 re-evaluation (None: K3t not used)."""
+        ws = getattr(self, "last_workspace", None)
+        if ws is None:
+            return None
+        out = torch.zeros(1, dtype=torch.int64, device=ws.device)
+        nat.call("moeb_linear_ambiguous_rows", nat.ptr(ws), self.shape.num_layers, nat.ptr(out),
+                 nat.stream_ptr())
+        return int(out.item())
+
     @property
     def supports_counts(self) -> bool:
         """predict_masks(counts=...) fills the replay's cache-independent
@@ -286,11 +297,16 @@ class LearnedLinearPredictor(DevicePredictor):
                      int(budget), int(bool(self.threshold)), int(warmup), nat.ptr(out),
                      nat.ptr(logits), nat.ptr(metrics), nat.stream_ptr())
             return out
+        ws_bytes = 0 if logits is not None else nat.load_library().moeb_linear_workspace_bytes(
+            packed.rows, s.num_layers, s.num_experts)
+        ws = nat.workspace(ws_bytes, packed.device)
+        self.last_workspace = ws
         nat.call("moeb_linear_predict_counts", nat.ptr(packed.truth), nat.ptr(packed.row_off),
                  packed.num_prompts, s.num_layers, s.num_experts,
                  nat.ptr(self.weights_on(packed.device)), float(self.history_decay),
-                 int(budget), int(bool(self.threshold)), int(warmup), nat.ptr(out),
-                 nat.ptr(logits), nat.ptr(metrics), nat.ptr(counts), nat.stream_ptr())
+                 int(budget), int(bool(self.threshold)), int(warmup), s.top_k, nat.ptr(out),
+                 nat.ptr(logits), nat.ptr(metrics), nat.ptr(counts), packed.rows, nat.ptr(ws),
+                 ws_bytes, nat.stream_ptr())
         return out
 
 
