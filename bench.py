@@ -219,6 +219,9 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "trace tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "hit_rate_10pct": {"learned_linear": rep.cache_hit_rate},
+        "counters": {"prompts": f"0..{n_sample - 1}", "measured_accesses": rep.measured_accesses,
+                     "cache_hits": rep.cache_hits, "prediction_hits": rep.prediction_hits,
+                     "uncovered_queries": rep.uncovered_queries},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -333,14 +336,17 @@ def run_ours(args):
     mc = m.MetricCounts.from_vector(vec.cpu().numpy(), E)
 
     # --- end to end through the public API with host buffers ---
-    # StreamingReplay: every step copies its pinned host trace rows (396 MB of
-    # expert ids, or 528 MB of masks with --e2e-format masks) to the device (copy stream, double-buffered so step i+1's copy overlaps
-    # step i's compute) and reads its counters + metrics back to pinned host
-    # memory; all inside the timed region.
-    # Host batches in the compact wire format: each row's k expert ids as u8
-    # (the reference trace's own representation, 6 B/row instead of an 8-byte
-    # mask), decoded into masks on the device after the copy.
-    if args.e2e_format == "ids":
+    # StreamingReplay: every step copies its pinned host trace rows to the
+    # device (copy stream, double-buffered so step i+1's copy overlaps step
+    # i's compute) and reads its counters + metrics back to pinned host
+    # memory; all inside the timed region. Host batches in a compact wire
+    # format decoded into masks on the device after the copy: by default each
+    # row's combinatorial rank (u32, 4 B/row: 264 MB per step), or its k
+    # expert ids as u8 (--e2e-format ids, 6 B/row, 396 MB), or the 8-byte
+    # masks (--e2e-format masks, 528 MB).
+    if args.e2e_format == "ranks":
+        truth_host = m.masks_to_ranks(packed.truth, C2["top_k"], E).cpu().pin_memory()
+    elif args.e2e_format == "ids":
         truth_host = m.masks_to_ids(packed.truth, C2["top_k"]).cpu().pin_memory()
     else:
         truth_host = packed.truth.cpu().pin_memory()
@@ -390,19 +396,23 @@ def run_ours(args):
 
     # --- roofline of the dominant kernel (HBM-bound integer work) ---
     bytes_per_row = 16  # truth mask read + predicted mask (read by K1 / written by K3)
-    dom = "k_cache_sim" if sim_ms >= lin_ms else "k_linear_predict"
+    # K3 runs as K3t (k_linear_tc: tensor-core column sums + top-k on packed
+    # keys) unless MOEB_K3=fp64 selects the SIMT fp64 kernel
+    k3_name = "k_linear_predict" if os.environ.get("MOEB_K3", "").startswith("f") else "k_linear_tc"
+    dom = "k_cache_sim" if sim_ms >= lin_ms else k3_name
     dom_ms = max(sim_ms, lin_ms)
     achieved = rows * bytes_per_row / (dom_ms / 1000.0) / 1e9
     # DRAM bytes per launch from the committed `ncu --set full` capture of the
     # same kernel on the same workload (profiles/traffic.json), scaled to this
     # run's rows per launch when the chunking differs.
-    traffic = None
+    traffic, limiter = None, None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             t = json.load(open(tpath)).get(dom)
             if t:
                 traffic = t["dram_bytes"] * (rows / len(pipe.bounds)) / t["rows"]
+                limiter = t.get("limiter")
         except Exception:
             traffic = None
 
@@ -414,6 +424,36 @@ def run_ours(args):
         dist.all_reduce(lru_c)
     lc = lru_c[0, 0].cpu().numpy()
     hit["lru_only"] = int(lc[1]) / int(lc[0])
+
+    # --- parity: the reference arm's own sample (prompts 0..255) through the
+    # drop-in replay_traces, against the counters the reference produced for
+    # it (tests/golden/c2_sample256.npz, made by tests/golden/make_c2_golden.py)
+    parity = None
+    gpath = os.path.join(ROOT, "tests", "golden", "c2_sample256.npz")
+    if rank == 0 and P >= 256 and os.path.exists(gpath):
+        g = np.load(gpath)
+        j = [int(x) for x in g["capacities"]].index(cap)
+        cfg = m.ReplayConfig(shape, m.CacheConfig(capacity_fraction=CAP_FRACTION,
+                                                  prefetch_budget=BUDGET),
+                             warmup_tokens=WARMUP_TOKENS)
+        sample = packed.select(0, 256)
+        rep = m.replay_traces(sample, pred, cfg)
+        got = np.concatenate([[rep.measured_accesses, rep.cache_hits, rep.prediction_hits,
+                               rep.uncovered_queries], rep.layer_accesses,
+                              rep.layer_cache_hits, rep.layer_prediction_hits])
+        want = g["counters_learned_linear"][j]
+        vec_s = m.metrics.metric_vector(E, dev)
+        pred.predict_masks(sample, BUDGET, WARMUP_TOKENS, metrics=vec_s)
+        met_eq = bool(np.array_equal(vec_s.cpu().numpy(), g["metrics_ints"]))
+        parity = {"sample": "prompts 0..255 x 363 tokens (the reference arm's sample at 16 "
+                            "host cores), learned_linear + LRU 10 %",
+                  "reference": {"measured_accesses": int(want[0]), "cache_hits": int(want[1]),
+                                "prediction_hits": int(want[2])},
+                  "ours": {"measured_accesses": int(got[0]), "cache_hits": int(got[1]),
+                           "prediction_hits": int(got[2])},
+                  "counters_equal": bool(np.array_equal(got, want)),
+                  "per_layer_equal": bool(np.array_equal(got[4:], want[4:])),
+                  "metric_counts_equal": met_eq}
 
     # --- the paper's transformer predictor (tcgen05 path) on a C2 slice ---
     tr_info = None
@@ -448,7 +488,7 @@ def run_ours(args):
             msum = sum(a.elapsed_time(b) for a, b, _ in lst) / nt
             fl = sum(f for _, _, f in lst) / nt
             ker[name] = {"ms": msum, "tflops": fl / (msum / 1e3) / 1e12}
-        tdom = max((k for k in ker if k.startswith("gemm")), key=lambda k: ker[k]["ms"])
+        tdom = max((k for k in ker if ker[k]["tflops"] > 0), key=lambda k: ker[k]["ms"])
         tot_flops = sum(sum(f for _, _, f in lst) for lst in timing.values()) / nt
         ct = cnt_t[0, 0].cpu().numpy()
         mct = m.MetricCounts.from_vector(vec_t.cpu().numpy(), E)
@@ -532,8 +572,11 @@ def run_ours(args):
             "config": _config(P, rows, cap, world),
             "e2e": {"value": e2e_value, "unit": "trace tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
-                    "host_format": ("u8 expert ids [rows][6], decoded on device (k_ids_to_masks)"
-                                    if args.e2e_format == "ids" else "int64 mask rows")},
+                    "host_format": {
+                        "ranks": "u32 combinatorial rank of each row's 6-expert set [rows], "
+                                 "decoded on device (k_ranks_to_masks)",
+                        "ids": "u8 expert ids [rows][6], decoded on device (k_ids_to_masks)",
+                        "masks": "int64 mask rows"}[args.e2e_format]},
             # per chunk: K3 (k_linear_predict) + K7 (k_metrics64) + K1s (k_stack_replay)
             # + K1 (k_cache_sim_warp over the prompts K1s left undecided)
             "gpu_launches": 4 * len(pipe.bounds) * args.steps,
@@ -541,12 +584,14 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic,
-                         "algorithmic_bytes": f"{bytes_per_row} B/row x {rows} rows"},
-            "kernels_ms": {"k_linear_predict": lin_ms, "k_cache_sim": sim_ms,
+                         "algorithmic_bytes": f"{bytes_per_row} B/row x {rows} rows",
+                         "limiter": limiter},
+            "kernels_ms": {k3_name: lin_ms, "k_cache_sim": sim_ms,
                            "k_metrics64": "overlapped with k_cache_sim (low-priority stream)"},
             "hit_rate_10pct": hit,
             "prediction": {"macro_f1": mc.macro_f1(), "position_accuracy": mc.position_accuracy,
                            "label_accuracy": mc.label_accuracy},
+            "parity": parity,
             "cpu_baseline": cpu_base,
             "transformer": tr_info,
             "eam_c4": eam_info,
@@ -566,9 +611,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--prompts", type=int, default=C2["prompts"])
-    ap.add_argument("--e2e-format", choices=["ids", "masks"], default="ids",
-                    help="host batch format of the end-to-end run: u8 expert ids (6 B/row, "
-                         "decoded on device) or the 8-byte mask rows")
+    ap.add_argument("--e2e-format", choices=["ranks", "ids", "masks"], default="ranks",
+                    help="host batch format of the end-to-end run: u32 combinatorial ranks "
+                         "(4 B/row), u8 expert ids (6 B/row), both decoded on device, or the "
+                         "8-byte mask rows")
     ap.add_argument("--chunks", type=int, default=1,
                     help="prompt chunks pipelined across the predict / replay streams")
     ap.add_argument("--no-cpu-baseline", action="store_true")

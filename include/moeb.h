@@ -222,6 +222,20 @@ int moeb_masks_to_ids(const uint64_t* masks, int64_t rows, int k, uint8_t* ids, 
                       void* stream);
 
 /*
+ * The 4-byte wire format of top-k rows: each row's rank in the combinatorial
+ * number system, N = sum_i C(c_i, i) over its ascending expert ids c_1 < ... <
+ * c_k (k <= 8, E <= 64, C(E, k) < 2^32; every validated reference row has
+ * exactly k ids, core.py:64-90).
+ *  moeb_ranks_to_masks: ranks [rows] -> masks [rows]; *bad = 1 if N >= C(E, k)
+ *  moeb_masks_to_ranks: masks [rows] -> ranks [rows]; *bad = 1 if a row's
+ *                       popcount != k
+ */
+int moeb_ranks_to_masks(const uint32_t* ranks, int64_t rows, int k, int E, uint64_t* masks,
+                        int* bad, void* stream);
+int moeb_masks_to_ranks(const uint64_t* masks, int64_t rows, int k, int E, uint32_t* ranks,
+                        int* bad, void* stream);
+
+/*
  * Rule-based predictors as mask tables (predictors.py:57-139).
  *  kind 0 lru_only (empty), 1 oracle (truth truncated to the `budget` lowest
  *  ids, :80-81), 2 next_layer_all (all E), 3 per-layer table

@@ -442,3 +442,88 @@ extern "C" int moeb_masks_to_ids(const uint64_t* masks, int64_t rows, int k, uin
   k_masks_to_ids<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, ids, bad);
   return moeb::check_launch("k_masks_to_ids");
 }
+
+// The tightest wire format of a top-k trace row: its rank in the
+// combinatorial number system (N = sum_i C(c_i, i) over the ascending ids
+// c_1 < ... < c_k), one u32 per row when C(E, k) < 2^32 (C(64, 6) = 74,974,368):
+// 4 bytes instead of the k-byte ids or the 8-byte mask. Every row of a
+// validated reference trace has exactly k distinct ids (core.py:64-90).
+namespace {
+constexpr int kBinN = 65, kBinK = 9;
+
+__device__ __forceinline__ void load_binom(uint32_t* tab) {  // C(n, j), n <= 64, j <= 8
+  for (int i = threadIdx.x; i < kBinN * kBinK; i += blockDim.x) {
+    const int n = i / kBinK, j = i % kBinK;
+    uint64_t c = 1;
+    for (int q = 0; q < j; ++q) c = c * (uint64_t)(n - q) / (uint64_t)(q + 1);
+    tab[i] = j > n ? 0u : (c > 0xffffffffull ? 0xffffffffu : (uint32_t)c);
+  }
+  __syncthreads();
+}
+
+__global__ void k_ranks_to_masks(const uint32_t* __restrict__ ranks, int64_t rows, int k, int E,
+                                 uint64_t* __restrict__ masks, int* __restrict__ bad) {
+  __shared__ uint32_t tab[kBinN * kBinK];
+  load_binom(tab);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t N = ranks[r];
+    uint64_t m = 0;
+    int hi = E;  // c_i < hi
+    bool ok = N < tab[E * kBinK + k];
+    for (int i = k; i >= 1; --i) {
+      // largest c in [i - 1, hi) with C(c, i) <= N (C(i - 1, i) = 0)
+      int lo = i - 1, up = hi;
+      while (up - lo > 1) {
+        const int mid = (lo + up) >> 1;
+        if (tab[mid * kBinK + i] <= N) lo = mid; else up = mid;
+      }
+      N -= tab[lo * kBinK + i];
+      m |= 1ull << lo;
+      hi = lo;
+    }
+    if (!ok) atomicExch(bad, 1);
+    masks[r] = ok ? m : 0ull;
+  }
+}
+
+__global__ void k_masks_to_ranks(const uint64_t* __restrict__ masks, int64_t rows, int k,
+                                 uint32_t* __restrict__ ranks, int* __restrict__ bad) {
+  __shared__ uint32_t tab[kBinN * kBinK];
+  load_binom(tab);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t m = masks[r];
+    if (__popcll(m) != k) atomicExch(bad, 1);
+    uint32_t N = 0;
+    for (int i = 1; i <= k && m; ++i) {
+      const int c = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      N += tab[c * kBinK + i];
+    }
+    ranks[r] = N;
+  }
+}
+}  // namespace
+
+extern "C" int moeb_ranks_to_masks(const uint32_t* ranks, int64_t rows, int k, int E,
+                                   uint64_t* masks, int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(ranks && masks && bad && rows >= 0 && k >= 1 && k <= 8 && E >= k && E <= 64,
+               "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_ranks_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(ranks, rows, k, E, masks, bad);
+  return moeb::check_launch("k_ranks_to_masks");
+}
+
+extern "C" int moeb_masks_to_ranks(const uint64_t* masks, int64_t rows, int k, int E,
+                                   uint32_t* ranks, int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(ranks && masks && bad && rows >= 0 && k >= 1 && k <= 8 && E >= k && E <= 64,
+               "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_masks_to_ranks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, ranks, bad);
+  return moeb::check_launch("k_masks_to_ranks");
+}

@@ -19,7 +19,7 @@ from . import _native as nat
 from .cache import POLICIES, CacheConfig
 from .core import ConfigError, ModelShape, RangeError
 from .metrics import MetricCounts, mask_metrics, metric_vector
-from .traces import PackedTraces, ids_to_masks, pack_traces
+from .traces import PackedTraces, ids_to_masks, pack_traces, ranks_to_masks
 
 
 @dataclass(frozen=True)
@@ -338,10 +338,11 @@ class StreamingReplay:
     row-balanced prompt ranges and the predictor starts on each range as it
     lands (the replay needs the whole batch's masks).
 
-    A host batch is either the int64 mask rows [rows][W] or, for E <= 64, the
-    compact wire format ``masks_to_ids`` produces (u8 [rows][k] expert ids,
-    k / 8 of the bytes for k = 6): the ids are copied and decoded into masks on
-    the copy stream (``ids_bad`` turns 1 if an id was >= E).
+    A host batch is either the int64 mask rows [rows][W] or, for E <= 64, a
+    compact wire format decoded into masks on the copy stream: the u8 expert
+    ids of ``masks_to_ids`` ([rows][k], 6 B/row at k = 6; ``ids_bad`` turns 1
+    if an id was >= E) or the int32 combinatorial ranks of ``masks_to_ranks``
+    ([rows], 4 B/row; ``ids_bad`` turns 1 for a rank >= C(E, k)).
 
     ``run`` returns, per batch, pinned host tensors (counters [C][4+3L],
     metrics [3E+3] or None), valid after ``torch.cuda.synchronize()`` (or the
@@ -399,7 +400,8 @@ class StreamingReplay:
             empty = getattr(predictor, "empty", False) and not metrics
             split = i == 0 and len(self.first_views) > 1 and not empty
             parts = []
-            compact = hb.dtype == torch.uint8  # [rows][k] expert ids, decoded on device
+            ranked = hb.dtype == torch.int32 and hb.dim() == 1  # [rows] combinatorial ranks
+            compact = ranked or hb.dtype == torch.uint8  # or [rows][k] expert ids
             with torch.cuda.stream(self.s_copy):
                 if freed[b] is not None:
                     for e in freed[b]:
@@ -407,14 +409,17 @@ class StreamingReplay:
                             self.s_copy.wait_event(e)
                 if compact:
                     ib = self.ids_bufs[b]
-                    if ib is None or ib.shape != hb.shape:
-                        ib = self.ids_bufs[b] = torch.empty(hb.shape, dtype=torch.uint8,
+                    if ib is None or ib.shape != hb.shape or ib.dtype != hb.dtype:
+                        ib = self.ids_bufs[b] = torch.empty(hb.shape, dtype=hb.dtype,
                                                             device=dev)
 
                 def land(dst, r0, r1):
                     if compact:
                         ib[r0:r1].copy_(hb[r0:r1], non_blocking=True)
-                        ids_to_masks(ib[r0:r1], E, dst, self.ids_bad)
+                        if ranked:
+                            ranks_to_masks(ib[r0:r1], shape.top_k, E, dst, self.ids_bad)
+                        else:
+                            ids_to_masks(ib[r0:r1], E, dst, self.ids_bad)
                     else:
                         dst.copy_(hb[r0:r1], non_blocking=True)
 

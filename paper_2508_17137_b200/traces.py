@@ -16,6 +16,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import math
+
 import numpy as np
 import torch
 
@@ -284,6 +286,32 @@ def masks_to_ids(truth: torch.Tensor, k: int) -> torch.Tensor:
     if int(bad.item()):
         raise RangeError(f"a row has more than {k} experts")
     return ids
+
+
+def masks_to_ranks(truth: torch.Tensor, k: int, num_experts: int) -> torch.Tensor:
+    """One-word expert masks -> the 4-byte wire format: each row's rank in
+    the combinatorial number system (sum_i C(c_i, i) over its ascending ids),
+    int32 holding the u32 rank (moeb_masks_to_ranks). Every row must carry
+    exactly k experts, as a validated reference trace row does."""
+    if math.comb(int(num_experts), int(k)) >= 2**32 or num_experts > 64 or k > 8:
+        raise ConfigError(f"rank wire format needs C(E, k) < 2^32, E <= 64, k <= 8")
+    t = truth.reshape(-1).contiguous()
+    out = torch.empty(t.numel(), dtype=torch.int32, device=t.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=t.device)
+    nat.call("moeb_masks_to_ranks", nat.ptr(t), t.numel(), int(k), int(num_experts),
+             nat.ptr(out), nat.ptr(bad), nat.stream_ptr())
+    if int(bad.item()):
+        raise RangeError(f"a row does not have exactly {k} experts")
+    return out
+
+
+def ranks_to_masks(ranks: torch.Tensor, k: int, num_experts: int, out: torch.Tensor,
+                   bad: torch.Tensor):
+    """Device decode of the rank rows into masks (moeb_ranks_to_masks); bad[0]
+    is set to 1 (asynchronously) if a rank is >= C(E, k)."""
+    nat.call("moeb_ranks_to_masks", nat.ptr(ranks), ranks.shape[0], int(k), int(num_experts),
+             nat.ptr(out), nat.ptr(bad), nat.stream_ptr())
+    return out
 
 
 def ids_to_masks(ids: torch.Tensor, num_experts: int, out: torch.Tensor, bad: torch.Tensor):

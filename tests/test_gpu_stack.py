@@ -67,6 +67,36 @@ def test_stack_replay_equals_exact(geom, ragged, warmup, monkeypatch):
         assert torch.equal(got_pp, want) and torch.equal(pp, want_pp), (masks is None, unbounded)
 
 
+@pytest.mark.parametrize("ragged", [False, True])
+def test_stack_replay_equals_exact_headline_length(ragged, monkeypatch):
+    """The bench's prompt length (C2: 363 decode tokens, 26 x 64 top-6,
+    warm-up 8) at every C3 capacity: K1s's bounded look-back (previous-token
+    formula, span unions, the per-warp row ring) across long prompts."""
+    import paper_2508_17137_b200 as m
+    m.load_library()
+    shape = m.ModelShape(26, 64, 6)
+    L = 26
+    packed = _packed(m, shape, 40, 363, 7, ragged)
+    w = np.random.default_rng(0).normal(0.0, 0.01, (64, 91))
+    model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
+    learned = m.make_predictor("learned_linear", shape, model=model).predict_masks(packed, 6, 8)
+    caps = [m.CacheConfig(capacity_fraction=f).resolve_capacity(shape)
+            for f in (0.05, 0.10, 0.15, 0.20, 0.25, 0.30, 0.40, 0.50)]
+    for masks in (learned, None):
+        streams = [(masks, None, False)]
+        monkeypatch.setenv("MOEB_K1_STACK", "0")
+        want, want_pp, _ = m.cache_replay(packed, streams, caps, 8, 6)
+        monkeypatch.setenv("MOEB_K1_STACK", "1")
+        got, pp, _ = m.cache_replay(packed, streams, caps, 8, 6)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want) and torch.equal(pp, want_pp), masks is None
+        assert int(want[0, 0, 0]) == sum(6 * (int(packed.row_off_host[p + 1] -
+                                                   packed.row_off_host[p]) // L - 8)
+                                          for p in range(40) if
+                                          (packed.row_off_host[p + 1] -
+                                           packed.row_off_host[p]) // L > 8)
+
+
 def test_stack_replay_several_streams(monkeypatch):
     """Several prediction streams in one call (blockIdx.y): per-stream lists
     of undecided prompts and per-stream upstream counts."""

@@ -61,3 +61,64 @@ def test_streaming_compact_ids_equals_masks():
     m.ids_to_masks(bad_ids, 64, back, bad)
     torch.cuda.synchronize()
     assert int(bad.item()) == 1
+
+
+@pytest.mark.parametrize("geom", [(26, 64, 6), (3, 64, 2), (5, 40, 4), (4, 48, 7)])
+def test_streaming_ranks_equals_masks(geom):
+    """Host batches as u32 combinatorial ranks (4 B/row, decoded on device)
+    give the counters and metrics of the mask batches; masks <-> ranks round
+    trip (every k-subset of small E enumerated); out-of-range ranks and rows
+    without exactly k experts are flagged."""
+    import itertools
+    import math
+
+    import paper_2508_17137_b200 as m
+    m.load_library()
+    L, E, k = geom
+    shape = m.ModelShape(L, E, k)
+    b = m.generate_packed(m.GeneratorConfig(40, 30, shape, max(8, k), 0.9, 4))
+    ranks = m.masks_to_ranks(b.truth, k, E)
+    assert ranks.shape == (b.rows,) and ranks.dtype == torch.int32
+    back = torch.empty_like(b.truth)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    m.ranks_to_masks(ranks, k, E, back, bad)
+    torch.cuda.synchronize()
+    assert torch.equal(back, b.truth) and int(bad.item()) == 0
+    # the combinatorial number system, restated: rank = sum_i C(c_i, i)
+    t = b.truth.reshape(-1).cpu().numpy().view(np.uint64)[:500]
+    r = ranks.cpu().numpy().view(np.uint32)[:500]
+    for mask, rank in zip(t, r):
+        ids = [e for e in range(E) if (int(mask) >> e) & 1]
+        assert sum(math.comb(c, i + 1) for i, c in enumerate(ids)) == int(rank)
+    if math.comb(E, k) <= 200000:  # every subset maps to 0 .. C(E, k) - 1 and back
+        subs = list(itertools.combinations(range(E), k))
+        mk = torch.tensor([sum(1 << e for e in s) - (1 << 64 if sum(1 << e for e in s) >= 1 << 63
+                                                     else 0) for s in subs],
+                          dtype=torch.int64, device="cuda")
+        rk = m.masks_to_ranks(mk, k, E)
+        assert sorted(rk.cpu().tolist()) == list(range(len(subs)))
+    if L == 26:
+        w = np.random.default_rng(2).normal(0.0, 0.01, (64, 91))
+        model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
+        pred = m.make_predictor("learned_linear", shape, model=model)
+        sr = m.StreamingReplay(shape, b.row_off_host, b.prompt_ids)
+        mask_host = b.truth.cpu().pin_memory()
+        rank_host = ranks.cpu().pin_memory()
+        r1 = sr.run(pred, [83, 166], 8, 6, [mask_host] * 3, metrics=True)
+        r2 = sr.run(pred, [83, 166], 8, 6, [rank_host] * 3, metrics=True)
+        torch.cuda.synchronize()
+        assert int(sr.ids_bad.item()) == 0
+        for (c1, v1), (c2, v2) in zip(r1, r2):
+            assert torch.equal(c1, c2) and torch.equal(v1, v2)
+    over = ranks.clone()
+    over[5] = math.comb(E, k)
+    m.ranks_to_masks(over, k, E, back, bad)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 1
+    wrong = b.truth.clone()
+    wrong[7] = 1
+    with pytest.raises(m.RangeError):
+        m.masks_to_ranks(wrong, k, E)
+    if k == 6:  # C(64, 8) >= 2^32: no 4-byte rank format
+        with pytest.raises(m.ConfigError):
+            m.masks_to_ranks(b.truth, 8, 64)
