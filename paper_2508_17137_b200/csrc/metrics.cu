@@ -451,9 +451,9 @@ extern "C" int moeb_masks_to_ids(const uint64_t* masks, int64_t rows, int k, uin
 namespace {
 constexpr int kBinN = 65, kBinK = 9;
 
-__device__ __forceinline__ void load_binom(uint32_t* tab) {  // C(n, j), n <= 64, j <= 8
+__device__ __forceinline__ void load_binom(uint32_t* tab) {  // tab[j * kBinN + n] = C(n, j)
   for (int i = threadIdx.x; i < kBinN * kBinK; i += blockDim.x) {
-    const int n = i / kBinK, j = i % kBinK;
+    const int j = i / kBinN, n = i % kBinN;
     uint64_t c = 1;
     for (int q = 0; q < j; ++q) c = c * (uint64_t)(n - q) / (uint64_t)(q + 1);
     tab[i] = j > n ? 0u : (c > 0xffffffffull ? 0xffffffffu : (uint32_t)c);
@@ -470,15 +470,18 @@ __global__ void k_ranks_to_masks(const uint32_t* __restrict__ ranks, int64_t row
     uint32_t N = ranks[r];
     uint64_t m = 0;
     int hi = E;  // c_i < hi
-    bool ok = N < tab[E * kBinK + k];
+    const bool ok = N < tab[k * kBinN + E];
     for (int i = k; i >= 1; --i) {
-      // largest c in [i - 1, hi) with C(c, i) <= N (C(i - 1, i) = 0)
-      int lo = i - 1, up = hi;
-      while (up - lo > 1) {
-        const int mid = (lo + up) >> 1;
-        if (tab[mid * kBinK + i] <= N) lo = mid; else up = mid;
+      // largest c in [i - 1, hi) with C(c, i) <= N (C(i - 1, i) = 0): a
+      // branch-free binary search of fixed length (no divergent trip counts)
+      const uint32_t* t = tab + i * kBinN;
+      int lo = i - 1;
+#pragma unroll
+      for (int step = 32; step; step >>= 1) {
+        const int c = lo + step;
+        lo = (c < hi && t[c] <= N) ? c : lo;
       }
-      N -= tab[lo * kBinK + i];
+      N -= t[lo];
       m |= 1ull << lo;
       hi = lo;
     }
@@ -499,7 +502,7 @@ __global__ void k_masks_to_ranks(const uint64_t* __restrict__ masks, int64_t row
     for (int i = 1; i <= k && m; ++i) {
       const int c = __ffsll((long long)m) - 1;
       m &= m - 1;
-      N += tab[c * kBinK + i];
+      N += tab[i * kBinN + c];
     }
     ranks[r] = N;
   }

@@ -331,8 +331,8 @@ class StreamingReplay:
     """Predict + replay over a sequence of host-resident batches of one prompt
     geometry (same row offsets), double-buffered: batch i+1's host->device
     copy runs on a copy stream while batch i is predicted and replayed on the
-    compute stream, and each batch's counters (plus fused prediction
-    metrics) go back to pinned host memory asynchronously. Throughput is
+    compute stream (three device buffers), and each batch's counters (plus
+    prediction metrics) go back to pinned host memory asynchronously. Throughput is
     max(copy, compute) per batch instead of their sum. The first batch has no
     compute to hide its copy behind, so it is copied in ``first_chunks``
     row-balanced prompt ranges and the predictor starts on each range as it
@@ -348,6 +348,12 @@ class StreamingReplay:
     metrics [3E+3] or None), valid after ``torch.cuda.synchronize()`` (or the
     returned event)."""
 
+    # device batch buffers: batch i+1 is copied while batch i computes, and a
+    # buffer is refilled only after the metrics pass (a low-priority stream
+    # that trails the compute stream) of the batch that used it two batches
+    # earlier, so the copy engine never waits for it
+    NBUF = 3
+
     def __init__(self, shape: ModelShape, row_off_host: np.ndarray, prompt_ids, device=None,
                  token_ids=None, first_chunks: int = 4):
         dev = torch.device(device) if device is not None else torch.device(
@@ -359,10 +365,11 @@ class StreamingReplay:
                                                      device=dev), off_d,
                                   np.asarray(row_off_host, dtype=np.int64),
                                   np.asarray(prompt_ids, dtype=np.int64), token_ids)
-                     for _ in range(2)]
-        self.ids_bufs = [None, None]  # device staging for compact (id) batches
+                     for _ in range(self.NBUF)]
+        self.ids_bufs = [None] * self.NBUF  # device staging for compact (id / rank) batches
         self.ids_bad = torch.zeros(1, dtype=torch.int32, device=dev)
         self.s_copy = torch.cuda.Stream(dev)
+        self.s_dec = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev, priority=-1)
         self.s_met = torch.cuda.Stream(dev, priority=0)
         self.device = dev
@@ -382,10 +389,11 @@ class StreamingReplay:
         L, E = shape.num_layers, shape.num_experts
         main = torch.cuda.current_stream(dev)
         self.s_copy.wait_stream(main)
+        self.s_dec.wait_stream(main)
         self.s_comp.wait_stream(main)
         self.s_met.wait_stream(main)
-        copied = [torch.cuda.Event(), torch.cuda.Event()]
-        freed = [None, None]
+        copied = [torch.cuda.Event() for _ in range(self.NBUF)]
+        freed = [None] * self.NBUF
         out = []
         host_batches = list(host_batches)
         # every batch's pinned read-back buffers up front, before any work is
@@ -395,7 +403,7 @@ class StreamingReplay:
                 for _ in host_batches]
         unbounded = bool(getattr(predictor, "unbounded_prefetch", False))
         for i, hb in enumerate(host_batches):
-            b = i % 2
+            b = i % self.NBUF
             buf = self.bufs[b]
             empty = getattr(predictor, "empty", False) and not metrics
             split = i == 0 and len(self.first_views) > 1 and not empty
@@ -414,27 +422,36 @@ class StreamingReplay:
                                                             device=dev)
 
                 def land(dst, r0, r1):
+                    """copy rows [r0, r1) (copy stream); compact rows are decoded
+                    into masks on the decode stream, so the copy engine goes on
+                    to the next range / batch meanwhile. Returns the event
+                    after which dst holds the masks."""
+                    done = torch.cuda.Event()
                     if compact:
                         ib[r0:r1].copy_(hb[r0:r1], non_blocking=True)
-                        if ranked:
-                            ranks_to_masks(ib[r0:r1], shape.top_k, E, dst, self.ids_bad)
-                        else:
-                            ids_to_masks(ib[r0:r1], E, dst, self.ids_bad)
+                        landed = torch.cuda.Event()
+                        landed.record(self.s_copy)
+                        self.s_dec.wait_event(landed)
+                        with torch.cuda.stream(self.s_dec):
+                            if ranked:
+                                ranks_to_masks(ib[r0:r1], shape.top_k, E, dst, self.ids_bad)
+                            else:
+                                ids_to_masks(ib[r0:r1], E, dst, self.ids_bad)
+                            done.record(self.s_dec)
                     else:
                         dst.copy_(hb[r0:r1], non_blocking=True)
+                        done.record(self.s_copy)
+                    return done
 
                 if split:  # first batch: copy range by range, predict as each lands
                     r0 = 0
                     for v in self.first_views:
                         r1 = r0 + v.rows
-                        land(v.truth, r0, r1)
-                        e = torch.cuda.Event()
-                        e.record(self.s_copy)
-                        parts.append(e)
+                        parts.append(land(v.truth, r0, r1))
                         r0 = r1
+                    copied[b] = parts[-1]
                 else:
-                    land(buf.truth, 0, buf.rows)
-                copied[b].record(self.s_copy)
+                    copied[b] = land(buf.truth, 0, buf.rows)
             with torch.cuda.stream(self.s_comp):
                 if not split:
                     self.s_comp.wait_event(copied[b])
@@ -485,6 +502,7 @@ class StreamingReplay:
                 out.append((c_h, v_h))
         main.wait_stream(self.s_comp)
         main.wait_stream(self.s_copy)
+        main.wait_stream(self.s_dec)
         main.wait_stream(self.s_met)
         return out
 
