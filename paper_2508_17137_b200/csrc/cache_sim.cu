@@ -35,10 +35,12 @@ constexpr uint64_t kPin = 1ull << 63;
 #define MOEB_HD __host__ __device__
 #ifdef __CUDA_ARCH__
 #define MOEB_ANY(x) __any_sync(__activemask(), (x))
+#define MOEB_GROUP_SYNC() __syncwarp(__activemask())
 __device__ __forceinline__ int moeb_ffs64(uint64_t x) { return __ffsll((long long)x); }
 __device__ __forceinline__ int moeb_popc64(uint64_t x) { return __popcll(x); }
 #else
 #define MOEB_ANY(x) (x)
+#define MOEB_GROUP_SYNC() ((void)0)
 inline int moeb_ffs64(uint64_t x) { return __builtin_ffsll((long long)x); }
 inline int moeb_popc64(uint64_t x) { return __builtin_popcountll(x); }
 #endif
@@ -181,14 +183,19 @@ struct LruState {
   }
 
   MOEB_HD __forceinline__ void compact() {
+    // every lane of the group runs this replicated loop over the shared queue:
+    // all lanes read an entry before any lane rewrites the queue
     uint32_t n = head;
     for (uint32_t i = head; i != tail; ++i) {
       const int k = q[i & qmask];
-      if (pos_of[k] == (uint16_t)i) {
+      const bool live = pos_of[k] == (uint16_t)i;
+      MOEB_GROUP_SYNC();
+      if (live) {
         q[n & qmask] = (uint16_t)k;
         pos_of[k] = (uint16_t)n;
         ++n;
       }
+      MOEB_GROUP_SYNC();
     }
     tail = n;
   }

@@ -181,12 +181,63 @@ def predict_stream(predictor, packed: PackedTraces, config: ReplayConfig, metric
     return masks, predictor.coverage(packed), bool(getattr(predictor, "unbounded_prefetch", False))
 
 
+def _group_world() -> int:
+    import torch.distributed as dist
+    return dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+
+
+def _job_devices(jobs: int, packed: PackedTraces) -> list:
+    """``jobs`` -> GPUs: the reference fans prompts out over
+    `jobs` worker processes (engine.py:222-238); here over up to `jobs`
+    visible GPUs of this process (the caller's device first)."""
+    n = min(max(1, int(jobs)), torch.cuda.device_count(), max(1, packed.num_prompts))
+    first = packed.device.index if packed.device.type == "cuda" else torch.cuda.current_device()
+    return [torch.device("cuda", (first + i) % torch.cuda.device_count()) for i in range(n)]
+
+
+def _replay_on_devices(packed: PackedTraces, predictor, config: ReplayConfig, caps, policy: str,
+                       per_prompt: bool, devices):
+    """Row-balanced prompt shards, one per device, launched asynchronously on
+    each device's current stream; counters summed (integer, order-free) and
+    per-prompt counters concatenated in prompt order on the host."""
+    budget, warmup = config.cache.prefetch_budget, config.warmup_tokens
+    launched = []
+    for i, dev in enumerate(devices):
+        shard = packed.shard(i, len(devices)).to(dev)
+        with torch.cuda.device(dev):
+            stream = predict_stream(predictor, shard, config)
+            counters, pp, _ = cache_replay(shard, [stream], caps, warmup, budget, policy,
+                                           per_prompt)
+        launched.append((shard, counters, pp))
+    vec = sum(c[0].cpu().numpy() for _, c, _ in launched)
+    pp = (np.concatenate([p[0].cpu().numpy() for _, _, p in launched], axis=1)
+          if per_prompt else None)
+    ids = np.concatenate([s.prompt_ids for s, _, _ in launched])
+    return vec, pp, ids
+
+
 def replay_traces(traces, predictor, config: ReplayConfig, jobs: int = 1, policy: str = "lru",
                   per_prompt: bool = True) -> SimReport:
-    """Replay every prompt; counters identical to the reference for any batch split."""
+    """Replay every prompt; counters identical to the reference for any batch
+    split and any ``jobs`` (engine.py:222-238; results are integer sums).
+
+    ``jobs`` maps to GPUs: with an initialised torch.distributed group of
+    more than one rank (one process per GPU, torchrun) every rank passes the
+    same traces, replays its row-balanced prompt shard and the counters are
+    all-reduced (``distributed.replay_sharded``; every rank returns the whole
+    report); otherwise ``jobs`` > 1 spreads the prompts over up to ``jobs``
+    GPUs visible to this process."""
     packed = _packed(traces, config.shape)
     _check_lengths(packed, config.warmup_tokens)
+    if _group_world() > 1:
+        from .distributed import replay_sharded
+        return replay_sharded(packed, predictor, config, policy=policy, per_prompt=per_prompt)
     cap = config.cache.resolve_capacity(config.shape)
+    devices = _job_devices(jobs, packed)
+    if len(devices) > 1:
+        vec, pp, ids = _replay_on_devices(packed, predictor, config, [cap], policy, per_prompt,
+                                          devices)
+        return SimReport.from_counters(config.shape, vec[0], None if pp is None else pp[0], ids)
     stream = predict_stream(predictor, packed, config)
     counters, pp, _ = cache_replay(packed, [stream], [cap], config.warmup_tokens,
                                    config.cache.prefetch_budget, policy, per_prompt)
@@ -578,13 +629,35 @@ def sweep(traces, predictor_factory, predictor_kind: str, capacities, shape: Mod
     _check_lengths(packed, warmup_tokens)
     cfgs = [ReplayConfig(shape, CacheConfig(capacity_fraction=f, prefetch_budget=prefetch_budget),
                          warmup_tokens, history_decay) for f in capacities]
-    stream = predict_stream(predictor_factory(), packed, cfgs[0])
     caps = [c.cache.resolve_capacity(shape) for c in cfgs]
-    counters, pp, _ = cache_replay(packed, [stream], caps, warmup_tokens, prefetch_budget, policy)
-    counters = counters.cpu().numpy()
-    pp = pp.cpu().numpy()
+    ids = packed.prompt_ids
+    if _group_world() > 1:  # one process per GPU: this rank's shard, counters all-reduced
+        import torch.distributed as dist
+        from .distributed import _all_reduce_sum
+        local = packed if packed.meta.get("presharded") else packed.shard(dist.get_rank(),
+                                                                          dist.get_world_size())
+        stream = predict_stream(predictor_factory(), local, cfgs[0])
+        counters, pp, _ = cache_replay(local, [stream], caps, warmup_tokens, prefetch_budget,
+                                       policy)
+        counters = _all_reduce_sum(counters).cpu().numpy()
+        gathered = [None] * dist.get_world_size()
+        dist.all_gather_object(gathered, (pp.cpu().numpy(), local.prompt_ids))
+        pp = np.concatenate([g[0] for g in gathered], axis=2)
+        ids = np.concatenate([g[1] for g in gathered])
+    else:
+        devices = _job_devices(jobs, packed)
+        if len(devices) > 1:
+            counters, pp, ids = _replay_on_devices(packed, predictor_factory(), cfgs[0], caps,
+                                                   policy, True, devices)
+            counters, pp = counters[None], pp[None]
+        else:
+            stream = predict_stream(predictor_factory(), packed, cfgs[0])
+            counters, pp, _ = cache_replay(packed, [stream], caps, warmup_tokens,
+                                           prefetch_budget, policy)
+            counters = counters.cpu().numpy()
+            pp = pp.cpu().numpy()
     return [SweepPoint(f, predictor_kind,
-                       SimReport.from_counters(shape, counters[0, j], pp[0, j], packed.prompt_ids))
+                       SimReport.from_counters(shape, counters[0, j], pp[0, j], ids))
             for j, f in enumerate(capacities)]
 
 

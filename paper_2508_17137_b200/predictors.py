@@ -144,18 +144,19 @@ class GlobalFrequencyPredictor(DevicePredictor):
         E = shape.num_experts
         # order[l] = ids by (-count, id): a stable argsort of -count
         self._order = np.argsort(-self.counts, axis=1, kind="stable")
-        self._tables: dict[int, torch.Tensor] = {}
+        self._tables: dict[tuple, torch.Tensor] = {}  # (budget, device) -> table
 
     def _table(self, budget: int, device) -> torch.Tensor:
-        if budget not in self._tables:
+        key = (budget, str(device))
+        if key not in self._tables:
             L, W = self.shape.num_layers, self.shape.mask_words
             m = min(budget, self.shape.num_experts)
             tab = np.zeros((L, W), dtype=np.uint64)
             for l in range(L):
                 for e in self._order[l, :m]:
                     tab[l, e >> 6] |= np.uint64(1) << np.uint64(e & 63)
-            self._tables[budget] = torch.from_numpy(tab.view(np.int64)).to(device)
-        return self._tables[budget]
+            self._tables[key] = torch.from_numpy(tab.view(np.int64)).to(device)
+        return self._tables[key]
 
     def predict_masks(self, packed, budget, warmup=0, metrics=None):
         return _policy(3, packed, budget, table=self._table(budget, packed.device))

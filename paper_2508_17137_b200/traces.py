@@ -110,6 +110,17 @@ class PackedTraces:
                             torch.from_numpy(off).to(self.device), off, self.prompt_ids[order],
                             tok, {})
 
+    def to(self, device) -> "PackedTraces":
+        """The same prompts on another device (one copy of the mask rows)."""
+        device = torch.device(device)
+        if device == self.device:
+            return self
+        return PackedTraces(self.shape, self.truth.to(device), self.row_off.to(device),
+                            self.row_off_host, self.prompt_ids,
+                            None if self.token_ids is None else self.token_ids.to(device),
+                            {k: v for k, v in self.meta.items()
+                             if k not in ("embeddings", "row_token_ids")})
+
     def shard(self, rank: int, world: int) -> "PackedTraces":
         """Contiguous prompt range of this rank with ~equal row counts."""
         if world <= 1:
