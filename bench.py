@@ -277,7 +277,10 @@ def run_ours(args):
 
     def step(timing=None):
         vec = m.metrics.metric_vector(E, dev)
-        counters = pipe.run(pred, [cap], WARMUP_TOKENS, BUDGET, metrics=vec, timing=timing)
+        # per-prompt counters too, as the reference's replay_traces fills
+        # SimReport.per_prompt (engine.py:75, 148)
+        counters = pipe.run(pred, [cap], WARMUP_TOKENS, BUDGET, metrics=vec, timing=timing,
+                            per_prompt=True)
         if world > 1:
             buf = torch.cat([counters.view(-1), vec])
             dist.all_reduce(buf)
@@ -352,13 +355,14 @@ def run_ours(args):
         truth_host = packed.truth.cpu().pin_memory()
     sr = m.StreamingReplay(shape, packed.row_off_host, packed.prompt_ids, dev)
     h2d = truth_host.numel() * truth_host.element_size()
-    d2h = (4 + 3 * L) * 8 + (3 * E + 3) * 8
+    d2h = (4 + 3 * L) * 8 + (3 * E + 3) * 8 + P * 4 * 8  # counters, metrics, per-prompt
 
     def e2e_run(n):
-        res = sr.run(pred, [cap], WARMUP_TOKENS, BUDGET, [truth_host] * n, metrics=True)
+        res = sr.run(pred, [cap], WARMUP_TOKENS, BUDGET, [truth_host] * n, metrics=True,
+                     per_prompt=True)
         if world > 1:
             torch.cuda.synchronize()
-            buf = torch.cat([torch.cat([c.view(-1), v]) for c, v in res]).to(dev)
+            buf = torch.cat([torch.cat([c.view(-1), v]) for c, v, _ in res]).to(dev)
             dist.all_reduce(buf)
             return buf.cpu()
         return res
@@ -393,6 +397,7 @@ def run_ours(args):
               file=sys.stderr)
     if world == 1:
         assert np.array_equal(res2[-1][0].numpy().reshape(-1), counters.cpu().numpy().reshape(-1))
+        assert np.array_equal(res2[-1][2].numpy(), pipe.last_per_prompt[0].cpu().numpy())
 
     # --- roofline of the dominant kernel (HBM-bound integer work) ---
     bytes_per_row = 16  # truth mask read + predicted mask (read by K1 / written by K3)

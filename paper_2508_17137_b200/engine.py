@@ -290,7 +290,7 @@ class PipelinedReplay:
         return sum(8 * (b - a + 1) for a, b in self.bounds)
 
     def run(self, predictor, capacities, warmup: int, budget: int, policy: str = "lru",
-            metrics=None, host_truth=None, counters=None, timing=None):
+            metrics=None, host_truth=None, counters=None, timing=None, per_prompt: bool = False):
         """Enqueue the pipeline; returns counters [1][C][4+3L] (device, ordered
         on the caller's current stream). ``metrics`` (int64 [3E+3]) receives the
         fused prediction metrics when the predictor supports them. ``timing``
@@ -305,6 +305,7 @@ class PipelinedReplay:
         for s in (self.s_copy, self.s_pred, self.s_sim, self.s_met):
             s.wait_stream(main)
         unbounded = bool(getattr(predictor, "unbounded_prefetch", False))
+        pps = []
         for ci, ((a, b), view) in enumerate(zip(self.bounds, self.views)):
             if host_truth is not None:
                 r0, r1 = int(packed.row_off_host[a]), int(packed.row_off_host[b])
@@ -337,13 +338,22 @@ class PipelinedReplay:
                 if ev:
                     e2, e3 = ev(), ev()
                     e2.record(self.s_sim)
-                cache_replay(view, [(masks, cov, unbounded)], capacities, warmup, budget,
-                             policy, want_per_prompt=False, counters=counters, given_counts=gc)
+                _, pp, _ = cache_replay(view, [(masks, cov, unbounded)], capacities, warmup,
+                                        budget, policy, want_per_prompt=per_prompt,
+                                        counters=counters, given_counts=gc)
                 if ev:
                     e3.record(self.s_sim)
                     timing.append(("replay", e2, e3, view.rows))
+                if per_prompt:
+                    pps.append(pp)
             if metrics is not None and masks is not None:
                 _overlapped_metrics(self.s_met, masks_ready, masks, view, warmup, metrics)
+        # per-prompt counters [1][C][P][4] (SimReport.per_prompt, engine.py:75)
+        self.last_per_prompt = None
+        if per_prompt:
+            with torch.cuda.stream(self.s_sim):
+                self.last_per_prompt = pps[0] if len(pps) == 1 else torch.cat(pps, dim=2)
+            self.last_per_prompt.record_stream(self.s_sim)
         main.wait_stream(self.s_sim)
         main.wait_stream(self.s_pred)
         main.wait_stream(self.s_met)
@@ -396,8 +406,8 @@ class StreamingReplay:
     ([rows], 4 B/row; ``ids_bad`` turns 1 for a rank >= C(E, k)).
 
     ``run`` returns, per batch, pinned host tensors (counters [C][4+3L],
-    metrics [3E+3] or None), valid after ``torch.cuda.synchronize()`` (or the
-    returned event)."""
+    metrics [3E+3] or None, and with ``per_prompt`` the per-prompt counters
+    [C][P][4]), valid after ``torch.cuda.synchronize()``."""
 
     # device batch buffers: batch i+1 is copied while batch i computes, and a
     # buffer is refilled only after the metrics pass (a low-priority stream
@@ -435,7 +445,7 @@ class StreamingReplay:
         return self.bufs[0].rows
 
     def run(self, predictor, capacities, warmup: int, budget: int, host_batches,
-            policy: str = "lru", metrics: bool = False, timing=None):
+            policy: str = "lru", metrics: bool = False, timing=None, per_prompt: bool = False):
         shape, dev = self.shape, self.device
         L, E = shape.num_layers, shape.num_experts
         main = torch.cuda.current_stream(dev)
@@ -449,8 +459,11 @@ class StreamingReplay:
         host_batches = list(host_batches)
         # every batch's pinned read-back buffers up front, before any work is
         # enqueued (a host allocation between launches would stall the pipeline)
+        P = self.bufs[0].num_prompts
         outs = [(torch.empty((len(capacities), 4 + 3 * L), dtype=torch.int64, pin_memory=True),
-                 torch.empty(3 * E + 3, dtype=torch.int64, pin_memory=True) if metrics else None)
+                 torch.empty(3 * E + 3, dtype=torch.int64, pin_memory=True) if metrics else None,
+                 torch.empty((len(capacities), P, 4), dtype=torch.int64, pin_memory=True)
+                 if per_prompt else None)
                 for _ in host_batches]
         unbounded = bool(getattr(predictor, "unbounded_prefetch", False))
         for i, hb in enumerate(host_batches):
@@ -528,12 +541,15 @@ class StreamingReplay:
                     cov = predictor.coverage(buf)
                 masks_ready = torch.cuda.Event()
                 masks_ready.record(self.s_comp)
-                cnt, _, _ = cache_replay(buf, [(masks, cov, unbounded)], capacities, warmup,
-                                         budget, policy, want_per_prompt=False, given_counts=gc)
+                cnt, pp, _ = cache_replay(buf, [(masks, cov, unbounded)], capacities, warmup,
+                                          budget, policy, want_per_prompt=per_prompt,
+                                          given_counts=gc)
                 ev = torch.cuda.Event()
                 ev.record(self.s_comp)
-                c_h, v_h = outs[i]
+                c_h, v_h, p_h = outs[i]
                 c_h.copy_(cnt[0], non_blocking=True)
+                if per_prompt:
+                    p_h.copy_(pp[0], non_blocking=True)
                 met_ev = None
                 if vec is not None:
                     # the metrics pass runs on its own (low-priority) stream and
@@ -550,7 +566,7 @@ class StreamingReplay:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(self.s_comp)
                     timing.append((e0, e1))
-                out.append((c_h, v_h))
+                out.append((c_h, v_h, p_h) if per_prompt else (c_h, v_h))
         main.wait_stream(self.s_comp)
         main.wait_stream(self.s_copy)
         main.wait_stream(self.s_dec)
