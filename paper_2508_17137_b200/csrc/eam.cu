@@ -22,6 +22,7 @@
 // to the lower index) picks the sketch; the prediction is a table lookup
 // topw[idx][l] precomputed by moeb_eam_prepare.
 #include <cfloat>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "common.cuh"
@@ -106,14 +107,14 @@ __global__ void __launch_bounds__(256) k_eam_predict(
 #pragma unroll
     for (int w = 0; w < W; ++w) tw[w] = __ldg(truth + r * W + w);
     if (t >= warmup) {
-      const double a_lo = 1.0 / (double)(t + 1);
       double best = -DBL_MAX;
       int bi = 0x7fffffff;
 #pragma unroll
       for (int j = 0; j < kSPT; ++j) {
         const int s = tid + j * nt;
         if (s < S) {
-          const double v = t > 0 ? dlo[j] * a_lo + dhi[j] / (double)t : dlo[j] * a_lo;
+          // score * t (t + 1): same argmax, no division (see k_eam_predict_tok)
+          const double v = t > 0 ? fma(dlo[j], (double)t, dhi[j] * (double)(t + 1)) : dlo[j];
           if (v > best) {  // ascending s within the thread: first max wins
             best = v;
             bi = s;
@@ -207,6 +208,143 @@ __global__ void __launch_bounds__(256) k_eam_predict(
   }
 }
 
+// K6 token-batched (E <= 64, S <= 128, L a template constant): thread s
+// owns sketch s and keeps its per-layer partial sums d_s(l') in registers; a
+// token's L rows are scored in one register pass, the L x S scores go to
+// shared memory, and each warp then takes the argmax of whole rows (lane =
+// 4 sketches, shuffles, ties to the lower index). Two block barriers per
+// token instead of two per row. The row's expert ids are decoded once per
+// token (by L threads, into shared memory), and the score is scaled by the
+// positive t (t + 1) -- score' = dlo t + dhi (t + 1), same argmax, no fp64
+// division (at t = 0: dlo).
+template <int L, int K>
+__global__ void __launch_bounds__(128) k_eam_predict_tok(
+    const uint64_t* __restrict__ truth, const int64_t* __restrict__ row_off, int E, int warmup,
+    const double* __restrict__ unit_t, const uint64_t* __restrict__ topw, int S,
+    int32_t* __restrict__ idx_out, uint64_t* __restrict__ pred) {
+  extern __shared__ __align__(16) unsigned char smem_tok[];
+  auto sc = reinterpret_cast<double(*)[128]>(smem_tok);  // [L][128] scores of the token's rows
+  // [L][8] element offsets (l E + ex) S of the rows' unit entries, ascending ex
+  auto offs = reinterpret_cast<int(*)[8]>(smem_tok + sizeof(double) * L * 128);
+  auto nks = reinterpret_cast<int*>(smem_tok + sizeof(double) * L * 128 + sizeof(int) * 8 * L);
+  const int p = blockIdx.x;
+  const int s = threadIdx.x, lane = s & 31, wid = s >> 5;
+  const bool live = s < S;
+  const double* us = unit_t + (live ? s : 0);
+  double d[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) d[l] = 0.0;
+  double dlo = 0.0, dhi = 0.0;
+  const int64_t r0 = row_off[p];
+  const int T = (int)((row_off[p + 1] - r0) / L);
+  for (int t = 0; t < T; ++t) {
+    if (s < L) {  // the row's unit-entry offsets, ascending expert id
+      uint64_t mm = __ldg(truth + r0 + (int64_t)t * L + s);
+      nks[s] = __popcll(mm);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int ex = mm ? __ffsll((long long)mm) - 1 : 0;
+        mm &= mm - 1;
+        offs[s][i] = (s * E + ex) * S;
+      }
+    }
+    __syncthreads();  // offsets of token t in; token t-1's argmax done with sc
+    const bool scored = t >= warmup;
+    const double ft = (double)t, ft1 = (double)(t + 1);
+    // the token's gathers in groups of kGrp layers, the next group's loads
+    // issued before this group's sums and recurrence (software pipelining;
+    // the loops are unrolled, so the buffer swap is register renaming)
+    constexpr int kGrp = 2;
+    double ga[kGrp][K], gb[kGrp][K];
+    bool fa[kGrp], fb[kGrp];
+    auto issue = [&](double (&gv)[kGrp][K], bool (&f)[kGrp], int l0) {
+#pragma unroll
+      for (int q = 0; q < kGrp; ++q) {
+        const int l = l0 + q;
+        f[q] = l < L && nks[l < L ? l : 0] == K;
+        if (f[q]) {
+          const int4 o0 = *reinterpret_cast<const int4*>(&offs[l][0]);
+          const int4 o1 = *reinterpret_cast<const int4*>(&offs[l][4]);
+          const int o[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+#pragma unroll
+          for (int i = 0; i < K; ++i) gv[q][i] = __ldg(us + o[i]);
+        }
+      }
+    };
+    issue(ga, fa, 0);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const int q = l % kGrp;
+      if (q == 0 && l + kGrp < L) issue(gb, fb, l + kGrp);
+      double g;
+      if (fa[q]) {  // the top-k row: summed in ascending expert order
+        g = ga[q][0];
+#pragma unroll
+        for (int i = 1; i < K; ++i) g += ga[q][i];
+      } else {  // any other expert count: in ascending order
+        g = 0.0;
+        uint64_t mm = __ldg(truth + r0 + (int64_t)t * L + l);
+        while (mm) {
+          const int ex = __ffsll((long long)mm) - 1;
+          mm &= mm - 1;
+          g += __ldg(us + (int64_t)(l * E + ex) * S);
+        }
+      }
+      if (q == kGrp - 1) {
+#pragma unroll
+        for (int a = 0; a < kGrp; ++a) {
+          fa[a] = fb[a];
+#pragma unroll
+          for (int i = 0; i < K; ++i) ga[a][i] = gb[a][i];
+        }
+      }
+      if (scored) sc[l][s] = live ? (t > 0 ? fma(dlo, ft, dhi * ft1) : dlo) : -DBL_MAX;
+      const double dold = d[l];
+      const double dnew = dold + g;
+      d[l] = dnew;
+      dhi -= dold;
+      dlo += dnew;
+    }
+    dhi = dlo;
+    dlo = 0.0;
+    __syncthreads();  // all scores of token t in
+    const int64_t rt = r0 + (int64_t)t * L;
+    if (scored) {
+      for (int l = wid; l < L; l += 4) {
+        double best = -DBL_MAX;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // ascending s within the lane: first max wins
+          const int ss = lane + 32 * j;
+          const double v = sc[l][ss];
+          if (ss < S && v > best) {
+            best = v;
+            bi = ss;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > best || (ov == best && oi < bi)) {
+            best = ov;
+            bi = oi;
+          }
+        }
+        if (lane == 0) {
+          if (idx_out) idx_out[rt + l] = bi;
+          pred[rt + l] = topw[(int64_t)bi * L + l];
+        }
+      }
+    } else {
+      for (int l = s; l < L; l += blockDim.x) {
+        if (idx_out) idx_out[rt + l] = -1;
+        pred[rt + l] = 0;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" int moeb_eam_prepare(const double* sketches, int S, int L, int E, int budget,
@@ -239,6 +377,23 @@ extern "C" int moeb_eam_predict(const uint64_t* truth, const int64_t* prompt_row
     return moeb::fail(MOEB_ESMEM, "eam state %zu B (L*S doubles) exceeds shared memory", smem);
   cudaStream_t s = moeb::as_stream(stream);
   const int W = moeb::words_for(E);
+  const char* env = getenv("MOEB_K6");  // MOEB_K6=row: the row-by-row kernel
+  if (W == 1 && S <= 128 && (L == 26 || L == 27) && !(env && env[0] == 'r')) {
+    const int tsm = (int)(sizeof(double) * L * 128 + sizeof(int) * 9 * L);
+#define MOEB_EAM_TOK(LL, KK)                                                                   \
+  do {                                                                                         \
+    moeb::set_smem(k_eam_predict_tok<LL, KK>, tsm);                                            \
+    k_eam_predict_tok<LL, KK><<<n_prompts, 128, tsm, s>>>(truth, prompt_row_off, E,            \
+                                                          warmup_tokens, unit_t, topw, S,       \
+                                                          idx_out, pred);                       \
+  } while (0)
+    if (L == 26)
+      MOEB_EAM_TOK(26, 6);
+    else
+      MOEB_EAM_TOK(27, 6);
+#undef MOEB_EAM_TOK
+    return moeb::check_launch("k_eam_predict_tok");
+  }
 #define MOEB_EAM_LAUNCH(WW)                                                                     \
   do {                                                                                         \
     cudaFuncSetAttribute(k_eam_predict<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
