@@ -100,10 +100,16 @@ class TransformerRef(nn.Module):
         return self.head2(F.gelu(self.head1(x)))
 
     @torch.no_grad()
-    def logits(self, token_ids_per_row, layer_ids_per_row, row_off):
+    def logits(self, token_ids_per_row, layer_ids_per_row, row_off, device="cpu"):
         """Logits for every trace row of CSR-packed prompts (rows in (token,
-        layer) order); windows never cross prompts."""
+        layer) order); windows never cross prompts. `device` runs the same
+        fp32 math on a GPU for large checks (TF32 off)."""
         W = self.spec.window
+        dev = torch.device(device)
+        if dev.type == "cuda":
+            torch.backends.cuda.matmul.allow_tf32 = False
+            torch.backends.cudnn.allow_tf32 = False
+        self.to(dev)
         tok = torch.as_tensor(token_ids_per_row, dtype=torch.int64)
         lay = torch.as_tensor(layer_ids_per_row, dtype=torch.int64)
         out = torch.empty(len(tok), self.spec.num_experts)
@@ -121,9 +127,10 @@ class TransformerRef(nn.Module):
                 ti[b, :e - s] = tok[s:e]
                 li[b, :e - s] = lay[s:e]
                 pad[b, :e - s] = False
-            y = self.forward_windows(ti, li, pad)
+            y = self.forward_windows(ti.to(dev), li.to(dev), pad.to(dev)).cpu()
             for b, (s, e) in enumerate(chunk):
                 out[s:e] = y[b, :e - s]
+        self.to("cpu")
         return out
 
 
