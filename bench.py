@@ -499,7 +499,9 @@ def run_ours(args):
         mct = m.MetricCounts.from_vector(vec_t.cpu().numpy(), E)
         tr_info = {
             "workload": f"C2 slice: {Pt} prompts x {C2['tokens']} tokens (rows {tpk.rows})",
-            "predictor": "transformer 4x(d512,h8,ff2048), windows 512, fp16 operands / fp32 acc",
+            "predictor": "transformer 4x(d512,h8,ff2048), windows 512",
+            "dtype": "fp16 GEMM/attention operands, fp32 accumulation, fp16 residual stream "
+                     "(fp32 LayerNorm statistics)",
             "trace_tok_per_s": Pt * C2["tokens"] / (tms / 1e3), "ms_per_step": tms,
             "tflops_achieved": tot_flops / (tms / 1e3) / 1e12, "kernels": ker,
             "roofline": {"bound": "tensor", "kernel": tdom, "achieved": ker[tdom]["tflops"],
@@ -625,8 +627,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eam-sketches", type=int, default=100000,
                     help="EAM library size for the C4 matcher leg (0: skip)")
-    ap.add_argument("--transformer-prompts", type=int, default=700,
-                    help="C2 prompts replayed with the transformer predictor (0: skip)")
+    ap.add_argument("--transformer-prompts", type=int, default=C2["prompts"],
+                    help="C2 prompts replayed with the transformer predictor (default: all of "
+                         "C2; 0: skip)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "0"))
     if world == 0 and args.gpus > 1:

@@ -314,6 +314,8 @@ int moeb_match_queries(const double* queries, int M, int D, const double* unit_t
  *    of each row, out16 (as int32) = its first argmax column (m-fastest raster)
  *  6 RESID_ADD: out32 += C + bias (fp32 residual stream, in place; the
  *    post-norm LayerNorm then runs as moeb_layernorm_rows)
+ *  7 RESID_ADD16: out16 += C + bias (16-bit residual stream, row stride ld16,
+ *    in place; then moeb_layernorm_rows16)
  * K % 64 == 0, N % 64 == 0.
  */
 int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, int N, int K, int fp16,
@@ -340,6 +342,11 @@ int moeb_embed_rows(const float* ptok, const float* play, const int32_t* token_i
  * out16 = 16-bit copy (the next GEMM's operand). */
 int moeb_layernorm_rows(float* x32, void* out16, const float* w, const float* b, int64_t rows,
                         float eps, int fp16, void* stream);
+/* The 16-bit residual stream's LayerNorm (512 columns, in place): x16 =
+ * LayerNorm(x16) with fp32 statistics; pairs with the GEMM epilogue
+ * EPI_RESID_ADD16 (out16 += A B^T + bias). */
+int moeb_layernorm_rows16(void* x16, const float* w, const float* b, int64_t rows, float eps,
+                          int fp16, void* stream);
 /* fp32 -> 16-bit (fp16 or bf16) conversion (weight packing). */
 int moeb_to16(const float* x, void* y, int64_t n, int fp16, void* stream);
 

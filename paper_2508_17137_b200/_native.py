@@ -61,6 +61,7 @@ _SIGS = {
     "moeb_embed_rows": [P, P, P, I32, I64, P, P, I32, P],
     "moeb_to16": [P, P, I64, I32, P],
     "moeb_layernorm_rows": [P, P, P, P, I64, ctypes.c_float, I32, P],
+    "moeb_layernorm_rows16": [P, P, P, I64, ctypes.c_float, I32, P],
     "moeb_eam_pack_library": [P, I32, I32, I32, P, P, P],
     "moeb_eam_pack_queries": [P, I32, I32, P, P],
     "moeb_eam_rerank": [P, P, I32, P, P, P, I32, I32, I32, DBL, P, P, P, P],

@@ -36,7 +36,8 @@ enum : int {
   EPI_BIAS_GELU = 3,
   EPI_RESID_LN = 4,
   EPI_ROWMAX = 5,  // per (row, N-tile): max value (out32) and first argmax column (out16 as int32)
-  EPI_RESID_ADD = 6  // out32 += C + bias (fp32 residual stream, in place; LN runs separately)
+  EPI_RESID_ADD = 6,   // out32 += C + bias (fp32 residual stream, in place; LN runs separately)
+  EPI_RESID_ADD16 = 7  // out16 += C + bias (16-bit residual stream, in place)
 };
 
 struct GemmArgs {
@@ -75,7 +76,8 @@ __global__ void __launch_bounds__(320, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
   constexpr int ACC = BN <= 256 ? 2 : 1;           // TMEM accumulator buffers
-  constexpr bool kTbuf = EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD;  // 32x33 transposes
+  constexpr bool kTbuf = EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD ||
+                         EPI == EPI_RESID_ADD16;  // 32x33 transposes
   constexpr uint32_t TMEM_COLS = BN * ACC <= 32 ? 32 : BN * ACC;
   constexpr int BROWS = PAIR ? BN / 2 : BN;        // B rows held by this CTA
   constexpr int TM = PAIR ? 2 * BM : BM;            // output rows per tile
@@ -349,6 +351,36 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
         pair_sync();
+      } else if (EPI == EPI_RESID_ADD16) {
+        // out16 += acc + bias (16-bit residual stream): as EPI_RESID_ADD,
+        // lanes walk columns through the padded transpose, 2 B per element
+        float* T = tbuf + ew * (32 * 33);
+        const int rowbase = tm * TM + rank * BM + quarter * 32;
+        uint16_t* o16 = static_cast<uint16_t*>(g.out16);
+        for (int c0 = cb; c0 < cb + HC; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(t0 + c0, r);
+          const int col = tn * BN + c0 + lane;
+          const float bl = bias_smem ? sbias[col] : (g.bias ? __ldg(g.bias + col) : 0.f);
+          uint16_t res[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int rr = rowbase + i;
+            res[i] = rr < g.M ? o16[(int64_t)rr * g.ld16 + col] : (uint16_t)0;
+          }
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int rr = rowbase + i;
+            const float x = FP16 ? __half2float(__ushort_as_half(res[i]))
+                                 : __bfloat162float(__ushort_as_bfloat16(res[i]));
+            if (rr < g.M) o16[(int64_t)rr * g.ld16 + col] = to16(x + (T[i * 33 + lane] + bl), FP16);
+          }
+          __syncwarp();
+        }
       } else if (EPI == EPI_RESID_ADD) {
         // out32 += acc + bias with coalesced residual I/O: each 32 x 32
         // accumulator chunk goes through a padded shared-memory transpose and
@@ -541,7 +573,7 @@ int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + (BN / 2) * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
-                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD) ? 8 * 32 * 33 * sizeof(float)
+                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD || EPI == EPI_RESID_ADD16) ? 8 * 32 * 33 * sizeof(float)
                                                                      : 0) +
                       8 * 32 * 8 + kBiasMax * sizeof(float) + 16 +
                       ((EPI == EPI_BIAS || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS_GELU)
@@ -574,7 +606,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
-                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD) ? 8 * 32 * 33 * sizeof(float)
+                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD || EPI == EPI_RESID_ADD16) ? 8 * 32 * 33 * sizeof(float)
                                                                      : 0) +
                       8 * 32 * 8 +
                       kBiasMax * sizeof(float) + 16;
@@ -599,10 +631,12 @@ int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   if (bn == 512) return launch_gemm<512, 2, EPI, FP16>(ta, tb, tc, g, s);
   if (bn == 256) {
     if (pair_mode()) {  // 2-SM tiles (M = 256): B tile split across the CTA pair
-      if (EPI == EPI_RESID_ADD) return launch_gemm_pair<256, 4, EPI, FP16>(ta, tb, tc, g, s);
+      if (EPI == EPI_RESID_ADD || EPI == EPI_RESID_ADD16)
+        return launch_gemm_pair<256, 4, EPI, FP16>(ta, tb, tc, g, s);
       return launch_gemm_pair<256, 5, EPI, FP16>(ta, tb, tc, g, s);
     }
-    if (EPI == EPI_RESID_ADD) return launch_gemm<256, 3, EPI, FP16>(ta, tb, tc, g, s);  // + transposes
+    if (EPI == EPI_RESID_ADD || EPI == EPI_RESID_ADD16)
+      return launch_gemm<256, 3, EPI, FP16>(ta, tb, tc, g, s);  // + transposes
     return launch_gemm<256, 4, EPI, FP16>(ta, tb, tc, g, s);
   }
   if (bn == 128) return launch_gemm<128, 6, EPI, FP16>(ta, tb, tc, g, s);
@@ -618,7 +652,7 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
   moeb::clear_error();
   MOEB_REQUIRE(A && B && M >= 1 && N >= 1 && K >= 1, "bad GEMM arguments");
   MOEB_REQUIRE(K % BK == 0, "K must be a multiple of %d (got %d)", BK, K);
-  MOEB_REQUIRE(epi >= EPI_F32 && epi <= EPI_RESID_ADD, "unknown epilogue %d", epi);
+  MOEB_REQUIRE(epi >= EPI_F32 && epi <= EPI_RESID_ADD16, "unknown epilogue %d", epi);
   int bn;
   if (epi == EPI_RESID_LN) {
     MOEB_REQUIRE(N == 512, "LayerNorm epilogue needs N == 512");
@@ -649,6 +683,7 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
     case EPI_BIAS_RELU: return fp16 ? dispatch<EPI_BIAS_RELU, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_BIAS_RELU, false>(ta, tb, tc, g, bn, s);
     case EPI_BIAS_GELU: return fp16 ? dispatch<EPI_BIAS_GELU, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_BIAS_GELU, false>(ta, tb, tc, g, bn, s);
     case EPI_RESID_ADD: return fp16 ? dispatch<EPI_RESID_ADD, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_RESID_ADD, false>(ta, tb, tc, g, bn, s);
+    case EPI_RESID_ADD16: return fp16 ? dispatch<EPI_RESID_ADD16, true>(ta, tb, tc, g, bn, s) : dispatch<EPI_RESID_ADD16, false>(ta, tb, tc, g, bn, s);
     case EPI_ROWMAX: return fp16 ? launch_gemm<256, 4, EPI_ROWMAX, true>(ta, tb, tc, g, s) : launch_gemm<256, 4, EPI_ROWMAX, false>(ta, tb, tc, g, s);
     default: return fp16 ? launch_gemm<512, 2, EPI_RESID_LN, true>(ta, tb, tc, g, s) : launch_gemm<512, 2, EPI_RESID_LN, false>(ta, tb, tc, g, s);
   }

@@ -36,6 +36,7 @@ WINDOW = 512
 LN_EPS = 1e-5
 EPI_F32, EPI_BIAS, EPI_BIAS_RELU, EPI_BIAS_GELU, EPI_RESID_LN = range(5)
 EPI_RESID_ADD = 6
+EPI_RESID_ADD16 = 7
 
 
 def init_state(num_layers: int, num_experts: int, seed: int = 0) -> dict:
@@ -118,6 +119,13 @@ class TransformerWeights:
                    device)
 
 
+def layernorm16(x16, w, b, rows, fp16, eps=1e-5):
+    """Post-norm LayerNorm of the 16-bit residual stream, in place
+    (moeb_layernorm_rows16)."""
+    nat.call("moeb_layernorm_rows16", nat.ptr(x16), nat.ptr(w), nat.ptr(b), rows, float(eps),
+             int(bool(fp16)), nat.stream_ptr())
+
+
 def layernorm(x32, x16, w, b, rows, fp16, eps=1e-5):
     """Post-norm LayerNorm of the first `rows` rows (moeb_layernorm_rows)."""
     nat.call("moeb_layernorm_rows", nat.ptr(x32), nat.ptr(x16), nat.ptr(w), nat.ptr(b), rows,
@@ -145,11 +153,17 @@ class TransformerPredictor:
     empty = False
 
     def __init__(self, weights: TransformerWeights, shape: ModelShape, threshold: bool = False,
-                 chunk_rows: int = 1 << 20):
+                 chunk_rows: int = 1 << 20, resid16: bool | None = None):
         if shape.num_experts != weights.num_experts:
             raise ConfigError("transformer width != number of experts")
         self.weights, self.shape, self.threshold = weights, shape, threshold
         self.chunk_rows = chunk_rows
+        # residual stream in the 16-bit operand format (the post-norm sum is
+        # rounded once before its LayerNorm): 8 B of HBM traffic per element
+        # and sublayer instead of the fp32 stream's 18. Default: with fp16
+        # operands (C1: threshold agreement 99.97 %); bf16's 8-bit mantissa
+        # keeps the fp32 stream
+        self.resid16 = weights.fp16 if resid16 is None else bool(resid16)
 
     def coverage(self, packed):
         return None
@@ -212,17 +226,34 @@ class TransformerPredictor:
                       nat.ptr(att), nat.ptr(ws_d), nat.ptr(wl_d), len(ws), WINDOW, M,
                       int(W.fp16),
                       nat.stream_ptr())
-                # residual add fused into the GEMM epilogue (fp32 stream, two
-                # TMEM accumulators so epilogue and mainloop overlap), then a
-                # streaming LayerNorm kernel over the rows
-                timed("gemm_out", 2.0 * M * D_MODEL * D_MODEL, gemm, att, lay["o"], M, D_MODEL,
-                      D_MODEL, EPI_RESID_ADD, bias=lay["o_b"], out32=h32, fp16=W.fp16)
-                timed("layernorm", 0.0, layernorm, h32, h16, lay["n1_w"], lay["n1_b"], M, W.fp16)
+                # residual add fused into the GEMM epilogue (two TMEM
+                # accumulators so epilogue and mainloop overlap), then a
+                # streaming LayerNorm kernel over the rows; 16-bit residual
+                # stream in place by default (see resid16)
+                if self.resid16:
+                    timed("gemm_out", 2.0 * M * D_MODEL * D_MODEL, gemm, att, lay["o"], M,
+                          D_MODEL, D_MODEL, EPI_RESID_ADD16, bias=lay["o_b"], out16=h16,
+                          fp16=W.fp16)
+                    timed("layernorm", 0.0, layernorm16, h16, lay["n1_w"], lay["n1_b"], M,
+                          W.fp16)
+                else:
+                    timed("gemm_out", 2.0 * M * D_MODEL * D_MODEL, gemm, att, lay["o"], M,
+                          D_MODEL, D_MODEL, EPI_RESID_ADD, bias=lay["o_b"], out32=h32,
+                          fp16=W.fp16)
+                    timed("layernorm", 0.0, layernorm, h32, h16, lay["n1_w"], lay["n1_b"], M,
+                          W.fp16)
                 timed("gemm_ffn1", 2.0 * M * D_FF * D_MODEL, gemm, h16, lay["f1"], M, D_FF,
                       D_MODEL, EPI_BIAS_RELU, bias=lay["f1_b"], out16=ff, fp16=W.fp16)
-                timed("gemm_ffn2", 2.0 * M * D_MODEL * D_FF, gemm, ff, lay["f2"], M, D_MODEL,
-                      D_FF, EPI_RESID_ADD, bias=lay["f2_b"], out32=h32, fp16=W.fp16)
-                timed("layernorm", 0.0, layernorm, h32, h16, lay["n2_w"], lay["n2_b"], M, W.fp16)
+                if self.resid16:
+                    timed("gemm_ffn2", 2.0 * M * D_MODEL * D_FF, gemm, ff, lay["f2"], M, D_MODEL,
+                          D_FF, EPI_RESID_ADD16, bias=lay["f2_b"], out16=h16, fp16=W.fp16)
+                    timed("layernorm", 0.0, layernorm16, h16, lay["n2_w"], lay["n2_b"], M,
+                          W.fp16)
+                else:
+                    timed("gemm_ffn2", 2.0 * M * D_MODEL * D_FF, gemm, ff, lay["f2"], M, D_MODEL,
+                          D_FF, EPI_RESID_ADD, bias=lay["f2_b"], out32=h32, fp16=W.fp16)
+                    timed("layernorm", 0.0, layernorm, h32, h16, lay["n2_w"], lay["n2_b"], M,
+                          W.fp16)
             timed("gemm_head", 2.0 * M * (D_HEAD_MLP * D_MODEL + E * D_HEAD_MLP), self._head,
                   h16, y, out[r0:r0 + M], M)
         return out

@@ -65,6 +65,17 @@ def test_gemm_epilogues(tr, fp16, M, N, K):
         tr.layernorm(h32, h16, lw, lb, M, fp16)
         torch.testing.assert_close(h32, want, atol=5e-3, rtol=1e-3)
         torch.testing.assert_close(h16.float(), want, atol=5e-3 + q, rtol=q)
+        # 16-bit residual stream: out16 += C + bias in place, LayerNorm in
+        # place (the default transformer path); reference on the rounded
+        # 16-bit residual, the sum rounded once to 16 bits
+        r16 = resid.to(dt)
+        h16 = r16.clone()
+        tr.gemm(a, b, M, N, K, tr.EPI_RESID_ADD16, bias=bias, out16=h16, fp16=fp16)
+        x = (r16.float() + ref).to(dt)
+        torch.testing.assert_close(h16.float(), x.float(), atol=tol + 2 * q, rtol=2 * q)
+        tr.layernorm16(h16, lw, lb, M, fp16)
+        want16 = torch.nn.functional.layer_norm(x.float(), (N,), lw, lb, 1e-5)
+        torch.testing.assert_close(h16.float(), want16, atol=5e-3 + 2 * q, rtol=2 * q)
 
 
 @pytest.mark.parametrize("impl", ["fa", "tc1", "mma"])
