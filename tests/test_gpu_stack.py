@@ -90,7 +90,7 @@ def test_stack_replay_equals_exact_headline_length(ragged, monkeypatch):
         got, pp, _ = m.cache_replay(packed, streams, caps, 8, 6)
         torch.cuda.synchronize()
         assert torch.equal(got, want) and torch.equal(pp, want_pp), masks is None
-        assert int(want[0, 0, 0]) == sum(6 * (int(packed.row_off_host[p + 1] -
+        assert int(want[0, 0, 0]) == sum(6 * L * (int(packed.row_off_host[p + 1] -
                                                    packed.row_off_host[p]) // L - 8)
                                           for p in range(40) if
                                           (packed.row_off_host[p + 1] -
