@@ -14,7 +14,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmoeb.so")
+# MOEB_LIB: another in-tree build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("MOEB_LIB") or os.path.join(_PKG, "libmoeb.so")
 
 _lib = None
 _checked = False

@@ -476,6 +476,8 @@ __device__ __forceinline__ float ex2_ftz(float x) {  // one MUFU.EX2
 
 constexpr int FA_CK = 64;      // keys per chunk
 constexpr int FA_NST = 3;      // ring stages (K 8 KB + V 8 KB each)
+constexpr int FA_NS = 2;       // S buffers in tensor memory (64 columns each)
+__device__ __forceinline__ uint32_t s_col(int b) { return b == 2 ? 192u : (uint32_t)b * 64u; }
 constexpr int FA_THREADS = 320;
 
 struct FaSmem {
@@ -502,9 +504,9 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;             // [FA_NST]
   uint64_t* kv_empty = kv_full + FA_NST;    // [FA_NST]
-  uint64_t* s_full = kv_empty + FA_NST;     // [2]
-  uint64_t* s_empty = s_full + 2;           // [2]
-  uint64_t* p_full = s_empty + 2;           // [2]
+  uint64_t* s_full = kv_empty + FA_NST;     // [FA_NS]
+  uint64_t* s_empty = s_full + FA_NS;       // [FA_NS]
+  uint64_t* p_full = s_empty + FA_NS;       // [2]
   uint64_t* p_empty = p_full + 2;           // [2]
   uint64_t* o_full = p_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + FaSmem::SLOT);
@@ -526,9 +528,11 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < FA_NS; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&s_empty[b], 8);
+    }
+    for (int b = 0; b < 2; ++b) {
       mbar_init(&p_full[b], 8);
       mbar_init(&p_empty[b], 1);
     }
@@ -539,7 +543,7 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;  // S buffers at +0 / +64, O at +128
+  const uint32_t tmem = *tmem_slot;  // S buffers at +0 / +64 / +192, O at +128
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer =====
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
         const int c = g < nch ? g : g - nch;
         const bool v = g >= nch;
         const int st = g % FA_NST;
-        mbar_wait(&kv_empty[st], ((g / FA_NST) & 1) ^ 1);
+        mbar_wait_sleep(&kv_empty[st], ((g / FA_NST) & 1) ^ 1);
         unsigned char* stg = ring + st * 16384;
         mbar_expect_tx(&kv_full[st], v ? 16384 : 8192);
         tma_load_2d(stg, &tm, &kv_full[st], 512 + head * 64, r0 + c * FA_CK);
@@ -563,28 +567,28 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
       const uint32_t idesc_s = umma_idesc_f16(TQ, FA_CK, ab);
       const uint32_t idesc_o = umma_idesc_f16(TQ, 64, ab) | (1u << 16);  // V MN-major
       int s_use = 0;
-      mbar_wait(q_full, 0);
+      mbar_wait_sleep(q_full, 0);
       auto issue_s = [&](int g) {
         const int st = g % FA_NST;
-        mbar_wait(&kv_full[st], (g / FA_NST) & 1);
-        const int b = s_use & 1;
-        mbar_wait(&s_empty[b], ((s_use >> 1) & 1) ^ 1);
+        mbar_wait_sleep(&kv_full[st], (g / FA_NST) & 1);
+        const int b = s_use % FA_NS;
+        mbar_wait_sleep(&s_empty[b], ((s_use / FA_NS) & 1) ^ 1);
         tc_fence_after();
         const uint32_t kb = smem_u32(ring + st * 16384);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          mma_f16_ss(tmem + b * 64, umma_desc_sw128(smem_u32(sQ) + k * 32),
+          mma_f16_ss(tmem + s_col(b), umma_desc_sw128(smem_u32(sQ) + k * 32),
                      umma_desc_sw128(kb + k * 32), idesc_s, k > 0);
         mma_commit(&s_full[b]);
         if (g < nch) mma_commit(&kv_empty[st]);  // pass 1: K chunk consumed
         ++s_use;
       };
       for (int g = 0; g < nch; ++g) issue_s(g);
-      issue_s(nch);
+      for (int c = 0; c < FA_NS - 1 && c < nch; ++c) issue_s(nch + c);
       for (int c = 0; c < nch; ++c) {
         const int g = nch + c;
-        if (c + 1 < nch) issue_s(g + 1);
-        mbar_wait(&p_full[c & 1], (c >> 1) & 1);
+        if (c + FA_NS - 1 < nch) issue_s(g + FA_NS - 1);
+        mbar_wait_sleep(&p_full[c & 1], (c >> 1) & 1);
         tc_fence_after();
         const uint32_t vb = smem_u32(ring + (g % FA_NST) * 16384 + 8192);
         const uint32_t pb = smem_u32(sP + (c & 1) * 16384);
@@ -606,11 +610,11 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
     int s_use = 0;
     float mx = -INFINITY;
     for (int c = 0; c < nch; ++c) {  // pass 1: row max
-      const int b = s_use & 1;
-      mbar_wait(&s_full[b], (s_use >> 1) & 1);
+      const int b = s_use % FA_NS;
+      mbar_wait(&s_full[b], (s_use / FA_NS) & 1);
       tc_fence_after();
       uint32_t r[32];
-      tmem_ld32(tq + b * 64, r);
+      tmem_ld32(tq + s_col(b), r);
       tmem_ld_wait();
       const int k0 = c * FA_CK + half * 32;
       if (k0 + 32 <= n) {  // full chunk: no key mask
@@ -632,11 +636,11 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
     const float ms = mx * sl2;
     float sum = 0.f;
     for (int c = 0; c < nch; ++c) {  // pass 2: P and row sum
-      const int b = s_use & 1;
-      mbar_wait(&s_full[b], (s_use >> 1) & 1);
+      const int b = s_use % FA_NS;
+      mbar_wait(&s_full[b], (s_use / FA_NS) & 1);
       tc_fence_after();
       uint32_t r[32];
-      tmem_ld32(tq + b * 64, r);
+      tmem_ld32(tq + s_col(b), r);
       tmem_ld_wait();
       tc_fence_before();
       __syncwarp();

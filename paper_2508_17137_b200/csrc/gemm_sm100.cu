@@ -76,8 +76,7 @@ __global__ void __launch_bounds__(320, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
   constexpr int ACC = BN <= 256 ? 2 : 1;           // TMEM accumulator buffers
-  constexpr bool kTbuf = EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD ||
-                         EPI == EPI_RESID_ADD16;  // 32x33 transposes
+  constexpr bool kTbuf = EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD;  // 32x33 transposes
   constexpr uint32_t TMEM_COLS = BN * ACC <= 32 ? 32 : BN * ACC;
   constexpr int BROWS = PAIR ? BN / 2 : BN;        // B rows held by this CTA
   constexpr int TM = PAIR ? 2 * BM : BM;            // output rows per tile
@@ -110,8 +109,8 @@ __global__ void __launch_bounds__(320, 1)
   float* sbias = sbias0 + (mis ? (16u - mis) / 4u : 0u);
   const bool bias_smem = g.bias != nullptr && g.N <= kBiasMax;
   // 16-bit output staging for TMA stores: per epilogue warp two [32][32] boxes
-  constexpr bool kTmaOut =
-      PAIR && (EPI == EPI_BIAS || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS_GELU);
+  constexpr bool kTmaOut = PAIR && (EPI == EPI_BIAS || EPI == EPI_BIAS_RELU ||
+                                    EPI == EPI_BIAS_GELU || EPI == EPI_RESID_ADD16);
   unsigned char* stg0 = reinterpret_cast<unsigned char*>(sbias + kBiasMax);
   unsigned char* sstage = stg0 + ((128u - (smem_u32(stg0) & 127u)) & 127u);
   if (bias_smem)
@@ -351,36 +350,6 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
         pair_sync();
-      } else if (EPI == EPI_RESID_ADD16) {
-        // out16 += acc + bias (16-bit residual stream): as EPI_RESID_ADD,
-        // lanes walk columns through the padded transpose, 2 B per element
-        float* T = tbuf + ew * (32 * 33);
-        const int rowbase = tm * TM + rank * BM + quarter * 32;
-        uint16_t* o16 = static_cast<uint16_t*>(g.out16);
-        for (int c0 = cb; c0 < cb + HC; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld32(t0 + c0, r);
-          const int col = tn * BN + c0 + lane;
-          const float bl = bias_smem ? sbias[col] : (g.bias ? __ldg(g.bias + col) : 0.f);
-          uint16_t res[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int rr = rowbase + i;
-            res[i] = rr < g.M ? o16[(int64_t)rr * g.ld16 + col] : (uint16_t)0;
-          }
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
-          __syncwarp();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int rr = rowbase + i;
-            const float x = FP16 ? __half2float(__ushort_as_half(res[i]))
-                                 : __bfloat162float(__ushort_as_bfloat16(res[i]));
-            if (rr < g.M) o16[(int64_t)rr * g.ld16 + col] = to16(x + (T[i * 33 + lane] + bl), FP16);
-          }
-          __syncwarp();
-        }
       } else if (EPI == EPI_RESID_ADD) {
         // out32 += acc + bias with coalesced residual I/O: each 32 x 32
         // accumulator chunk goes through a padded shared-memory transpose and
@@ -412,16 +381,54 @@ __global__ void __launch_bounds__(320, 1)
         }
       } else {
         unsigned char* wstage = sstage + ew * 4096;  // this warp's two 2 KB boxes
+        // 16-bit residual rows (in place) are loaded one 32-column chunk
+        // ahead, so their HBM latency overlaps the previous chunk
+        const uint4* res_row = reinterpret_cast<const uint4*>(
+            reinterpret_cast<const uint16_t*>(g.out16) + (int64_t)row * g.ld16 + tn * BN);
+        uint4 rnext[4];
+        if (EPI == EPI_RESID_ADD16 && rv) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rnext[q] = res_row[(cb >> 3) + q];
+        }
         for (int c0 = cb; c0 < cb + HC; c0 += 32) {
           uint32_t r[32];
           tmem_ld32(t0 + c0, r);
           const int col = tn * BN + c0;
+          uint4 rcur[4];
+          if (EPI == EPI_RESID_ADD16 && rv) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) rcur[q] = rnext[q];
+            if (c0 + 32 < cb + HC) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) rnext[q] = res_row[((c0 + 32) >> 3) + q];
+            }
+          }
           float4 bb[8];
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             bb[q] = bias_smem ? reinterpret_cast<const float4*>(sbias + col)[q]
                     : g.bias  ? __ldg(reinterpret_cast<const float4*>(g.bias + col) + q)
                               : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (EPI == EPI_RESID_ADD16 && rv) {  // 16-bit residual row chunk (64 B), in place
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = rcur[q];
+              const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {  // elements 8q + 4h .. + 3 -> bb[2q + h]
+                float2 f0, f1;
+                if (FP16) {
+                  f0 = __half22float2(*reinterpret_cast<const __half2*>(&w4[2 * h]));
+                  f1 = __half22float2(*reinterpret_cast<const __half2*>(&w4[2 * h + 1]));
+                } else {
+                  f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[2 * h]));
+                  f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[2 * h + 1]));
+                }
+                float4& b4 = bb[2 * q + h];
+                b4 = make_float4(b4.x + f0.x, b4.y + f0.y, b4.z + f1.x, b4.w + f1.y);
+              }
+            }
+          }
           if (EPI == EPI_RESID_ADD && rv) {  // residual row chunk, loaded under the TMEM load
             const float4* res = reinterpret_cast<const float4*>(g.out32 + (int64_t)row * g.N + col);
 #pragma unroll
@@ -573,10 +580,11 @@ int launch_gemm_pair(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + (BN / 2) * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
-                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD || EPI == EPI_RESID_ADD16) ? 8 * 32 * 33 * sizeof(float)
+                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD) ? 8 * 32 * 33 * sizeof(float)
                                                                      : 0) +
                       8 * 32 * 8 + kBiasMax * sizeof(float) + 16 +
-                      ((EPI == EPI_BIAS || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS_GELU)
+                      ((EPI == EPI_BIAS || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS_GELU ||
+                        EPI == EPI_RESID_ADD16)
                            ? 8 * 4096 + 128
                            : 0);
   auto k = k_gemm<BN, STAGES, EPI, FP16, true>;
@@ -606,7 +614,7 @@ int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap&
   constexpr int ACC = BN <= 256 ? 2 : 1;
   const size_t smem = 1024 + (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) +
                       8 * (2 * STAGES + 2 * ACC) + 16 +
-                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD || EPI == EPI_RESID_ADD16) ? 8 * 32 * 33 * sizeof(float)
+                      ((EPI == EPI_RESID_LN || EPI == EPI_RESID_ADD) ? 8 * 32 * 33 * sizeof(float)
                                                                      : 0) +
                       8 * 32 * 8 +
                       kBiasMax * sizeof(float) + 16;
@@ -631,12 +639,10 @@ int dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc
   if (bn == 512) return launch_gemm<512, 2, EPI, FP16>(ta, tb, tc, g, s);
   if (bn == 256) {
     if (pair_mode()) {  // 2-SM tiles (M = 256): B tile split across the CTA pair
-      if (EPI == EPI_RESID_ADD || EPI == EPI_RESID_ADD16)
-        return launch_gemm_pair<256, 4, EPI, FP16>(ta, tb, tc, g, s);
+      if (EPI == EPI_RESID_ADD) return launch_gemm_pair<256, 4, EPI, FP16>(ta, tb, tc, g, s);
       return launch_gemm_pair<256, 5, EPI, FP16>(ta, tb, tc, g, s);
     }
-    if (EPI == EPI_RESID_ADD || EPI == EPI_RESID_ADD16)
-      return launch_gemm<256, 3, EPI, FP16>(ta, tb, tc, g, s);  // + transposes
+    if (EPI == EPI_RESID_ADD) return launch_gemm<256, 3, EPI, FP16>(ta, tb, tc, g, s);  // + transposes
     return launch_gemm<256, 4, EPI, FP16>(ta, tb, tc, g, s);
   }
   if (bn == 128) return launch_gemm<128, 6, EPI, FP16>(ta, tb, tc, g, s);
@@ -668,7 +674,8 @@ extern "C" int moeb_gemm(const void* A, int lda, const void* B, int ldb, int M, 
   CUtensorMap ta, tb, tc;
   if (int rc = make_map(&ta, A, M, K, lda, BM, fp16)) return rc;
   memset(&tc, 0, sizeof(tc));
-  const bool tma_out = epi >= EPI_BIAS && epi <= EPI_BIAS_GELU && bn == 256 && pair_mode();
+  const bool tma_out = ((epi >= EPI_BIAS && epi <= EPI_BIAS_GELU) || epi == EPI_RESID_ADD16) &&
+                       bn == 256 && pair_mode();
   if (tma_out) {  // 16-bit output tile stores by TMA (32 x 32 boxes)
     if (int rc = make_out_map(&tc, out16, M, N, ld16, fp16)) return rc;
   }

@@ -54,7 +54,11 @@ def main():
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / args.steps
-    out = {"rows": packed.rows, "tokens": packed.rows // 26, "ms": ms,
+    timing = {}
+    pred.forward_logits(packed, timing=timing)
+    torch.cuda.synchronize()
+    stages = {k: round(sum(a.elapsed_time(b) for a, b, _ in v), 3) for k, v in timing.items()}
+    out = {"rows": packed.rows, "tokens": packed.rows // 26, "ms": ms, "stages_ms": stages,
            "trace_tok_per_s": packed.rows / 26 / (ms / 1e3),
            "tflops_total": (dense + attn) / (ms / 1e3) / 1e12,
            "dense_tflop": dense / 1e12, "attn_tflop": attn / 1e12, "init_s": init_s}
