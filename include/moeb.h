@@ -533,6 +533,55 @@ int moeb_sqdist_update(const double* X, const double* xn, const double* c, const
 int moeb_cluster_means(const double* X, const int64_t* members, const int64_t* offs, int k,
                        int64_t D, double* centroids, void* stream);
 
+/*
+ * Transformer predictor training: the
+ * backward pass and AdamW around the forward kernels. The backward GEMMs are
+ * moeb_gemm calls on transposed 16-bit operands (dX = dY W with W^T, dW =
+ * dY^T X with the transposed activations); these are the rest. All 16-bit
+ * tensors are fp16 when `fp16`, else bf16; gradients of activations carry
+ * the loss scale; fp32 outputs accumulate (+=).
+ *  moeb_transpose16: out[C][ld_out] = in[R][ld_in]^T
+ *  moeb_colsum16: out[N] += sum over rows of in[M][ld] (bias gradients)
+ *  moeb_layernorm_bwd16: 512-wide post-norm LayerNorm backward from the
+ *    pre-norm rows x16 (statistics recomputed): dx16 = LN'(dy16); dw, db +=
+ *  moeb_relu_bwd16: d[i] = 0 where act[i] <= 0
+ *  moeb_gelu_fwd16 / moeb_gelu_bwd16: g = gelu(u) (erf); d *= gelu'(u)
+ *  moeb_bce_logits_grad: BCEWithLogits(z, bits of truth rows), mean over
+ *    M x E: *loss_sum += sum of the element losses, dz16 = (sigmoid(z) - y)
+ *    * scale / (M E)
+ *  moeb_attention_bwd: windowed attention backward (K5's layout: qkv
+ *    [rows][1536], o / dout [rows][512]) -> dqkv [rows][1536]; lse2, dsum
+ *    [rows][8] scratch (softmax log2-normaliser, rowsum(dO * O))
+ *  moeb_gather_inputs16: F[M][2560] = [tok16[token] | lay16[layer]]
+ *  moeb_layer_emb_grad: dlay[layer[r]][c] += d[r][c] (512 columns)
+ *  moeb_cast_f32_to_16: y = 16-bit(x)
+ *  moeb_sumsq_f32: *out += sum g^2 (fp64)
+ *  moeb_adamw_f32: one torch.optim.AdamW step on n parameters, gradient
+ *    multiplied by gscale (loss-scale removal x clipping factor)
+ */
+int moeb_transpose16(const void* in, int64_t R, int C, int ld_in, void* out, int ld_out,
+                     void* stream);
+int moeb_colsum16(const void* in, int64_t M, int N, int ld, float* out, int fp16, void* stream);
+int moeb_layernorm_bwd16(const void* dy16, const void* x16, const float* w, int64_t M, float eps,
+                         void* dx16, float* dw, float* db, int fp16, void* stream);
+int moeb_relu_bwd16(void* d, const void* act, int64_t n, int fp16, void* stream);
+int moeb_gelu_fwd16(const void* u, void* g, int64_t n, int fp16, void* stream);
+int moeb_gelu_bwd16(void* d, const void* u, int64_t n, int fp16, void* stream);
+int moeb_bce_logits_grad(const float* z, const uint64_t* truth, int64_t M, int E, float scale,
+                         void* dz16, double* loss_sum, int fp16, void* stream);
+int moeb_attention_bwd(const void* qkv, const void* o, const void* dout, const int64_t* win_start,
+                       const int32_t* win_len, int n_windows, int max_len, void* dqkv,
+                       float* lse2, float* dsum, int fp16, void* stream);
+int moeb_gather_inputs16(const void* tok16, const void* lay16, const int32_t* token,
+                         const int32_t* layer, int64_t M, void* F, void* stream);
+int moeb_layer_emb_grad(const void* d, int ld, int64_t M, const int32_t* layer, int nl,
+                        float* dlay, int fp16, void* stream);
+int moeb_cast_f32_to_16(const float* x, int64_t n, void* y, int fp16, void* stream);
+int moeb_sumsq_f32(const float* g, int64_t n, double* out, void* stream);
+int moeb_adamw_f32(float* p, const float* g, float* m, float* v, int64_t n, float lr, float beta1,
+                   float beta2, float eps, float weight_decay, int step, float gscale,
+                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,20 @@ _SIGS = {
     "moeb_to16": [P, P, I64, I32, P],
     "moeb_layernorm_rows": [P, P, P, P, I64, ctypes.c_float, I32, P],
     "moeb_layernorm_rows16": [P, P, P, I64, ctypes.c_float, I32, P],
+    "moeb_transpose16": [P, I64, I32, I32, P, I32, P],
+    "moeb_colsum16": [P, I64, I32, I32, P, I32, P],
+    "moeb_layernorm_bwd16": [P, P, P, I64, ctypes.c_float, P, P, P, I32, P],
+    "moeb_relu_bwd16": [P, P, I64, I32, P],
+    "moeb_gelu_fwd16": [P, P, I64, I32, P],
+    "moeb_gelu_bwd16": [P, P, I64, I32, P],
+    "moeb_bce_logits_grad": [P, P, I64, I32, ctypes.c_float, P, P, I32, P],
+    "moeb_attention_bwd": [P, P, P, P, P, I32, I32, P, P, P, I32, P],
+    "moeb_gather_inputs16": [P, P, P, P, I64, P, P],
+    "moeb_layer_emb_grad": [P, I32, I64, P, I32, P, I32, P],
+    "moeb_cast_f32_to_16": [P, I64, P, I32, P],
+    "moeb_sumsq_f32": [P, I64, P, P],
+    "moeb_adamw_f32": [P, P, P, P, I64, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                       ctypes.c_float, ctypes.c_float, I32, ctypes.c_float, P],
     "moeb_eam_pack_library": [P, I32, I32, I32, P, P, P],
     "moeb_eam_pack_queries": [P, I32, I32, P, P],
     "moeb_eam_rerank": [P, P, I32, P, P, P, I32, I32, I32, DBL, P, P, P, P],
