@@ -114,6 +114,23 @@ int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* const* preds,
                            void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * K1m -- exact LRU replay of every capacity in one pass by stack distances
+ * (E <= 64, prompts of <= 32768 rows, no coverage / hit-mask output). Valid
+ * when every capacity exceeds the keys prefetched in any row (C > budget, or
+ * C > E for an unbounded stream): then no pin binds and nothing is rejected
+ * (cache.py:93-154), and a touch hits iff it was prefetched in its row or
+ * fewer than C distinct keys were accessed since its previous access.
+ * Counters as moeb_cache_sim (+=), for n_caps <= 16 capacities in ascending order;
+ * max_prompt_rows sizes the per-prompt shared-memory state.
+ */
+int moeb_cache_replay_stack(const uint64_t* truth, const uint64_t* const* preds,
+                            const int32_t* unbounded, int n_preds, const int64_t* prompt_row_off,
+                            int n_prompts, int L, int E, int warmup_tokens,
+                            const int64_t* capacities, int n_caps, int budget,
+                            int64_t max_prompt_rows, int64_t* counters, int64_t* per_prompt,
+                            void* stream);
+
+/*
  * ExpertCache op stream (cache.py:58-154) for one cache, executed on device:
  * ops[i] = 0 begin_step, 1 touch(keys[i]), 2 prefetch([keys[i]]).
  * results[i] = touch hit / prefetch inserted. keys = layer*E + expert.

@@ -37,6 +37,7 @@ I32, I64, DBL = ctypes.c_int, ctypes.c_int64, ctypes.c_double
 _SIGS = {
     "moeb_cache_sim": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P, I64, P,
                        ctypes.c_size_t, P],
+    "moeb_cache_replay_stack": [P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I64, P, P, P],
     "moeb_cache_sim_counted": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P,
                                P, I64, P, ctypes.c_size_t, P],
     "moeb_cache_ops": [P, P, I64, I32, I32, I64, I32, P, P],

@@ -1854,3 +1854,298 @@ extern "C" int moeb_cache_ops(const int32_t* ops, const int32_t* keys, int64_t n
          : W == 3 ? launch_ops<3>(a, policy, ops, keys, n, results, s)
                   : launch_ops<4>(a, policy, ops, keys, n, results, s);
 }
+
+// ---------------------------------------------------------------------------
+// K1m: exact multi-capacity LRU replay by stack distances (E <= 64).
+//
+// When every capacity C exceeds the number of keys prefetched in any row,
+// no pin can bind and nothing is rejected (cache.py:93-154), so the cache is
+// a pure LRU over each prompt's access sequence -- per row, sorted(pred)[:
+// budget] then the truth keys ascending (engine.py:172-184) -- and a touch of
+// key x hits iff it was prefetched in the same row or fewer than C distinct
+// keys were accessed since its previous access (Mattson's stack distance D).
+// D does not depend on C, so one pass decides every capacity at once.
+//
+// One warp per (prompt, prediction stream), state in shared memory:
+//   lr[L][64]   last access of each key: (row << 7) | pos, pos = expert id +
+//               64 if it was a truth key there (the row's access order)
+//   cnt[row]    number of keys whose last access is that row (u8), with
+//               32-row block sums blk[] and 1024-row super sums sup[]
+// For a touch of x (not prefetched in this row) whose last access is at
+// row rx (same layer) and position px:
+//   D = #{keys, last access row > rx}            (cnt suffix: blocked sum)
+//     + #{layer-l keys, last access row == rx, position > px}
+//     + #{keys accessed in this row before x not counted above}
+// then the row's keys move to this row in the structure.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kMaxMultiCaps = 16;
+constexpr uint32_t kNever = 0xffffffffu;
+
+struct MultiArgs {
+  const uint64_t* truth;
+  const uint64_t* preds[MOEB_MAX_PREDS];
+  uint32_t unbounded_bits;
+  const int64_t* row_off;
+  int P, L, E, warmup, budget, n_caps;
+  int64_t caps[kMaxMultiCaps];
+  int rmax;                 // max rows of one prompt (shared-memory sizing)
+  int off_cnt, off_blk, off_sup, off_ctr, warp_bytes;
+  int64_t* counters;        // [n_preds][n_caps][4 + 3L]
+  int64_t* per_prompt;      // nullable [n_preds][n_caps][P][4]
+};
+
+__global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_m[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int si = blockIdx.y;
+  unsigned char* base = smem_m + (size_t)warp * a.warp_bytes;
+  uint32_t* lr = reinterpret_cast<uint32_t*>(base);
+  uint32_t* cnt32 = reinterpret_cast<uint32_t*>(base + a.off_cnt);
+  uint32_t* blk = reinterpret_cast<uint32_t*>(base + a.off_blk);
+  uint32_t* sup = reinterpret_cast<uint32_t*>(base + a.off_sup);
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(base + a.off_ctr);
+  const int L = a.L, C = a.n_caps;
+  // ctr: [0, L) accesses, [L, 2L) prediction hits, then per layer a
+  // histogram over h = the number of capacities <= D ([2L + l (C+1) + h));
+  // touches with D below every capacity (and prefetched ones) land in h = 0.
+  // A capacity c hits exactly the touches with h <= c. Per prompt the same
+  // histogram (last C + 1 entries) gives the per-prompt counters.
+  const int nctr = 2 * L + L * (C + 1);
+  unsigned long long* pph = ctr + nctr;
+  for (int i = lane; i < nctr; i += 32) ctr[i] = 0ull;
+  // hlut[D] = #capacities <= D (block-shared, D in [0, L * 64])
+  unsigned char* hlut = smem_m + (size_t)(blockDim.x >> 5) * a.warp_bytes;
+  for (int d = threadIdx.x; d <= L * 64; d += blockDim.x) {
+    int h = 0;
+    for (int c = 0; c < C; ++c) h += a.caps[c] <= d;
+    hlut[d] = (unsigned char)h;
+  }
+  __syncthreads();
+  const uint64_t* pred = a.preds[si];
+  const bool unbounded = (a.unbounded_bits >> si) & 1u;
+  const uint64_t emask = a.E >= 64 ? ~0ull : ((1ull << a.E) - 1ull);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int p = blockIdx.x * (blockDim.x >> 5) + warp; p < a.P; p += nwarps) {
+    const int64_t r0 = a.row_off[p];
+    const int R = (int)(a.row_off[p + 1] - r0);
+    const int nblk = (R + 31) >> 5, nsup = (R + 1023) >> 10;
+    for (int i = lane; i < L * 64; i += 32) lr[i] = kNever;
+    // zeroed over whole 32-row blocks / 1024-row super blocks: the suffix
+    // sums read those spans without bounds tests
+    for (int i = lane; i < nblk * 8; i += 32) cnt32[i] = 0u;
+    for (int i = lane; i < nsup * 32; i += 32) blk[i] = 0u;
+    for (int i = lane; i < nsup; i += 32) sup[i] = 0u;
+    for (int i = lane; i <= C; i += 32) pph[i] = 0ull;
+    __syncwarp();
+    const unsigned char* cnt = reinterpret_cast<const unsigned char*>(cnt32);
+    int64_t pp_acc = 0, pp_ph = 0;
+    for (int rb = 0; rb < R; rb += 32) {
+      // this batch's rows, one per lane
+      const int rl = rb + lane;
+      const uint64_t xt = rl < R ? a.truth[r0 + rl] : 0ull;
+      const uint64_t xp = (rl < R && pred) ? pred[r0 + rl] : 0ull;
+      const int nb = min(32, R - rb);
+      for (int i = 0; i < nb; ++i) {
+        const int rr = rb + i;
+        const int l = rr % L, t = rr / L;
+        const uint64_t x = __shfl_sync(0xffffffffu, xt, i) & emask;
+        const uint64_t pm = __shfl_sync(0xffffffffu, xp, i) & emask;
+        const bool measured = t >= a.warmup;
+        // warm-up rows only touch their truth keys (engine.py:160-167): no
+        // prediction, no prefetch
+        uint64_t K = measured ? pm : 0ull;
+        if (!unbounded && measured) {  // sorted(pred)[:budget]: the lowest `budget` ids
+          uint64_t rest = pm;
+          for (int j = 0; j < a.budget && rest; ++j) rest &= rest - 1;
+          K = pm & ~rest;
+        }
+        const uint64_t A = K | x;
+        const uint32_t v0 = lr[l * 64 + lane], v1 = lr[l * 64 + 32 + lane];
+        // touches not prefetched in this row
+        uint64_t miss = x & ~K;
+        uint32_t hist0 = (uint32_t)__popcll(x & K);  // h = 0: hit at every capacity
+        while (miss) {
+          const int e = __ffsll((long long)miss) - 1;
+          miss &= miss - 1;
+          const uint32_t vx = __shfl_sync(0xffffffffu, e < 32 ? v0 : v1, e & 31);
+          int h = C;  // first access: a miss at every capacity
+          if (vx != kNever) {
+            const int rx = (int)(vx >> 7);
+            const uint32_t px = vx & 127u;
+            // rows after rx: partial 32-row block, the blocks of its
+            // 1024-row super block, the super blocks after it (entries past
+            // the current row are still zero)
+            const int rho = (rx & ~31) + lane;
+            const int b = ((rx >> 10) << 5) + lane;
+            const int sidx = (rx >> 10) + 1 + lane;
+            uint32_t part = rho > rx ? cnt[rho] : 0u;
+            part += b > (rx >> 5) ? blk[b] : 0u;
+            part += sidx < nsup ? sup[sidx] : 0u;
+            // layer-l keys: counted in the suffix (row > rx) / after x in row rx
+            // (never-accessed keys hold 0xffffffff: row field larger than any rx,
+            // so they are excluded by the explicit test)
+            const uint32_t rx7 = (uint32_t)rx << 7;
+            const bool g0 = v0 != kNever && v0 >= rx7 + 128u;
+            const bool g1 = v1 != kNever && v1 >= rx7 + 128u;
+            const bool f0 = v0 > vx && v0 < rx7 + 128u;
+            const bool f1 = v1 > vx && v1 < rx7 + 128u;
+            const uint64_t gt = (uint64_t)__ballot_sync(0xffffffffu, g0) |
+                                ((uint64_t)__ballot_sync(0xffffffffu, g1) << 32);
+            const uint64_t af = (uint64_t)__ballot_sync(0xffffffffu, f0) |
+                                ((uint64_t)__ballot_sync(0xffffffffu, f1) << 32);
+            const uint64_t xb = 1ull << e;
+            const uint64_t before = K | (x & (xb - 1ull));
+            const int D = (int)__reduce_add_sync(0xffffffffu, part) + __popcll(af) +
+                          __popcll(before & ~(gt | af) & ~xb);
+            h = hlut[min(D, a.L * 64)];  // #capacities <= D
+          }
+          if (h == 0) ++hist0;
+          else if (measured && lane == 0) {
+            ctr[2 * L + l * (C + 1) + h] += 1ull;
+            pph[h] += 1ull;
+          }
+        }
+        if (measured) {
+          const int acc = __popcll(x), ph = __popcll(x & pm);
+          if (lane == 0) {
+            ctr[l] += (unsigned long long)acc;
+            ctr[L + l] += (unsigned long long)ph;
+            ctr[2 * L + l * (C + 1)] += (unsigned long long)hist0;
+            pph[0] += (unsigned long long)hist0;
+          }
+          pp_acc += acc;
+          pp_ph += ph;
+        }
+        // the row's keys move to this row: (rr << 7) | position in the row
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int e = lane + 32 * hh;
+          if ((A >> e) & 1ull) {
+            const uint32_t old = hh ? v1 : v0;
+            if (old != kNever) {
+              const int ro = (int)(old >> 7);
+              atomicSub(&cnt32[ro >> 2], 1u << (8 * (ro & 3)));
+              atomicSub(&blk[ro >> 5], 1u);
+              atomicSub(&sup[ro >> 10], 1u);
+            }
+            lr[l * 64 + e] = ((uint32_t)rr << 7) | (uint32_t)(e + (((x >> e) & 1ull) ? 64 : 0));
+          }
+        }
+        if (lane == 0) {
+          const uint32_t n = (uint32_t)__popcll(A);
+          atomicAdd(&cnt32[rr >> 2], n << (8 * (rr & 3)));
+          atomicAdd(&blk[rr >> 5], n);
+          atomicAdd(&sup[rr >> 10], n);
+        }
+        __syncwarp();
+      }
+    }
+    if (a.per_prompt && lane == 0) {
+      int64_t cum = 0;
+      for (int c = 0; c < C; ++c) {
+        cum += (int64_t)pph[c];
+        int64_t* o = a.per_prompt + (((int64_t)si * C + c) * a.P + p) * 4;
+        o[0] += pp_acc;
+        o[1] += cum;
+        o[2] += pp_ph;
+      }
+    }
+    __syncwarp();
+  }
+  // flush this warp's counters (capacity c hits = histogram prefix up to c)
+  const int nc = 4 + 3 * L;
+  for (int l = lane; l < L; l += 32) {
+    const unsigned long long acc = ctr[l], ph = ctr[L + l];
+    unsigned long long cum = 0;
+    for (int c = 0; c < C; ++c) {
+      cum += ctr[2 * L + l * (C + 1) + c];
+      unsigned long long* o =
+          reinterpret_cast<unsigned long long*>(a.counters + ((int64_t)si * C + c) * nc);
+      if (acc) {
+        atomicAdd(o + 0, acc);
+        atomicAdd(o + 4 + l, acc);
+      }
+      if (ph) {
+        atomicAdd(o + 2, ph);
+        atomicAdd(o + 4 + 2 * L + l, ph);
+      }
+      if (cum) {
+        atomicAdd(o + 1, cum);
+        atomicAdd(o + 4 + L + l, cum);
+      }
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" int moeb_cache_replay_stack(const uint64_t* truth, const uint64_t* const* preds,
+                                       const int32_t* unbounded, int n_preds,
+                                       const int64_t* prompt_row_off, int n_prompts, int L, int E,
+                                       int warmup_tokens, const int64_t* capacities, int n_caps,
+                                       int budget, int64_t max_prompt_rows, int64_t* counters,
+                                       int64_t* per_prompt, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(truth && prompt_row_off && counters && capacities, "null argument");
+  MOEB_REQUIRE(n_preds >= 1 && n_preds <= MOEB_MAX_PREDS, "n_preds must be in [1, %d]",
+               MOEB_MAX_PREDS);
+  MOEB_REQUIRE(n_prompts >= 1 && L >= 1 && L <= 255 && E >= 1 && E <= 64, "unsupported shape");
+  MOEB_REQUIRE(n_caps >= 1 && n_caps <= kMaxMultiCaps, "n_caps must be in [1, %d]",
+               kMaxMultiCaps);
+  MOEB_REQUIRE(max_prompt_rows >= 0 && max_prompt_rows <= 32768,
+               "the stack replay takes prompts of up to 32768 rows");
+  MOEB_REQUIRE(warmup_tokens >= 0 && budget >= 1, "bad warmup/budget");
+  MultiArgs a{};
+  a.truth = truth;
+  int kmax = budget;
+  for (int i = 0; i < n_preds; ++i) {
+    a.preds[i] = preds ? preds[i] : nullptr;
+    if (unbounded && unbounded[i]) {
+      a.unbounded_bits |= 1u << i;
+      kmax = E;
+    }
+  }
+  for (int c = 0; c < n_caps; ++c) {
+    // exact only while no pin can bind: C > the keys prefetched in any row
+    MOEB_REQUIRE(capacities[c] > kmax && capacities[c] <= (int64_t)L * E,
+                 "capacity %lld: the stack replay needs %d < C <= L*E",
+                 (long long)capacities[c], kmax);
+    MOEB_REQUIRE(c == 0 || capacities[c] >= capacities[c - 1],
+                 "the stack replay takes capacities in ascending order");
+    a.caps[c] = capacities[c];
+  }
+  a.row_off = prompt_row_off;
+  a.P = n_prompts;
+  a.L = L;
+  a.E = E;
+  a.warmup = warmup_tokens;
+  a.budget = budget;
+  a.n_caps = n_caps;
+  a.rmax = (int)max_prompt_rows;
+  const int R = a.rmax + 1;
+  a.off_cnt = align16(4LL * L * 64);
+  a.off_blk = a.off_cnt + align16((R + 31) / 32 * 32);
+  a.off_sup = a.off_blk + align16(4LL * 32 * ((R + 1023) / 1024));
+  a.off_ctr = a.off_sup + align16(4LL * ((R + 1023) / 1024 + 1));
+  a.warp_bytes = a.off_ctr + align16(8LL * (2 * L + L * (n_caps + 1) + n_caps + 1));
+  a.counters = counters;
+  a.per_prompt = per_prompt;
+  const int max_block = moeb::max_smem_per_block();
+  int nw = 4;
+  const int lut = align16(L * 64 + 1);
+  while (nw > 1 && (int64_t)nw * a.warp_bytes + lut > max_block) --nw;
+  if ((int64_t)nw * a.warp_bytes + lut > max_block)
+    return moeb::fail(MOEB_ESMEM, "stack replay state %d B/prompt exceeds shared memory",
+                      a.warp_bytes);
+  const size_t smem = (size_t)nw * a.warp_bytes + align16(L * 64 + 1);
+  moeb::set_smem(k_stack_multi, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stack_multi, 32 * nw, smem);
+  const int64_t want = (n_prompts + nw - 1) / nw;
+  const int64_t cap = (int64_t)(per_sm > 0 ? per_sm : 1) * moeb::num_sms();
+  const unsigned gx = (unsigned)(want < cap ? want : cap);
+  k_stack_multi<<<dim3(gx, (unsigned)n_preds), 32 * nw, smem, moeb::as_stream(stream)>>>(a);
+  return moeb::check_launch("k_stack_multi");
+}

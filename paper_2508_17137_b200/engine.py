@@ -12,6 +12,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import torch
 
@@ -126,9 +128,55 @@ def _check_lengths(packed: PackedTraces, warmup: int) -> None:
                           f"tokens, not more than warmup_tokens={warmup}")
 
 
+def _stack_multi_caps(packed, streams, capacities, budget, policy, want_hits):
+    """Indices of the capacities K1m takes (see cache_replay). MOEB_K1M=0
+    disables it, MOEB_K1M=all uses it for every capacity it is exact for."""
+    mode = os.environ.get("MOEB_K1M", "")
+    shape = packed.shape
+    if mode == "0" or policy != "lru" or want_hits or shape.num_experts > 64:
+        return []
+    if any(c is not None for _, c, _ in streams) or not packed.num_prompts:
+        return []
+    if int(np.max(np.diff(packed.row_off_host))) > 32768:
+        return []
+    kmax = shape.num_experts if any(u for _, _, u in streams) else budget
+    if mode == "all":
+        return [j for j, c in enumerate(capacities) if c > kmax]
+    # K1s decides the small capacities of predicted streams in ~1 ms; K1m's
+    # one pass costs about as much as 5 capacities of the exact kernel, so it
+    # takes over when it replaces at least 6 of them
+    keys = shape.num_layers * shape.num_experts
+    with_preds = all(mk is not None for mk, _, _ in streams)
+    lo = max(kmax, int(0.12 * keys)) if with_preds else kmax
+    idx = [j for j, c in enumerate(capacities) if c > lo]
+    return idx if len(idx) >= 6 else []
+
+
+def _stack_multi(packed, streams, capacities, idx, warmup, budget, counters, per_prompt):
+    shape = packed.shape
+    L = shape.num_layers
+    rmax = int(np.max(np.diff(packed.row_off_host)))
+    idx = sorted(idx, key=lambda j: capacities[j])  # the kernel takes ascending capacities
+    for g in range(0, len(idx), 16):
+        sel = idx[g:g + 16]
+        sc = torch.zeros((len(streams), len(sel), 4 + 3 * L), dtype=torch.int64,
+                         device=packed.device)
+        sp = (torch.zeros((len(streams), len(sel), packed.num_prompts, 4), dtype=torch.int64,
+                          device=packed.device) if per_prompt is not None else None)
+        nat.call("moeb_cache_replay_stack", nat.ptr(packed.truth),
+                 nat.ptr_array([m for m, _, _ in streams]),
+                 nat.i32_array([int(bool(u)) for _, _, u in streams]), len(streams),
+                 nat.ptr(packed.row_off), packed.num_prompts, L, shape.num_experts, int(warmup),
+                 nat.i64_array([capacities[j] for j in sel]), len(sel), int(budget), rmax,
+                 nat.ptr(sc), nat.ptr(sp), nat.stream_ptr())
+        counters[:, sel] += sc
+        if per_prompt is not None:
+            per_prompt[:, sel] += sp
+
+
 def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget: int,
                  policy: str = "lru", want_per_prompt: bool = True, want_hits: bool = False,
-                 counters=None, given_counts=None):
+                 counters=None, given_counts=None, _per_prompt=None, _no_multi=False):
     """Run K1 for every (prediction stream, capacity) pair in one call.
 
     ``streams`` is a list of (masks | None, coverage | None, unbounded).
@@ -150,9 +198,28 @@ def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget:
     elif tuple(counters.shape) != (n, C, 4 + 3 * L) or counters.dtype != torch.int64:
         raise ConfigError("counters must be int64 [streams][capacities][4+3L]")
     per_prompt = (torch.zeros((n, C, P, 4), dtype=torch.int64, device=dev)
-                  if want_per_prompt else None)
+                  if want_per_prompt else _per_prompt)
     hits = (torch.zeros((n, C, packed.rows, shape.mask_words), dtype=torch.int64, device=dev)
             if want_hits else None)
+    # K1m (moeb_cache_replay_stack): every capacity above the K1s range
+    # (and above the keys a row can prefetch, so no pin binds) in one exact
+    # stack-distance pass; the others take K1s / the exact kernel below
+    multi = ([] if _no_multi else
+             _stack_multi_caps(packed, streams, capacities, budget, policy, want_hits))
+    if multi:
+        _stack_multi(packed, streams, capacities, multi, warmup, budget, counters, per_prompt)
+        rest = [j for j in range(C) if j not in multi]
+        if not rest:
+            return counters, per_prompt, hits
+        sub_c = counters[:, rest].contiguous()
+        sub_p = per_prompt[:, rest].contiguous() if per_prompt is not None else None
+        cache_replay(packed, streams, [capacities[j] for j in rest], warmup, budget, policy,
+                     want_per_prompt=False, counters=sub_c, given_counts=given_counts,
+                     _per_prompt=sub_p, _no_multi=True)
+        counters[:, rest] = sub_c
+        if per_prompt is not None:
+            per_prompt[:, rest] = sub_p
+        return counters, per_prompt, hits
     lib = nat.load_library()
     ws_bytes = lib.moeb_cache_sim_workspace_bytes(min(n, 16), P)
     ws = nat.workspace(ws_bytes, dev)

@@ -123,3 +123,64 @@ def test_stack_replay_several_streams(monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(got, want)
     assert torch.equal(got_pp, want) and torch.equal(pp, want_pp)
+
+
+@pytest.mark.parametrize("geom", [(26, 64, 6), (3, 64, 2), (5, 40, 4)])
+@pytest.mark.parametrize("ragged", [False, True])
+@pytest.mark.parametrize("warmup", [0, 8])
+def test_stack_multi_equals_exact(geom, ragged, warmup, monkeypatch):
+    """K1m (every capacity above the prefetch budget in one stack-distance
+    pass, moeb_cache_replay_stack) == the exact kernel: counters and
+    per-prompt counters, learned / empty (lru_only) / over-budget random /
+    unbounded all-ones predictions, several streams per call."""
+    import paper_2508_17137_b200 as m
+    m.load_library()
+    L, E, k = geom
+    shape = m.ModelShape(L, E, k)
+    packed = _packed(m, shape, 37, 70, 11 + L, ragged)
+    rng = np.random.default_rng(L * E)
+    w = rng.normal(0.0, 0.01, (E, L + E + 1))
+    model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
+    learned = m.make_predictor("learned_linear", shape, model=model).predict_masks(packed, k, warmup)
+    rows = packed.rows
+    wide = torch.from_numpy(rng.integers(0, 2**62, rows, dtype=np.int64)).cuda().reshape(-1, 1)
+    wide &= (1 << E) - 1 if E < 64 else -1
+    ones = torch.full((rows, 1), (1 << E) - 1 if E < 64 else -1, dtype=torch.int64, device="cuda")
+    keys = L * E
+    caps = sorted({k + 1, k + 3, 13, 20, max(k + 1, keys // 20), keys // 10, keys // 4,
+                   keys // 2, keys})
+    for streams in ([(learned, None, False), (None, None, False), (wide, None, False)],
+                    [(ones, None, True)]):
+        cs = [c for c in caps if c > (E if streams[0][2] else k)]
+        monkeypatch.setenv("MOEB_K1M", "0")
+        monkeypatch.setenv("MOEB_K1_STACK", "0")
+        want, want_pp, _ = m.cache_replay(packed, streams, cs, warmup, k)
+        monkeypatch.setenv("MOEB_K1M", "all")
+        monkeypatch.delenv("MOEB_K1_STACK")
+        got, got_pp, _ = m.cache_replay(packed, streams, cs, warmup, k)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want), (len(streams), (got - want).abs().sum().item())
+        assert torch.equal(got_pp, want_pp)
+
+
+def test_stack_multi_headline_sweep(monkeypatch):
+    """The C3 sweep's capacities on 363-token prompts: K1m for 15-50 %,
+    K1s for 5 / 10 % (the default split) == the exact kernel everywhere."""
+    import paper_2508_17137_b200 as m
+    m.load_library()
+    shape = m.ModelShape(26, 64, 6)
+    packed = _packed(m, shape, 24, 363, 7, False)
+    w = np.random.default_rng(0).normal(0.0, 0.01, (64, 91))
+    model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
+    learned = m.make_predictor("learned_linear", shape, model=model).predict_masks(packed, 6, 8)
+    caps = [m.CacheConfig(capacity_fraction=f).resolve_capacity(shape)
+            for f in (0.05, 0.10, 0.15, 0.20, 0.25, 0.30, 0.40, 0.50)]
+    streams = [(learned, None, False), (None, None, False)]
+    monkeypatch.setenv("MOEB_K1M", "0")
+    monkeypatch.setenv("MOEB_K1_STACK", "0")
+    want, want_pp, _ = m.cache_replay(packed, streams, caps, 8, 6)
+    monkeypatch.delenv("MOEB_K1M")
+    monkeypatch.delenv("MOEB_K1_STACK")
+    got, got_pp, _ = m.cache_replay(packed, streams, caps, 8, 6)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want) and torch.equal(got_pp, want_pp)
