@@ -1903,9 +1903,10 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
   unsigned char* base = smem_m + (size_t)warp * a.warp_bytes;
   uint32_t* lr = reinterpret_cast<uint32_t*>(base);
   uint32_t* cnt32 = reinterpret_cast<uint32_t*>(base + a.off_cnt);
-  uint32_t* blk = reinterpret_cast<uint32_t*>(base + a.off_blk);
+  uint32_t* blk32 = reinterpret_cast<uint32_t*>(base + a.off_blk);  // u16 block sums
+  const uint16_t* blk = reinterpret_cast<const uint16_t*>(blk32);
   uint32_t* sup = reinterpret_cast<uint32_t*>(base + a.off_sup);
-  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(base + a.off_ctr);
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(base + a.off_ctr);  // flushed as int64
   const int L = a.L, C = a.n_caps;
   // ctr: [0, L) accesses, [L, 2L) prediction hits, then per layer a
   // histogram over h = the number of capacities <= D ([2L + l (C+1) + h));
@@ -1913,8 +1914,8 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
   // A capacity c hits exactly the touches with h <= c. Per prompt the same
   // histogram (last C + 1 entries) gives the per-prompt counters.
   const int nctr = 2 * L + L * (C + 1);
-  unsigned long long* pph = ctr + nctr;
-  for (int i = lane; i < nctr; i += 32) ctr[i] = 0ull;
+  uint32_t* pph = ctr + nctr;
+  for (int i = lane; i < nctr; i += 32) ctr[i] = 0u;
   // hlut[D] = #capacities <= D (block-shared, D in [0, L * 64])
   unsigned char* hlut = smem_m + (size_t)(blockDim.x >> 5) * a.warp_bytes;
   for (int d = threadIdx.x; d <= L * 64; d += blockDim.x) {
@@ -1935,9 +1936,9 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
     // zeroed over whole 32-row blocks / 1024-row super blocks: the suffix
     // sums read those spans without bounds tests
     for (int i = lane; i < nblk * 8; i += 32) cnt32[i] = 0u;
-    for (int i = lane; i < nsup * 32; i += 32) blk[i] = 0u;
+    for (int i = lane; i < nsup * 16; i += 32) blk32[i] = 0u;
     for (int i = lane; i < nsup; i += 32) sup[i] = 0u;
-    for (int i = lane; i <= C; i += 32) pph[i] = 0ull;
+    for (int i = lane; i <= C; i += 32) pph[i] = 0u;
     __syncwarp();
     const unsigned char* cnt = reinterpret_cast<const unsigned char*>(cnt32);
     int64_t pp_acc = 0, pp_ph = 0;
@@ -1981,7 +1982,7 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
             const int b = ((rx >> 10) << 5) + lane;
             const int sidx = (rx >> 10) + 1 + lane;
             uint32_t part = rho > rx ? cnt[rho] : 0u;
-            part += b > (rx >> 5) ? blk[b] : 0u;
+            part += b > (rx >> 5) ? (uint32_t)blk[b] : 0u;
             part += sidx < nsup ? sup[sidx] : 0u;
             // layer-l keys: counted in the suffix (row > rx) / after x in row rx
             // (never-accessed keys hold 0xffffffff: row field larger than any rx,
@@ -2003,17 +2004,17 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
           }
           if (h == 0) ++hist0;
           else if (measured && lane == 0) {
-            ctr[2 * L + l * (C + 1) + h] += 1ull;
-            pph[h] += 1ull;
+            ctr[2 * L + l * (C + 1) + h] += 1u;
+            pph[h] += 1u;
           }
         }
         if (measured) {
           const int acc = __popcll(x), ph = __popcll(x & pm);
           if (lane == 0) {
-            ctr[l] += (unsigned long long)acc;
-            ctr[L + l] += (unsigned long long)ph;
-            ctr[2 * L + l * (C + 1)] += (unsigned long long)hist0;
-            pph[0] += (unsigned long long)hist0;
+            ctr[l] += (uint32_t)acc;
+            ctr[L + l] += (uint32_t)ph;
+            ctr[2 * L + l * (C + 1)] += hist0;
+            pph[0] += hist0;
           }
           pp_acc += acc;
           pp_ph += ph;
@@ -2027,7 +2028,7 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
             if (old != kNever) {
               const int ro = (int)(old >> 7);
               atomicSub(&cnt32[ro >> 2], 1u << (8 * (ro & 3)));
-              atomicSub(&blk[ro >> 5], 1u);
+              atomicSub(&blk32[ro >> 6], 1u << (16 * ((ro >> 5) & 1)));
               atomicSub(&sup[ro >> 10], 1u);
             }
             lr[l * 64 + e] = ((uint32_t)rr << 7) | (uint32_t)(e + (((x >> e) & 1ull) ? 64 : 0));
@@ -2036,7 +2037,7 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
         if (lane == 0) {
           const uint32_t n = (uint32_t)__popcll(A);
           atomicAdd(&cnt32[rr >> 2], n << (8 * (rr & 3)));
-          atomicAdd(&blk[rr >> 5], n);
+          atomicAdd(&blk32[rr >> 6], n << (16 * ((rr >> 5) & 1)));
           atomicAdd(&sup[rr >> 10], n);
         }
         __syncwarp();
@@ -2057,10 +2058,10 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
   // flush this warp's counters (capacity c hits = histogram prefix up to c)
   const int nc = 4 + 3 * L;
   for (int l = lane; l < L; l += 32) {
-    const unsigned long long acc = ctr[l], ph = ctr[L + l];
+    const unsigned long long acc = ctr[l], ph = ctr[L + l];  // u32 -> u64
     unsigned long long cum = 0;
     for (int c = 0; c < C; ++c) {
-      cum += ctr[2 * L + l * (C + 1) + c];
+      cum += (unsigned long long)ctr[2 * L + l * (C + 1) + c];
       unsigned long long* o =
           reinterpret_cast<unsigned long long*>(a.counters + ((int64_t)si * C + c) * nc);
       if (acc) {
@@ -2127,9 +2128,9 @@ extern "C" int moeb_cache_replay_stack(const uint64_t* truth, const uint64_t* co
   const int R = a.rmax + 1;
   a.off_cnt = align16(4LL * L * 64);
   a.off_blk = a.off_cnt + align16((R + 31) / 32 * 32);
-  a.off_sup = a.off_blk + align16(4LL * 32 * ((R + 1023) / 1024));
+  a.off_sup = a.off_blk + align16(2LL * 32 * ((R + 1023) / 1024));
   a.off_ctr = a.off_sup + align16(4LL * ((R + 1023) / 1024 + 1));
-  a.warp_bytes = a.off_ctr + align16(8LL * (2 * L + L * (n_caps + 1) + n_caps + 1));
+  a.warp_bytes = a.off_ctr + align16(4LL * (2 * L + L * (n_caps + 1) + n_caps + 1));
   a.counters = counters;
   a.per_prompt = per_prompt;
   const int max_block = moeb::max_smem_per_block();

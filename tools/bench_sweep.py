@@ -26,6 +26,9 @@ CAPS = [0.05, 0.10, 0.15, 0.20, 0.25, 0.30, 0.40, 0.50]
 
 
 def timed(fn):
+    """CUDA-event time of one call, after one untimed warm-up call (lazy
+    module loading, workspace allocation)."""
+    fn()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
