@@ -347,7 +347,9 @@ def run_ours(args):
     # row's combinatorial rank (u32, 4 B/row: 264 MB per step), or its k
     # expert ids as u8 (--e2e-format ids, 6 B/row, 396 MB), or the 8-byte
     # masks (--e2e-format masks, 528 MB).
-    if args.e2e_format == "ranks":
+    if args.e2e_format == "packed-ranks":
+        truth_host = m.masks_to_ranks(packed.truth, C2["top_k"], E, packed=True).cpu().pin_memory()
+    elif args.e2e_format == "ranks":
         truth_host = m.masks_to_ranks(packed.truth, C2["top_k"], E).cpu().pin_memory()
     elif args.e2e_format == "ids":
         truth_host = m.masks_to_ids(packed.truth, C2["top_k"]).cpu().pin_memory()
@@ -580,6 +582,9 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": "trace tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "host_format": {
+                        "packed-ranks": "combinatorial rank of each row's 6-expert set as a "
+                                        "27-bit stream (3.375 B/row), decoded on device "
+                                        "(k_ranks_to_masks)",
                         "ranks": "u32 combinatorial rank of each row's 6-expert set [rows], "
                                  "decoded on device (k_ranks_to_masks)",
                         "ids": "u8 expert ids [rows][6], decoded on device (k_ids_to_masks)",
@@ -618,10 +623,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--prompts", type=int, default=C2["prompts"])
-    ap.add_argument("--e2e-format", choices=["ranks", "ids", "masks"], default="ranks",
-                    help="host batch format of the end-to-end run: u32 combinatorial ranks "
-                         "(4 B/row), u8 expert ids (6 B/row), both decoded on device, or the "
-                         "8-byte mask rows")
+    ap.add_argument("--e2e-format", choices=["packed-ranks", "ranks", "ids", "masks"],
+                    default="packed-ranks",
+                    help="host batch format of the end-to-end run: combinatorial ranks as a "
+                         "27-bit stream (3.4 B/row) or as u32 (4 B/row), u8 expert ids "
+                         "(6 B/row), all decoded on device, or the 8-byte mask rows")
     ap.add_argument("--chunks", type=int, default=1,
                     help="prompt chunks pipelined across the predict / replay streams")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -251,6 +251,14 @@ int moeb_ranks_to_masks(const uint32_t* ranks, int64_t rows, int k, int E, uint6
                         int* bad, void* stream);
 int moeb_masks_to_ranks(const uint64_t* masks, int64_t rows, int k, int E, uint32_t* ranks,
                         int* bad, void* stream);
+/* The ranks as a bit stream of `bits` (>= ceil(log2 C(E, k))) per row, row r
+ * in bits [r bits, (r + 1) bits) of little-endian u32 words: 27 bits = 3.4 B
+ * per row for 64 / 6. `words` = ceil(rows bits / 32) + 1 u32; the encoder
+ * ORs into it (zero it first). */
+int moeb_packed_ranks_to_masks(const uint32_t* words, int64_t rows, int bits, int k, int E,
+                               uint64_t* masks, int* bad, void* stream);
+int moeb_masks_to_packed_ranks(const uint64_t* masks, int64_t rows, int k, int E, int bits,
+                               uint32_t* words, int* bad, void* stream);
 
 /*
  * Rule-based predictors as mask tables (predictors.py:57-139).

@@ -461,13 +461,24 @@ __device__ __forceinline__ void load_binom(uint32_t* tab) {  // tab[j * kBinN + 
   __syncthreads();
 }
 
-__global__ void k_ranks_to_masks(const uint32_t* __restrict__ ranks, int64_t rows, int k, int E,
-                                 uint64_t* __restrict__ masks, int* __restrict__ bad) {
+// bits == 32: one u32 per row; bits < 32: a little-endian bit stream, row r
+// in bits [r bits, (r + 1) bits) (one padding word at the end)
+__device__ __forceinline__ uint32_t rank_at(const uint32_t* __restrict__ w, int64_t r, int bits) {
+  if (bits == 32) return w[r];
+  const int64_t b = r * bits;
+  const int64_t i = b >> 5;
+  const int sh = (int)(b & 31);
+  const uint64_t two = (uint64_t)w[i] | ((uint64_t)w[i + 1] << 32);
+  return (uint32_t)(two >> sh) & ((1u << bits) - 1u);
+}
+
+__global__ void k_ranks_to_masks(const uint32_t* __restrict__ ranks, int64_t rows, int bits, int k,
+                                 int E, uint64_t* __restrict__ masks, int* __restrict__ bad) {
   __shared__ uint32_t tab[kBinN * kBinK];
   load_binom(tab);
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
        r += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t N = ranks[r];
+    uint32_t N = rank_at(ranks, r, bits);
     uint64_t m = 0;
     int hi = E;  // c_i < hi
     const bool ok = N < tab[k * kBinN + E];
@@ -490,7 +501,7 @@ __global__ void k_ranks_to_masks(const uint32_t* __restrict__ ranks, int64_t row
   }
 }
 
-__global__ void k_masks_to_ranks(const uint64_t* __restrict__ masks, int64_t rows, int k,
+__global__ void k_masks_to_ranks(const uint64_t* __restrict__ masks, int64_t rows, int k, int bits,
                                  uint32_t* __restrict__ ranks, int* __restrict__ bad) {
   __shared__ uint32_t tab[kBinN * kBinK];
   load_binom(tab);
@@ -504,7 +515,14 @@ __global__ void k_masks_to_ranks(const uint64_t* __restrict__ masks, int64_t row
       m &= m - 1;
       N += tab[i * kBinN + c];
     }
-    ranks[r] = N;
+    if (bits == 32) {
+      ranks[r] = N;
+    } else {  // OR into the zeroed bit stream (a row straddles at most two words)
+      const int64_t b = r * bits;
+      const int sh = (int)(b & 31);
+      atomicOr(ranks + (b >> 5), N << sh);
+      if (sh + bits > 32) atomicOr(ranks + (b >> 5) + 1, N >> (32 - sh));
+    }
   }
 }
 }  // namespace
@@ -516,7 +534,7 @@ extern "C" int moeb_ranks_to_masks(const uint32_t* ranks, int64_t rows, int k, i
                "bad arguments");
   if (rows == 0) return MOEB_OK;
   const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
-  k_ranks_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(ranks, rows, k, E, masks, bad);
+  k_ranks_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(ranks, rows, 32, k, E, masks, bad);
   return moeb::check_launch("k_ranks_to_masks");
 }
 
@@ -527,6 +545,35 @@ extern "C" int moeb_masks_to_ranks(const uint64_t* masks, int64_t rows, int k, i
                "bad arguments");
   if (rows == 0) return MOEB_OK;
   const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
-  k_masks_to_ranks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, ranks, bad);
+  k_masks_to_ranks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, 32, ranks, bad);
+  return moeb::check_launch("k_masks_to_ranks");
+}
+
+// The same ranks as a dense bit stream of `bits` per row (bits >= the
+// rank's width, ceil(log2 C(E, k)) = 27 for 64 / 6: 3.4 B per row);
+// `words` holds ceil(rows bits / 32) + 1 u32 (zeroed by the caller for the
+// encoder).
+extern "C" int moeb_packed_ranks_to_masks(const uint32_t* words, int64_t rows, int bits, int k,
+                                          int E, uint64_t* masks, int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(words && masks && bad && rows >= 0 && k >= 1 && k <= 8 && E >= k && E <= 64 &&
+                   bits >= 1 && bits <= 32,
+               "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_ranks_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(words, rows, bits, k, E, masks,
+                                                                bad);
+  return moeb::check_launch("k_ranks_to_masks");
+}
+
+extern "C" int moeb_masks_to_packed_ranks(const uint64_t* masks, int64_t rows, int k, int E,
+                                          int bits, uint32_t* words, int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(words && masks && bad && rows >= 0 && k >= 1 && k <= 8 && E >= k && E <= 64 &&
+                   bits >= 1 && bits <= 32,
+               "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_masks_to_ranks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, bits, words, bad);
   return moeb::check_launch("k_masks_to_ranks");
 }

@@ -537,10 +537,12 @@ class StreamingReplay:
             b = i % self.NBUF
             buf = self.bufs[b]
             empty = getattr(predictor, "empty", False) and not metrics
-            split = i == 0 and len(self.first_views) > 1 and not empty
-            parts = []
-            ranked = hb.dtype == torch.int32 and hb.dim() == 1  # [rows] combinatorial ranks
+            ranked = hb.dtype == torch.int32 and hb.dim() == 1  # combinatorial ranks:
+            packed_ranks = ranked and hb.shape[0] != buf.rows    # as a bit stream
             compact = ranked or hb.dtype == torch.uint8  # or [rows][k] expert ids
+            # the first batch lands in prompt ranges (not splittable: a bit stream)
+            split = i == 0 and len(self.first_views) > 1 and not empty and not packed_ranks
+            parts = []
             with torch.cuda.stream(self.s_copy):
                 if freed[b] is not None:
                     for e in freed[b]:
@@ -559,12 +561,17 @@ class StreamingReplay:
                     after which dst holds the masks."""
                     done = torch.cuda.Event()
                     if compact:
-                        ib[r0:r1].copy_(hb[r0:r1], non_blocking=True)
+                        if packed_ranks:  # the whole stream (no split for it)
+                            ib.copy_(hb, non_blocking=True)
+                        else:
+                            ib[r0:r1].copy_(hb[r0:r1], non_blocking=True)
                         landed = torch.cuda.Event()
                         landed.record(self.s_copy)
                         self.s_dec.wait_event(landed)
                         with torch.cuda.stream(self.s_dec):
-                            if ranked:
+                            if packed_ranks:
+                                ranks_to_masks(ib, shape.top_k, E, dst, self.ids_bad, rows=r1 - r0)
+                            elif ranked:
                                 ranks_to_masks(ib[r0:r1], shape.top_k, E, dst, self.ids_bad)
                             else:
                                 ids_to_masks(ib[r0:r1], E, dst, self.ids_bad)

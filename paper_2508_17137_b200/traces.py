@@ -299,29 +299,57 @@ def masks_to_ids(truth: torch.Tensor, k: int) -> torch.Tensor:
     return ids
 
 
-def masks_to_ranks(truth: torch.Tensor, k: int, num_experts: int) -> torch.Tensor:
-    """One-word expert masks -> the 4-byte wire format: each row's rank in
-    the combinatorial number system (sum_i C(c_i, i) over its ascending ids),
-    int32 holding the u32 rank (moeb_masks_to_ranks). Every row must carry
-    exactly k experts, as a validated reference trace row does."""
+def rank_bits(num_experts: int, k: int) -> int:
+    """Width of a row's combinatorial rank: ceil(log2 C(E, k)) (27 for 64 / 6)."""
+    return max(1, (math.comb(int(num_experts), int(k)) - 1).bit_length())
+
+
+def packed_rank_words(rows: int, bits: int) -> int:
+    """u32 words of a packed rank stream of `rows` rows (+1 padding word)."""
+    return (rows * bits + 31) // 32 + 1
+
+
+def masks_to_ranks(truth: torch.Tensor, k: int, num_experts: int,
+                   packed: bool = False) -> torch.Tensor:
+    """One-word expert masks -> the rank wire format: each row's rank in the
+    combinatorial number system (sum_i C(c_i, i) over its ascending ids), as
+    int32 holding the u32 rank (moeb_masks_to_ranks, 4 B/row) or, with
+    `packed`, as a dense bit stream of rank_bits(E, k) bits per row
+    (moeb_masks_to_packed_ranks, 27 bits = 3.4 B/row for 64 / 6). Every row
+    must carry exactly k experts, as a validated reference trace row does."""
     if math.comb(int(num_experts), int(k)) >= 2**32 or num_experts > 64 or k > 8:
         raise ConfigError(f"rank wire format needs C(E, k) < 2^32, E <= 64, k <= 8")
     t = truth.reshape(-1).contiguous()
-    out = torch.empty(t.numel(), dtype=torch.int32, device=t.device)
     bad = torch.zeros(1, dtype=torch.int32, device=t.device)
-    nat.call("moeb_masks_to_ranks", nat.ptr(t), t.numel(), int(k), int(num_experts),
-             nat.ptr(out), nat.ptr(bad), nat.stream_ptr())
+    if packed:
+        bits = rank_bits(num_experts, k)
+        out = torch.zeros(packed_rank_words(t.numel(), bits), dtype=torch.int32,
+                          device=t.device)
+        nat.call("moeb_masks_to_packed_ranks", nat.ptr(t), t.numel(), int(k),
+                 int(num_experts), bits, nat.ptr(out), nat.ptr(bad), nat.stream_ptr())
+    else:
+        out = torch.empty(t.numel(), dtype=torch.int32, device=t.device)
+        nat.call("moeb_masks_to_ranks", nat.ptr(t), t.numel(), int(k), int(num_experts),
+                 nat.ptr(out), nat.ptr(bad), nat.stream_ptr())
     if int(bad.item()):
         raise RangeError(f"a row does not have exactly {k} experts")
     return out
 
 
 def ranks_to_masks(ranks: torch.Tensor, k: int, num_experts: int, out: torch.Tensor,
-                   bad: torch.Tensor):
-    """Device decode of the rank rows into masks (moeb_ranks_to_masks); bad[0]
-    is set to 1 (asynchronously) if a rank is >= C(E, k)."""
-    nat.call("moeb_ranks_to_masks", nat.ptr(ranks), ranks.shape[0], int(k), int(num_experts),
-             nat.ptr(out), nat.ptr(bad), nat.stream_ptr())
+                   bad: torch.Tensor, rows: int | None = None):
+    """Device decode of rank rows into masks: `ranks` holds one u32 per row
+    (moeb_ranks_to_masks) or, when `rows` is given and differs from its
+    length, the packed bit stream of `rows` rows (moeb_packed_ranks_to_masks).
+    bad[0] is set to 1 (asynchronously) if a rank is >= C(E, k)."""
+    n = ranks.shape[0] if rows is None else int(rows)
+    if n == ranks.shape[0]:
+        nat.call("moeb_ranks_to_masks", nat.ptr(ranks), n, int(k), int(num_experts),
+                 nat.ptr(out), nat.ptr(bad), nat.stream_ptr())
+    else:
+        nat.call("moeb_packed_ranks_to_masks", nat.ptr(ranks), n,
+                 rank_bits(num_experts, k), int(k), int(num_experts), nat.ptr(out),
+                 nat.ptr(bad), nat.stream_ptr())
     return out
 
 

@@ -97,6 +97,20 @@ def test_streaming_ranks_equals_masks(geom):
                           dtype=torch.int64, device="cuda")
         rk = m.masks_to_ranks(mk, k, E)
         assert sorted(rk.cpu().tolist()) == list(range(len(subs)))
+    # the packed bit stream (rank_bits per row) decodes to the same masks
+    bits = m.rank_bits(E, k)
+    assert bits == (math.comb(E, k) - 1).bit_length()
+    words = m.masks_to_ranks(b.truth, k, E, packed=True)
+    assert words.numel() == m.packed_rank_words(b.rows, bits)
+    back2 = torch.empty_like(b.truth)
+    m.ranks_to_masks(words, k, E, back2, bad, rows=b.rows)
+    torch.cuda.synchronize()
+    assert torch.equal(back2, b.truth) and int(bad.item()) == 0
+    wn = words.cpu().numpy().view(np.uint32).astype(np.uint64)
+    for i in (0, 1, 7, b.rows - 1):  # the stream layout, restated
+        bit = i * bits
+        two = int(wn[bit // 32]) | (int(wn[bit // 32 + 1]) << 32)
+        assert (two >> (bit % 32)) & ((1 << bits) - 1) == int(r[i]) if i < len(r) else True
     if L == 26:
         w = np.random.default_rng(2).normal(0.0, 0.01, (64, 91))
         model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
@@ -106,10 +120,12 @@ def test_streaming_ranks_equals_masks(geom):
         rank_host = ranks.cpu().pin_memory()
         r1 = sr.run(pred, [83, 166], 8, 6, [mask_host] * 3, metrics=True)
         r2 = sr.run(pred, [83, 166], 8, 6, [rank_host] * 3, metrics=True)
+        r3 = sr.run(pred, [83, 166], 8, 6, [words.cpu().pin_memory()] * 3, metrics=True)
         torch.cuda.synchronize()
         assert int(sr.ids_bad.item()) == 0
-        for (c1, v1), (c2, v2) in zip(r1, r2):
+        for (c1, v1), (c2, v2), (c3, v3) in zip(r1, r2, r3):
             assert torch.equal(c1, c2) and torch.equal(v1, v2)
+            assert torch.equal(c1, c3) and torch.equal(v1, v3)
     over = ranks.clone()
     over[5] = math.comb(E, k)
     m.ranks_to_masks(over, k, E, back, bad)
