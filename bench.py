@@ -330,6 +330,11 @@ def run_ours(args):
     value = tokens_per_rank * world / (ms / 1000.0) * args.steps
     # per-step kernel time of each stage (sum over the step's chunk launches;
     # launches of the two stages overlap on separate streams)
+    if os.environ.get("MOEB_BENCH_DEBUG"):  # diagnosis: per-step predict / replay times
+        print("predict ms per step:", [round(a.elapsed_time(b), 2) for k, a, b, _ in timing
+                                       if k == "predict"], file=sys.stderr)
+        print("replay ms per step:", [round(a.elapsed_time(b), 2) for k, a, b, _ in timing
+                                      if k == "replay"], file=sys.stderr)
     lin_ms = sum(a.elapsed_time(b) for k, a, b, _ in timing if k == "predict") / args.steps
     sim_ms = sum(a.elapsed_time(b) for k, a, b, _ in timing if k == "replay") / args.steps
     n_launch = len(timing) // args.steps

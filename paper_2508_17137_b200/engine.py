@@ -339,6 +339,7 @@ class PipelinedReplay:
         self.views = [packed.select(a, b) for a, b in self.bounds]
         self._host_off = None
         dev = packed.device
+        self._mbufs = {}  # persistent masks per chunk (predictors with out=)
         self.s_copy = torch.cuda.Stream(dev)
         self.s_pred = torch.cuda.Stream(dev)
         self.s_sim = torch.cuda.Stream(dev, priority=-1)
@@ -390,7 +391,8 @@ class PipelinedReplay:
                         e0, e1 = ev(), ev()
                         e0.record(self.s_pred)
                     gc = _counts_buffer(predictor, shape, packed.device)
-                    masks = predictor.predict_masks(view, budget, warmup, **_counts_kw(gc))
+                    masks = predictor.predict_masks(view, budget, warmup, **_counts_kw(gc),
+                                                    **_out_kw(predictor, self._mbufs, ci, view))
                     if ev:
                         e1.record(self.s_pred)
                         timing.append(("predict", e0, e1, view.rows))
@@ -440,6 +442,19 @@ def _counts_buffer(predictor, shape, device):
 
 def _counts_kw(gc):
     return {} if gc is None else {"counts": gc[0]}
+
+
+def _out_kw(predictor, bufs: dict, key, packed: PackedTraces):
+    """A persistent masks buffer per pipeline slot for predictors that take
+    out= (a fresh 528 MB tensor per step makes the caching allocator fall
+    back to cudaMalloc / cudaFree, which synchronise, inside the pipeline)."""
+    if not getattr(predictor, "supports_out", False):
+        return {}
+    b = bufs.get(key)
+    if b is None or b.shape[0] != packed.rows:
+        b = bufs[key] = torch.empty((packed.rows, packed.shape.mask_words), dtype=torch.int64,
+                                    device=packed.device)
+    return {"out": b}
 
 
 def _overlapped_metrics(s_met, masks_ready, masks, view, warmup, out):
@@ -496,6 +511,7 @@ class StreamingReplay:
                      for _ in range(self.NBUF)]
         self.ids_bufs = [None] * self.NBUF  # device staging for compact (id / rank) batches
         self.ids_bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._mbufs = {}  # persistent masks per buffer slot (predictors with out=)
         self.s_copy = torch.cuda.Stream(dev)
         self.s_dec = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev, priority=-1)
@@ -611,7 +627,8 @@ class StreamingReplay:
                     cov = predictor.coverage(buf)
                 else:
                     gc = _counts_buffer(predictor, shape, dev)
-                    masks = predictor.predict_masks(buf, budget, warmup, **_counts_kw(gc))
+                    masks = predictor.predict_masks(buf, budget, warmup, **_counts_kw(gc),
+                                                    **_out_kw(predictor, self._mbufs, b, buf))
                     cov = predictor.coverage(buf)
                 masks_ready = torch.cuda.Event()
                 masks_ready.record(self.s_comp)

@@ -269,6 +269,20 @@ class LearnedLinearPredictor(DevicePredictor):
             self._w[key] = tab
         return self._w[key]
 
+    def _workspace(self, nbytes: int, device):
+        """K3t's scratch, kept per (device, stream) and grown when needed:
+        calls on one stream are ordered, so reusing it is safe, and a fresh
+        600 MB allocation per call could make the caching allocator fall back
+        to cudaMalloc (and its implicit synchronisation) in a pipeline."""
+        if nbytes <= 0:
+            return None
+        key = (str(device), torch.cuda.current_stream(device).cuda_stream)
+        cache = self.__dict__.setdefault("_ws", {})
+        ws = cache.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = cache[key] = nat.workspace(nbytes, device)
+        return ws
+
     def ambiguous_rows(self) -> int | None:
         """Rows of the last predict_masks call that the tensor-core kernel
         (K3t) handed to the exact fp64 re-evaluation (None: K3t not used)."""
@@ -286,9 +300,17 @@ class LearnedLinearPredictor(DevicePredictor):
         counters (E <= 64 kernel only)."""
         return self.shape.num_experts <= 64
 
-    def predict_masks(self, packed, budget, warmup=0, metrics=None, logits=None, counts=None):
+    # predict_masks(out=...) writes into a caller-owned [rows][W] int64 buffer
+    # (pipelines keep one per batch slot instead of allocating 528 MB a step)
+    supports_out = True
+
+    def predict_masks(self, packed, budget, warmup=0, metrics=None, logits=None, counts=None,
+                      out=None):
         s = self.shape
-        out = _empty(packed)
+        if out is None:
+            out = _empty(packed)
+        elif tuple(out.shape) != (packed.rows, s.mask_words) or out.dtype != torch.int64:
+            raise ConfigError("out must be int64 [rows][mask words]")
         if counts is not None and s.num_experts > 64:
             raise ConfigError("fused replay counts need E <= 64")
         if s.num_experts > 64:
@@ -300,7 +322,7 @@ class LearnedLinearPredictor(DevicePredictor):
             return out
         ws_bytes = 0 if logits is not None else nat.load_library().moeb_linear_workspace_bytes(
             packed.rows, s.num_layers, s.num_experts)
-        ws = nat.workspace(ws_bytes, packed.device)
+        ws = self._workspace(ws_bytes, packed.device)
         self.last_workspace = ws
         nat.call("moeb_linear_predict_counts", nat.ptr(packed.truth), nat.ptr(packed.row_off),
                  packed.num_prompts, s.num_layers, s.num_experts,
