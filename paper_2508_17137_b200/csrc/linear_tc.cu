@@ -57,22 +57,30 @@ namespace {
 using namespace moeb::tc;
 
 constexpr int kRows = 128;      // streams per CTA (TMEM lanes, MMA M)
-constexpr int kStages = 3;      // A-tile ring (x rows of tokens t, t+1, t+2)
+// A-tile ring: token t's MMA reads stage t % 2 while the threads write
+// token t + 1's rows into the other (the stage of token t - 1, whose MMA
+// completed before its scores were read)
+constexpr int kStages = 2;
 constexpr int kThreads = 160;   // 4 score/selection warps + 1 MMA warp
 constexpr int kTileA = kRows * 128;  // 128 rows x 64 fp16, SW128
 constexpr int kTileB = 128 * 128;    // 128 rows (hi outputs, lo outputs) x 64 fp16, SW128
-constexpr int kTabBytes = 2 * kTileB;  // Bx (experts), Bl (layer bias)
-constexpr int kLookahead = 5;   // mask rows loaded this many tokens ahead
+constexpr int kTileL = 128 * 64;     // 128 rows x 32 fp16 (layer one-hot / bias rows), SW64
+constexpr int kTabBytes = kTileB + kTileL;  // Bx (experts, SW128), Bl (layer bias, SW64)
+constexpr int kLookahead = 2;   // mask rows loaded this many tokens ahead
+// One N = 128 accumulator (hi | lo limb columns), not two: token t + 1's MMA
+// is issued when token t's scores have been read and runs while token t + 1
+// is selected, so it needs no second buffer (128 TMEM columns per CTA)
+constexpr int kTmemCols = 128;
 
-// smem layout
+// smem layout (69 KB per CTA)
 constexpr int OFF_A = 0;
-constexpr int OFF_AL = OFF_A + kStages * kTileA;  // constant one-hot tile
-constexpr int OFF_B = OFF_AL + kTileA;
-constexpr int OFF_LUT = OFF_B + kTabBytes;        // nibble -> 4 x fp16 {0, 1}
-constexpr int kXSlots = 8;      // per-stream ring of mask rows (cp.async, kLookahead + 2 <= 8)
+constexpr int OFF_B = OFF_A + kStages * kTileA;   // Bx (SW128) then Bl (SW64)
+constexpr int OFF_AL = OFF_B + kTabBytes;         // constant one-hot tile (SW64)
+constexpr int OFF_LUT = OFF_AL + kTileL;          // nibble -> 4 x fp16 {0, 1}
+constexpr int kXSlots = 4;      // per-stream ring of mask rows (cp.async, kLookahead + 2 <= 4)
 constexpr int OFF_XR = OFF_LUT + 16 * 8;          // [kXSlots][kRows] uint64 mask rows
 constexpr int OFF_BAR = OFF_XR + kXSlots * kRows * 8;
-constexpr int kSmem = OFF_BAR + 128 + 1024;       // + alignment slack
+constexpr int kSmem = OFF_BAR + 64 + 1024;        // + alignment slack
 
 struct TcConsts {
   float lam;     // fp32(decay)
@@ -97,6 +105,12 @@ inline size_t ws_list_off(int L) { return (ws_list_n_off(L) + 8 + 15) & ~(size_t
 // refine list (after the fp64 list): entries of kRefineFloats floats = the
 // row's 64 fp32 scores, then {E, 0, prompt, token * L + layer}
 constexpr int kRefineFloats = 68;
+
+// 64-byte swizzle (K = 32 fp16 per row; 8-row atoms of 512 B): byte offset
+// of 16-B chunk `chunk` (0..3) of row `row`
+__host__ __device__ inline int sw64(int row, int chunk) {
+  return (row >> 3) * 512 + (row & 7) * 64 + ((chunk ^ ((row >> 1) & 3)) << 4);
+}
 
 __host__ __device__ inline int sw128(int row, int chunk) {  // byte offset of a 16-B chunk
   return row * 128 + ((chunk ^ (row & 7)) << 4);
@@ -153,14 +167,18 @@ __global__ void __launch_bounds__(256) k_linear_tc_prep(const double* __restrict
     eta = fmax(eta, fabs(r - (double)__half2float(lo)));
     if (k < 64) cmax = fmax(cmax, fabs(w));
     else cbmax = fmax(cbmax, fabs(w));
-    const int kk = k & 63, half_tile = k >> 6;
+    const int kk = k & 63;
     // output column of expert i: within each 32-column half, experts m and
     // m + 16 on columns 2m and 2m + 1, so one tcgen05.ld register pair holds
     // the score pair the main kernel keeps in one float2
     const int ci = (i & 32) + 2 * (i & 15) + ((i >> 4) & 1);
-    *reinterpret_cast<__half*>(tab + half_tile * kTileB + sw128(ci, kk >> 3) + (kk & 7) * 2) = hi;
-    *reinterpret_cast<__half*>(tab + half_tile * kTileB + sw128(64 + ci, kk >> 3) + (kk & 7) * 2) =
-        lo;
+    if (k < 64) {  // Bx: SW128, K = 64
+      *reinterpret_cast<__half*>(tab + sw128(ci, kk >> 3) + (kk & 7) * 2) = hi;
+      *reinterpret_cast<__half*>(tab + sw128(64 + ci, kk >> 3) + (kk & 7) * 2) = lo;
+    } else if (kk < 32) {  // Bl: SW64, K = 32 (layers)
+      *reinterpret_cast<__half*>(tab + kTileB + sw64(ci, kk >> 3) + (kk & 7) * 2) = hi;
+      *reinterpret_cast<__half*>(tab + kTileB + sw64(64 + ci, kk >> 3) + (kk & 7) * 2) = lo;
+    }
   }
   // 3. initial scores z_0 = b_l (scaled, fp32)
   float* z0 = reinterpret_cast<float*>(ws + WS_Z0);
@@ -497,7 +515,8 @@ __device__ __forceinline__ void refine_release(const TcArgs& a, int from, int to
         make_float4(0.0f, 0.0f, 0.0f, __int_as_float(-1));
 }
 
-// KT > 0: two CTAs per SM (<= 204 registers); the generic path keeps more
+// KT > 0: two CTAs per SM (<= 204 registers; three would need <= 128 and
+// spill -- measured 6.7 ms vs 4.1); the generic path keeps more
 template <int KT>
 __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const TcArgs a) {
   extern __shared__ unsigned char smem_raw[];
@@ -508,10 +527,10 @@ __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const Tc
   unsigned char* sB = smem + OFF_B;
   uint4* lut = reinterpret_cast<uint4*>(smem + OFF_LUT);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* a_full = bar;          // [3], 128 arrivals
-  uint64_t* acc_full = bar + 3;    // [2], tcgen05.commit
-  uint64_t* acc_empty = bar + 5;   // [2], 128 arrivals
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+  uint64_t* a_full = bar;          // [kStages], 128 arrivals
+  uint64_t* acc_full = bar + 2;    // tcgen05.commit
+  uint64_t* acc_empty = bar + 3;   // 128 arrivals
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // tables -> smem (already in the swizzled layout), byte LUT
@@ -530,13 +549,11 @@ __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const Tc
   }
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&a_full[i], kRows);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&acc_full[i], 1);
-      mbar_init(&acc_empty[i], kRows);
-    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, kRows);
     fence_mbar_init();
   }
-  if (warp == 4) tmem_alloc<256>(tmem_slot);
+  if (warp == 4) tmem_alloc<kTmemCols>(tmem_slot);
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
@@ -555,20 +572,20 @@ __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const Tc
       for (int g = blockIdx.x; g < a.n_groups; g += gridDim.x) {
         const int tmax = group_tmax(a, (int64_t)g * kRows);
         for (int t = 0; t < tmax; ++t, ++u) {
-          const uint32_t st = u % kStages, buf = u & 1;
+          const uint32_t st = u % kStages;
           mbar_wait_sleep(&a_full[st], (u / kStages) & 1);
-          mbar_wait_sleep(&acc_empty[buf], ((u >> 1) & 1) ^ 1);
+          mbar_wait_sleep(acc_empty, (u & 1) ^ 1);  // token u - 1's scores read
           tc_fence_after();
-          const uint32_t d = tmem + buf * 128;
           const uint32_t ax = smem_u32(sA + st * kTileA);
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_f16_ss(d, umma_desc_sw128(ax + k * 32), umma_desc_sw128(b0 + k * 32), IDESC, k != 0);
+            mma_f16_ss(tmem, umma_desc_sw128(ax + k * 32), umma_desc_sw128(b0 + k * 32), IDESC,
+                       k != 0);
 #pragma unroll
-          for (int k = 0; k < 2; ++k)
-            mma_f16_ss(d, umma_desc_sw128(al + k * 32), umma_desc_sw128(b0 + kTileB + k * 32),
+          for (int k = 0; k < 2; ++k)  // layer one-hot x bias rows, K = 32 (SW64)
+            mma_f16_ss(tmem, umma_desc_sw64(al + k * 32), umma_desc_sw64(b0 + kTileB + k * 32),
                        IDESC, 1);
-          mma_commit(&acc_full[buf]);
+          mma_commit(acc_full);
         }
       }
     }
@@ -590,17 +607,18 @@ __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const Tc
       const int64_t r0 = a.row_off[p];
       const int T = live ? (int)((a.row_off[p + 1] - r0) / L) : 0;
       const uint64_t* xs = a.truth + r0 + l;  // row t at xs[t * L]
-      // one-hot layer row (bias MMA); the previous group's MMAs are complete
+      // one-hot layer row (bias MMA, K = 32, SW64); the previous group's
+      // MMAs are complete
       {
         uint4 zero = make_uint4(0, 0, 0, 0);
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 4; ++c) {
           uint4 v = zero;
           if (live && (l >> 3) == c) {
             uint32_t* w = reinterpret_cast<uint32_t*>(&v);
             w[(l & 7) >> 1] = (l & 1) ? 0x3C000000u : 0x3C00u;
           }
-          *reinterpret_cast<uint4*>(sAL + sw128(row, c)) = v;
+          *reinterpret_cast<uint4*>(sAL + sw64(row, c)) = v;
         }
       }
       // scores as pairs (element i0(w), i0(w) + 16), i0(w) = w < 16 ? w : w + 16, so
@@ -622,21 +640,26 @@ __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const Tc
       const uint32_t xslot = smem_u32(smem + OFF_XR) + (uint32_t)row * 8u;
 #pragma unroll
       for (int j = 0; j <= kLookahead; ++j) x_async(xslot, j, xs, L, T);
-      x_wait<kLookahead - 1>();
-      // A rows for tokens 0 and 1
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        if (j < tmax) {
-          put_row(smem_u32(sA + ((u + j) % kStages) * kTileA), smem_u32(lut), row, x_at(xslot, j));
-          fence_proxy_async();
-          mbar_arrive(&a_full[(u + j) % kStages]);
-        }
+      x_wait<kLookahead>();  // token 0 landed
+      // A rows for token 0
+      if (tmax > 0) {
+        put_row(smem_u32(sA + (u % kStages) * kTileA), smem_u32(lut), row, x_at(xslot, 0));
+        fence_proxy_async();
+        mbar_arrive(&a_full[u % kStages]);
       }
       int acc_k = 0, acc_ph = 0;
       for (int t = 0; t < tmax; ++t, ++u) {
         const bool valid = t < T;
-        x_wait<kLookahead - 2>();  // tokens <= t + 2 landed
+        x_wait<kLookahead - 1>();  // tokens <= t + 1 landed
         const uint64_t x = x_at(xslot, t);
+        // ---- A row for token t + 1 (its stage held token t - 1, whose MMA
+        // completed before token t - 1's scores were read) ----
+        if (t + 1 < tmax) {
+          const uint32_t st = (u + 1) % kStages;
+          put_row(smem_u32(sA + st * kTileA), smem_u32(lut), row, x_at(xslot, t + 1));
+          fence_proxy_async();
+          mbar_arrive(&a_full[st]);
+        }
         // ---- selection on z_t ----
         uint64_t pm = 0;
         bool amb = tainted, defer = false;
@@ -715,23 +738,15 @@ __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const Tc
             if (!amb && !defer) acc_ph += __popcll(x & pm);
           }
         }
-        // ---- A row for token t + 2 (its stage was read by MMA t - 1, complete) ----
-        if (t + 2 < tmax) {
-          const uint32_t st = (u + 2) % kStages;
-          put_row(smem_u32(sA + st * kTileA), smem_u32(lut), row, x_at(xslot, t + 2));
-          fence_proxy_async();
-          mbar_arrive(&a_full[st]);
-        }
         // ---- z_{t+1} = decay z_t + G_t ----
-        const uint32_t buf = u & 1;
-        mbar_wait_sleep(&acc_full[buf], (u >> 1) & 1);
+        mbar_wait_sleep(acc_full, u & 1);
         tc_fence_after();
         const float2 lam2 = make_float2(cst.lam, cst.lam);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t gh[32], gl[32];
-          tmem_ld32(lane_base + buf * 128 + h * 32, gh);
-          tmem_ld32(lane_base + buf * 128 + 64 + h * 32, gl);
+          tmem_ld32(lane_base + h * 32, gh);
+          tmem_ld32(lane_base + 64 + h * 32, gl);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
@@ -743,7 +758,7 @@ __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const Tc
           }
         }
         tc_fence_before();
-        mbar_arrive(&acc_empty[buf]);
+        mbar_arrive(acc_empty);
         // ---- error bound ----
         // per rounding 2^-23 of its operands' magnitude: the FFMA (|z_t| and
         // |z_{t+1}| <= |z_t| + |G|) incl. fp32(decay), the hi + lo add (|G|),
@@ -773,7 +788,7 @@ __global__ void __launch_bounds__(kThreads, KT > 0 ? 2 : 1) k_linear_tc(const Tc
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
-    tmem_dealloc<256>(tmem);
+    tmem_dealloc<kTmemCols>(tmem);
   }
 }
 
