@@ -1,5 +1,7 @@
 """StreamingReplay (double-buffered host batches) gives exactly the counters
 and metrics of a direct replay of each batch."""
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -63,6 +65,22 @@ def test_streaming_compact_ids_equals_masks():
     assert int(bad.item()) == 1
 
 
+def test_rank_decode_exhaustive_64_6():
+    """Every one of the C(64, 6) = 74,974,368 ranks decodes (floating-point
+    estimate + 5-entry window per level) and re-encodes to itself."""
+    import paper_2508_17137_b200 as m
+    m.load_library()
+    n = math.comb(64, 6)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for lo in range(0, n, 1 << 25):
+        rs = torch.arange(lo, min(n, lo + (1 << 25)), device="cuda", dtype=torch.int64)
+        rs = rs.to(torch.int32)
+        ms = torch.empty((rs.numel(), 1), dtype=torch.int64, device="cuda")
+        m.ranks_to_masks(rs, 6, 64, ms, bad)
+        assert torch.equal(m.masks_to_ranks(ms, 6, 64), rs)
+    assert int(bad.item()) == 0
+
+
 @pytest.mark.parametrize("geom", [(26, 64, 6), (3, 64, 2), (5, 40, 4), (4, 48, 7)])
 def test_streaming_ranks_equals_masks(geom):
     """Host batches as u32 combinatorial ranks (4 B/row, decoded on device)
@@ -97,6 +115,14 @@ def test_streaming_ranks_equals_masks(geom):
                           dtype=torch.int64, device="cuda")
         rk = m.masks_to_ranks(mk, k, E)
         assert sorted(rk.cpu().tolist()) == list(range(len(subs)))
+    # every rank of a large random sample decodes and re-encodes to itself
+    # (the decoder starts from a floating-point estimate per level)
+    g = torch.Generator(device="cuda").manual_seed(L * E + k)
+    rs = torch.randint(0, math.comb(E, k), (1 << 20,), device="cuda", generator=g,
+                       dtype=torch.int64).to(torch.int32)
+    ms = torch.empty((1 << 20, 1), dtype=torch.int64, device="cuda")
+    m.ranks_to_masks(rs, k, E, ms, bad)
+    assert torch.equal(m.masks_to_ranks(ms, k, E), rs) and int(bad.item()) == 0
     # the packed bit stream (rank_bits per row) decodes to the same masks
     bits = m.rank_bits(E, k)
     assert bits == (math.comb(E, k) - 1).bit_length()
