@@ -25,6 +25,7 @@
 #include <cuda.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "tc_sm100.cuh"
@@ -705,6 +706,484 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
   if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
+// ---------------------------------------------------------------------------
+// One-pass persistent tcgen05 attention (default). One CTA per SM loops over
+// work items = (window, head, pair of 128-query tiles); the two tiles of a
+// pair share every K/V chunk the TMA brings in. 320 threads:
+//   warp 0   TMA: the pair's Q tiles (double-buffered: the next item's Q
+//            lands while this item runs), then 64-key K + V chunks through
+//            a 4-stage ring that runs ahead across items
+//   warp 1   MMA: S_t = Q_t K_c^T two chunks ahead of the softmax (three
+//            64-column TMEM buffers per tile), O_t += P_t V_c behind it (V
+//            MN-major from its natural layout)
+//   warps 2-5 / 6-9  softmax of tile 0 / tile 1, thread = query row = TMEM
+//            lane, all 64 keys of a chunk per thread: online softmax with a
+//            lazily advanced running max (the max only moves, and O in TMEM
+//            is only rescaled, when a chunk's max exceeds it by more than
+//            2^8 -- P <= 256 stays exact in 16 bits, the final O / rowsum is
+//            shift-invariant); P = exp2(S - m) 16-bit into SW128 shared
+//            memory; O / rowsum on the way out
+// TMEM: tile t has S buffers at 256t + {0, 64, 128} and O at 256t + 192.
+// ---------------------------------------------------------------------------
+constexpr int FB_CK = 64;
+constexpr int FB_NST = 4;
+constexpr int FB_NS = 3;
+constexpr int FB_THREADS = 320;  // TMA, MMA, 2 tiles x 4 softmax warps
+constexpr float FB_SLACK = 8.f;  // log2 headroom of the lazily advanced max
+#ifndef FB_EMU
+#define FB_EMU 0
+#endif
+// 2^x for a pair on the FMA pipe (x <= 2^8; clamped at -126: the exponent
+// field cannot wrap): the integer part by the 1.5 * 2^23 rounding trick, 2^f
+// on [-1/2, 1/2] by a degree-4 polynomial (relative error 2.7e-6, below the
+// 16-bit P rounding), the exponent added into the bits. Can take part of
+// the softmax's exponentials off the 16-per-clock MUFU (FB_EMU pairs of 8).
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 big = make_float2(12582912.f, 12582912.f);
+  const float2 t = __fadd2_rn(x, big);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(big, make_float2(-t.x, -t.y)));
+  float2 p = __ffma2_rn(f, make_float2(0.009570102207362652f, 0.009570102207362652f),
+                        make_float2(0.05591786280274391f, 0.05591786280274391f));
+  p = __ffma2_rn(p, f, make_float2(0.240247443318367f, 0.240247443318367f));
+  p = __ffma2_rn(p, f, make_float2(0.6931217908859253f, 0.6931217908859253f));
+  p = __ffma2_rn(p, f, make_float2(0.9999992847442627f, 0.9999992847442627f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+struct FbSmem {
+  static constexpr int Q = 0;                        // [2 bufs][2 tiles] 16 KB
+  static constexpr int RING = 65536;                 // FB_NST x (K 8 KB + V 8 KB)
+  static constexpr int P = RING + FB_NST * 16384;    // [2 tiles][2 bufs] 16 KB
+  static constexpr int BAR = P + 4 * 16384;
+  static constexpr int NBAR = 2 * FB_NST + 2 * 4 + 2 * 2 * FB_NS + 2 * 2 * 2 + 2 * 2;
+  static constexpr int SLOT = BAR + NBAR * 8;
+  static constexpr int BYTES = SLOT + 16;
+};
+
+#ifdef FB_TRACE
+__device__ unsigned long long g_fbtrace[16384];
+// per-role slices of 4096 events, no atomics (a store does not stall the role)
+#define FBT(code, c)                                                                   \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && it < (int)gridDim.x * 4 && fbt_i < 4096)                    \
+      g_fbtrace[fbt_base + fbt_i++] = ((unsigned long long)(code) << 56) |             \
+          ((unsigned long long)((c) & 0xff) << 48) | (clock64() & 0xffffffffffffull);   \
+  } while (0)
+#else
+#define FBT(code, c) do {} while (0)
+#endif
+
+struct FbItem {
+  int r0, n, q0, ntile, head;
+};
+
+template <bool FP16>
+__global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
+    const __grid_constant__ CUtensorMap tm, uint16_t* __restrict__ out,
+    const int64_t* __restrict__ win_start, const int32_t* __restrict__ win_len, int n_items,
+    int pshift) {
+  using namespace moeb::tc;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // no runtime integer division anywhere in this kernel: it compiles to
+  // I2F / MUFU.RCP / F2I, and the MUFU queue is full of the softmax's EX2
+  const int npair = 1 << pshift;  // query-tile pairs per (window, head): 1 or 2
+  unsigned char* sQ = smem_raw + FbSmem::Q;
+  unsigned char* ring = smem_raw + FbSmem::RING;
+  unsigned char* sP = smem_raw + FbSmem::P;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + FbSmem::BAR);
+  uint64_t* kv_full = bars;                  // [FB_NST]
+  uint64_t* kv_empty = kv_full + FB_NST;     // [FB_NST]
+  uint64_t* q_full = kv_empty + FB_NST;      // [2 tiles][2 bufs]
+  uint64_t* q_empty = q_full + 4;            // [2][2]
+  uint64_t* s_full = q_empty + 4;            // [2 tiles][FB_NS]
+  uint64_t* s_empty = s_full + 2 * FB_NS;    // [2][FB_NS]
+  uint64_t* p_full = s_empty + 2 * FB_NS;    // [2 tiles][2 bufs]
+  uint64_t* p_empty = p_full + 4;            // [2][2]
+  uint64_t* o_full = p_empty + 4;            // [2]
+  uint64_t* o_empty = o_full + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + FbSmem::SLOT);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tm);
+    for (int i = 0; i < FB_NST; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&o_full[t], 1);
+      mbar_init(&o_empty[t], 4);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&q_full[2 * t + b], 1);
+        mbar_init(&q_empty[2 * t + b], 1);
+        mbar_init(&p_full[2 * t + b], 4);
+        mbar_init(&p_empty[2 * t + b], 1);
+      }
+      for (int b = 0; b < FB_NS; ++b) {
+        mbar_init(&s_full[FB_NS * t + b], 1);
+        mbar_init(&s_empty[FB_NS * t + b], 4);
+      }
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // a work item's geometry, identical in every role. Each role is a whole
+  // warp; lane i holds the window length / start of local item k0 + i, so
+  // the global loads are waited on once per 32 items (an mbarrier wait
+  // behind an outstanding load otherwise stalls on it)
+  struct GeoCache {
+    int k0, n, r0;
+  };
+  auto fetch = [&](GeoCache& gc, int k) {
+    FbItem g{0, 0, 0, 0, 0};
+    const int it = blockIdx.x + k * gridDim.x;
+    if (it >= n_items) return g;
+    const int kb = k & ~31;
+    if (kb != gc.k0) {
+      gc.k0 = kb;
+      const int itl = blockIdx.x + (kb + lane) * gridDim.x;
+      if (itl < n_items) {
+        const int w = itl >> (pshift + 3);
+        gc.n = __ldg(win_len + w);
+        gc.r0 = (int)__ldg(win_start + w);
+      }
+    }
+    g.n = __shfl_sync(0xffffffffu, gc.n, k & 31);
+    g.r0 = __shfl_sync(0xffffffffu, gc.r0, k & 31);
+    const int pair = it & (npair - 1);
+    g.head = (it >> pshift) & 7;
+    g.q0 = pair * 2 * TQ;
+    g.ntile = g.q0 >= g.n ? 0 : (g.q0 + TQ >= g.n ? 1 : 2);
+    return g;
+  };
+
+  if (warp == 0) {
+    {  // ===== TMA producer: the whole warp, one elected lane issues =====
+      uint32_t g = 0, qi[2] = {0, 0};
+#ifdef FB_TRACE
+      int fbt_i = 0;
+      const int fbt_base = 3 * 4096;
+#endif
+      int it = 0;
+      auto load_q = [&](const FbItem& w) {
+        for (int t = 0; t < w.ntile; ++t) {
+          const int qb = qi[t] & 1;
+          FBT(12, t);
+          mbar_wait_sleep(&q_empty[2 * t + qb], ((qi[t] >> 1) & 1) ^ 1);
+          FBT(13, t);
+          if (elect_one()) {
+            mbar_expect_tx(&q_full[2 * t + qb], TQ * 128);
+            unsigned char* dq = sQ + (2 * qb + t) * 16384;
+            tma_load_2d(dq, &tm, &q_full[2 * t + qb], w.head * 64, w.r0 + w.q0 + t * TQ);
+            tma_load_2d(dq + 8192, &tm, &q_full[2 * t + qb], w.head * 64,
+                        w.r0 + w.q0 + t * TQ + 64);
+          }
+          __syncwarp();
+          ++qi[t];
+        }
+      };
+      GeoCache gc{-32, 0, 0};
+      bool q_ahead = false;  // the current item's Q was issued during the previous item
+      for (int k = 0; (it = blockIdx.x + k * gridDim.x) < n_items; ++k) {
+        const FbItem cur = fetch(gc, k);
+        if (cur.ntile == 0) continue;
+        if (!q_ahead) load_q(cur);
+        q_ahead = false;
+        const int nch = (cur.n + FB_CK - 1) / FB_CK;
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int st = g % FB_NST;
+          FBT(14, c);
+          mbar_wait_sleep(&kv_empty[st], ((g / FB_NST) & 1) ^ 1);
+          FBT(15, c);
+          if (elect_one()) {
+            unsigned char* stg = ring + st * 16384;
+            mbar_expect_tx(&kv_full[st], 16384);
+            tma_load_2d(stg, &tm, &kv_full[st], 512 + cur.head * 64, cur.r0 + c * FB_CK);
+            tma_load_2d(stg + 8192, &tm, &kv_full[st], 1024 + cur.head * 64, cur.r0 + c * FB_CK);
+          }
+          __syncwarp();
+          // the next item's Q (double-buffered) a few chunks before it is needed
+          if (c == (nch > 2 ? 2 : nch - 1)) {
+            const FbItem nxt = fetch(gc, k + 1);
+            if (nxt.ntile > 0) {
+              load_q(nxt);
+              q_ahead = true;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    {  // ===== MMA issuer: the whole warp, one elected lane issues =====
+#ifdef FB_TRACE
+      int fbt_i = 0;
+      const int fbt_base = 0;
+#endif
+      const int ab = FP16 ? 0 : 1;
+      const uint32_t idesc_s = umma_idesc_f16(TQ, FB_CK, ab);
+      const uint32_t idesc_o = umma_idesc_f16(TQ, 64, ab) | (1u << 16);  // V MN-major
+      // descriptors advance by (bytes >> 4) in their low bits (no carry:
+      // shared addresses < 256 KB)
+      const uint64_t dq0 = umma_desc_sw128(smem_u32(sQ));
+      const uint64_t dring = umma_desc_sw128(smem_u32(ring));
+      const uint64_t dp0 = umma_desc_sw128(smem_u32(sP));
+      uint32_t g = 0, qi[2] = {0, 0}, su[2] = {0, 0}, pu[2] = {0, 0}, oi[2] = {0, 0};
+      GeoCache gcache{-32, 0, 0};
+      for (int k = 0, it; (it = blockIdx.x + k * gridDim.x) < n_items; ++k) {
+        const FbItem cur = fetch(gcache, k);
+        if (cur.ntile == 0) continue;
+        const int ntile = cur.ntile;
+        const int nch = (cur.n + FB_CK - 1) / FB_CK;
+        uint64_t dq[2];
+        FBT(8, 0);
+        for (int t = 0; t < ntile; ++t) {
+          const int qb = qi[t] & 1;
+#ifdef FB_TRACE
+          {
+            uint32_t done;
+            asm volatile(
+                "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                "selp.b32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(smem_u32(&q_full[2 * t + qb])), "r"((qi[t] >> 1) & 1)
+                : "memory");
+            FBT(7, done + 2 * t);
+          }
+#endif
+          mbar_wait(&q_full[2 * t + qb], (qi[t] >> 1) & 1);
+          FBT(9 + t, 0);
+          dq[t] = dq0 + (uint64_t)((2 * qb + t) * (16384 >> 4));
+        }
+        auto issue_s = [&](int c) {  // S_t = Q_t K_c^T for both tiles
+          FBT(1, c);
+          const uint32_t gc = g + c;
+          const int st = gc % FB_NST;
+          mbar_wait(&kv_full[st], (gc / FB_NST) & 1);
+          FBT(11, c);
+          const uint64_t dk = dring + (uint64_t)(st * (16384 >> 4));
+          for (int t = 0; t < ntile; ++t) {
+            const int b = su[t] % FB_NS;
+            mbar_wait(&s_empty[FB_NS * t + b], ((su[t] / FB_NS) & 1) ^ 1);
+            tc_fence_after();
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_f16_ss(tmem + 256 * t + 64 * b, dq[t] + 2 * k, dk + 2 * k, idesc_s, k > 0);
+              mma_commit(&s_full[FB_NS * t + b]);
+              if (c == nch - 1) mma_commit(&q_empty[2 * t + (qi[t] & 1)]);
+            }
+            __syncwarp();
+            FBT(2 + t, c);
+            ++su[t];
+          }
+        };
+        auto issue_pv = [&](int c) {  // O_t += P_t V_c for both tiles
+          FBT(4, c);
+          const uint32_t gc = g + c;
+          const int st = gc % FB_NST;
+          const uint64_t dv = dring + (uint64_t)((st * 16384 + 8192) >> 4);
+          for (int t = 0; t < ntile; ++t) {
+            const int b = pu[t] & 1;
+            mbar_wait(&p_full[2 * t + b], (pu[t] >> 1) & 1);
+            if (c == 0) mbar_wait(&o_empty[t], (oi[t] & 1) ^ 1);
+            tc_fence_after();
+            const uint64_t dp = dp0 + (uint64_t)((2 * t + b) * (16384 >> 4));
+            if (elect_one()) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_f16_ss(tmem + 256 * t + 192, dp + 2 * k, dv + k * (2048 >> 4), idesc_o,
+                           (c | k) != 0);
+              mma_commit(&p_empty[2 * t + b]);
+            }
+            __syncwarp();
+            FBT(5 + t, c);
+            ++pu[t];
+          }
+          if (elect_one()) mma_commit(&kv_empty[st]);
+          __syncwarp();
+        };
+        issue_s(0);
+        if (nch > 1) issue_s(1);
+        for (int c = 0; c < nch; ++c) {
+          if (c + 2 < nch) issue_s(c + 2);
+          issue_pv(c);
+        }
+        g += nch;
+        if (elect_one())
+          for (int t = 0; t < ntile; ++t) mma_commit(&o_full[t]);
+        __syncwarp();
+        for (int t = 0; t < ntile; ++t) {
+          ++oi[t];
+          ++qi[t];
+        }
+      }
+    }
+  } else {
+    // ===== softmax: warps 2-5 tile 0, warps 6-9 tile 1 =====
+    // thread = query row = TMEM lane, all 64 keys of a chunk; software
+    // pipelined: chunk c+1's S is loaded from TMEM while chunk c's
+    // exponentials run, so the load and its barrier wait leave the MUFU
+    // phase's critical path
+    const int t = (warp - 2) >> 2, quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t tq = tmem + ((uint32_t)(quarter * 32) << 16) + 256 * t;
+    const float sl2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
+    uint32_t j = 0, oi = 0;
+#ifdef FB_TRACE
+    int fbt_i = 0;
+    const int fbt_base = 4096 * (1 + t);
+#endif
+    auto load_s = [&](uint32_t jj, uint32_t (&r)[64]) {
+      const int sb = jj % FB_NS;
+      mbar_wait(&s_full[FB_NS * t + sb], (jj / FB_NS) & 1);
+      tc_fence_after();
+      tmem_ld32(tq + 64 * sb, *reinterpret_cast<uint32_t(*)[32]>(r));
+      tmem_ld32(tq + 64 * sb + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+    };
+    auto release_s = [&](uint32_t jj, uint32_t (&r)[64]) {
+      tmem_ld_wait_regs(*reinterpret_cast<uint32_t(*)[32]>(r));
+      reg_barrier32(*reinterpret_cast<uint32_t(*)[32]>(r + 32));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[FB_NS * t + jj % FB_NS]);
+    };
+    GeoCache gcache{-32, 0, 0};
+    for (int k = 0, it; (it = blockIdx.x + k * gridDim.x) < n_items; ++k) {
+      const FbItem cur = fetch(gcache, k);
+      if (t >= cur.ntile) continue;
+      const int n = cur.n;
+      const int nch = (n + FB_CK - 1) / FB_CK;
+      float m = 0.f, l0 = 0.f, l1 = 0.f, l2 = 0.f, l3 = 0.f;
+      uint32_t r[64];
+      load_s(j, r);
+      release_s(j, r);
+      for (int c = 0; c < nch; ++c, ++j) {
+        if (lane == 0 && quarter == 2) FBT(18 + 8 * t, c);
+        const int kv = n - c * FB_CK;  // valid keys in this chunk
+        if (kv < FB_CK) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i >= kv) r[i] = __float_as_uint(-INFINITY);
+        }
+        float mm[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float a = __uint_as_float(r[16 * q]);
+#pragma unroll
+          for (int i = 1; i < 16; ++i) a = fmaxf(a, __uint_as_float(r[16 * q + i]));
+          mm[q] = a;
+        }
+        const float cm = fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])) * sl2;
+        float alpha = 1.f;
+        if (c == 0) {
+          m = cm;
+        } else if (cm > m + FB_SLACK) {
+          alpha = ex2_ftz(m - cm);
+          l0 *= alpha;
+          l1 *= alpha;
+          l2 *= alpha;
+          l3 *= alpha;
+          m = cm;
+        }
+        if (c > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+          // rescale this warp's O rows once the previous chunk's P V landed
+          const uint32_t jp = j - 1;
+          mbar_wait(&p_empty[2 * t + (jp & 1)], (jp >> 1) & 1);
+          tc_fence_after();
+          uint32_t o[32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            tmem_ld32(tq + 192 + 32 * h, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(tq + 192 + 32 * h, o);
+          }
+          tmem_st_wait();
+        }
+        uint32_t pk[32];
+        float2 la = make_float2(0.f, 0.f), lb = make_float2(0.f, 0.f);
+        const float2 sl22 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {  // pairs; the last FB_EMU of 8 on the FMA pipe
+          float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * u]), __uint_as_float(r[2 * u + 1])),
+                                sl22, nm2);
+          if ((u & 7) >= 8 - FB_EMU) {
+            x = exp2_fma2(x);
+          } else {
+            x.x = ex2_ftz(x.x);
+            x.y = ex2_ftz(x.y);
+          }
+          if (u & 1)
+            lb = __fadd2_rn(lb, x);
+          else
+            la = __fadd2_rn(la, x);
+          pk[u] = pack2<FP16>(x.x, x.y);
+        }
+        l0 += la.x;
+        l1 += la.y;
+        l2 += lb.x;
+        l3 += lb.y;
+        // next chunk's S: its wait and TMEM load overlap the P store below
+        if (c + 1 < nch) load_s(j + 1, r);
+        if (lane == 0 && quarter == 2) FBT(19 + 8 * t, c);
+        const int pb = j & 1;
+        if (j >= 2) mbar_wait(&p_empty[2 * t + pb], ((j >> 1) - 1) & 1);  // P V of chunk j-2
+        if (lane == 0 && quarter == 2) FBT(20 + 8 * t, c);
+        unsigned char* dst = sP + (2 * t + pb) * 16384;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<uint4*>(dst + sw128(row, q)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[2 * t + pb]);
+        if (lane == 0 && quarter == 2) FBT(21 + 8 * t, c);
+        if (c + 1 < nch) release_s(j + 1, r);
+      }
+      // ---- O / rowsum -> out ----
+      if (lane == 0 && quarter == 2) FBT(22 + 8 * t, 0);
+      mbar_wait(&o_full[t], oi & 1);
+      if (lane == 0 && quarter == 2) FBT(23 + 8 * t, 0);
+      ++oi;
+      tc_fence_after();
+      uint32_t o0[32], o1[32];
+      tmem_ld32(tq + 192, o0);
+      tmem_ld32(tq + 224, o1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[t]);
+      const float inv = 1.f / ((l0 + l1) + (l2 + l3));
+      if (cur.q0 + t * TQ + row < n) {
+        uint4* dst = reinterpret_cast<uint4*>(
+            out + ((int64_t)cur.r0 + cur.q0 + t * TQ + row) * 512 + cur.head * 64);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t* o = q < 4 ? o0 + 8 * q : o1 + 8 * (q - 4);
+          dst[q] = make_uint4(
+              pack2<FP16>(__uint_as_float(o[0]) * inv, __uint_as_float(o[1]) * inv),
+              pack2<FP16>(__uint_as_float(o[2]) * inv, __uint_as_float(o[3]) * inv),
+              pack2<FP16>(__uint_as_float(o[4]) * inv, __uint_as_float(o[5]) * inv),
+              pack2<FP16>(__uint_as_float(o[6]) * inv, __uint_as_float(o[7]) * inv));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -735,6 +1214,15 @@ int qkv_map(CUtensorMap* m, const void* qkv, int64_t rows, bool fp16) {
 
 }  // namespace
 
+#ifdef FB_TRACE
+// debug builds only (-DFB_TRACE, tools/fb_trace_probe.py): CTA 0's event
+// timeline of the last k_window_attention_fb launch
+extern "C" int moeb_debug_fb_trace(unsigned long long* dst, int n) {
+  cudaMemcpyFromSymbol(dst, g_fbtrace, sizeof(unsigned long long) * (size_t)n);
+  return n;
+}
+#endif
+
 extern "C" int moeb_window_attention(const void* qkv, void* out, const int64_t* win_start,
                                      const int32_t* win_len, int n_windows, int max_len,
                                      int64_t rows, int fp16, void* stream) {
@@ -745,9 +1233,27 @@ extern "C" int moeb_window_attention(const void* qkv, void* out, const int64_t* 
   if (n_windows == 0) return MOEB_OK;
   dim3 grid((unsigned)n_windows, 8, (unsigned)((max_len + QB - 1) / QB));
   cudaStream_t s = moeb::as_stream(stream);
-  const char* env = getenv("MOEB_ATTN");  // "mma": mma.sync baseline, "tc1": one-pass tcgen05
-  const char mode = env ? env[0] : 'f';
+  // MOEB_ATTN: unset / "fb" persistent one-pass (default), "fa" two-pass
+  // warp-specialised, "tc1" whole-window single CTA, "mma" mma.sync baseline
+  const char* env = getenv("MOEB_ATTN");
+  const char mode = !env || !strcmp(env, "fb") ? 'p' : !strcmp(env, "fa") ? 'f'
+                    : !strcmp(env, "tc1") ? 't' : 'm';
   const int nqb = (max_len + TQ - 1) / TQ;
+  if (mode == 'p' && max_len <= TKMAX && rows < (1ll << 31)) {
+    CUtensorMap tm;
+    if (int rc = qkv_map(&tm, qkv, rows, fp16 != 0)) return rc;
+    auto k = fp16 ? k_window_attention_fb<true> : k_window_attention_fb<false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FbSmem::BYTES);
+    const int pshift = nqb > 2 ? 1 : 0;  // pairs of 128-query tiles: 1 or 2 (max_len <= 512)
+    const int64_t items = (int64_t)n_windows * 8 << pshift;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = (int)(items < sms ? items : sms);
+    k<<<grid, FB_THREADS, FbSmem::BYTES, s>>>(tm, static_cast<uint16_t*>(out), win_start, win_len,
+                                             (int)items, pshift);
+    return moeb::check_launch("k_window_attention_fb");
+  }
   if (mode == 'f' && max_len <= TKMAX && rows < (1ll << 31)) {
     CUtensorMap tm;
     if (int rc = qkv_map(&tm, qkv, rows, fp16 != 0)) return rc;

@@ -78,19 +78,31 @@ def test_gemm_epilogues(tr, fp16, M, N, K):
         torch.testing.assert_close(h16.float(), want16, atol=5e-3 + 2 * q, rtol=2 * q)
 
 
-@pytest.mark.parametrize("impl", ["fa", "tc1", "mma"])
+@pytest.mark.parametrize("spiky", [False, True])
+@pytest.mark.parametrize("impl", ["fb", "fa", "tc1", "mma"])
 @pytest.mark.parametrize("fp16", [True, False])
-def test_window_attention(tr, fp16, impl, monkeypatch):
-    """warp-specialised tcgen05 kernel (default), the one-pass tcgen05 kernel
-    (MOEB_ATTN=tc1) and the mma.sync baseline (MOEB_ATTN=mma)."""
+def test_window_attention(tr, fp16, impl, spiky, monkeypatch):
+    """persistent one-pass tcgen05 kernel (default), the two-pass
+    warp-specialised kernel (MOEB_ATTN=fa), the whole-window kernel
+    (MOEB_ATTN=tc1) and the mma.sync baseline (MOEB_ATTN=mma). `spiky` scales
+    scattered keys so that later 64-key chunks raise a row's max by far more
+    than the one-pass kernel's 2^8 slack (its O rescale path) and others sit
+    far below it (underflowing terms)."""
     from paper_2508_17137_b200 import _native as nat
     monkeypatch.setenv("MOEB_ATTN", impl)
     dt = torch.float16 if fp16 else torch.bfloat16
-    off = np.array([0, 700, 700 + 512, 700 + 512 + 37, 700 + 512 + 37 + 1100])
+    off = np.array([0, 700, 700 + 512, 700 + 512 + 37, 700 + 512 + 37 + 1100, 700 + 512 + 37 +
+                    1100 + 129, 700 + 512 + 37 + 1100 + 129 + 300])
     ws, wl = tr.windows_of(off)
     rows = int(off[-1])
     g = torch.Generator(device="cuda").manual_seed(3)
-    qkv = torch.randn(rows, 1536, device="cuda", generator=g).to(dt)
+    qkv = torch.randn(rows, 1536, device="cuda", generator=g)
+    if spiky:
+        scale = torch.ones(rows, 1, device="cuda")
+        idx = torch.randint(0, rows, (rows // 40,), device="cuda", generator=g)
+        scale[idx] = torch.rand(len(idx), 1, device="cuda", generator=g) * 12.0
+        qkv[:, 512:1024] *= scale
+    qkv = qkv.to(dt)
     out = torch.zeros(rows, 512, device="cuda", dtype=dt)
     ws_d, wl_d = torch.from_numpy(ws).cuda(), torch.from_numpy(wl).cuda()  # keep alive
     nat.call("moeb_window_attention", nat.ptr(qkv), nat.ptr(out), nat.ptr(ws_d), nat.ptr(wl_d),
