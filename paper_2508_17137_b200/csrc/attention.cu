@@ -9,16 +9,14 @@
 // and O += P V with mma.sync m16n8k16 (fp32 accumulate), online softmax in
 // fp32 (exp2 form).
 //
-// k_window_attention_tc (default) runs both products on the 5th-generation
-// tensor cores: S = Q K^T (M = 128 queries, N <= 256 keys per tcgen05.mma,
-// fp32 in tensor memory, the whole 512-key window in all 512 TMEM columns),
-// an exact two-pass softmax read back with tcgen05.ld (thread = query row),
-// unnormalised P = exp2(S - max) written 16-bit into 128-byte-swizzled shared
-// memory (the freed K buffer, 256 keys at a time) and O += P V with V as an
-// MN-major operand straight from its natural [key][d] layout; O (64 TMEM
-// columns, reusing S's first half) is scaled by 1/rowsum on the way out.
-// The mma.sync kernel above stays selectable (MOEB_ATTN=mma) as the
-// comparison baseline.
+// k_window_attention_fb (default, below) is a persistent one-pass tcgen05
+// kernel: S = Q K^T and O += P V on the tensor cores with S, P and O in
+// tensor memory, a lazily advanced running max, two CTAs per SM (one
+// 128-query tile each). k_window_attention_fa (MOEB_ATTN=fa) is the
+// two-pass warp-specialised kernel it replaced, k_window_attention_tc
+// (MOEB_ATTN=tc1) the whole-window single-CTA kernel (S for all 512 keys in
+// the 512 TMEM columns, an exact two-pass softmax, P through shared memory),
+// and the mma.sync kernel above (MOEB_ATTN=mma) the comparison baseline.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -707,28 +705,38 @@ __global__ void __launch_bounds__(FA_THREADS, 2) k_window_attention_fa(
 }
 
 // ---------------------------------------------------------------------------
-// One-pass persistent tcgen05 attention (default). One CTA per SM loops over
-// work items = (window, head, pair of 128-query tiles); the two tiles of a
-// pair share every K/V chunk the TMA brings in. 320 threads:
-//   warp 0   TMA: the pair's Q tiles (double-buffered: the next item's Q
+// One-pass persistent tcgen05 attention (default). Persistent CTAs loop over
+// work items = (window, head, group of NT 128-query tiles); NT = 1 by default
+// (two CTAs per SM whose softmax warps run out of phase), NT = 2 shares each
+// K / V chunk between two tiles of one CTA (MOEB_ATTN_NT=2). 64 + 128 NT
+// threads:
+//   warp 0   TMA: the group's Q tiles (double-buffered: the next item's Q
 //            lands while this item runs), then 64-key K + V chunks through
 //            a 4-stage ring that runs ahead across items
 //   warp 1   MMA: S_t = Q_t K_c^T two chunks ahead of the softmax (three
-//            64-column TMEM buffers per tile), O_t += P_t V_c behind it (V
-//            MN-major from its natural layout)
-//   warps 2-5 / 6-9  softmax of tile 0 / tile 1, thread = query row = TMEM
-//            lane, all 64 keys of a chunk per thread: online softmax with a
-//            lazily advanced running max (the max only moves, and O in TMEM
-//            is only rescaled, when a chunk's max exceeds it by more than
-//            2^8 -- P <= 256 stays exact in 16 bits, the final O / rowsum is
-//            shift-invariant); P = exp2(S - m) 16-bit into SW128 shared
-//            memory; O / rowsum on the way out
+//            64-column TMEM buffers per tile), O_t += P_t V_c behind it with
+//            P read from tensor memory (A operand in TMEM, V MN-major from
+//            its natural layout); the S buffer is released by the commit
+//            after its P V
+//   4 warps per tile  softmax, thread = query row = TMEM lane, all 64 keys
+//            of a chunk per thread, the next chunk's S loaded while this
+//            chunk's exponentials run: online softmax with a lazily advanced
+//            running max (the max only moves, and O in TMEM is only
+//            rescaled, when a chunk's max exceeds it by more than 2^8 -- P
+//            <= 256 stays exact in 16 bits, O / rowsum is shift-invariant);
+//            P = exp2(S - m) 16-bit written over the chunk's S columns
+//            (tcgen05.st); O / rowsum on the way out
+// Every role is a whole warp (warp-uniform control flow, one elected lane
+// issues TMA / MMA / commits); no runtime integer division or MUFU
+// reciprocal outside the exponentials (their XU queue is the busiest pipe).
 // TMEM: tile t has S buffers at 256t + {0, 64, 128} and O at 256t + 192.
 // ---------------------------------------------------------------------------
 constexpr int FB_CK = 64;
 constexpr int FB_NST = 4;
 constexpr int FB_NS = 3;
-constexpr int FB_THREADS = 320;  // TMA, MMA, 2 tiles x 4 softmax warps
+#ifndef FB_NT_DEFAULT
+#define FB_NT_DEFAULT 1
+#endif
 constexpr float FB_SLACK = 8.f;  // log2 headroom of the lazily advanced max
 #ifndef FB_EMU
 #define FB_EMU 0
@@ -753,14 +761,17 @@ __device__ __forceinline__ float2 exp2_fma2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
+// NT query tiles per CTA: NT = 2 (one CTA per SM, 512 TMEM columns) or
+// NT = 1 (two CTAs per SM, 256 columns each)
+template <int NT>
 struct FbSmem {
-  static constexpr int Q = 0;                        // [2 bufs][2 tiles] 16 KB
-  static constexpr int RING = 65536;                 // FB_NST x (K 8 KB + V 8 KB)
-  static constexpr int P = RING + FB_NST * 16384;    // [2 tiles][2 bufs] 16 KB
-  static constexpr int BAR = P + 4 * 16384;
+  static constexpr int Q = 0;                        // [2 bufs][NT tiles] 16 KB
+  static constexpr int RING = 2 * NT * 16384;        // FB_NST x (K 8 KB + V 8 KB)
+  static constexpr int BAR = RING + FB_NST * 16384;
   static constexpr int NBAR = 2 * FB_NST + 2 * 4 + 2 * 2 * FB_NS + 2 * 2 * 2 + 2 * 2;
   static constexpr int SLOT = BAR + NBAR * 8;
   static constexpr int BYTES = SLOT + 16;
+  static constexpr int THREADS = 64 + 128 * NT;
 };
 
 #ifdef FB_TRACE
@@ -776,12 +787,23 @@ __device__ unsigned long long g_fbtrace[16384];
 #define FBT(code, c) do {} while (0)
 #endif
 
+// 1/x for x in [1, 2^127) on the FMA pipe (bit-trick seed, three Newton
+// steps: relative error ~1e-7): a MUFU.RCP would queue behind the softmax's
+// EX2 stream
+__device__ __forceinline__ float rcp_fma(float x) {
+  float y = __int_as_float(0x7EF311C3 - __float_as_int(x));
+  y = y * fmaf(-x, y, 2.f);
+  y = y * fmaf(-x, y, 2.f);
+  y = y * fmaf(-x, y, 2.f);
+  return y;
+}
+
 struct FbItem {
   int r0, n, q0, ntile, head;
 };
 
-template <bool FP16>
-__global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
+template <bool FP16, int NT>
+__global__ void __launch_bounds__(FbSmem<NT>::THREADS, 2 / NT) k_window_attention_fb(
     const __grid_constant__ CUtensorMap tm, uint16_t* __restrict__ out,
     const int64_t* __restrict__ win_start, const int32_t* __restrict__ win_len, int n_items,
     int pshift) {
@@ -789,11 +811,11 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // no runtime integer division anywhere in this kernel: it compiles to
   // I2F / MUFU.RCP / F2I, and the MUFU queue is full of the softmax's EX2
-  const int npair = 1 << pshift;  // query-tile pairs per (window, head): 1 or 2
-  unsigned char* sQ = smem_raw + FbSmem::Q;
-  unsigned char* ring = smem_raw + FbSmem::RING;
-  unsigned char* sP = smem_raw + FbSmem::P;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + FbSmem::BAR);
+  using Smem = FbSmem<NT>;
+  const int npair = 1 << pshift;  // groups of NT query tiles per (window, head)
+  unsigned char* sQ = smem_raw + Smem::Q;
+  unsigned char* ring = smem_raw + Smem::RING;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + Smem::BAR);
   uint64_t* kv_full = bars;                  // [FB_NST]
   uint64_t* kv_empty = kv_full + FB_NST;     // [FB_NST]
   uint64_t* q_full = kv_empty + FB_NST;      // [2 tiles][2 bufs]
@@ -804,7 +826,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
   uint64_t* p_empty = p_full + 4;            // [2][2]
   uint64_t* o_full = p_empty + 4;            // [2]
   uint64_t* o_empty = o_full + 2;            // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + FbSmem::SLOT);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + Smem::SLOT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -824,12 +846,12 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
       }
       for (int b = 0; b < FB_NS; ++b) {
         mbar_init(&s_full[FB_NS * t + b], 1);
-        mbar_init(&s_empty[FB_NS * t + b], 4);
+        mbar_init(&s_empty[FB_NS * t + b], 1);
       }
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  if (warp == 1) tmem_alloc<256 * NT>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -860,8 +882,8 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
     g.r0 = __shfl_sync(0xffffffffu, gc.r0, k & 31);
     const int pair = it & (npair - 1);
     g.head = (it >> pshift) & 7;
-    g.q0 = pair * 2 * TQ;
-    g.ntile = g.q0 >= g.n ? 0 : (g.q0 + TQ >= g.n ? 1 : 2);
+    g.q0 = pair * NT * TQ;
+    g.ntile = g.q0 >= g.n ? 0 : (NT == 1 || g.q0 + TQ >= g.n ? 1 : 2);
     return g;
   };
 
@@ -881,7 +903,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
           FBT(13, t);
           if (elect_one()) {
             mbar_expect_tx(&q_full[2 * t + qb], TQ * 128);
-            unsigned char* dq = sQ + (2 * qb + t) * 16384;
+            unsigned char* dq = sQ + (NT * qb + t) * 16384;
             tma_load_2d(dq, &tm, &q_full[2 * t + qb], w.head * 64, w.r0 + w.q0 + t * TQ);
             tma_load_2d(dq + 8192, &tm, &q_full[2 * t + qb], w.head * 64,
                         w.r0 + w.q0 + t * TQ + 64);
@@ -934,7 +956,6 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
       // shared addresses < 256 KB)
       const uint64_t dq0 = umma_desc_sw128(smem_u32(sQ));
       const uint64_t dring = umma_desc_sw128(smem_u32(ring));
-      const uint64_t dp0 = umma_desc_sw128(smem_u32(sP));
       uint32_t g = 0, qi[2] = {0, 0}, su[2] = {0, 0}, pu[2] = {0, 0}, oi[2] = {0, 0};
       GeoCache gcache{-32, 0, 0};
       for (int k = 0, it; (it = blockIdx.x + k * gridDim.x) < n_items; ++k) {
@@ -960,7 +981,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
 #endif
           mbar_wait(&q_full[2 * t + qb], (qi[t] >> 1) & 1);
           FBT(9 + t, 0);
-          dq[t] = dq0 + (uint64_t)((2 * qb + t) * (16384 >> 4));
+          dq[t] = dq0 + (uint64_t)((NT * qb + t) * (16384 >> 4));
         }
         auto issue_s = [&](int c) {  // S_t = Q_t K_c^T for both tiles
           FBT(1, c);
@@ -992,16 +1013,17 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
           const uint64_t dv = dring + (uint64_t)((st * 16384 + 8192) >> 4);
           for (int t = 0; t < ntile; ++t) {
             const int b = pu[t] & 1;
+            const int sb = pu[t] % FB_NS;  // P sits in its S buffer's first 32 columns
             mbar_wait(&p_full[2 * t + b], (pu[t] >> 1) & 1);
             if (c == 0) mbar_wait(&o_empty[t], (oi[t] & 1) ^ 1);
             tc_fence_after();
-            const uint64_t dp = dp0 + (uint64_t)((2 * t + b) * (16384 >> 4));
             if (elect_one()) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_f16_ss(tmem + 256 * t + 192, dp + 2 * k, dv + k * (2048 >> 4), idesc_o,
-                           (c | k) != 0);
+                mma_f16_ts(tmem + 256 * t + 192, tmem + 256 * t + 64 * sb + 8 * k,
+                           dv + k * (2048 >> 4), idesc_o, (c | k) != 0);
               mma_commit(&p_empty[2 * t + b]);
+              mma_commit(&s_empty[FB_NS * t + sb]);  // S/P buffer free once P V ran
             }
             __syncwarp();
             FBT(5 + t, c);
@@ -1048,12 +1070,9 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
       tmem_ld32(tq + 64 * sb, *reinterpret_cast<uint32_t(*)[32]>(r));
       tmem_ld32(tq + 64 * sb + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
     };
-    auto release_s = [&](uint32_t jj, uint32_t (&r)[64]) {
+    auto release_s = [&](uint32_t jj, uint32_t (&r)[64]) {  // S of chunk jj in registers
       tmem_ld_wait_regs(*reinterpret_cast<uint32_t(*)[32]>(r));
       reg_barrier32(*reinterpret_cast<uint32_t(*)[32]>(r + 32));
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[FB_NS * t + jj % FB_NS]);
     };
     GeoCache gcache{-32, 0, 0};
     for (int k = 0, it; (it = blockIdx.x + k * gridDim.x) < n_items; ++k) {
@@ -1136,14 +1155,11 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
         if (c + 1 < nch) load_s(j + 1, r);
         if (lane == 0 && quarter == 2) FBT(19 + 8 * t, c);
         const int pb = j & 1;
-        if (j >= 2) mbar_wait(&p_empty[2 * t + pb], ((j >> 1) - 1) & 1);  // P V of chunk j-2
         if (lane == 0 && quarter == 2) FBT(20 + 8 * t, c);
-        unsigned char* dst = sP + (2 * t + pb) * 16384;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<uint4*>(dst + sw128(row, q)) =
-              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        fence_async_smem();
+        // P (16-bit pairs) over the first 32 columns of this chunk's S
+        // buffer: the A operand of P V straight from tensor memory
+        tmem_st32(tq + 64 * (j % FB_NS), pk);
+        tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[2 * t + pb]);
@@ -1163,7 +1179,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[t]);
-      const float inv = 1.f / ((l0 + l1) + (l2 + l3));
+      const float inv = rcp_fma((l0 + l1) + (l2 + l3));
       if (cur.q0 + t * TQ + row < n) {
         uint4* dst = reinterpret_cast<uint4*>(
             out + ((int64_t)cur.r0 + cur.q0 + t * TQ + row) * 512 + cur.head * 64);
@@ -1181,7 +1197,7 @@ __global__ void __launch_bounds__(FB_THREADS, 1) k_window_attention_fb(
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  if (warp == 1) tmem_dealloc<256 * NT>(tmem);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1242,16 +1258,26 @@ extern "C" int moeb_window_attention(const void* qkv, void* out, const int64_t* 
   if (mode == 'p' && max_len <= TKMAX && rows < (1ll << 31)) {
     CUtensorMap tm;
     if (int rc = qkv_map(&tm, qkv, rows, fp16 != 0)) return rc;
-    auto k = fp16 ? k_window_attention_fb<true> : k_window_attention_fb<false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, FbSmem::BYTES);
-    const int pshift = nqb > 2 ? 1 : 0;  // pairs of 128-query tiles: 1 or 2 (max_len <= 512)
+    // MOEB_ATTN_NT: 1 = one query tile per CTA, two CTAs per SM (default); 2 =
+    // two tiles sharing each K / V chunk, one CTA per SM
+    const char* nte = getenv("MOEB_ATTN_NT");
+    const int nt = nte ? (nte[0] == '1' ? 1 : 2) : FB_NT_DEFAULT;
+    auto k = nt == 1 ? (fp16 ? k_window_attention_fb<true, 1> : k_window_attention_fb<false, 1>)
+                     : (fp16 ? k_window_attention_fb<true, 2> : k_window_attention_fb<false, 2>);
+    const int bytes = nt == 1 ? FbSmem<1>::BYTES : FbSmem<2>::BYTES;
+    const int threads = nt == 1 ? FbSmem<1>::THREADS : FbSmem<2>::THREADS;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    // groups of nt 128-query tiles per (window, head), a power of two
+    const int groups = (nqb + nt - 1) / nt;
+    const int pshift = groups > 2 ? 2 : groups > 1 ? 1 : 0;
     const int64_t items = (int64_t)n_windows * 8 << pshift;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = (int)(items < sms ? items : sms);
-    k<<<grid, FB_THREADS, FbSmem::BYTES, s>>>(tm, static_cast<uint16_t*>(out), win_start, win_len,
-                                             (int)items, pshift);
+    const int64_t slots = (int64_t)sms * (2 / nt);
+    const int grid = (int)(items < slots ? items : slots);
+    k<<<grid, threads, bytes, s>>>(tm, static_cast<uint16_t*>(out), win_start, win_len, (int)items,
+                                   pshift);
     return moeb::check_launch("k_window_attention_fb");
   }
   if (mode == 'f' && max_len <= TKMAX && rows < (1ll << 31)) {

@@ -79,17 +79,19 @@ def test_gemm_epilogues(tr, fp16, M, N, K):
 
 
 @pytest.mark.parametrize("spiky", [False, True])
-@pytest.mark.parametrize("impl", ["fb", "fa", "tc1", "mma"])
+@pytest.mark.parametrize("impl", ["fb", "fb1", "fa", "tc1", "mma"])
 @pytest.mark.parametrize("fp16", [True, False])
 def test_window_attention(tr, fp16, impl, spiky, monkeypatch):
-    """persistent one-pass tcgen05 kernel (default), the two-pass
+    """persistent one-pass tcgen05 kernel (default; fb1 = one query tile per
+    CTA, two CTAs per SM), the two-pass
     warp-specialised kernel (MOEB_ATTN=fa), the whole-window kernel
     (MOEB_ATTN=tc1) and the mma.sync baseline (MOEB_ATTN=mma). `spiky` scales
     scattered keys so that later 64-key chunks raise a row's max by far more
     than the one-pass kernel's 2^8 slack (its O rescale path) and others sit
     far below it (underflowing terms)."""
     from paper_2508_17137_b200 import _native as nat
-    monkeypatch.setenv("MOEB_ATTN", impl)
+    monkeypatch.setenv("MOEB_ATTN", impl[:2] if impl == "fb1" else impl)
+    monkeypatch.setenv("MOEB_ATTN_NT", "1" if impl == "fb1" else "2")
     dt = torch.float16 if fp16 else torch.bfloat16
     off = np.array([0, 700, 700 + 512, 700 + 512 + 37, 700 + 512 + 37 + 1100, 700 + 512 + 37 +
                     1100 + 129, 700 + 512 + 37 + 1100 + 129 + 300])
