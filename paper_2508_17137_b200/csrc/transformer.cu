@@ -116,45 +116,45 @@ __global__ void __launch_bounds__(256) k_layernorm_rows(float* __restrict__ x32,
 
 // The 16-bit residual stream's LayerNorm: x16 [rows][512] normalised in
 // place (fp32 statistics and arithmetic, one 16-bit read and write per
-// element: 4 B/element instead of the fp32 stream's 10). Warp per row, lane =
-// columns [8 lane + 256 q, +8).
+// element: 4 B/element instead of the fp32 stream's 10). A warp owns LN_RPW
+// consecutive rows, lane = columns [8 lane + 256 q, +8): all of its rows'
+// loads are issued before the first row is reduced (LN_RPW x 1 KB in flight
+// per warp), and gamma / beta stay in registers across its rows.
+constexpr int LN_RPW = 4;
+
+template <bool FP16>
+__device__ __forceinline__ void unpack8(const uint4 u, float* v) {
+  const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 f;
+    if (FP16)
+      f = __half22float2(*reinterpret_cast<const __half2*>(&w4[j]));
+    else
+      f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[j]));
+    v[2 * j] = f.x;
+    v[2 * j + 1] = f.y;
+  }
+}
+
 template <bool FP16>
 __global__ void __launch_bounds__(256) k_layernorm_rows16(uint16_t* __restrict__ x16,
                                                           const float* __restrict__ w,
                                                           const float* __restrict__ b,
                                                           int64_t rows, float eps) {
-  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (r >= rows) return;
+  const int64_t r0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * LN_RPW;
+  if (r0 >= rows) return;
   const int lane = threadIdx.x & 31;
-  uint4* xr = reinterpret_cast<uint4*>(x16 + r * 512);
-  float v[16];
-  float s = 0.f;
+  const int nr = rows - r0 < LN_RPW ? (int)(rows - r0) : LN_RPW;
+  uint4 u[LN_RPW][2];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const uint4 u = xr[q * 32 + lane];
-    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float2 f;
-      if (FP16) {
-        f = __half22float2(*reinterpret_cast<const __half2*>(&w4[j]));
-      } else {
-        f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w4[j]));
-      }
-      v[q * 8 + 2 * j] = f.x;
-      v[q * 8 + 2 * j + 1] = f.y;
-      s += f.x + f.y;
+  for (int i = 0; i < LN_RPW; ++i)
+    if (i < nr) {
+      const uint4* xr = reinterpret_cast<const uint4*>(x16 + (r0 + i) * 512);
+      u[i][0] = xr[lane];
+      u[i][1] = xr[32 + lane];
     }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  const float mean = s * (1.f / 512.f);
-  float s2 = 0.f;
-#pragma unroll
-  for (int i = 0; i < 16; ++i) s2 += (v[i] - mean) * (v[i] - mean);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-  const float rstd = rsqrtf(s2 * (1.f / 512.f) + eps);
+  float ww[16], bb[16];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int c = q * 256 + lane * 8;
@@ -162,22 +162,51 @@ __global__ void __launch_bounds__(256) k_layernorm_rows16(uint16_t* __restrict__
     const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + c + 4));
     const float4 b0 = __ldg(reinterpret_cast<const float4*>(b + c));
     const float4 b1 = __ldg(reinterpret_cast<const float4*>(b + c + 4));
-    const float ww[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-    const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    uint32_t p[4];
+    const float wq[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+    const float bq[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float y0 = (v[q * 8 + 2 * j] - mean) * rstd * ww[2 * j] + bb[2 * j];
-      const float y1 = (v[q * 8 + 2 * j + 1] - mean) * rstd * ww[2 * j + 1] + bb[2 * j + 1];
-      if (FP16) {
-        const __half2 h = __floats2half2_rn(y0, y1);
-        p[j] = *reinterpret_cast<const uint32_t*>(&h);
-      } else {
-        const __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
-        p[j] = *reinterpret_cast<const uint32_t*>(&h);
-      }
+    for (int j = 0; j < 8; ++j) {
+      ww[q * 8 + j] = wq[j];
+      bb[q * 8 + j] = bq[j];
     }
-    xr[q * 32 + lane] = make_uint4(p[0], p[1], p[2], p[3]);
+  }
+#pragma unroll
+  for (int i = 0; i < LN_RPW; ++i) {
+    if (i >= nr) break;
+    float v[16];
+    unpack8<FP16>(u[i][0], v);
+    unpack8<FP16>(u[i][1], v + 8);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += v[k];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s * (1.f / 512.f);
+    float s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s2 += (v[k] - mean) * (v[k] - mean);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    const float rstd = rsqrtf(s2 * (1.f / 512.f) + eps);
+    uint4* xr = reinterpret_cast<uint4*>(x16 + (r0 + i) * 512);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t p[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int k = q * 8 + 2 * j;
+        const float y0 = (v[k] - mean) * rstd * ww[k] + bb[k];
+        const float y1 = (v[k + 1] - mean) * rstd * ww[k + 1] + bb[k + 1];
+        if (FP16) {
+          const __half2 h = __floats2half2_rn(y0, y1);
+          p[j] = *reinterpret_cast<const uint32_t*>(&h);
+        } else {
+          const __nv_bfloat162 h = __floats2bfloat162_rn(y0, y1);
+          p[j] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+      }
+      xr[q * 32 + lane] = make_uint4(p[0], p[1], p[2], p[3]);
+    }
   }
 }
 
@@ -188,7 +217,7 @@ extern "C" int moeb_layernorm_rows16(void* x16, const float* w, const float* b, 
   moeb::clear_error();
   MOEB_REQUIRE(x16 && w && b && rows >= 0, "bad args");
   if (rows == 0) return MOEB_OK;
-  const unsigned blocks = (unsigned)((rows * 32 + 255) / 256);
+  const unsigned blocks = (unsigned)(((rows + LN_RPW - 1) / LN_RPW * 32 + 255) / 256);
   cudaStream_t s = moeb::as_stream(stream);
   if (fp16)
     k_layernorm_rows16<true><<<blocks, 256, 0, s>>>(static_cast<uint16_t*>(x16), w, b, rows, eps);
