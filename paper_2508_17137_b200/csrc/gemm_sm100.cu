@@ -185,12 +185,16 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (the leader CTA of a pair) =====
-    if (lane == 0 && leader) {
+    // ===== MMA issuer (the leader CTA of a pair): the whole warp runs the
+    // loop in warp-uniform control flow (descriptors in uniform registers),
+    // one elected lane issues
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      const uint64_t da0 = umma_desc_sw128(smem_u32(sA));
+      const uint64_t db0 = umma_desc_sw128(smem_u32(sB));
       for (int tile = tile0; tile < num_tiles; tile += tstride) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);  // epilogue drained this buffer
         tc_fence_after();
@@ -198,29 +202,36 @@ __global__ void __launch_bounds__(320, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
-          const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+          // descriptors advance by (bytes >> 4) in their low bits
+          const uint64_t a0 = da0 + (uint64_t)((stage * A_BYTES) >> 4);
+          const uint64_t b0 = db0 + (uint64_t)((stage * B_BYTES) >> 4);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = umma_desc_sw128(a0 + k * 32);
+            for (int k = 0; k < BK / 16; ++k) {
 #pragma unroll
-            for (int j = 0; j < BN / UMMA_N; ++j) {
-              const uint64_t bd = umma_desc_sw128(b0 + j * UMMA_N * 128 + k * 32);
-              if (PAIR) mma_f16_ss_pair(d_tmem + j * UMMA_N, ad, bd, IDESC, (kb | k) != 0);
-              else mma_f16_ss(d_tmem + j * UMMA_N, ad, bd, IDESC, (kb | k) != 0);
+              for (int j = 0; j < BN / UMMA_N; ++j) {
+                const uint64_t ad = a0 + 2 * k;
+                const uint64_t bd = b0 + (uint64_t)((j * UMMA_N * 128) >> 4) + 2 * k;
+                if (PAIR) mma_f16_ss_pair(d_tmem + j * UMMA_N, ad, bd, IDESC, (kb | k) != 0);
+                else mma_f16_ss(d_tmem + j * UMMA_N, ad, bd, IDESC, (kb | k) != 0);
+              }
             }
+            // frees the smem stage (of both CTAs) when these MMAs finish
+            if (PAIR) mma_commit_pair(&empty[stage], 3);
+            else mma_commit(&empty[stage]);
           }
-          // frees the smem stage (of both CTAs) when these MMAs finish
-          if (PAIR) mma_commit_pair(&empty[stage], 3);
-          else mma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
         // accumulator ready for the epilogue(s)
-        if (PAIR) mma_commit_pair(&tfull[acc], 3);
-        else mma_commit(&tfull[acc]);
+        if (elect_one()) {
+          if (PAIR) mma_commit_pair(&tfull[acc], 3);
+          else mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
         if (++acc == ACC) {
           acc = 0;
           acc_phase ^= 1;
