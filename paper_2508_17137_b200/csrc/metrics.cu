@@ -7,6 +7,8 @@
 // K2 replaces top_k_experts / predict_topk (learner.py:164-181).
 // Policy masks replace OraclePredictor / LruOnlyPredictor /
 // NextLayerAllPredictor / GlobalFrequencyPredictor.predict (predictors.py:57-139).
+#include <cstring>
+
 #include "common.cuh"
 
 namespace {
@@ -501,6 +503,92 @@ __global__ void k_ranks_to_masks(const uint32_t* __restrict__ ranks, int64_t row
   }
 }
 
+// Table-seeded decode: digit i's candidate c comes from a byte table indexed
+// by the residual's top bits (tab_i[j] = largest c with C(c, i) <= j << s_i,
+// at most 4096 entries per digit), then c moves up while C(c + 1, i) <= N --
+// no step for almost every row (C(c, i) grows past the bucket width for all
+// but the smallest residuals). Digit 1 is the residual itself. About a
+// fifth of the binary search's instructions and dependent shared loads.
+constexpr int kSeedBits = 12;
+struct SeedTabs {
+  int shift[kBinK];
+  int base[kBinK];  // byte offset of digit i's table
+  int bytes;
+};
+
+__device__ __forceinline__ void seed_tabs(SeedTabs& st, const uint32_t* tab, int k, int E) {
+  int off = 0;
+  for (int i = 2; i <= k; ++i) {
+    const uint32_t top = tab[i * kBinN + E];  // C(E, i): every residual is below it
+    const int bl = 32 - __clz(top);
+    st.shift[i] = bl > kSeedBits ? bl - kSeedBits : 0;
+    st.base[i] = off;
+    off += (int)(top >> st.shift[i]) + 1;
+  }
+  st.bytes = off;
+}
+
+__global__ void k_ranks_to_masks_seeded(const uint32_t* __restrict__ ranks, int64_t rows,
+                                        int bits, int k, int E, uint64_t* __restrict__ masks,
+                                        int* __restrict__ bad) {
+  __shared__ uint32_t tab[kBinN * kBinK];
+  __shared__ unsigned char seed[(kBinK - 2) * ((1 << kSeedBits) + 2)];
+  load_binom(tab);
+  SeedTabs st;
+  seed_tabs(st, tab, k, E);
+  for (int i = 2; i <= k; ++i) {
+    const uint32_t* t = tab + i * kBinN;
+    const int n = (int)(t[E] >> st.shift[i]) + 1;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const uint32_t v = (uint32_t)j << st.shift[i];
+      int lo = i - 1;  // largest c < E with C(c, i) <= v (C(i - 1, i) = 0)
+#pragma unroll
+      for (int step = 32; step; step >>= 1) {
+        const int c = lo + step;
+        lo = (c < E && t[c] <= v) ? c : lo;
+      }
+      seed[st.base[i] + j] = (unsigned char)lo;
+    }
+  }
+  __syncthreads();
+  // kRowsPT rows per thread and iteration: independent dependency chains
+  constexpr int kRowsPT = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += kRowsPT * stride) {
+    uint32_t N[kRowsPT];
+    bool ok[kRowsPT], in[kRowsPT];
+    uint64_t m[kRowsPT];
+#pragma unroll
+    for (int q = 0; q < kRowsPT; ++q) {
+      in[q] = r + q * stride < rows;
+      N[q] = in[q] ? rank_at(ranks, r + q * stride, bits) : 0u;
+      ok[q] = N[q] < tab[k * kBinN + E];
+      if (!ok[q]) N[q] = 0;  // keeps the table index in range; the row is zeroed below
+      m[q] = 0ull;
+    }
+    for (int i = k; i >= 2; --i) {
+      const uint32_t* t = tab + i * kBinN;
+      const unsigned char* sd = seed + st.base[i];
+      const int sh = st.shift[i];
+#pragma unroll
+      for (int q = 0; q < kRowsPT; ++q) {
+        int c = sd[N[q] >> sh];
+        while (c + 1 < E && t[c + 1] <= N[q]) ++c;
+        N[q] -= t[c];
+        m[q] |= 1ull << c;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kRowsPT; ++q) {
+      if (!in[q]) continue;
+      m[q] |= 1ull << (N[q] & 63);  // digit 1: C(c, 1) = c
+      if (!ok[q]) atomicExch(bad, 1);
+      masks[r + q * stride] = ok[q] ? m[q] : 0ull;
+    }
+  }
+}
+
 __global__ void k_masks_to_ranks(const uint64_t* __restrict__ masks, int64_t rows, int k, int bits,
                                  uint32_t* __restrict__ ranks, int* __restrict__ bad) {
   __shared__ uint32_t tab[kBinN * kBinK];
@@ -525,6 +613,11 @@ __global__ void k_masks_to_ranks(const uint64_t* __restrict__ masks, int64_t row
     }
   }
 }
+// MOEB_RANK_DECODE=search: the fixed-length binary search (comparison)
+bool rank_decode_seeded() {
+  const char* e = getenv("MOEB_RANK_DECODE");
+  return !(e && !strcmp(e, "search"));
+}
 }  // namespace
 
 extern "C" int moeb_ranks_to_masks(const uint32_t* ranks, int64_t rows, int k, int E,
@@ -534,7 +627,12 @@ extern "C" int moeb_ranks_to_masks(const uint32_t* ranks, int64_t rows, int k, i
                "bad arguments");
   if (rows == 0) return MOEB_OK;
   const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
-  k_ranks_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(ranks, rows, 32, k, E, masks, bad);
+  if (rank_decode_seeded())
+    k_ranks_to_masks_seeded<<<blocks, 256, 0, moeb::as_stream(stream)>>>(ranks, rows, 32, k, E,
+                                                                         masks, bad);
+  else
+    k_ranks_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(ranks, rows, 32, k, E, masks,
+                                                                  bad);
   return moeb::check_launch("k_ranks_to_masks");
 }
 
@@ -561,8 +659,12 @@ extern "C" int moeb_packed_ranks_to_masks(const uint32_t* words, int64_t rows, i
                "bad arguments");
   if (rows == 0) return MOEB_OK;
   const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
-  k_ranks_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(words, rows, bits, k, E, masks,
-                                                                bad);
+  if (rank_decode_seeded())
+    k_ranks_to_masks_seeded<<<blocks, 256, 0, moeb::as_stream(stream)>>>(words, rows, bits, k, E,
+                                                                         masks, bad);
+  else
+    k_ranks_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(words, rows, bits, k, E, masks,
+                                                                  bad);
   return moeb::check_launch("k_ranks_to_masks");
 }
 
