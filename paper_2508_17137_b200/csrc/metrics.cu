@@ -327,7 +327,8 @@ extern "C" int moeb_metrics(const uint64_t* pred, const uint64_t* truth,
   const int threads = 256;
   cudaStream_t s = moeb::as_stream(stream);
   if (W == 1) {  // persistent bit-sliced kernel: 4 CTAs per SM, equal row ranges per warp
-    const int blocks = 4 * moeb::num_sms();
+    const char* kb = getenv("MOEB_K7_CTAS");  // CTAs per SM (A/B of the overlap footprint)
+    const int blocks = (kb ? atoi(kb) : 4) * moeb::num_sms();
     k_metrics64<<<blocks, threads, 0, s>>>(pred, truth, prompt_row_off, n_prompts, L, E,
                                            warmup_tokens, metrics);
     return moeb::check_launch("k_metrics64");
