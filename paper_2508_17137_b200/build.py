@@ -47,7 +47,8 @@ def _compile(src: str) -> str:
     with open(os.path.join(BUILD, f"ptxas_{name}.log"), "w") as fh:
         fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed for {src}:\n{res.stderr[-6000:]}")
+        errs = "\n".join(ln for ln in res.stderr.splitlines() if "error" in ln.lower())
+        raise RuntimeError(f"nvcc failed for {src}:\n{errs[:6000] or res.stderr[-6000:]}")
     return obj
 
 

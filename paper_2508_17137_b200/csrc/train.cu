@@ -27,6 +27,8 @@
 #include <cuda_fp16.h>
 
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -458,6 +460,350 @@ __global__ void __launch_bounds__(256) k_attn_bwd_kv(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Attention backward on the tensor cores (default): the same two passes as
+// the fp32 SIMT kernels above, with every product an mma.sync m16n8k16 (16-bit
+// operands, fp32 accumulation): per (window, head, 64-query block) 4 warps x
+// 16 query rows -- S = Q K^T twice (row statistics, then P), dP = dO V^T,
+// dS = P (dP - dsum), dQ += dS K; per (window, head, 64-key block) 4 warps x
+// 16 key rows -- S^T = K Q^T, dP^T = V dO^T, dV += P^T dO, dK += dS^T Q. P
+// and dS enter the second products as 16-bit A fragments straight from the
+// accumulators; K / V / Q / dO tiles are staged by cp.async (double-buffered
+// key / query blocks) in XOR-swizzled shared memory and read with ldmatrix
+// (.trans for the [key][d] operands of dQ, dV and dK). MOEB_ATTN_BWD=simt
+// selects the fp32 kernels.
+// ---------------------------------------------------------------------------
+template <bool FP16>
+__device__ __forceinline__ void bmma(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                     uint32_t a3, uint32_t b0, uint32_t b1) {
+  if (FP16)
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  else
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+template <bool FP16>
+__device__ __forceinline__ uint32_t bpack2(float x, float y) {
+  if (FP16) {
+    const __half2 h = __floats2half2_rn(x, y);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void bcp16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void bcp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bcp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ int bswz(int row, int col) {  // [64][64] 16-bit, 16-B chunks
+  return row * 64 + ((((col >> 3) ^ (row & 7)) << 3) | (col & 7));
+}
+__device__ __forceinline__ uint32_t bsmem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bldsm(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void bldsm_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+// [64 rows][64] 16-bit block (rows >= n zero-filled) -> swizzled tile, async
+__device__ __forceinline__ void btile_async(uint16_t* tile, const uint16_t* src, int ld, int n) {
+  for (int i = threadIdx.x; i < 64 * 8; i += blockDim.x) {
+    const int row = i >> 3, ch = i & 7;
+    const bool v = row < n;
+    bcp16(bsmem(tile + bswz(row, ch * 8)), src + (int64_t)(v ? row : 0) * ld + ch * 8,
+                     v);
+  }
+}
+// A fragments (16 rows of this warp x 64 columns, 4 k-steps) of a swizzled tile
+__device__ __forceinline__ void a_frags(const uint16_t* tile, int warp, int lane,
+                                        uint32_t (&fr)[4][4]) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int row = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+    const int col = ks * 16 + (lane >> 4) * 8;
+    bldsm(bsmem(tile + bswz(row, col)), fr[ks]);
+  }
+}
+// acc[16 x 64] = A (fragments, 16 x 64) . B^T with B a [64 rows][64] tile
+// (row = output column): the S = Q K^T pattern
+template <bool FP16>
+__device__ __forceinline__ void mm_abt(float (&acc)[8][4], const uint32_t (&fa)[4][4],
+                                       const uint16_t* B, int lane) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      uint32_t b[4];
+      const int row = jp * 16 + (lane & 7) + (lane >> 4) * 8;
+      const int col = ks * 16 + ((lane >> 3) & 1) * 8;
+      bldsm(bsmem(B + bswz(row, col)), b);
+      bmma<FP16>(acc[2 * jp], fa[ks][0], fa[ks][1], fa[ks][2], fa[ks][3], b[0], b[1]);
+      bmma<FP16>(acc[2 * jp + 1], fa[ks][0], fa[ks][1], fa[ks][2], fa[ks][3], b[2],
+                           b[3]);
+    }
+}
+// acc[16 x 64] += X (16 x 64 accumulator-layout values, packed to A
+// fragments) . B with B a [64 rows = k][64 cols = n] tile: the O += P V pattern
+template <bool FP16>
+__device__ __forceinline__ void mm_acc_ab(float (&acc)[8][4], const float (&x)[8][4],
+                                          const uint16_t* B, int lane) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const uint32_t a0 = bpack2<FP16>(x[2 * ks][0], x[2 * ks][1]);
+    const uint32_t a1 = bpack2<FP16>(x[2 * ks][2], x[2 * ks][3]);
+    const uint32_t a2 = bpack2<FP16>(x[2 * ks + 1][0], x[2 * ks + 1][1]);
+    const uint32_t a3 = bpack2<FP16>(x[2 * ks + 1][2], x[2 * ks + 1][3]);
+#pragma unroll
+    for (int jp = 0; jp < 4; ++jp) {
+      uint32_t b[4];
+      const int row = ks * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+      const int col = jp * 16 + (lane >> 4) * 8;
+      bldsm_t(bsmem(B + bswz(row, col)), b);
+      bmma<FP16>(acc[2 * jp], a0, a1, a2, a3, b[0], b[1]);
+      bmma<FP16>(acc[2 * jp + 1], a0, a1, a2, a3, b[2], b[3]);
+    }
+  }
+}
+
+template <bool FP16>
+__global__ void __launch_bounds__(128) k_attn_bwd_q_mma(
+    const uint16_t* __restrict__ qkv, const uint16_t* __restrict__ o,
+    const uint16_t* __restrict__ dout, const int64_t* __restrict__ win_start,
+    const int32_t* __restrict__ win_len, int nqb, uint16_t* __restrict__ dqkv,
+    float* __restrict__ lse2_out, float* __restrict__ dsum_out) {
+  extern __shared__ __align__(128) unsigned char bsm_q[];  // 48 KB tiles + row sums
+  uint16_t* sQ = reinterpret_cast<uint16_t*>(bsm_q);
+  uint16_t* sdO = sQ + 64 * 64;
+  uint16_t(*sK)[64 * 64] = reinterpret_cast<uint16_t(*)[64 * 64]>(sdO + 64 * 64);
+  uint16_t(*sV)[64 * 64] = sK + 2;
+  float* sdsum = reinterpret_cast<float*>(sV + 2);
+  const int qb = blockIdx.x % nqb, head = (blockIdx.x / nqb) % 8, w = blockIdx.x / (nqb * 8);
+  const int n = win_len[w];
+  if (qb * 64 >= n) return;
+  const int64_t r0 = win_start[w];
+  const int64_t q0 = r0 + qb * 64;
+  const int nq = min(64, n - qb * 64);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  const uint16_t* Kg = qkv + r0 * 1536 + 512 + head * 64;
+  const uint16_t* Vg = qkv + r0 * 1536 + 1024 + head * 64;
+  btile_async(sQ, qkv + q0 * 1536 + head * 64, 1536, nq);
+  btile_async(sdO, dout + q0 * 512 + head * 64, 512, nq);
+  btile_async(sK[0], Kg, 1536, n);
+  bcp_commit();
+  if (threadIdx.x < 64) {  // dsum = rowsum(dO o O), fp32 from global
+    float acc = 0.f;
+    if (threadIdx.x < nq) {
+      const uint16_t* orow = o + (q0 + threadIdx.x) * 512 + head * 64;
+      const uint16_t* drow = dout + (q0 + threadIdx.x) * 512 + head * 64;
+      for (int d = 0; d < 64; ++d) acc += ld16<FP16>(orow + d) * ld16<FP16>(drow + d);
+    }
+    sdsum[threadIdx.x] = acc;
+  }
+  bcp_wait0();
+  __syncthreads();
+  uint32_t qa[4][4], da[4][4];
+  a_frags(sQ, warp, lane, qa);
+  a_frags(sdO, warp, lane, da);
+  const int nkb = (n + 63) / 64;
+  // pass A: running max / sum of exp2 per query row (rows g, g + 8)
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int cur = kb & 1;
+    if (kb + 1 < nkb) btile_async(sK[cur ^ 1], Kg + (int64_t)(kb + 1) * 64 * 1536, 1536,
+                                  n - (kb + 1) * 64);
+    bcp_commit();
+    float s[8][4];
+    mm_abt<FP16>(s, qa, sK[cur], lane);
+    const int nk = min(64, n - kb * 64);
+    float mnew[2] = {mrow[0], mrow[1]};
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int key = j * 8 + tig * 2 + (u & 1);
+        s[j][u] = key < nk ? s[j][u] * kSl2 : -INFINITY;
+        mnew[u >> 1] = fmaxf(mnew[u >> 1], s[j][u]);
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      mnew[h] = fmaxf(mnew[h], __shfl_xor_sync(0xffffffffu, mnew[h], 1));
+      mnew[h] = fmaxf(mnew[h], __shfl_xor_sync(0xffffffffu, mnew[h], 2));
+    }
+    float sum[2] = {0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) sum[u >> 1] += exp2f(s[j][u] - mnew[u >> 1]);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      lrow[h] = lrow[h] * exp2f(mrow[h] - mnew[h]) + sum[h];
+      mrow[h] = mnew[h];
+    }
+    bcp_wait0();
+    __syncthreads();
+  }
+  float lse[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 1);
+    lrow[h] += __shfl_xor_sync(0xffffffffu, lrow[h], 2);
+    lse[h] = mrow[h] + log2f(lrow[h]);
+  }
+  const int rl[2] = {warp * 16 + g, warp * 16 + g + 8};
+  const float ds[2] = {sdsum[rl[0]], sdsum[rl[1]]};
+  // pass B: P, dP = dO V^T, dS = P (dP - dsum), dQ += dS K
+  float dq[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
+  btile_async(sK[0], Kg, 1536, n);
+  btile_async(sV[0], Vg, 1536, n);
+  bcp_commit();
+  bcp_wait0();
+  __syncthreads();
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int cur = kb & 1;
+    if (kb + 1 < nkb) {
+      btile_async(sK[cur ^ 1], Kg + (int64_t)(kb + 1) * 64 * 1536, 1536, n - (kb + 1) * 64);
+      btile_async(sV[cur ^ 1], Vg + (int64_t)(kb + 1) * 64 * 1536, 1536, n - (kb + 1) * 64);
+    }
+    bcp_commit();
+    float s[8][4], dp[8][4];
+    mm_abt<FP16>(s, qa, sK[cur], lane);
+    mm_abt<FP16>(dp, da, sV[cur], lane);
+    const int nk = min(64, n - kb * 64);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int key = j * 8 + tig * 2 + (u & 1);
+        const float p = key < nk ? exp2f(s[j][u] * kSl2 - lse[u >> 1]) : 0.f;
+        s[j][u] = p * (dp[j][u] - ds[u >> 1]);
+      }
+    mm_acc_ab<FP16>(dq, s, sK[cur], lane);
+    bcp_wait0();
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int col = head * 64 + j * 8 + tig * 2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (rl[h] < nq)
+        *reinterpret_cast<uint32_t*>(dqkv + (q0 + rl[h]) * 1536 + col) =
+            bpack2<FP16>(dq[j][2 * h] * 0.125f, dq[j][2 * h + 1] * 0.125f);
+  }
+  if (tig == 0)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (rl[h] < nq) {
+        lse2_out[(q0 + rl[h]) * 8 + head] = lse[h];
+        dsum_out[(q0 + rl[h]) * 8 + head] = ds[h];
+      }
+}
+
+template <bool FP16>
+__global__ void __launch_bounds__(128) k_attn_bwd_kv_mma(
+    const uint16_t* __restrict__ qkv, const uint16_t* __restrict__ dout,
+    const int64_t* __restrict__ win_start, const int32_t* __restrict__ win_len, int nkb,
+    const float* __restrict__ lse2, const float* __restrict__ dsum_in,
+    uint16_t* __restrict__ dqkv) {
+  extern __shared__ __align__(128) unsigned char bsm_kv[];  // 48 KB tiles + row statistics
+  uint16_t* sK = reinterpret_cast<uint16_t*>(bsm_kv);
+  uint16_t* sV = sK + 64 * 64;
+  uint16_t(*sQ)[64 * 64] = reinterpret_cast<uint16_t(*)[64 * 64]>(sV + 64 * 64);
+  uint16_t(*sdO)[64 * 64] = sQ + 2;
+  float(*slse)[64] = reinterpret_cast<float(*)[64]>(sdO + 2);
+  float(*sds)[64] = slse + 2;
+  const int kb = blockIdx.x % nkb, head = (blockIdx.x / nkb) % 8, w = blockIdx.x / (nkb * 8);
+  const int n = win_len[w];
+  if (kb * 64 >= n) return;
+  const int64_t r0 = win_start[w];
+  const int64_t k0 = r0 + kb * 64;
+  const int nk = min(64, n - kb * 64);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tig = lane & 3;
+  const uint16_t* Qg = qkv + r0 * 1536 + head * 64;
+  const uint16_t* dOg = dout + r0 * 512 + head * 64;
+  auto stage = [&](int qb, int buf) {
+    btile_async(sQ[buf], Qg + (int64_t)qb * 64 * 1536, 1536, n - qb * 64);
+    btile_async(sdO[buf], dOg + (int64_t)qb * 64 * 512, 512, n - qb * 64);
+    if (threadIdx.x < 64) {
+      const int q = qb * 64 + threadIdx.x;
+      slse[buf][threadIdx.x] = q < n ? lse2[(r0 + q) * 8 + head] : 0.f;
+      sds[buf][threadIdx.x] = q < n ? dsum_in[(r0 + q) * 8 + head] : 0.f;
+    }
+  };
+  btile_async(sK, qkv + k0 * 1536 + 512 + head * 64, 1536, nk);
+  btile_async(sV, qkv + k0 * 1536 + 1024 + head * 64, 1536, nk);
+  stage(0, 0);
+  bcp_commit();
+  bcp_wait0();
+  __syncthreads();
+  uint32_t ka[4][4], va[4][4];
+  a_frags(sK, warp, lane, ka);
+  a_frags(sV, warp, lane, va);
+  const int kl[2] = {warp * 16 + g, warp * 16 + g + 8};  // this thread's key rows
+  float dk[8][4], dv[8][4];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dk[j][u] = dv[j][u] = 0.f;
+  const int nqb = (n + 63) / 64;
+  for (int qb = 0; qb < nqb; ++qb) {
+    const int cur = qb & 1;
+    if (qb + 1 < nqb) stage(qb + 1, cur ^ 1);
+    bcp_commit();
+    float s[8][4], dp[8][4];
+    mm_abt<FP16>(s, ka, sQ[cur], lane);   // S^T [key][query]
+    mm_abt<FP16>(dp, va, sdO[cur], lane); // dP^T
+    const int nq = min(64, n - qb * 64);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = j * 8 + tig * 2 + (u & 1);
+        const bool ok = q < nq && kl[u >> 1] < nk;
+        const float p = ok ? exp2f(s[j][u] * kSl2 - slse[cur][q]) : 0.f;
+        s[j][u] = p;                                   // P^T
+        dp[j][u] = p * (dp[j][u] - sds[cur][q]);      // dS^T
+      }
+    mm_acc_ab<FP16>(dv, s, sdO[cur], lane);
+    mm_acc_ab<FP16>(dk, dp, sQ[cur], lane);
+    bcp_wait0();
+    __syncthreads();
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int col = head * 64 + j * 8 + tig * 2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (kl[h] < nk) {
+        uint16_t* row = dqkv + (k0 + kl[h]) * 1536;
+        *reinterpret_cast<uint32_t*>(row + 512 + col) =
+            bpack2<FP16>(dk[j][2 * h] * 0.125f, dk[j][2 * h + 1] * 0.125f);
+        *reinterpret_cast<uint32_t*>(row + 1024 + col) =
+            bpack2<FP16>(dv[j][2 * h], dv[j][2 * h + 1]);
+      }
+  }
+}
+
 // F[row] = [tok16[token[row]] (2048) | lay16[layer[row]] (512)], 16-bit
 __global__ void k_gather_inputs16(const uint16_t* __restrict__ tok16,
                                   const uint16_t* __restrict__ lay16,
@@ -639,6 +985,28 @@ extern "C" int moeb_attention_bwd(const void* qkv, const void* o, const void* do
   if (n_windows == 0) return MOEB_OK;
   cudaStream_t s = moeb::as_stream(stream);
   const int nb = (max_len + AT - 1) / AT;
+  const char* env = getenv("MOEB_ATTN_BWD");
+  if (!(env && !strcmp(env, "simt"))) {  // tensor cores (mma.sync)
+    const unsigned grid = (unsigned)((int64_t)n_windows * 8 * nb);
+    const int sq = 6 * 64 * 64 * 2 + 64 * 4, skv = 6 * 64 * 64 * 2 + 4 * 64 * 4;
+    moeb::set_smem(k_attn_bwd_q_mma<true>, sq);
+    moeb::set_smem(k_attn_bwd_q_mma<false>, sq);
+    moeb::set_smem(k_attn_bwd_kv_mma<true>, skv);
+    moeb::set_smem(k_attn_bwd_kv_mma<false>, skv);
+    MOEB_FP16_SWITCH(fp16, k_attn_bwd_q_mma, <<<grid, 128, sq, s>>>(
+                                                 static_cast<const uint16_t*>(qkv),
+                                                 static_cast<const uint16_t*>(o),
+                                                 static_cast<const uint16_t*>(dout), win_start,
+                                                 win_len, nb, static_cast<uint16_t*>(dqkv), lse2,
+                                                 dsum));
+    if (int rc = moeb::check_launch("k_attn_bwd_q_mma")) return rc;
+    MOEB_FP16_SWITCH(fp16, k_attn_bwd_kv_mma, <<<grid, 128, skv, s>>>(
+                                                  static_cast<const uint16_t*>(qkv),
+                                                  static_cast<const uint16_t*>(dout), win_start,
+                                                  win_len, nb, lse2, dsum,
+                                                  static_cast<uint16_t*>(dqkv)));
+    return moeb::check_launch("k_attn_bwd_kv_mma");
+  }
   const size_t smq = sizeof(float) * (5 * AT * (AT + 1) + 2 * AT);
   const size_t smkv = sizeof(float) * (6 * AT * (AT + 1) + 2 * AT);
   moeb::set_smem(k_attn_bwd_q<true>, (int)smq);
