@@ -26,6 +26,9 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ea
   -o gpurun_out/prof_${TAG}_k6 python tools/k6_probe.py 2000 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stack_multi -c 1 \
   -o gpurun_out/prof_${TAG}_k1m python tools/k1m_probe.py 2000 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_window_attention_fb -c 1 \
+  -o gpurun_out/prof_${TAG}_attn python tools/bench_transformer.py > /dev/null 2>&1
+timeout 600 python tools/rank_decode_probe.py > gpurun_out/rank_decode_$TAG.log 2>&1
 timeout 600 python tools/bench_sweep.py c3 > gpurun_out/c3_$TAG.log 2>&1; tail -1 gpurun_out/c3_$TAG.log | cut -c1-200
 timeout 600 python tools/bench_sweep.py c5 > gpurun_out/c5_$TAG.log 2>&1; tail -1 gpurun_out/c5_$TAG.log | cut -c1-200
 timeout 600 python tools/bench_transformer.py > gpurun_out/transformer_$TAG.json 2>&1
