@@ -823,8 +823,7 @@ __global__ void __launch_bounds__(FbSmem<NT>::THREADS, 2 / NT) k_window_attentio
   uint64_t* s_full = q_empty + 4;            // [2 tiles][FB_NS]
   uint64_t* s_empty = s_full + 2 * FB_NS;    // [2][FB_NS]
   uint64_t* p_full = s_empty + 2 * FB_NS;    // [2 tiles][2 bufs]
-  uint64_t* p_empty = p_full + 4;            // [2][2]
-  uint64_t* o_full = p_empty + 4;            // [2]
+  uint64_t* o_full = p_full + 4;             // [2]
   uint64_t* o_empty = o_full + 2;            // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + Smem::SLOT);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -842,7 +841,6 @@ __global__ void __launch_bounds__(FbSmem<NT>::THREADS, 2 / NT) k_window_attentio
         mbar_init(&q_full[2 * t + b], 1);
         mbar_init(&q_empty[2 * t + b], 1);
         mbar_init(&p_full[2 * t + b], 4);
-        mbar_init(&p_empty[2 * t + b], 1);
       }
       for (int b = 0; b < FB_NS; ++b) {
         mbar_init(&s_full[FB_NS * t + b], 1);
@@ -1022,7 +1020,6 @@ __global__ void __launch_bounds__(FbSmem<NT>::THREADS, 2 / NT) k_window_attentio
               for (int k = 0; k < 4; ++k)
                 mma_f16_ts(tmem + 256 * t + 192, tmem + 256 * t + 64 * sb + 8 * k,
                            dv + k * (2048 >> 4), idesc_o, (c | k) != 0);
-              mma_commit(&p_empty[2 * t + b]);
               mma_commit(&s_empty[FB_NS * t + sb]);  // S/P buffer free once P V ran
             }
             __syncwarp();
@@ -1115,7 +1112,9 @@ __global__ void __launch_bounds__(FbSmem<NT>::THREADS, 2 / NT) k_window_attentio
         if (c > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           // rescale this warp's O rows once the previous chunk's P V landed
           const uint32_t jp = j - 1;
-          mbar_wait(&p_empty[2 * t + (jp & 1)], (jp >> 1) & 1);
+          // (the S buffer's release is committed after that P V; its next
+          // release needs P of chunk jp + FB_NS, not produced yet)
+          mbar_wait(&s_empty[FB_NS * t + jp % FB_NS], (jp / FB_NS) & 1);
           tc_fence_after();
           uint32_t o[32];
 #pragma unroll
