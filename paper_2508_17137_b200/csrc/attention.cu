@@ -1064,8 +1064,7 @@ __global__ void __launch_bounds__(FbSmem<NT>::THREADS, 2 / NT) k_window_attentio
       const int sb = jj % FB_NS;
       mbar_wait(&s_full[FB_NS * t + sb], (jj / FB_NS) & 1);
       tc_fence_after();
-      tmem_ld32(tq + 64 * sb, *reinterpret_cast<uint32_t(*)[32]>(r));
-      tmem_ld32(tq + 64 * sb + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+      tmem_ld64(tq + 64 * sb, r);
     };
     auto release_s = [&](uint32_t jj, uint32_t (&r)[64]) {  // S of chunk jj in registers
       tmem_ld_wait_regs(*reinterpret_cast<uint32_t(*)[32]>(r));
