@@ -360,7 +360,8 @@ int moeb_window_attention(const void* qkv, void* out, const int64_t* win_start,
                           int fp16, void* stream);
 
 /* Transformer input rows: out32[r] = ptok[token_ids[r / L]] + play[r % L]
- * (factorised input projection), out16 = 16-bit copy. Rows of 512. */
+ * (factorised input projection), out16 = 16-bit copy. Rows of 512. out32
+ * may be null (the 16-bit residual stream needs only out16). */
 int moeb_embed_rows(const float* ptok, const float* play, const int32_t* token_ids, int L,
                     int64_t rows, float* out32, void* out16, int fp16, void* stream);
 /* Post-norm LayerNorm of 512-wide rows: x32 = LN(x32; w, b, eps) in place,

@@ -208,16 +208,27 @@ class TransformerPredictor:
             e1.record()
             timing.setdefault(name, []).append((e0, e1, flops))
 
-        for lo, hi in self._chunks(packed):
-            sub = packed.select(lo, hi)
-            r0 = int(packed.row_off_host[lo])
-            M = sub.rows
-            ws, wl = windows_of(sub.row_off_host)
-            ws_d = torch.from_numpy(ws).to(dev)
-            wl_d = torch.from_numpy(wl).to(dev)
-            tok = sub.token_ids.contiguous()
+        # every chunk's windows in one pinned upload (a pageable copy per
+        # chunk would stall the launch stream)
+        chunks = list(self._chunks(packed))
+        roh = packed.row_off_host
+        wins = [windows_of(roh[lo:hi + 1] - roh[lo]) for lo, hi in chunks]
+        sizes = [len(ws) for ws, _ in wins]
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        ws_all = torch.from_numpy(np.concatenate([ws for ws, _ in wins])).pin_memory().to(
+            dev, non_blocking=True)
+        wl_all = torch.from_numpy(np.concatenate([wl for _, wl in wins])).pin_memory().to(
+            dev, non_blocking=True)
+        for ci, (lo, hi) in enumerate(chunks):
+            r0, r1 = int(roh[lo]), int(roh[hi])
+            M = r1 - r0
+            ws, wl = wins[ci]
+            ws_d = ws_all[offs[ci]:offs[ci + 1]]
+            wl_d = wl_all[offs[ci]:offs[ci + 1]]
+            tok = packed.token_ids[r0 // L:r1 // L]  # whole prompts: r0, r1 multiples of L
             nat.call("moeb_embed_rows", nat.ptr(W.ptok), nat.ptr(W.play), nat.ptr(tok), L, M,
-                     nat.ptr(h32), nat.ptr(h16), int(W.fp16), nat.stream_ptr())
+                     nat.ptr(None if self.resid16 else h32), nat.ptr(h16), int(W.fp16),
+                     nat.stream_ptr())
             att_flops = 4 * float(np.sum(wl.astype(np.float64) ** 2)) * D_MODEL
             for lay in W.layers:
                 timed("gemm_qkv", 2.0 * M * 3 * D_MODEL * D_MODEL, gemm, h16, lay["qkv"], M,
