@@ -93,8 +93,9 @@ def test_window_attention(tr, fp16, impl, spiky, monkeypatch):
     monkeypatch.setenv("MOEB_ATTN", impl[:2] if impl == "fb1" else impl)
     monkeypatch.setenv("MOEB_ATTN_NT", "1" if impl == "fb1" else "2")
     dt = torch.float16 if fp16 else torch.bfloat16
-    off = np.array([0, 700, 700 + 512, 700 + 512 + 37, 700 + 512 + 37 + 1100, 700 + 512 + 37 +
-                    1100 + 129, 700 + 512 + 37 + 1100 + 129 + 300])
+    # prompt lengths: windows of 512 and of 1, 37, 64, 65, 128, 129, 188, 300, 384, 385
+    lens = [700, 512, 37, 1100, 129, 300, 1, 64, 65, 128, 384, 385]
+    off = np.concatenate([[0], np.cumsum(lens)])
     ws, wl = tr.windows_of(off)
     rows = int(off[-1])
     g = torch.Generator(device="cuda").manual_seed(3)
