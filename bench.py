@@ -589,14 +589,16 @@ def run_ours(args):
                     "host_format": {
                         "packed-ranks": "combinatorial rank of each row's 6-expert set as a "
                                         "27-bit stream (3.375 B/row), decoded on device "
-                                        "(k_ranks_to_masks)",
+                                        "(k_ranks_to_masks_seeded)",
                         "ranks": "u32 combinatorial rank of each row's 6-expert set [rows], "
-                                 "decoded on device (k_ranks_to_masks)",
+                                 "decoded on device (k_ranks_to_masks_seeded)",
                         "ids": "u8 expert ids [rows][6], decoded on device (k_ids_to_masks)",
                         "masks": "int64 mask rows"}[args.e2e_format]},
-            # per chunk: K3 (k_linear_predict) + K7 (k_metrics64) + K1s (k_stack_replay)
-            # + K1 (k_cache_sim_warp over the prompts K1s left undecided)
-            "gpu_launches": 4 * len(pipe.bounds) * args.steps,
+            # per chunk and step: K3t (k_linear_tc_prep, k_linear_tc, k_linear_tc_refine,
+            # k_linear_rows_exact, the gated fp64 k_linear_predict, k_linear_tc_finalize),
+            # K1s (k_stack_replay) + K1 (k_cache_sim_warp over the prompts K1s left
+            # undecided), K7 (k_metrics64)
+            "gpu_launches": 9 * len(pipe.bounds) * args.steps,
             "pipeline": {"chunks": len(pipe.bounds), "streams": "predict || replay (|| H2D in e2e)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
