@@ -86,10 +86,15 @@ int moeb_device_check(void);
  *  workspace        [workspace_bytes] scratch, >= moeb_cache_sim_workspace_bytes
  *                   (n_preds, n_prompts) for the stack-distance replay K1s (its
  *                   undecided-prompt list); NULL / smaller -> every prompt is
- *                   replayed by the exact kernel (same results, slower)
+ *                   replayed by the exact kernel (same results, slower).
+ *                   >= moeb_cache_sim_workspace_bytes_shape(n_preds, n_prompts,
+ *                   L, E): also the LRU key -> queue-position tables of shapes
+ *                   with more than 8192 keys (V3: 58 x 256) in global memory,
+ *                   so that more simulations fit each SM (same results)
  *  Limit: every prompt has fewer than 2^31 - 64 rows (the caller checks).
  */
 size_t moeb_cache_sim_workspace_bytes(int n_preds, int n_prompts);
+size_t moeb_cache_sim_workspace_bytes_shape(int n_preds, int n_prompts, int L, int E);
 int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* preds,
                    const uint8_t* const* covered, const int32_t* unbounded, int n_preds,
                    const int64_t* prompt_row_off, int n_prompts, int L, int E,

@@ -114,6 +114,7 @@ _SIGS = {
 SIZE_QUERIES = {
     "moeb_linear_table_doubles": [I32, I32],
     "moeb_cache_sim_workspace_bytes": [I32, I32],
+    "moeb_cache_sim_workspace_bytes_shape": [I32, I32, I32, I32],
     "moeb_linear_workspace_bytes": [I64, I32, I32],
 }
 

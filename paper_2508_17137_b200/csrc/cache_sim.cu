@@ -72,6 +72,11 @@ struct SimArgs {
   // caller workspace (moeb_cache_sim_workspace_bytes), host-side use only
   void* ws;
   size_t ws_bytes;
+  // nullable: LRU key -> queue-position tables in global memory, [n_preds][P]
+  // [L*E] u16 (from the caller's workspace, moeb_cache_sim_workspace_bytes_shape)
+  // instead of shared memory, for shapes whose table would cap the resident
+  // simulations per SM (V3: 29.7 KB of a 39.6 KB state)
+  uint16_t* pos_g;
   // per-simulation shared-memory layout (bytes)
   int off_r, off_q, off_k, off_c, sim_bytes;
   uint32_t magic;  // layer_of(key) = (key * magic) >> 22
@@ -661,13 +666,13 @@ void layout(SimArgs& a, int policy, bool general) {
     uint32_t qn = 64;  // >= 2 * cap: compaction at most every cap pushes
     while (qn < 2 * a.cap + 32) qn <<= 1;
     a.qmask = qn - 1;
-    a.off_r = align16(2 * NK);  // pos_of
+    a.off_r = (a.pos_g && !general) ? 0 : align16(2 * NK);  // pos_of (unless in global memory)
     a.off_q = align16(a.off_r + rbytes);
     a.off_k = 0;
     a.sim_bytes = align16(a.off_q + 2LL * qn) + 16;  // +16 B skews smem banks
   } else {
     a.qmask = 0;
-    a.off_r = align16(2 * NK);  // slot_of
+    a.off_r = (a.pos_g && !general) ? 0 : align16(2 * NK);  // slot_of (unless in global memory)
     a.off_q = align16(a.off_r + rbytes);  // vals [cap] u64, skeys [cap] u16
     a.off_k = 0;
     a.sim_bytes = align16(a.off_q + 10LL * a.cap) + 16;
@@ -809,6 +814,10 @@ __global__ void __launch_bounds__(128) k_cache_sim_warp(const SimArgs a) {
     unsigned char* base = smem + a.off_c + (size_t)sl * a.sim_bytes;
     LruState<W, ES, false> st;
     st.init(base, a, L);  // every lane of the group holds the same state
+    // the key-position table of this (stream, prompt) in global memory: no
+    // initialisation needed (an entry is read only for a key pushed by this
+    // simulation, and every push writes it)
+    if (a.pos_g) st.pos_of = a.pos_g + ((int64_t)pi * a.P + p) * ((int64_t)L * E);
     uint16_t* pos_of = st.pos_of;
     uint16_t* q = st.q;
     uint64_t* R = st.R;
@@ -1147,7 +1156,10 @@ __global__ void __launch_bounds__(128) k_cache_sim_lfu_warp(const SimArgs a) {
   const int p = blockIdx.x * nw + wib;
   if (p < a.P) {
     unsigned char* base = smem + a.off_c + (size_t)wib * a.sim_bytes;
-    uint16_t* slot_of = reinterpret_cast<uint16_t*>(base);
+    // key -> slot: shared memory, or this simulation's table in global memory
+    // (read only for resident keys, written at their insert: no initialisation)
+    uint16_t* slot_of = a.pos_g ? a.pos_g + ((int64_t)pi * a.P + p) * ((int64_t)L * E)
+                                : reinterpret_cast<uint16_t*>(base);
     uint64_t* Rs = reinterpret_cast<uint64_t*>(base + a.off_r);
     uint64_t* vals = reinterpret_cast<uint64_t*>(base + a.off_q);
     uint16_t* skeys = reinterpret_cast<uint16_t*>(base + a.off_q + 8 * a.cap);
@@ -1395,6 +1407,19 @@ int launch_lfu_warp(SimArgs a, cudaStream_t s) {
   if (head + (int64_t)nw * a.sim_bytes > max_block)
     return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
                       a.sim_bytes, max_block);
+  {  // the block size that keeps the most simulations resident per SM
+    const int64_t sm = moeb::max_smem_per_sm();
+    int best = nw, best_sims = 0;
+    for (int w = nw; w >= 1; --w) {
+      const int64_t blocks =
+          std::min<int64_t>(sm / (head + (int64_t)w * a.sim_bytes + 1024), 64 / w);
+      if (blocks * w > best_sims) {
+        best_sims = (int)(blocks * w);
+        best = w;
+      }
+    }
+    nw = best;
+  }
   const size_t smem = head + (size_t)nw * a.sim_bytes;
   auto k = (a.hits || a.any_cov) ? k_cache_sim_lfu_warp<W, true> : k_cache_sim_lfu_warp<W, false>;
   moeb::set_smem(k, (int)smem);
@@ -1648,6 +1673,22 @@ template <int W, int ES, int G>
 int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
   int nw = 4;  // warps per block
   while (nw > 1 && head + (int64_t)nw * (32 / G) * a.sim_bytes > max_block) --nw;
+  {
+    // small states (the key-position table in global memory): the block size
+    // that keeps the most simulations resident per SM (blocks of 4 warps
+    // would strand up to a block's worth of shared memory)
+    const int64_t sm = moeb::max_smem_per_sm();
+    int best = nw, best_sims = 0;
+    for (int w = nw; w >= 1; --w) {
+      const int64_t per_block = head + (int64_t)w * (32 / G) * a.sim_bytes + 1024;
+      const int64_t blocks = std::min<int64_t>(sm / per_block, 64 / w);
+      if (blocks * w * (32 / G) > best_sims) {
+        best_sims = (int)(blocks * w * (32 / G));
+        best = w;
+      }
+    }
+    nw = best;
+  }
   if (head + (int64_t)nw * (32 / G) * a.sim_bytes > max_block) {
     if (head + (int64_t)a.sim_bytes > max_block)
       return moeb::fail(MOEB_ESMEM, "cache state %d B/sim exceeds %d B of shared memory",
@@ -1743,6 +1784,24 @@ extern "C" size_t moeb_cache_sim_workspace_bytes(int n_preds, int n_prompts) {
   return sizeof(int32_t) * ((size_t)n_preds * n_prompts + n_preds);
 }
 
+namespace {
+// keys above which the LRU key-position table goes to global memory: its
+// 2 B per key would otherwise leave fewer than ~8 simulations per SM
+constexpr int kGlobalPosKeys = 8192;
+size_t list_bytes_aligned(int n_preds, int n_prompts) {
+  return (moeb_cache_sim_workspace_bytes(n_preds, n_prompts) + 255) / 256 * 256;
+}
+size_t pos_table_bytes(int n_preds, int n_prompts, int L, int E) {
+  if ((int64_t)L * E <= kGlobalPosKeys) return 0;
+  return sizeof(uint16_t) * (size_t)n_preds * n_prompts * (size_t)L * E;
+}
+}  // namespace
+
+extern "C" size_t moeb_cache_sim_workspace_bytes_shape(int n_preds, int n_prompts, int L, int E) {
+  if (n_preds < 1 || n_prompts < 1 || L < 1 || E < 1) return 0;
+  return list_bytes_aligned(n_preds, n_prompts) + pos_table_bytes(n_preds, n_prompts, L, E);
+}
+
 extern "C" int moeb_cache_sim(const uint64_t* truth, const uint64_t* const* preds,
                               const uint8_t* const* covered, const int32_t* unbounded,
                               int n_preds, const int64_t* prompt_row_off, int n_prompts, int L,
@@ -1794,6 +1853,13 @@ extern "C" int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* con
   a.given = given_counts;
   a.ws = workspace;
   a.ws_bytes = workspace ? workspace_bytes : 0;
+  {
+    const size_t tb = pos_table_bytes(n_preds, n_prompts, L, E);
+    const size_t lb = list_bytes_aligned(n_preds, n_prompts);
+    const char* env = getenv("MOEB_K1_POS");  // "smem": keep the table in shared memory
+    if (tb && a.ws_bytes >= lb + tb && !(env && env[0] == 's'))
+      a.pos_g = reinterpret_cast<uint16_t*>(static_cast<unsigned char*>(workspace) + lb);
+  }
   const int nc = 4 + 3 * L;
   cudaStream_t s = moeb::as_stream(stream);
   for (int c = 0; c < n_caps; ++c) {

@@ -221,7 +221,7 @@ def cache_replay(packed: PackedTraces, streams, capacities, warmup: int, budget:
             per_prompt[:, rest] = sub_p
         return counters, per_prompt, hits
     lib = nat.load_library()
-    ws_bytes = lib.moeb_cache_sim_workspace_bytes(min(n, 16), P)
+    ws_bytes = lib.moeb_cache_sim_workspace_bytes_shape(min(n, 16), P, L, shape.num_experts)
     ws = nat.workspace(ws_bytes, dev)
     for lo in range(0, n, 16):
         chunk = streams[lo:lo + 16]
