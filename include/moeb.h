@@ -126,13 +126,21 @@ int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* const* preds,
  * (cache.py:93-154), and a touch hits iff it was prefetched in its row or
  * fewer than C distinct keys were accessed since its previous access.
  * Counters as moeb_cache_sim (+=), for n_caps <= 16 capacities in ascending order;
- * max_prompt_rows sizes the per-prompt shared-memory state.
+ * max_prompt_rows sizes the per-prompt shared-memory state. max_row_keys: an
+ * upper bound on the experts of any truth row (ModelShape.top_k for validated
+ * traces; 0 = unknown): with budget + max_row_keys <= 15 the per-row key
+ * counts are kept as 4-bit fields (half the shared memory, same results).
+ * workspace (nullable, >= moeb_cache_replay_stack_workspace_bytes(n_preds,
+ * n_prompts, L) bytes): the per-key last-access tables live there instead of
+ * in shared memory, so more prompts are replayed per SM (same results).
  */
+size_t moeb_cache_replay_stack_workspace_bytes(int n_preds, int n_prompts, int L);
 int moeb_cache_replay_stack(const uint64_t* truth, const uint64_t* const* preds,
                             const int32_t* unbounded, int n_preds, const int64_t* prompt_row_off,
                             int n_prompts, int L, int E, int warmup_tokens,
                             const int64_t* capacities, int n_caps, int budget,
-                            int64_t max_prompt_rows, int64_t* counters, int64_t* per_prompt,
+                            int64_t max_prompt_rows, int max_row_keys, int64_t* counters,
+                            int64_t* per_prompt, void* workspace, size_t workspace_bytes,
                             void* stream);
 
 /*

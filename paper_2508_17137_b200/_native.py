@@ -32,12 +32,13 @@ class NativeError(RuntimeError):
 
 
 P = ctypes.c_void_p
-I32, I64, DBL = ctypes.c_int, ctypes.c_int64, ctypes.c_double
+I32, I64, DBL, SZ = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
 
 _SIGS = {
     "moeb_cache_sim": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P, I64, P,
                        ctypes.c_size_t, P],
-    "moeb_cache_replay_stack": [P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I64, P, P, P],
+    "moeb_cache_replay_stack": [P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I64, I32, P, P,
+                                P, SZ, P],
     "moeb_cache_sim_counted": [P, P, P, P, I32, P, I32, I32, I32, I32, P, I32, I32, I32, P, P, P,
                                P, I64, P, ctypes.c_size_t, P],
     "moeb_cache_ops": [P, P, I64, I32, I32, I64, I32, P, P],
@@ -115,6 +116,7 @@ SIZE_QUERIES = {
     "moeb_linear_table_doubles": [I32, I32],
     "moeb_cache_sim_workspace_bytes": [I32, I32],
     "moeb_cache_sim_workspace_bytes_shape": [I32, I32, I32, I32],
+    "moeb_cache_replay_stack_workspace_bytes": [I32, I32, I32],
     "moeb_linear_workspace_bytes": [I64, I32, I32],
 }
 

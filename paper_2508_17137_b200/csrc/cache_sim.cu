@@ -1960,14 +1960,18 @@ struct MultiArgs {
   int off_cnt, off_blk, off_sup, off_ctr, warp_bytes;
   int64_t* counters;        // [n_preds][n_caps][4 + 3L]
   int64_t* per_prompt;      // nullable [n_preds][n_caps][P][4]
+  uint32_t* lr_g;           // nullable: lr tables [n_preds][P][L * 64] in global memory
 };
 
+// NIB: per-row counts as 4-bit fields (rows touch at most 15 keys: budget +
+// top-k <= 15, no unbounded stream), half the shared memory of u8 counts
+template <bool NIB>
 __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
   extern __shared__ __align__(16) unsigned char smem_m[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int si = blockIdx.y;
   unsigned char* base = smem_m + (size_t)warp * a.warp_bytes;
-  uint32_t* lr = reinterpret_cast<uint32_t*>(base);
+  uint32_t* lr = reinterpret_cast<uint32_t*>(base);  // or per prompt in global memory
   uint32_t* cnt32 = reinterpret_cast<uint32_t*>(base + a.off_cnt);
   uint32_t* blk32 = reinterpret_cast<uint32_t*>(base + a.off_blk);  // u16 block sums
   const uint16_t* blk = reinterpret_cast<const uint16_t*>(blk32);
@@ -1998,16 +2002,20 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
     const int64_t r0 = a.row_off[p];
     const int R = (int)(a.row_off[p + 1] - r0);
     const int nblk = (R + 31) >> 5, nsup = (R + 1023) >> 10;
+    if (a.lr_g) lr = a.lr_g + ((int64_t)si * a.P + p) * (L * 64);
     for (int i = lane; i < L * 64; i += 32) lr[i] = kNever;
     // zeroed over whole 32-row blocks / 1024-row super blocks: the suffix
     // sums read those spans without bounds tests
-    for (int i = lane; i < nblk * 8; i += 32) cnt32[i] = 0u;
+    for (int i = lane; i < nblk * (NIB ? 4 : 8); i += 32) cnt32[i] = 0u;
     for (int i = lane; i < nsup * 16; i += 32) blk32[i] = 0u;
     for (int i = lane; i < nsup; i += 32) sup[i] = 0u;
     for (int i = lane; i <= C; i += 32) pph[i] = 0u;
     __syncwarp();
     const unsigned char* cnt = reinterpret_cast<const unsigned char*>(cnt32);
     int64_t pp_acc = 0, pp_ph = 0;
+    // the next row's layer entries, loaded one row ahead (with L > 1 a row
+    // never changes another layer's entries; L == 1 reloads after the update)
+    uint32_t nv0 = lr[lane], nv1 = lr[32 + lane];
     for (int rb = 0; rb < R; rb += 32) {
       // this batch's rows, one per lane
       const int rl = rb + lane;
@@ -2029,7 +2037,12 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
           K = pm & ~rest;
         }
         const uint64_t A = K | x;
-        const uint32_t v0 = lr[l * 64 + lane], v1 = lr[l * 64 + 32 + lane];
+        const uint32_t v0 = nv0, v1 = nv1;
+        if (L > 1) {
+          const int ln = l + 1 == L ? 0 : l + 1;
+          nv0 = lr[ln * 64 + lane];
+          nv1 = lr[ln * 64 + 32 + lane];
+        }
         // touches not prefetched in this row
         uint64_t miss = x & ~K;
         uint32_t hist0 = (uint32_t)__popcll(x & K);  // h = 0: hit at every capacity
@@ -2047,7 +2060,9 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
             const int rho = (rx & ~31) + lane;
             const int b = ((rx >> 10) << 5) + lane;
             const int sidx = (rx >> 10) + 1 + lane;
-            uint32_t part = rho > rx ? cnt[rho] : 0u;
+            uint32_t part = rho > rx ? (NIB ? (cnt32[rho >> 3] >> (4 * (rho & 7))) & 15u
+                                            : (uint32_t)cnt[rho])
+                                     : 0u;
             part += b > (rx >> 5) ? (uint32_t)blk[b] : 0u;
             part += sidx < nsup ? sup[sidx] : 0u;
             // layer-l keys: counted in the suffix (row > rx) / after x in row rx
@@ -2093,7 +2108,10 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
             const uint32_t old = hh ? v1 : v0;
             if (old != kNever) {
               const int ro = (int)(old >> 7);
-              atomicSub(&cnt32[ro >> 2], 1u << (8 * (ro & 3)));
+              if (NIB)
+                atomicSub(&cnt32[ro >> 3], 1u << (4 * (ro & 7)));
+              else
+                atomicSub(&cnt32[ro >> 2], 1u << (8 * (ro & 3)));
               atomicSub(&blk32[ro >> 6], 1u << (16 * ((ro >> 5) & 1)));
               atomicSub(&sup[ro >> 10], 1u);
             }
@@ -2102,11 +2120,18 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
         }
         if (lane == 0) {
           const uint32_t n = (uint32_t)__popcll(A);
-          atomicAdd(&cnt32[rr >> 2], n << (8 * (rr & 3)));
+          if (NIB)
+            atomicAdd(&cnt32[rr >> 3], n << (4 * (rr & 7)));
+          else
+            atomicAdd(&cnt32[rr >> 2], n << (8 * (rr & 3)));
           atomicAdd(&blk32[rr >> 6], n << (16 * ((rr >> 5) & 1)));
           atomicAdd(&sup[rr >> 10], n);
         }
         __syncwarp();
+        if (L == 1) {
+          nv0 = lr[lane];
+          nv1 = lr[32 + lane];
+        }
       }
     }
     if (a.per_prompt && lane == 0) {
@@ -2148,12 +2173,18 @@ __global__ void __launch_bounds__(128) k_stack_multi(const MultiArgs a) {
 
 }  // namespace
 
+extern "C" size_t moeb_cache_replay_stack_workspace_bytes(int n_preds, int n_prompts, int L) {
+  if (n_preds < 1 || n_prompts < 1 || L < 1) return 0;
+  return sizeof(uint32_t) * (size_t)n_preds * n_prompts * (size_t)L * 64;
+}
+
 extern "C" int moeb_cache_replay_stack(const uint64_t* truth, const uint64_t* const* preds,
                                        const int32_t* unbounded, int n_preds,
                                        const int64_t* prompt_row_off, int n_prompts, int L, int E,
                                        int warmup_tokens, const int64_t* capacities, int n_caps,
-                                       int budget, int64_t max_prompt_rows, int64_t* counters,
-                                       int64_t* per_prompt, void* stream) {
+                                       int budget, int64_t max_prompt_rows, int max_row_keys,
+                                       int64_t* counters, int64_t* per_prompt, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
   moeb::clear_error();
   MOEB_REQUIRE(truth && prompt_row_off && counters && capacities, "null argument");
   MOEB_REQUIRE(n_preds >= 1 && n_preds <= MOEB_MAX_PREDS, "n_preds must be in [1, %d]",
@@ -2192,8 +2223,15 @@ extern "C" int moeb_cache_replay_stack(const uint64_t* truth, const uint64_t* co
   a.n_caps = n_caps;
   a.rmax = (int)max_prompt_rows;
   const int R = a.rmax + 1;
-  a.off_cnt = align16(4LL * L * 64);
-  a.off_blk = a.off_cnt + align16((R + 31) / 32 * 32);
+  const char* env = getenv("MOEB_K1M_LR");  // "smem": keep the lr tables in shared memory
+  if (workspace && workspace_bytes >= moeb_cache_replay_stack_workspace_bytes(n_preds, n_prompts, L) &&
+      !(env && env[0] == 's'))
+    a.lr_g = static_cast<uint32_t*>(workspace);
+  a.off_cnt = a.lr_g ? 0 : align16(4LL * L * 64);
+  // 4-bit row counts when no row can touch more than 15 keys
+  const char* nenv = getenv("MOEB_K1M_NIB");  // "0": u8 counts
+  const bool nib = max_row_keys > 0 && kmax + max_row_keys <= 15 && !(nenv && nenv[0] == '0');
+  a.off_blk = a.off_cnt + align16((R + 31) / 32 * (nib ? 16 : 32));
   a.off_sup = a.off_blk + align16(2LL * 32 * ((R + 1023) / 1024));
   a.off_ctr = a.off_sup + align16(4LL * ((R + 1023) / 1024 + 1));
   a.warp_bytes = a.off_ctr + align16(4LL * (2 * L + L * (n_caps + 1) + n_caps + 1));
@@ -2207,12 +2245,13 @@ extern "C" int moeb_cache_replay_stack(const uint64_t* truth, const uint64_t* co
     return moeb::fail(MOEB_ESMEM, "stack replay state %d B/prompt exceeds shared memory",
                       a.warp_bytes);
   const size_t smem = (size_t)nw * a.warp_bytes + align16(L * 64 + 1);
-  moeb::set_smem(k_stack_multi, (int)smem);
+  auto kern = nib ? k_stack_multi<true> : k_stack_multi<false>;
+  moeb::set_smem(kern, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stack_multi, 32 * nw, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * nw, smem);
   const int64_t want = (n_prompts + nw - 1) / nw;
   const int64_t cap = (int64_t)(per_sm > 0 ? per_sm : 1) * moeb::num_sms();
   const unsigned gx = (unsigned)(want < cap ? want : cap);
-  k_stack_multi<<<dim3(gx, (unsigned)n_preds), 32 * nw, smem, moeb::as_stream(stream)>>>(a);
+  kern<<<dim3(gx, (unsigned)n_preds), 32 * nw, smem, moeb::as_stream(stream)>>>(a);
   return moeb::check_launch("k_stack_multi");
 }

@@ -157,6 +157,11 @@ def _stack_multi(packed, streams, capacities, idx, warmup, budget, counters, per
     L = shape.num_layers
     rmax = int(np.max(np.diff(packed.row_off_host)))
     idx = sorted(idx, key=lambda j: capacities[j])  # the kernel takes ascending capacities
+    # the per-key last-access tables in caller-owned global memory (more
+    # prompts resident per SM than with them in shared memory)
+    ws_bytes = nat.load_library().moeb_cache_replay_stack_workspace_bytes(
+        len(streams), packed.num_prompts, L)
+    ws = nat.workspace(ws_bytes, packed.device)
     for g in range(0, len(idx), 16):
         sel = idx[g:g + 16]
         sc = torch.zeros((len(streams), len(sel), 4 + 3 * L), dtype=torch.int64,
@@ -168,7 +173,7 @@ def _stack_multi(packed, streams, capacities, idx, warmup, budget, counters, per
                  nat.i32_array([int(bool(u)) for _, _, u in streams]), len(streams),
                  nat.ptr(packed.row_off), packed.num_prompts, L, shape.num_experts, int(warmup),
                  nat.i64_array([capacities[j] for j in sel]), len(sel), int(budget), rmax,
-                 nat.ptr(sc), nat.ptr(sp), nat.stream_ptr())
+                 shape.top_k, nat.ptr(sc), nat.ptr(sp), nat.ptr(ws), ws_bytes, nat.stream_ptr())
         counters[:, sel] += sc
         if per_prompt is not None:
             per_prompt[:, sel] += sp
