@@ -1757,6 +1757,13 @@ int launch_lru_g(SimArgs a, cudaStream_t s, int head, int max_block) {
 template <int W>
 int launch_sim(SimArgs a, int policy, cudaStream_t s) {
   const int max_block = moeb::max_smem_per_block();
+  if (policy == MOEB_POLICY_LFU && a.pos_g) {
+    const char* env = getenv("MOEB_LFU_KERNEL");
+    if (env && env[0] == 't') {  // the thread-per-simulation kernel keeps its tables in shared memory
+      a.pos_g = nullptr;
+      layout(a, policy, false);
+    }
+  }
   const int head = align16(4LL * 3 * a.L);  // block counters
   a.off_c = head;
   if (a.magic == 0) return moeb::fail(MOEB_EINVAL, "layer magic failed for E=%d", a.E);

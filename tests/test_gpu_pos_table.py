@@ -44,7 +44,7 @@ def test_global_position_table_equals_shared(policy, ragged, warmup, monkeypatch
     assert lib.moeb_cache_sim_workspace_bytes_shape(2, 30, L, E) >= 2 * 30 * L * E * 2
     assert lib.moeb_cache_sim_workspace_bytes_shape(2, 30, 26, 64) == \
         (lib.moeb_cache_sim_workspace_bytes(2, 30) + 255) // 256 * 256
-    packed = _packed(m, shape, 30, 40, 11, ragged)
+    packed = _packed(m, shape, 16, 32, 11, ragged)
     rows, W = packed.rows, shape.mask_words
     rng = np.random.default_rng(5)
     sparse = rng.integers(0, 2**63 - 1, (rows, W), dtype=np.int64)
