@@ -22,6 +22,7 @@ cap() {  # regex name skip
 cap "^k_linear_tc$" k3t 1
 cap "k_stack_replay" k1s 1
 cap "k_ranks_to_masks" ranks 1
+cap "k_metrics64" k7 1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_eam_predict_tok -c 1 \
   -o gpurun_out/prof_${TAG}_k6 python tools/k6_probe.py 2000 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_stack_multi -c 1 \
