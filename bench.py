@@ -273,7 +273,9 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    pipe = m.PipelinedReplay(packed, args.chunks)
+    # --overlap-steps: step i+1's predictor runs while step i's replay and
+    # metrics finish (two mask buffers; the timed region ends after a join)
+    pipe = m.PipelinedReplay(packed, args.chunks, overlap_steps=args.overlap_steps)
 
     def step(timing=None):
         vec = m.metrics.metric_vector(E, dev)
@@ -282,10 +284,21 @@ def run_ours(args):
         counters = pipe.run(pred, [cap], WARMUP_TOKENS, BUDGET, metrics=vec, timing=timing,
                             per_prompt=True)
         if world > 1:
-            buf = torch.cat([counters.view(-1), vec])
-            dist.all_reduce(buf)
-            counters, vec = buf[:counters.numel()].view(counters.shape), buf[counters.numel():]
+            # the counter reduce (NCCL) waits on this step's replay and metrics
+            # streams only, so overlapped steps keep overlapping
+            s_comm.wait_stream(pipe.s_sim)
+            s_comm.wait_stream(pipe.s_met)
+            s_comm.wait_stream(stream)
+            with torch.cuda.stream(s_comm):
+                buf = torch.cat([counters.view(-1), vec])
+                dist.all_reduce(buf)
+                counters = buf[:counters.numel()].view(counters.shape)
+                vec = buf[counters.numel():]
+            if not pipe.overlap:
+                stream.wait_stream(s_comm)
         return counters, vec
+
+    s_comm = torch.cuda.Stream(dev)
 
     # --- warm-up ---
     # The clock sampler (an nvidia-smi process) starts before the warm-up so
@@ -315,6 +328,8 @@ def run_ours(args):
         start.record(stream)
         for _ in range(args.steps):
             counters, vec = step(timing)
+        pipe.join()
+        stream.wait_stream(s_comm)
         end.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -342,6 +357,41 @@ def run_ours(args):
 
     c = counters[0, 0].cpu().numpy()
     mc = m.MetricCounts.from_vector(vec.cpu().numpy(), E)
+
+    # --- the same steps issued as a stream of batches: step i+1's predictor
+    # (K3t) beside step i's replay and metrics (two mask buffers), the last
+    # step joined before the end event. Reported beside the headline, whose
+    # per-kernel times stay attributable (K3t slows from 4.0 to ~4.8 ms when
+    # it shares the SMs with K1s).
+    pipelined = None
+    if not pipe.overlap:
+        pipe2 = m.PipelinedReplay(packed, args.chunks, overlap_steps=True)
+        for _ in range(max(3, args.warmup)):
+            pipe2.run(pred, [cap], WARMUP_TOKENS, BUDGET, metrics=m.metrics.metric_vector(E, dev),
+                      per_prompt=True)
+        pipe2.join()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s3, t3 = ev(), ev()
+        s3.record(stream)
+        for _ in range(args.steps):
+            c3 = pipe2.run(pred, [cap], WARMUP_TOKENS, BUDGET,
+                           metrics=m.metrics.metric_vector(E, dev), per_prompt=True)
+        pipe2.join()
+        t3.record(stream)
+        torch.cuda.synchronize()
+        ms3 = s3.elapsed_time(t3)
+        if world > 1:
+            t = torch.tensor([ms3], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms3 = float(t.item())
+        if world == 1:  # (with more ranks c holds the reduced counters)
+            assert np.array_equal(c3[0, 0].cpu().numpy(), c), "pipelined steps changed the counters"
+        pipelined = {"value": tokens_per_rank * world / (ms3 / 1000.0) * args.steps,
+                     "ms_per_step": ms3 / args.steps,
+                     "how": "step i+1's K3t beside step i's K1s + K7 (two mask buffers)"}
+        del pipe2
 
     # --- end to end through the public API with host buffers ---
     # StreamingReplay: every step copies its pinned host trace rows to the
@@ -599,7 +649,9 @@ def run_ours(args):
             # K1s (k_stack_replay) + K1 (k_cache_sim_warp over the prompts K1s left
             # undecided), K7 (k_metrics64)
             "gpu_launches": 9 * len(pipe.bounds) * args.steps,
-            "pipeline": {"chunks": len(pipe.bounds), "streams": "predict || replay (|| H2D in e2e)"},
+            "pipeline": {"chunks": len(pipe.bounds), "streams": "predict || replay (|| H2D in e2e)",
+                         "overlap_steps": pipe.overlap},
+            "pipelined_steps": pipelined,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": traffic,
@@ -635,6 +687,8 @@ def main():
                     help="host batch format of the end-to-end run: combinatorial ranks as a "
                          "27-bit stream (3.4 B/row) or as u32 (4 B/row), u8 expert ids "
                          "(6 B/row), all decoded on device, or the 8-byte mask rows")
+    ap.add_argument("--overlap-steps", action="store_true",
+                    help="overlap step i+1's predictor with step i's replay")
     ap.add_argument("--chunks", type=int, default=1,
                     help="prompt chunks pipelined across the predict / replay streams")
     ap.add_argument("--no-cpu-baseline", action="store_true")

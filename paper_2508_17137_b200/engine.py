@@ -333,8 +333,18 @@ class PipelinedReplay:
     otherwise serialise the streams).
     """
 
-    def __init__(self, packed: PackedTraces, chunks: int = 4):
+    def __init__(self, packed: PackedTraces, chunks: int = 4, overlap_steps: bool = False):
+        """``overlap_steps``: consecutive ``run`` calls overlap -- call i+1's
+        predictor runs while call i's replay and metrics finish (two mask
+        buffers used alternately; the predictor stream has the highest
+        priority so its persistent kernel is placed first and the replay fills
+        the resources it leaves). ``run`` then returns without ordering the
+        caller's stream after the work: call ``join()`` before reading any
+        result."""
         self.packed = packed
+        self.overlap = bool(overlap_steps)
+        self._slot = 0
+        self._slot_done = {}
         P = packed.num_prompts
         chunks = max(1, min(int(chunks), P))
         targets = np.arange(1, chunks) * (packed.rows / chunks)
@@ -346,7 +356,7 @@ class PipelinedReplay:
         dev = packed.device
         self._mbufs = {}  # persistent masks per chunk (predictors with out=)
         self.s_copy = torch.cuda.Stream(dev)
-        self.s_pred = torch.cuda.Stream(dev)
+        self.s_pred = torch.cuda.Stream(dev, priority=-2 if self.overlap else 0)
         self.s_sim = torch.cuda.Stream(dev, priority=-1)
         self.s_met = torch.cuda.Stream(dev, priority=0)
 
@@ -377,6 +387,13 @@ class PipelinedReplay:
                                    dtype=torch.int64, device=packed.device)
         for s in (self.s_copy, self.s_pred, self.s_sim, self.s_met):
             s.wait_stream(main)
+        slot = self._slot
+        if self.overlap:
+            # this slot's mask buffers were last read by the replay / metrics
+            # of the call before the previous one
+            for done in self._slot_done.get(slot, ()):
+                self.s_pred.wait_event(done)
+            self._slot ^= 1
         unbounded = bool(getattr(predictor, "unbounded_prefetch", False))
         pps = []
         for ci, ((a, b), view) in enumerate(zip(self.bounds, self.views)):
@@ -397,7 +414,7 @@ class PipelinedReplay:
                         e0.record(self.s_pred)
                     gc = _counts_buffer(predictor, shape, packed.device)
                     masks = predictor.predict_masks(view, budget, warmup, **_counts_kw(gc),
-                                                    **_out_kw(predictor, self._mbufs, ci, view))
+                                                    **_out_kw(predictor, self._mbufs, (slot, ci), view))
                     if ev:
                         e1.record(self.s_pred)
                         timing.append(("predict", e0, e1, view.rows))
@@ -428,13 +445,24 @@ class PipelinedReplay:
             with torch.cuda.stream(self.s_sim):
                 self.last_per_prompt = pps[0] if len(pps) == 1 else torch.cat(pps, dim=2)
             self.last_per_prompt.record_stream(self.s_sim)
-        main.wait_stream(self.s_sim)
-        main.wait_stream(self.s_pred)
-        main.wait_stream(self.s_met)
+        if self.overlap:
+            done = (torch.cuda.Event(), torch.cuda.Event())
+            done[0].record(self.s_sim)
+            done[1].record(self.s_met)
+            self._slot_done[slot] = done
+        else:
+            self.join()
         counters.record_stream(self.s_sim)
         if metrics is not None:
             metrics.record_stream(self.s_met)
         return counters
+
+    def join(self):
+        """Order the caller's stream after every launched call."""
+        main = torch.cuda.current_stream(self.packed.device)
+        main.wait_stream(self.s_sim)
+        main.wait_stream(self.s_pred)
+        main.wait_stream(self.s_met)
 
 
 def _counts_buffer(predictor, shape, device):
@@ -520,6 +548,11 @@ class StreamingReplay:
         self.s_copy = torch.cuda.Stream(dev)
         self.s_dec = torch.cuda.Stream(dev)
         self.s_comp = torch.cuda.Stream(dev, priority=-1)
+        # MOEB_STREAM_OVERLAP=1: batch i's replay on its own stream, beside
+        # batch i+1's predictor (measured: no end-to-end gain -- the batch
+        # decode and the predictor already fill the GPU -- so off by default)
+        self.s_rep = (torch.cuda.Stream(dev, priority=-1)
+                      if os.environ.get("MOEB_STREAM_OVERLAP") == "1" else self.s_comp)
         self.s_met = torch.cuda.Stream(dev, priority=0)
         self.device = dev
         P = len(prompt_ids)
@@ -540,6 +573,7 @@ class StreamingReplay:
         self.s_copy.wait_stream(main)
         self.s_dec.wait_stream(main)
         self.s_comp.wait_stream(main)
+        self.s_rep.wait_stream(main)
         self.s_met.wait_stream(main)
         copied = [torch.cuda.Event() for _ in range(self.NBUF)]
         freed = [None] * self.NBUF
@@ -637,11 +671,16 @@ class StreamingReplay:
                     cov = predictor.coverage(buf)
                 masks_ready = torch.cuda.Event()
                 masks_ready.record(self.s_comp)
+            for t in (masks, cov, gc):
+                if t is not None:
+                    t.record_stream(self.s_rep)
+            self.s_rep.wait_event(masks_ready)
+            with torch.cuda.stream(self.s_rep):
                 cnt, pp, _ = cache_replay(buf, [(masks, cov, unbounded)], capacities, warmup,
                                           budget, policy, want_per_prompt=per_prompt,
                                           given_counts=gc)
                 ev = torch.cuda.Event()
-                ev.record(self.s_comp)
+                ev.record(self.s_rep)
                 c_h, v_h, p_h = outs[i]
                 c_h.copy_(cnt[0], non_blocking=True)
                 if per_prompt:
@@ -660,10 +699,11 @@ class StreamingReplay:
                 freed[b] = (ev, met_ev)
                 if timing is not None:
                     e1 = torch.cuda.Event(enable_timing=True)
-                    e1.record(self.s_comp)
+                    e1.record(self.s_rep)
                     timing.append((e0, e1))
                 out.append((c_h, v_h, p_h) if per_prompt else (c_h, v_h))
         main.wait_stream(self.s_comp)
+        main.wait_stream(self.s_rep)
         main.wait_stream(self.s_copy)
         main.wait_stream(self.s_dec)
         main.wait_stream(self.s_met)

@@ -323,6 +323,18 @@ def test_pipelined_replay_matches_single_call(pkg, chunks):
     want3, _, _ = pkg.cache_replay(packed, [(None, None, False)], [166], 8, 6, policy="lfu",
                                    want_per_prompt=False)
     assert torch.equal(pipe.run(lru, [166], 8, 6, policy="lfu"), want3)
+    # overlapped steps (step i+1's predictor beside step i's replay, two mask
+    # buffers): every step's counters, metrics and per-prompt counters equal
+    want_pp = pkg.cache_replay(packed, [(masks, None, False)], [40, 166], 8, 6)[1]
+    pipe3 = pkg.PipelinedReplay(packed, chunks, overlap_steps=True)
+    outs = []
+    for _ in range(5):
+        v = pkg.metrics.metric_vector(64, packed.device)
+        outs.append((pipe3.run(pred, [40, 166], 8, 6, metrics=v, per_prompt=True), v,
+                     pipe3.last_per_prompt))
+    pipe3.join()
+    for c, v, pp in outs:
+        assert torch.equal(c, want) and torch.equal(v, vec) and torch.equal(pp, want_pp)
 
 
 @pytest.mark.parametrize("L,E,budget,decay", [(5, 64, 6, 0.0), (3, 40, 5, 0.5), (4, 64, 1, 0.0),
