@@ -310,11 +310,19 @@ def run_ours(args):
     clocks = ClockSampler(torch.cuda.current_device()).__enter__()
     t_w = time.perf_counter()
     n_w = 0
-    while n_w < args.warmup or time.perf_counter() - t_w < 2.0:
+    while True:
         counters, vec = step()
         n_w += 1
         if n_w % 8 == 0:
             torch.cuda.synchronize()
+        done = n_w >= args.warmup and time.perf_counter() - t_w >= 2.0
+        if world > 1:  # every rank runs the same number of steps (each has collectives)
+            flag = torch.tensor([0 if done else 1], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            done = int(flag.item()) == 0
+        if done:
+            break
+    pipe.join()
     torch.cuda.synchronize()
 
     # --- timed region: device clock, max over ranks ---
@@ -492,13 +500,18 @@ def run_ours(args):
     # it (tests/golden/c2_sample256.npz, made by tests/golden/make_c2_golden.py)
     parity = None
     gpath = os.path.join(ROOT, "tests", "golden", "c2_sample256.npz")
-    if rank == 0 and P >= 256 and os.path.exists(gpath):
+    if P >= 256 and os.path.exists(gpath):
         g = np.load(gpath)
         j = [int(x) for x in g["capacities"]].index(cap)
         cfg = m.ReplayConfig(shape, m.CacheConfig(capacity_fraction=CAP_FRACTION,
                                                   prefetch_budget=BUDGET),
                              warmup_tokens=WARMUP_TOKENS)
-        sample = packed.select(0, 256)
+        # every rank calls the drop-in replay_traces on the same sample (prompts
+        # 0..255): with a process group it shards the prompts over the ranks
+        # and all-reduces the counters (distributed.replay_sharded)
+        sample = packed.select(0, 256) if rank == 0 else m.generate_packed(
+            m.GeneratorConfig(256, C2["tokens"], shape, C2["hot"], C2["skew"], C2["seed"],
+                              first_prompt_id=0), dev)
         rep = m.replay_traces(sample, pred, cfg)
         got = np.concatenate([[rep.measured_accesses, rep.cache_hits, rep.prediction_hits,
                                rep.uncovered_queries], rep.layer_accesses,
@@ -676,6 +689,9 @@ def run_ours(args):
 
 
 def main():
+    if os.environ.get("MOEB_BENCH_STACKS"):  # diagnosis: dump every thread's stack after N s
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["MOEB_BENCH_STACKS"]), exit=False)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
