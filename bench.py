@@ -407,24 +407,32 @@ def run_ours(args):
     # i's compute) and reads its counters + metrics back to pinned host
     # memory; all inside the timed region. Host batches in a compact wire
     # format decoded into masks on the device after the copy: by default each
-    # row's combinatorial rank (u32, 4 B/row: 264 MB per step), or its k
-    # expert ids as u8 (--e2e-format ids, 6 B/row, 396 MB), or the 8-byte
-    # masks (--e2e-format masks, 528 MB).
+    # row's 6 expert ids at 6 bits (--e2e-format ids6, 4.5 B/row: 297 MB per
+    # step, a shift decode of 0.32 ms), or its combinatorial rank as a 27-bit
+    # stream (packed-ranks, 3.375 B/row, 223 MB, a digit-search decode of
+    # 0.68 ms on the SMs the predictor needs: 429 M vs 449 M trace tok/s end
+    # to end), sorted id pairs in 11 bits (idpairs, 4.125 B/row, 0.43 ms
+    # decode: 429 M), u32 ranks, u8 ids (6 B/row) or the 8-byte masks.
     if args.e2e_format == "packed-ranks":
         truth_host = m.masks_to_ranks(packed.truth, C2["top_k"], E, packed=True).cpu().pin_memory()
     elif args.e2e_format == "ranks":
         truth_host = m.masks_to_ranks(packed.truth, C2["top_k"], E).cpu().pin_memory()
     elif args.e2e_format == "ids":
         truth_host = m.masks_to_ids(packed.truth, C2["top_k"]).cpu().pin_memory()
+    elif args.e2e_format == "ids6":
+        truth_host = m.masks_to_ids6(packed.truth, C2["top_k"]).cpu().pin_memory()
+    elif args.e2e_format == "idpairs":
+        truth_host = m.masks_to_idpairs(packed.truth, C2["top_k"]).cpu().pin_memory()
     else:
         truth_host = packed.truth.cpu().pin_memory()
+    wire = args.e2e_format if args.e2e_format in ("ids6", "idpairs") else None
     sr = m.StreamingReplay(shape, packed.row_off_host, packed.prompt_ids, dev)
     h2d = truth_host.numel() * truth_host.element_size()
     d2h = (4 + 3 * L) * 8 + (3 * E + 3) * 8 + P * 4 * 8  # counters, metrics, per-prompt
 
     def e2e_run(n):
         res = sr.run(pred, [cap], WARMUP_TOKENS, BUDGET, [truth_host] * n, metrics=True,
-                     per_prompt=True)
+                     per_prompt=True, wire=wire)
         if world > 1:
             torch.cuda.synchronize()
             buf = torch.cat([torch.cat([c.view(-1), v]) for c, v, _ in res]).to(dev)
@@ -455,6 +463,7 @@ def run_ours(args):
         s3 = ev()
         s3.record(stream)
         sr.run(pred, [cap], WARMUP_TOKENS, BUDGET, [truth_host] * args.steps, metrics=True,
+               wire=wire,
                timing=tl)
         torch.cuda.synchronize()
         print("e2e batches (start ms, compute ms):",
@@ -656,6 +665,12 @@ def run_ours(args):
                         "ranks": "u32 combinatorial rank of each row's 6-expert set [rows], "
                                  "decoded on device (k_ranks_to_masks_seeded)",
                         "ids": "u8 expert ids [rows][6], decoded on device (k_ids_to_masks)",
+                        "ids6": "each row's 6 ascending expert ids at 6 bits as a 36-bit "
+                                "stream (4.5 B/row), decoded on device (k_ids6_to_masks)",
+                        "idpairs": "each row's 6 ascending expert ids as 3 sorted pairs, a "
+                                   "pair (a < b) as C(b, 2) + a in 11 bits: a 33-bit stream "
+                                   "(4.125 B/row), decoded on device by table lookups "
+                                   "(k_idpairs_to_masks)",
                         "masks": "int64 mask rows"}[args.e2e_format]},
             # per chunk and step: K3t (k_linear_tc_prep, k_linear_tc, k_linear_tc_refine,
             # k_linear_rows_exact, the gated fp64 k_linear_predict, k_linear_tc_finalize),
@@ -698,10 +713,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--prompts", type=int, default=C2["prompts"])
-    ap.add_argument("--e2e-format", choices=["packed-ranks", "ranks", "ids", "masks"],
-                    default="packed-ranks",
-                    help="host batch format of the end-to-end run: combinatorial ranks as a "
-                         "27-bit stream (3.4 B/row) or as u32 (4 B/row), u8 expert ids "
+    ap.add_argument("--e2e-format", choices=["packed-ranks", "idpairs", "ranks", "ids6", "ids",
+                                             "masks"],
+                    default="ids6",
+                    help="host batch format of the end-to-end run: 6-bit expert ids (4.5 B/row), "
+                         "combinatorial ranks as a 27-bit stream (3.4 B/row) or as u32 "
+                         "(4 B/row), 11-bit sorted id pairs (4.1 B/row), u8 expert ids "
                          "(6 B/row), all decoded on device, or the 8-byte mask rows")
     ap.add_argument("--overlap-steps", action="store_true",
                     help="overlap step i+1's predictor with step i's replay")

@@ -272,6 +272,24 @@ int moeb_packed_ranks_to_masks(const uint32_t* words, int64_t rows, int bits, in
                                uint64_t* masks, int* bad, void* stream);
 int moeb_masks_to_packed_ranks(const uint64_t* masks, int64_t rows, int k, int E, int bits,
                                uint32_t* words, int* bad, void* stream);
+/* Packed expert ids: each row's k ascending ids at 6 bits (E <= 64) in a
+ * little-endian bit stream, row r in bits [6 k r, 6 k (r + 1)): 4.5 B per row
+ * at k = 6, decoded with shifts (`words`: ceil(6 k rows / 32) + 2 u32, zeroed
+ * by the caller for the encoder). *bad = 1 if a row does not hold exactly k
+ * distinct experts. Host wire format of the end-to-end replay (no reference
+ * counterpart: the reference reads rows from CSV, traceio.py:47-106). */
+int moeb_ids6_to_masks(const uint32_t* words, int64_t rows, int k, uint64_t* masks, int* bad,
+                       void* stream);
+int moeb_masks_to_ids6(const uint64_t* masks, int64_t rows, int k, uint32_t* words, int* bad,
+                       void* stream);
+/* Packed id pairs: the k ascending ids two at a time, each sorted pair
+ * (a < b) as C(b, 2) + a in 11 bits (an odd k's last id in 6 bits): 33 bits
+ * per row at k = 6, decoded by table lookups. Same stream layout and error
+ * behaviour as the packed ids above (bits per row = 11 (k / 2) + 6 (k % 2)). */
+int moeb_idpairs_to_masks(const uint32_t* words, int64_t rows, int k, uint64_t* masks, int* bad,
+                          void* stream);
+int moeb_masks_to_idpairs(const uint64_t* masks, int64_t rows, int k, uint32_t* words, int* bad,
+                          void* stream);
 
 /*
  * Rule-based predictors as mask tables (predictors.py:57-139).

@@ -50,6 +50,10 @@ _SIGS = {
     "moeb_ranks_to_masks": [P, I64, I32, I32, P, P, P],
     "moeb_masks_to_ranks": [P, I64, I32, I32, P, P, P],
     "moeb_packed_ranks_to_masks": [P, I64, I32, I32, I32, P, P, P],
+    "moeb_ids6_to_masks": [P, I64, I32, P, P, P],
+    "moeb_idpairs_to_masks": [P, I64, I32, P, P, P],
+    "moeb_masks_to_idpairs": [P, I64, I32, P, P, P],
+    "moeb_masks_to_ids6": [P, I64, I32, P, P, P],
     "moeb_masks_to_packed_ranks": [P, I64, I32, I32, I32, P, P, P],
     "moeb_mask_head": [P, I64, I32, I32, I32, P, P],
     "moeb_metrics": [P, P, P, I32, I32, I32, I32, P, P],

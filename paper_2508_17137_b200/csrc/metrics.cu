@@ -697,3 +697,160 @@ extern "C" int moeb_masks_to_packed_ranks(const uint64_t* masks, int64_t rows, i
   k_masks_to_ranks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, bits, words, bad);
   return moeb::check_launch("k_masks_to_ranks");
 }
+
+// Packed expert ids: each row's k ascending ids at 6 bits each (E <= 64) in a
+// little-endian bit stream, row r in bits [6 k r, 6 k (r + 1)) -- 4.5 B per
+// row at k = 6, one more byte than the 27-bit combinatorial rank, but
+// decoded with shifts instead of the rank's digit searches (`words` holds
+// ceil(6 k rows / 32) + 2 u32; zeroed by the caller for the encoder).
+namespace {
+__device__ __forceinline__ uint64_t ids6_row(const uint32_t* __restrict__ w, int64_t r, int k) {
+  const int64_t b = r * 6 * k;
+  const int64_t i = b >> 5;
+  const int sh = (int)(b & 31);
+  const uint64_t lo = (uint64_t)__ldg(w + i) | ((uint64_t)__ldg(w + i + 1) << 32);
+  uint64_t v = lo >> sh;
+  if (sh + 6 * k > 64) v |= (uint64_t)__ldg(w + i + 2) << (64 - sh);  // sh > 0 here
+  return v;
+}
+
+__global__ void k_ids6_to_masks(const uint32_t* __restrict__ words, int64_t rows, int k,
+                                uint64_t* __restrict__ masks, int* __restrict__ bad) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = ids6_row(words, r, k);
+    uint64_t m = 0;
+    for (int j = 0; j < k; ++j) m |= 1ull << ((v >> (6 * j)) & 63u);
+    if (__popcll(m) != k) atomicExch(bad, 1);  // repeated ids: not a top-k row
+    masks[r] = m;
+  }
+}
+
+__global__ void k_masks_to_ids6(const uint64_t* __restrict__ masks, int64_t rows, int k,
+                                uint32_t* __restrict__ words, int* __restrict__ bad) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t m = masks[r];
+    if (__popcll(m) != k) atomicExch(bad, 1);
+    uint64_t v = 0;
+    for (int j = 0; j < k && m; ++j) {
+      v |= (uint64_t)(__ffsll((long long)m) - 1) << (6 * j);
+      m &= m - 1;
+    }
+    const int64_t b = r * 6 * k;
+    const int sh = (int)(b & 31);
+    uint32_t* w = words + (b >> 5);
+    atomicOr(w, (uint32_t)(v << sh));
+    if (sh + 6 * k > 32) atomicOr(w + 1, (uint32_t)(sh ? v >> (32 - sh) : v >> 32));
+    if (sh + 6 * k > 64) atomicOr(w + 2, (uint32_t)(v >> (64 - sh)));  // sh > 0 here
+  }
+}
+}  // namespace
+
+extern "C" int moeb_ids6_to_masks(const uint32_t* words, int64_t rows, int k, uint64_t* masks,
+                                  int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(words && masks && bad && rows >= 0 && k >= 1 && k <= 8, "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_ids6_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(words, rows, k, masks, bad);
+  return moeb::check_launch("k_ids6_to_masks");
+}
+
+extern "C" int moeb_masks_to_ids6(const uint64_t* masks, int64_t rows, int k, uint32_t* words,
+                                  int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(words && masks && bad && rows >= 0 && k >= 1 && k <= 8, "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_masks_to_ids6<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, words, bad);
+  return moeb::check_launch("k_masks_to_ids6");
+}
+
+// Packed id pairs: a row's k ascending ids taken two at a time, each sorted
+// pair (a < b) as its rank C(b, 2) + a < 2016 in 11 bits (an odd k's last id
+// in 6 bits): 33 bits = 4.125 B per row at k = 6 -- 0.75 B more than the
+// 27-bit combinatorial rank, but decoded by three lookups into a 4 KB
+// shared-memory table instead of six digit searches. Little-endian bit
+// stream, row r in bits [bits r, bits (r + 1)), bits = 11 (k / 2) + 6 (k % 2)
+// (`words`: ceil(bits rows / 32) + 2 u32, zeroed by the caller for the encoder).
+namespace {
+__host__ __device__ constexpr int idpair_bits(int k) { return 11 * (k / 2) + 6 * (k % 2); }
+
+__global__ void k_idpairs_to_masks(const uint32_t* __restrict__ words, int64_t rows, int k,
+                                   uint64_t* __restrict__ masks, int* __restrict__ bad) {
+  __shared__ uint16_t tab[2016];  // pair rank -> a | b << 6
+  for (int i = threadIdx.x; i < 2016; i += blockDim.x) {
+    int b = 1;
+    while ((b + 1) * b / 2 <= i) ++b;
+    tab[i] = (uint16_t)((i - b * (b - 1) / 2) | (b << 6));
+  }
+  __syncthreads();
+  const int bits = idpair_bits(k);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b0 = r * bits;
+    const int64_t i = b0 >> 5;
+    const int sh = (int)(b0 & 31);
+    uint64_t v = ((uint64_t)__ldg(words + i) | ((uint64_t)__ldg(words + i + 1) << 32)) >> sh;
+    if (sh + bits > 64) v |= (uint64_t)__ldg(words + i + 2) << (64 - sh);  // sh > 0 here
+    uint64_t m = 0;
+    bool ok = true;
+    for (int j = 0; j < k / 2; ++j) {
+      const uint32_t pr = (uint32_t)(v >> (11 * j)) & 2047u;
+      ok = ok && pr < 2016u;
+      const uint32_t ab = tab[pr < 2016u ? pr : 0u];
+      m |= (1ull << (ab & 63u)) | (1ull << (ab >> 6));
+    }
+    if (k & 1) m |= 1ull << ((v >> (11 * (k / 2))) & 63u);
+    if (!ok || __popcll(m) != k) atomicExch(bad, 1);
+    masks[r] = m;
+  }
+}
+
+__global__ void k_masks_to_idpairs(const uint64_t* __restrict__ masks, int64_t rows, int k,
+                                   uint32_t* __restrict__ words, int* __restrict__ bad) {
+  const int bits = idpair_bits(k);
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t m = masks[r];
+    if (__popcll(m) != k) atomicExch(bad, 1);
+    uint64_t v = 0;
+    int j = 0;
+    for (; j + 1 < k && m; j += 2) {
+      const uint32_t a = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      const uint32_t b = m ? __ffsll((long long)m) - 1 : a;
+      m &= m - 1;
+      v |= (uint64_t)(b * (b - 1) / 2 + a) << (11 * (j / 2));
+    }
+    if ((k & 1) && m) v |= (uint64_t)(__ffsll((long long)m) - 1) << (11 * (k / 2));
+    const int64_t b0 = r * bits;
+    const int sh = (int)(b0 & 31);
+    uint32_t* w = words + (b0 >> 5);
+    atomicOr(w, (uint32_t)(v << sh));
+    if (sh + bits > 32) atomicOr(w + 1, (uint32_t)(sh ? v >> (32 - sh) : v >> 32));
+    if (sh + bits > 64) atomicOr(w + 2, (uint32_t)(v >> (64 - sh)));  // sh > 0 here
+  }
+}
+}  // namespace
+
+extern "C" int moeb_idpairs_to_masks(const uint32_t* words, int64_t rows, int k, uint64_t* masks,
+                                     int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(words && masks && bad && rows >= 0 && k >= 1 && k <= 8, "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 4LL * moeb::num_sms());
+  k_idpairs_to_masks<<<blocks, 256, 0, moeb::as_stream(stream)>>>(words, rows, k, masks, bad);
+  return moeb::check_launch("k_idpairs_to_masks");
+}
+
+extern "C" int moeb_masks_to_idpairs(const uint64_t* masks, int64_t rows, int k, uint32_t* words,
+                                     int* bad, void* stream) {
+  moeb::clear_error();
+  MOEB_REQUIRE(words && masks && bad && rows >= 0 && k >= 1 && k <= 8, "bad arguments");
+  if (rows == 0) return MOEB_OK;
+  const int blocks = (int)std::min<int64_t>((rows + 255) / 256, 8LL * moeb::num_sms());
+  k_masks_to_idpairs<<<blocks, 256, 0, moeb::as_stream(stream)>>>(masks, rows, k, words, bad);
+  return moeb::check_launch("k_masks_to_idpairs");
+}

@@ -21,7 +21,8 @@ from . import _native as nat
 from .cache import POLICIES, CacheConfig
 from .core import ConfigError, ModelShape, RangeError
 from .metrics import MetricCounts, mask_metrics, metric_vector
-from .traces import PackedTraces, ids_to_masks, pack_traces, ranks_to_masks
+from .traces import (PackedTraces, ids6_to_masks, ids_to_masks, idpairs_to_masks, pack_traces,
+                     ranks_to_masks)
 
 
 @dataclass(frozen=True)
@@ -566,7 +567,12 @@ class StreamingReplay:
         return self.bufs[0].rows
 
     def run(self, predictor, capacities, warmup: int, budget: int, host_batches,
-            policy: str = "lru", metrics: bool = False, timing=None, per_prompt: bool = False):
+            policy: str = "lru", metrics: bool = False, timing=None, per_prompt: bool = False,
+            wire: str | None = None):
+        """``wire="ids6"`` / ``"idpairs"``: the host batches are packed
+        6-bit id / id-pair streams (``masks_to_ids6`` / ``masks_to_idpairs``);
+        otherwise the format follows the batch's dtype / shape (masks, u8 ids,
+        ranks)."""
         shape, dev = self.shape, self.device
         L, E = shape.num_layers, shape.num_experts
         main = torch.cuda.current_stream(dev)
@@ -592,11 +598,13 @@ class StreamingReplay:
             b = i % self.NBUF
             buf = self.bufs[b]
             empty = getattr(predictor, "empty", False) and not metrics
-            ranked = hb.dtype == torch.int32 and hb.dim() == 1  # combinatorial ranks:
+            ids6 = wire in ("ids6", "idpairs")  # packed ids / id pairs (a bit stream)
+            ranked = not ids6 and hb.dtype == torch.int32 and hb.dim() == 1  # combinatorial ranks:
             packed_ranks = ranked and hb.shape[0] != buf.rows    # as a bit stream
-            compact = ranked or hb.dtype == torch.uint8  # or [rows][k] expert ids
+            compact = ids6 or ranked or hb.dtype == torch.uint8  # or [rows][k] expert ids
             # the first batch lands in prompt ranges (not splittable: a bit stream)
-            split = i == 0 and len(self.first_views) > 1 and not empty and not packed_ranks
+            split = (i == 0 and len(self.first_views) > 1 and not empty and not packed_ranks
+                     and not ids6)
             parts = []
             with torch.cuda.stream(self.s_copy):
                 if freed[b] is not None:
@@ -616,7 +624,7 @@ class StreamingReplay:
                     after which dst holds the masks."""
                     done = torch.cuda.Event()
                     if compact:
-                        if packed_ranks:  # the whole stream (no split for it)
+                        if packed_ranks or ids6:  # the whole stream (no split for it)
                             ib.copy_(hb, non_blocking=True)
                         else:
                             ib[r0:r1].copy_(hb[r0:r1], non_blocking=True)
@@ -624,7 +632,11 @@ class StreamingReplay:
                         landed.record(self.s_copy)
                         self.s_dec.wait_event(landed)
                         with torch.cuda.stream(self.s_dec):
-                            if packed_ranks:
+                            if wire == "idpairs":
+                                idpairs_to_masks(ib, shape.top_k, r1 - r0, dst, self.ids_bad)
+                            elif ids6:
+                                ids6_to_masks(ib, shape.top_k, r1 - r0, dst, self.ids_bad)
+                            elif packed_ranks:
                                 ranks_to_masks(ib, shape.top_k, E, dst, self.ids_bad, rows=r1 - r0)
                             elif ranked:
                                 ranks_to_masks(ib[r0:r1], shape.top_k, E, dst, self.ids_bad)

@@ -353,6 +353,76 @@ def ranks_to_masks(ranks: torch.Tensor, k: int, num_experts: int, out: torch.Ten
     return out
 
 
+def ids6_words(rows: int, k: int) -> int:
+    """u32 words of a packed 6-bit id stream of `rows` rows (+2 padding words)."""
+    return (rows * 6 * k + 31) // 32 + 2
+
+
+def masks_to_ids6(truth: torch.Tensor, k: int) -> torch.Tensor:
+    """One-word expert masks -> the packed-id wire format: each row's k
+    ascending ids at 6 bits (E <= 64) in a bit stream, 4.5 B per row at k = 6
+    (moeb_masks_to_ids6), as int32 words (StreamingReplay.run(wire="ids6")
+    decodes them with moeb_ids6_to_masks). Every row must carry exactly k
+    experts, as a validated reference trace row does."""
+    if k > 8:
+        raise ConfigError("the packed-id wire format takes k <= 8")
+    t = truth.reshape(-1).contiguous()
+    out = torch.zeros(ids6_words(t.numel(), k), dtype=torch.int32, device=t.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=t.device)
+    nat.call("moeb_masks_to_ids6", nat.ptr(t), t.numel(), int(k), nat.ptr(out), nat.ptr(bad),
+             nat.stream_ptr())
+    if int(bad.item()):
+        raise RangeError(f"a row does not have exactly {k} experts")
+    return out
+
+
+def ids6_to_masks(words: torch.Tensor, k: int, rows: int, out: torch.Tensor, bad: torch.Tensor):
+    """Device decode of a packed 6-bit id stream into masks; bad[0] is set to 1
+    (asynchronously) if a row does not hold k distinct experts."""
+    nat.call("moeb_ids6_to_masks", nat.ptr(words), int(rows), int(k), nat.ptr(out), nat.ptr(bad),
+             nat.stream_ptr())
+    return out
+
+
+def idpair_bits(k: int) -> int:
+    """Bits per row of the packed id-pair format: 11 per sorted pair, 6 for an
+    odd k's last id (33 at k = 6)."""
+    return 11 * (k // 2) + 6 * (k % 2)
+
+
+def idpair_words(rows: int, k: int) -> int:
+    """u32 words of a packed id-pair stream of `rows` rows (+2 padding words)."""
+    return (rows * idpair_bits(k) + 31) // 32 + 2
+
+
+def masks_to_idpairs(truth: torch.Tensor, k: int) -> torch.Tensor:
+    """One-word expert masks -> the packed id-pair wire format: each row's
+    ascending ids two at a time, a sorted pair (a < b) as C(b, 2) + a in 11
+    bits (4.125 B per row at k = 6; moeb_masks_to_idpairs), as int32 words
+    (StreamingReplay.run(wire="idpairs") decodes them with
+    moeb_idpairs_to_masks: three lookups into a 4 KB table per row). Every row
+    must carry exactly k experts, as a validated reference trace row does."""
+    if k > 8:
+        raise ConfigError("the packed id-pair wire format takes k <= 8")
+    t = truth.reshape(-1).contiguous()
+    out = torch.zeros(idpair_words(t.numel(), k), dtype=torch.int32, device=t.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=t.device)
+    nat.call("moeb_masks_to_idpairs", nat.ptr(t), t.numel(), int(k), nat.ptr(out), nat.ptr(bad),
+             nat.stream_ptr())
+    if int(bad.item()):
+        raise RangeError(f"a row does not have exactly {k} experts")
+    return out
+
+
+def idpairs_to_masks(words: torch.Tensor, k: int, rows: int, out: torch.Tensor,
+                     bad: torch.Tensor):
+    """Device decode of a packed id-pair stream into masks; bad[0] is set to 1
+    (asynchronously) if a row does not hold k distinct experts."""
+    nat.call("moeb_idpairs_to_masks", nat.ptr(words), int(rows), int(k), nat.ptr(out),
+             nat.ptr(bad), nat.stream_ptr())
+    return out
+
+
 def ids_to_masks(ids: torch.Tensor, num_experts: int, out: torch.Tensor, bad: torch.Tensor):
     """Device decode of the compact rows into masks (moeb_ids_to_masks); bad[0]
     is set to 1 (asynchronously) if an id is >= num_experts."""

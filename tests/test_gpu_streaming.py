@@ -164,3 +164,87 @@ def test_streaming_ranks_equals_masks(geom):
     if k == 6:  # C(64, 8) >= 2^32: no 4-byte rank format
         with pytest.raises(m.ConfigError):
             m.masks_to_ranks(b.truth, 8, 64)
+
+
+def _restate_row(fmt, v, k):
+    """A row's ids from its bit field, as the format docs state it."""
+    if fmt == "ids6":
+        return [(v >> (6 * j)) & 63 for j in range(k)]
+    ids = []
+    for j in range(k // 2):
+        pr = (v >> (11 * j)) & 2047
+        b = max(q for q in range(1, 64) if q * (q - 1) // 2 <= pr)
+        ids += [pr - b * (b - 1) // 2, b]
+    if k % 2:
+        ids.append((v >> (11 * (k // 2))) & 63)
+    return ids
+
+
+@pytest.mark.parametrize("fmt", ["ids6", "idpairs"])
+@pytest.mark.parametrize("geom", [(26, 64, 6), (3, 64, 2), (5, 40, 4), (4, 48, 7), (2, 64, 8)])
+def test_streaming_ids6_equals_masks(geom, fmt):
+    """Host batches as packed 6-bit expert ids (4.5 B/row at k = 6, decoded
+    with shifts) or packed sorted id pairs (11 bits per pair, 4.125 B/row,
+    decoded by table lookups) give the counters, per-prompt counters and
+    metrics of the mask batches; masks <-> stream round trip on a 1M-row
+    random sample (ids 0 and 63 included); the stream layout restated; rows
+    without exactly k distinct experts are flagged."""
+    import paper_2508_17137_b200 as m
+    m.load_library()
+    L, E, k = geom
+    shape = m.ModelShape(L, E, k)
+    enc = m.masks_to_ids6 if fmt == "ids6" else m.masks_to_idpairs
+    dec = m.ids6_to_masks if fmt == "ids6" else m.idpairs_to_masks
+    bits = 6 * k if fmt == "ids6" else 11 * (k // 2) + 6 * (k % 2)
+    b = m.generate_packed(m.GeneratorConfig(40, 30, shape, max(8, k), 0.9, 4))
+    words = enc(b.truth, k)
+    assert words.dtype == torch.int32 and words.numel() == (b.rows * bits + 31) // 32 + 2
+    back = torch.empty_like(b.truth)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dec(words, k, b.rows, back, bad)
+    torch.cuda.synchronize()
+    assert torch.equal(back, b.truth) and int(bad.item()) == 0
+    wn = words.cpu().numpy().view(np.uint32)
+    stream = int.from_bytes(wn.tobytes(), "little")
+    t = b.truth.reshape(-1).cpu().numpy().view(np.uint64)
+    for i in (0, 1, 2, 7, b.rows // 2, b.rows - 1):  # the stream layout, restated
+        v = (stream >> (bits * i)) & ((1 << bits) - 1)
+        ids = [e for e in range(64) if (int(t[i]) >> e) & 1]
+        assert _restate_row(fmt, v, k) == ids
+    # random k-subsets of 64 experts (E = 64), 1M rows
+    rng = np.random.default_rng(L + k)
+    n = 1 << 20
+    keys = rng.random((n, 64)).argsort(axis=1)[:, :k]
+    keys[0] = np.arange(k)
+    keys[1] = np.arange(64 - k, 64)
+    ms_np = np.zeros(n, dtype=np.uint64)
+    for j in range(k):
+        ms_np |= np.uint64(1) << keys[:, j].astype(np.uint64)
+    ms = torch.from_numpy(ms_np.view(np.int64)).cuda().reshape(-1, 1)
+    w2 = enc(ms, k)
+    out = torch.empty_like(ms)
+    dec(w2, k, n, out, bad)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ms) and int(bad.item()) == 0
+    if L == 26:
+        w = np.random.default_rng(2).normal(0.0, 0.01, (64, 91))
+        model = m.LinearModel(shape, m.LearnerConfig(epochs=0), w, trained=True)
+        pred = m.make_predictor("learned_linear", shape, model=model)
+        sr = m.StreamingReplay(shape, b.row_off_host, b.prompt_ids)
+        r1 = sr.run(pred, [83, 166], 8, 6, [b.truth.cpu().pin_memory()] * 3, metrics=True,
+                    per_prompt=True)
+        r2 = sr.run(pred, [83, 166], 8, 6, [words.cpu().pin_memory()] * 4, metrics=True,
+                    per_prompt=True, wire=fmt)
+        torch.cuda.synchronize()
+        assert int(sr.ids_bad.item()) == 0
+        for (c1, v1, p1), (c2, v2, p2) in zip(r1, r2):
+            assert torch.equal(c1, c2) and torch.equal(v1, v2) and torch.equal(p1, p2)
+    wrong = b.truth.clone()
+    wrong[7] = 1
+    with pytest.raises(m.RangeError):
+        enc(wrong, k)
+    dup = words.clone()  # all-ones fields: a repeated id 63 / a pair rank >= C(64, 2)
+    dup[0] = -1
+    dec(dup, k, b.rows, back, bad)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 1
