@@ -3,7 +3,9 @@ ranks (gloo, both ranks on cuda:0 as bench.py's MOEB_BENCH_ONE_DEVICE path
 does on a one-GPU box): each rank passes the same traces, replays its
 row-balanced prompt shard on the GPU, and every rank returns a SimReport
 bit-identical to the one-process replay, per-prompt counters included -- the
-analogue of the reference's jobs-invariance test (test_engine.py:104-119).
+analogue of the reference's jobs-invariance test (test_engine.py:104-119);
+the sharded metric counters (distributed.metrics_sharded) equal the
+one-process prediction_metrics.
 jobs > 1 in one process with one visible GPU is the one-device replay."""
 import os
 import socket
@@ -45,9 +47,20 @@ def _summary(rep):
                    for pid, c in rep.per_prompt.items()))
 
 
+def _metrics(mc):
+    return (mc.tp.tolist(), mc.fp.tolist(), mc.fn.tolist(), mc.positions, mc.exact,
+            mc.label_correct)
+
+
 def _results(m):
     shape, packed, model, cfg = _setup(m)
     out = {}
+    lin = m.make_predictor("learned_linear", shape, model=model)
+    if dist.is_initialized():  # the sharded metric counters (one all-reduce)
+        from paper_2508_17137_b200.distributed import metrics_sharded
+        out["metrics"] = _metrics(metrics_sharded(packed, lin, cfg))
+    else:
+        out["metrics"] = _metrics(m.prediction_metrics(packed, lin, cfg))
     for kind in ("learned_linear", "lru_only"):
         pred = (m.make_predictor(kind, shape, model=model) if kind == "learned_linear"
                 else m.make_predictor(kind, shape))
