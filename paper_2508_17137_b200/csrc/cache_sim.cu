@@ -1467,7 +1467,10 @@ __device__ __forceinline__ uint64_t after_last(uint64_t k, uint64_t t, int x) {
 }
 
 template <bool KPH>  // KPH: also the cache-independent counters (else a.given is added)
-__global__ void __launch_bounds__(128) k_stack_replay(const SimArgs a, int H, int dmax,
+// (128, 10): at most 48 registers, so ten blocks (40 warps) fit an SM -- the
+// shared-memory limit -- and C2's 6,994 prompt warps take 1.2 resident rounds
+// instead of 1.5 (step 5.14 -> 5.04 ms, profiles/r02_k1s_launch_bounds_ab.log)
+__global__ void __launch_bounds__(128, 10) k_stack_replay(const SimArgs a, int H, int dmax,
                                                       int32_t* plist, int32_t* plist_n) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr unsigned FULL = 0xffffffffu;
