@@ -128,8 +128,9 @@ int moeb_cache_sim_counted(const uint64_t* truth, const uint64_t* const* preds,
  * Counters as moeb_cache_sim (+=), for n_caps <= 16 capacities in ascending order;
  * max_prompt_rows sizes the per-prompt shared-memory state. max_row_keys: an
  * upper bound on the experts of any truth row (ModelShape.top_k for validated
- * traces; 0 = unknown): with budget + max_row_keys <= 15 the per-row key
- * counts are kept as 4-bit fields (half the shared memory, same results).
+ * traces; 0 = unknown): with budget + max_row_keys <= 15 and MOEB_K1M_NIB=1
+ * the per-row key counts are kept as 4-bit fields (half the shared memory,
+ * same results).
  * workspace (nullable, >= moeb_cache_replay_stack_workspace_bytes(n_preds,
  * n_prompts, L) bytes): the per-key last-access tables live there instead of
  * in shared memory, so more prompts are replayed per SM (same results).

@@ -2238,9 +2238,11 @@ extern "C" int moeb_cache_replay_stack(const uint64_t* truth, const uint64_t* co
       !(env && env[0] == 's'))
     a.lr_g = static_cast<uint32_t*>(workspace);
   a.off_cnt = a.lr_g ? 0 : align16(4LL * L * 64);
-  // 4-bit row counts when no row can touch more than 15 keys
-  const char* nenv = getenv("MOEB_K1M_NIB");  // "0": u8 counts
-  const bool nib = max_row_keys > 0 && kmax + max_row_keys <= 15 && !(nenv && nenv[0] == '0');
+  // 4-bit row counts when no row can touch more than 15 keys: opt-in
+  // (MOEB_K1M_NIB=1; measured no faster than u8 counts, and a truth row with
+  // more than max_row_keys experts would overflow its field)
+  const char* nenv = getenv("MOEB_K1M_NIB");
+  const bool nib = max_row_keys > 0 && kmax + max_row_keys <= 15 && nenv && nenv[0] == '1';
   a.off_blk = a.off_cnt + align16((R + 31) / 32 * (nib ? 16 : 32));
   a.off_sup = a.off_blk + align16(2LL * 32 * ((R + 1023) / 1024));
   a.off_ctr = a.off_sup + align16(4LL * ((R + 1023) / 1024 + 1));

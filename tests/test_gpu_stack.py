@@ -128,19 +128,19 @@ def test_stack_replay_several_streams(monkeypatch):
 @pytest.mark.parametrize("geom", [(26, 64, 6), (3, 64, 2), (5, 40, 4)])
 @pytest.mark.parametrize("ragged", [False, True])
 @pytest.mark.parametrize("warmup", [0, 8])
-@pytest.mark.parametrize("variant", ["default", "smem_u8"])
+@pytest.mark.parametrize("variant", ["default", "smem_u8", "nib"])
 def test_stack_multi_equals_exact(geom, ragged, warmup, variant, monkeypatch):
     """K1m (every capacity above the prefetch budget in one stack-distance
     pass, moeb_cache_replay_stack) == the exact kernel: counters and
     per-prompt counters, learned / empty (lru_only) / over-budget random /
-    unbounded all-ones predictions, several streams per call. Both layouts:
-    last-access tables in the caller's global workspace with 4-bit row counts
-    (the default when budget + top-k <= 15) and everything in shared memory
-    with u8 counts."""
+    unbounded all-ones predictions, several streams per call. Three layouts:
+    last-access tables in the caller's global workspace (default), everything
+    in shared memory, and 4-bit row counts (opt-in, budget + top-k <= 15)."""
     import paper_2508_17137_b200 as m
     if variant == "smem_u8":
         monkeypatch.setenv("MOEB_K1M_LR", "smem")
-        monkeypatch.setenv("MOEB_K1M_NIB", "0")
+    if variant == "nib":  # 4-bit row counts (opt-in)
+        monkeypatch.setenv("MOEB_K1M_NIB", "1")
     m.load_library()
     L, E, k = geom
     shape = m.ModelShape(L, E, k)
